@@ -1,0 +1,336 @@
+"""Benchmark: SLQ edge·probe·steps/s on BASELINE.json configs[1] (C2).
+
+Workload (one "step" = one full signature computation over the graph):
+  SBM n=100,000, 10 equal blocks, p_in=1e-3, p_out=1e-5 (seeded synthetic), normalized Laplacian,
+  n_v=100 Rademacher probes x s=15 Lanczos steps (full CGS reorth, the reference default),
+  heat + wave traces on 250 log-spaced t in [1e-2, 1e2], fp64 (``--dtype f32`` for fp32 storage).
+  Units per step = nnz * n_v * s (one stored nonzero x one probe x one operator application).
+
+Arms:
+  default            hand-written sm_100a kernels through libslq_b200.so
+  --impl reference   the CPU oracle port of the reference algorithm (oracle/slq_oracle.py, numpy +
+                     scipy, all host threads) on the same config; rank 0 only.
+
+Timing: W warm-up steps, then K timed steps, each bracketed by CUDA events on the launching stream;
+L2 is flushed (256 MiB write) between timed steps, outside the events.  Multi-GPU: one process per
+GPU (torchrun), weak scaling: rank r runs probes [100r, 100r+100) and the rules are all-gathered
+over NCCL; device time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = {"workload": "C2 SBM n=100000 blocks=10 p_in=1e-3 p_out=1e-5, normalized Laplacian, "
+                        "heat+wave T=250 t in [1e-2,1e2]",
+            "graph": "sbm", "n": 100_000, "blocks": 10, "p_in": 1e-3, "p_out": 1e-5, "graph_seed": 0,
+            "n_v_per_gpu": 100, "lanczos_steps": 15, "T": 250, "reorth": "full CGS (reference default)",
+            "l2": "flushed between timed steps (256 MiB write), outside the timed events"}
+METRIC = "SLQ edge·probe·steps/sec"
+UNIT = "edge·probe·step/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_graph():
+    from paper_2003_01282_b200 import synth
+
+    return synth.sbm(WORKLOAD["n"], WORKLOAD["blocks"], WORKLOAD["p_in"], WORKLOAD["p_out"],
+                     seed=WORKLOAD["graph_seed"])
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, bf16 copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_baseline(g, n_v, s, grid, threads, max_probes=None):
+    """Oracle port of the reference algorithm timed on the host cores (bounded sample)."""
+    from oracle import slq_oracle as O
+
+    probes = n_v if max_probes is None else min(n_v, max_probes)
+    t0 = time.perf_counter()
+    op = O.make_block_operator(g, O.NORMALIZED_LAPLACIAN)
+    rules = O.slq_rules(op, probes, s, 0, threads=threads)
+    O.heat_from_rules(rules, g.n, grid)
+    O.wave_from_rules(rules, g.n, grid)
+    dt = time.perf_counter() - t0
+    units = g.nnz * probes * s
+    return units / dt, dt, probes
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    from oracle import slq_oracle as O
+
+    g = build_graph()
+    s, n_v = WORKLOAD["lanczos_steps"], WORKLOAD["n_v_per_gpu"]
+    grid = O.time_grid(1e-2, 1e2, WORKLOAD["T"])
+    threads = os.cpu_count() or 1
+    vals, times = [], []
+    for k in range(args.warmup + args.steps):
+        v, dt, probes = cpu_baseline(g, n_v, s, grid, threads, max_probes=args.ref_probes)
+        if k >= args.warmup:
+            vals.append(v)
+            times.append(dt)
+    value = float(np.mean(vals))
+    sample = f"first {probes} of {n_v} probes of the C2 workload (per-probe cost is independent of n_v), oracle port"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SBM)",
+            "config": dict(WORKLOAD, parallelism="cpu threads"), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def algorithmic_bytes(g, c, s, vb):
+    """Per-class algorithmic DRAM bytes of one Lanczos run on one chunk of c probes."""
+    n, nnz = g.n, g.nnz
+    row = c * vb
+    spmm = s * (nnz * (row + 4) + n * (2 * row + 24))
+    dot = sum(n * row * (i + 2) for i in range(s - 1))
+    upd = sum(n * row * (i + 3) for i in range(s - 1))
+    return {"spmm": spmm, "cgs_dot": dot, "cgs_update": upd}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_01282_b200 import _lib
+    from paper_2003_01282_b200.descriptors import TimeGrid, netlsd_heat_wave_slq
+    from paper_2003_01282_b200.device import DeviceGraph, gauss_rules
+    from paper_2003_01282_b200.dist import gather_rules_arrays
+    from paper_2003_01282_b200.graphs import Graph
+    from paper_2003_01282_b200.slq import SlqConfig
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g = build_graph()
+    s, n_v = WORKLOAD["lanczos_steps"], WORKLOAD["n_v_per_gpu"]
+    total_probes = n_v * world
+    grid = TimeGrid(1e-2, 1e2, WORKLOAD["T"])
+    dtype = args.dtype
+    vb = 8 if dtype == "f64" else 4
+    tgrid = torch.as_tensor(grid.values, device=dev)
+    off_d = torch.as_tensor(g.row_offsets, device=dev)
+    cols_d = torch.as_tensor(g.col_indices, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        # device-resident input: prepare + probes + Lanczos + rules + quadrature + aggregate
+        dg = DeviceGraph.__new__(DeviceGraph)
+        import ctypes
+
+        dg.device, dg.graph, dg.n = dev, g, g.n
+        dg.handle = ctypes.c_void_p()
+        _lib.check(_lib.load().slq_graph_create(g.n, g.nnz, off_d.data_ptr(), cols_d.data_ptr(), None,
+                                                stream.cuda_stream, ctypes.byref(dg.handle)))
+        rules = dg.rules("normalized_laplacian", 0, rank * n_v, n_v, s, dtype=dtype)
+        if world > 1:
+            nodes, weights, steps = gather_rules_arrays(rules.nodes, rules.weights, rules.steps, total_probes)
+            rules = type(rules)(nodes, weights, steps, g.n)
+        out = []
+        for fn in (_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM):
+            out.append(rules.estimate(rules.quadrature(tgrid, fn)))
+        del dg
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    launches0 = _lib.launch_count()
+    _lib.profile_begin()
+    times = []
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    prof = _lib.profile_end()
+    launches = _lib.launch_count() - launches0
+    clocks = sampler.stop() if sampler else None
+    ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    units_step = g.nnz * n_v * s * world
+    value = units_step / (ms * 1e-3)
+
+    # ---- e2e through the public API with host (pinned) buffers ----
+    pin_off = torch.as_tensor(g.row_offsets).pin_memory()
+    pin_cols = torch.as_tensor(g.col_indices).pin_memory()
+    pin_w = torch.as_tensor(g.weights).pin_memory()
+    e2e_times = []
+    cfg = SlqConfig(n_v=n_v, s=s, seed=0)
+    h2d = (g.n + 1) * 8 + g.nnz * 8
+    for k in range(args.warmup + args.steps):
+        gh = Graph(n=g.n, row_offsets=pin_off.numpy(), col_indices=pin_cols.numpy(), weights=pin_w.numpy(), m=g.m)
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        heat, wave = netlsd_heat_wave_slq(gh, grid, cfg, dtype=dtype, with_hash=False)
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            e2e_times.append(time.perf_counter() - t0)
+    d2h = 3 * 2 * WORKLOAD["T"] * 8
+    e2e_s = float(np.mean(e2e_times))
+    e2e_value = g.nnz * n_v * s / e2e_s
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    # ---- roofline of the dominant kernel class ----
+    peak, peak_src = measured_peaks()
+    ab = algorithmic_bytes(g, n_v, s, vb)
+    per_class = {}
+    for k in ("spmm", "cgs_dot", "cgs_update"):
+        t_ms = prof[k]["ms"]
+        per_class[k] = {"ms_per_step": t_ms / args.steps, "launches_per_step": prof[k]["launches"] / args.steps,
+                        "GB_per_step": ab[k] / 1e9,
+                        "achieved_GBs": (ab[k] * args.steps / (t_ms * 1e-3) / 1e9) if t_ms > 0 else None}
+    dom = max(per_class, key=lambda k: per_class[k]["ms_per_step"])
+    ach = per_class[dom]["achieved_GBs"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded SBM, BASELINE configs[1] shape)",
+        "config": dict(WORKLOAD, parallelism=f"probe-sharded x{world}" if world > 1 else "single GPU",
+                       total_probes=total_probes, nnz=g.nnz),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": (ach / peak) if ach else None, "traffic": args.traffic, "peak_source": peak_src},
+        "kernels": per_class,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "seconds_per_signature": e2e_s,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "netlsd_heat_wave_slq(Graph on pinned host arrays) incl. H2D, device prepare, D2H"},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        v, dt, probes = cpu_baseline(g, n_v, s, grid.values, os.cpu_count() or 1, max_probes=args.ref_probes)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                                "sample": f"first {probes} of {n_v} probes of the same C2 workload, {dt:.1f} s "
+                                          "(oracle/slq_oracle.py: numpy+scipy port of the reference)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
+    ap.add_argument("--ref-probes", type=int, default=None,
+                    help="probes timed in the CPU arms (default: all n_v)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes/launch of the dominant kernel")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: --warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,160 @@
+/*
+ * slq_b200.h — C ABI of libslq_b200.so, the B200 (sm_100a) stochastic Lanczos
+ * quadrature engine.  Plain pointers and sizes only; no torch types.
+ *
+ * Reference interfaces replaced (all paths under /root/reference/pkg/src/spectrace/):
+ *
+ *   slq_graph_create / _host     operators.py:52-62  (_adjacency, degrees) and the
+ *                                operator set-up of make_operator, operators.py:65-102
+ *   slq_operator_apply           LinearOperator.apply closures, operators.py:76-99
+ *   slq_operator_interval        LinearOperator.interval, operators.py:79-101
+ *   slq_lanczos                  slq._collect_rules/_probe_rule (slq.py:63-86) minus the
+ *                                eigensolve: probe draw, lanczos_tridiagonalize
+ *                                (lanczos.py:79-145) with CGS reorth (lanczos.py:70-76)
+ *   slq_gauss_rules              quadrature_rule (lanczos.py:148-163) + node clip (slq.py:76-77)
+ *   slq_quadrature               _apply_rule over the whole grid (slq.py:89-95, 153-168)
+ *   slq_estimate                 _estimate_from (slq.py:98-105)
+ *   slq_probes / slq_probe_state _draw_probe + seeding (slq.py:63-72)
+ *
+ * Conventions
+ *   - Every data pointer is a DEVICE pointer unless the name ends in _host.
+ *   - Matrices are row-major with an explicit leading dimension (ld, in elements).
+ *   - Work is stream-ordered on the given cudaStream_t (passed as void*; NULL =
+ *     legacy default stream).  No call synchronises the device except the
+ *     _host variants and slq_profile_end.
+ *   - Return value: SLQ_OK or an error code; slq_last_error() gives a
+ *     thread-local message.  The Python layer maps codes to the reference's
+ *     exceptions (ValueError, TridiagonalEigenError, RuntimeError).
+ *   - Reentrant: a graph handle is immutable after creation; concurrent calls
+ *     on one handle from different streams are allowed (workspace is
+ *     stream-ordered, allocated per call).
+ */
+#ifndef SLQ_B200_H
+#define SLQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SLQ_OK 0
+#define SLQ_ERR_VALUE 1      /* invalid argument / undefined operator  -> ValueError           */
+#define SLQ_ERR_EIGEN 2      /* tridiagonal eigensolver did not converge -> TridiagonalEigenError */
+#define SLQ_ERR_CUDA 3       /* CUDA runtime error                     -> RuntimeError          */
+#define SLQ_ERR_NONFINITE 4  /* f non-finite at a node (slq.py:91-94)  -> ValueError           */
+#define SLQ_ERR_ALLOC 5      /* device allocation failed               -> MemoryError           */
+
+/* operator kinds (operators.py:31-34) */
+#define SLQ_LAPLACIAN 0
+#define SLQ_NORMALIZED_LAPLACIAN 1
+#define SLQ_DENSITY 2
+
+/* vector storage precision inside the Lanczos recurrence (reductions are always fp64) */
+#define SLQ_F64 0
+#define SLQ_F32 1
+
+/* integrands for slq_quadrature: f(t, x) at clamped nodes x */
+#define SLQ_FN_HEAT 0      /* exp(-t x)                 descriptors.py:132-134 */
+#define SLQ_FN_WAVE_RE 1   /* cos(t x)                  Re exp(-i t x)          */
+#define SLQ_FN_WAVE_IM 2   /* -sin(t x)                 Im exp(-i t x)          */
+#define SLQ_FN_XLOGX 3     /* x ln x (0 at x<=0)        descriptors.py:220-224  */
+#define SLQ_FN_IDENTITY 4  /* x                                                  */
+
+typedef struct slq_graph slq_graph;
+
+typedef struct slq_graph_info_t {
+  int64_t n;
+  int64_t nnz;          /* stored nonzeros = row_offsets[n] */
+  double trace_l;       /* tr L = sum of degrees (operators.py:93) */
+  double max_degree;
+  int64_t isolated;     /* vertices of degree 0 */
+  int32_t unit_weights; /* 1 when every weight is exactly 1.0 (weights dropped on device) */
+  int32_t ntiles;       /* SpMM row tiles (fixed per graph; reduction order depends only on them) */
+} slq_graph_info_t;
+
+/* Build the device graph from DEVICE CSR arrays (canonical layout of graphs.py:110-132):
+ * int64 offsets[n+1], int64 cols[nnz] (sorted per row), float64 weights[nnz] or NULL
+ * (NULL = every weight 1.0).  The arrays are copied/narrowed; the caller keeps ownership. */
+int slq_graph_create(int64_t n, int64_t nnz, const int64_t* offsets, const int64_t* cols,
+                     const double* weights, void* stream, slq_graph** out);
+/* Same from HOST arrays (the end-to-end plugin entry: H2D copies happen inside). */
+int slq_graph_create_host(int64_t n, int64_t nnz, const int64_t* offsets_host,
+                          const int64_t* cols_host, const double* weights_host, void* stream,
+                          slq_graph** out);
+int slq_graph_info(const slq_graph* g, slq_graph_info_t* out);
+void slq_graph_destroy(slq_graph* g);
+
+/* Copy the prepared degree vector d = A.1 and dinv = 1/sqrt(d) (0 if isolated) into [n]
+ * device buffers (either may be NULL).  operators.py:58-62, 84-86. */
+int slq_graph_degrees(const slq_graph* g, double* degree, double* dinv, void* stream);
+
+/* Spectrum bounds used for node clamping (operators.py:79,90,101). */
+int slq_operator_interval(const slq_graph* g, int kind, double* lo, double* hi);
+
+/* Y = Op(X) for ncols columns; X, Y are [n][ld] float64.  Bit-identical to the
+ * reference closure on each column (sequential in-row sums, no FMA). */
+int slq_operator_apply(const slq_graph* g, int kind, const double* x, double* y, int64_t ncols,
+                       int64_t ld, void* stream);
+
+/* Lanczos tridiagonals for probes [probe_begin, probe_begin+count) of seed `seed`.
+ * Probes: Rademacher from PCG64(SeedSequence(seed, spawn_key=(i,))) (slq.py:63-73).
+ * steps: requested s (clamped to n, lanczos.py:105); reorth: 1 on, 0 off, -1 = reference
+ * default (on iff s <= 100, lanczos.py:106-107).  dtype: SLQ_F64 / SLQ_F32 vector storage.
+ * Outputs (ld = steps): alpha[count][steps], beta[count][steps] (entries >= steps_out-1 unused),
+ * steps_out[count] = achieved steps (breakdown shortens, lanczos.py:133-134).
+ * Per-probe results do not depend on count, probe_begin or chunking. */
+int slq_lanczos(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count,
+                int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
+                void* stream);
+
+/* Same recurrence from caller-given unit start vectors q0[n][ldq] (column j = start vector j);
+ * the lanczos_tridiagonalize(op, q0, s) entry (lanczos.py:79-104). */
+int slq_lanczos_start(const slq_graph* g, int kind, const double* q0, int64_t ldq, int64_t count,
+                      int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
+                      void* stream);
+
+/* Gauss rules of `count` tridiagonals (alpha/beta rows of length ld, steps[count]):
+ * nodes ascending, clamped to [lo, hi]; weights = squared first eigenvector entries.
+ * info[p] = 0 ok, else the eigensolver failed for probe p (returns SLQ_ERR_EIGEN). */
+int slq_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count,
+                    int ld, double lo, double hi, double* nodes, double* weights, int32_t* info,
+                    void* stream);
+
+/* per_vector[T][count] = sum_k weights[p][k] * f(t, nodes[p][k]) over k < steps[p]. */
+int slq_quadrature(const double* nodes, const double* weights, const int32_t* steps, int64_t count,
+                   int ld, const double* t, int64_t T, int fn, double* per_vector, void* stream);
+
+/* value[t] = n * mean_p per_vector[t][p]; std_error[t] = std(n*pv, ddof=1)/sqrt(count). */
+int slq_estimate(const double* per_vector, int64_t T, int64_t count, double n, double* value,
+                 double* std_error, void* stream);
+
+/* Rademacher probes as +-1.0 into out[n][ld] (column j = probe probe_begin+j). */
+int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int64_t n, double* out,
+               int64_t ld, void* stream);
+/* Host: PCG64 (state_hi, state_lo, inc_hi, inc_lo) of SeedSequence(seed, spawn_key=(index,)). */
+int slq_probe_state(uint64_t seed, uint64_t index, uint64_t out_host[4]);
+
+/* Batched block-diagonal path (C3): per-graph heat signatures of many small graphs stacked
+ * in one block-diagonal CSR.  vertex_offsets[G+1] (device int64) delimit the graphs; each
+ * graph uses probes 0..n_v-1 restricted to its own n_g vertices (stream prefixes, q0 = v/sqrt(n_g)).
+ * Outputs: nodes/weights [G][n_v][steps], steps_out [G][n_v]. */
+int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs,
+                        int kind, uint64_t seed, int n_v, int steps, int dtype, double* nodes,
+                        double* weights, int32_t* steps_out, void* stream);
+
+/* Diagnostics */
+const char* slq_last_error(void);
+uint64_t slq_launch_count(void);                /* kernels launched by this library so far */
+void slq_profile_begin(void);                   /* start per-class CUDA-event timing */
+/* Stop timing (synchronises the recorded events); fills ms[class] and launches[class] for
+ * up to `n` classes: 0 prepare, 1 probe, 2 spmm, 3 cgs_dot, 4 cgs_update, 5 reduce, 6 eig,
+ * 7 quad, 8 estimate, 9 batched.  Returns the number of classes. */
+int slq_profile_end(double* ms, int64_t* launches, int n);
+const char* slq_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLQ_B200_H */

@@ -1,0 +1,136 @@
+"""ctypes binding of libslq_b200.so (C ABI in include/slq_b200.h).
+
+There is no fallback: if the library is missing or no CUDA device is present,
+every compute entry point raises ``SlqLibraryError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import SlqLibraryError, TridiagonalEigenError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslq_b200.so")
+
+SLQ_OK, SLQ_ERR_VALUE, SLQ_ERR_EIGEN, SLQ_ERR_CUDA, SLQ_ERR_NONFINITE, SLQ_ERR_ALLOC = range(6)
+LAPLACIAN, NORMALIZED_LAPLACIAN, DENSITY = 0, 1, 2
+F64, F32 = 0, 1
+FN_HEAT, FN_WAVE_RE, FN_WAVE_IM, FN_XLOGX, FN_IDENTITY = range(5)
+
+KERNEL_CLASSES = ("prepare", "probe", "spmm", "cgs_dot", "cgs_update", "reduce", "eig", "quad",
+                  "estimate", "batched")
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_u64 = ctypes.c_uint64
+_dbl = ctypes.c_double
+_int = ctypes.c_int
+
+
+class GraphInfo(ctypes.Structure):
+    _fields_ = [("n", _i64), ("nnz", _i64), ("trace_l", _dbl), ("max_degree", _dbl),
+                ("isolated", _i64), ("unit_weights", _i32), ("ntiles", _i32)]
+
+
+_SIGS = {
+    "slq_graph_create": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
+    "slq_graph_create_host": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
+    "slq_graph_info": (_int, [_vp, ctypes.POINTER(GraphInfo)]),
+    "slq_graph_destroy": (None, [_vp]),
+    "slq_graph_degrees": (_int, [_vp, _vp, _vp]),
+    "slq_operator_interval": (_int, [_vp, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
+    "slq_operator_apply": (_int, [_vp, _int, _vp, _vp, _i64, _i64, _vp]),
+    "slq_lanczos": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "slq_lanczos_start": (_int, [_vp, _int, _vp, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "slq_gauss_rules": (_int, [_vp, _vp, _vp, _i64, _int, _dbl, _dbl, _vp, _vp, _vp, _vp]),
+    "slq_quadrature": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _i64, _int, _vp, _vp]),
+    "slq_estimate": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp]),
+    "slq_probes": (_int, [_u64, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "slq_probe_state": (_int, [_u64, _u64, ctypes.POINTER(_u64)]),
+    "slq_lanczos_batched": (_int, [_vp, _vp, _i64, _int, _u64, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "slq_last_error": (ctypes.c_char_p, []),
+    "slq_launch_count": (_u64, []),
+    "slq_profile_begin": (None, []),
+    "slq_profile_end": (_int, [ctypes.POINTER(_dbl), ctypes.POINTER(_i64), _int]),
+    "slq_build_info": (ctypes.c_char_p, []),
+}
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library (no CUDA device needed: loading only resolves symbols)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise SlqLibraryError(
+            f"{path} is missing; build it with `python -m paper_2003_01282_b200.build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def check(rc: int, alpha=None, beta=None) -> None:
+    if rc == SLQ_OK:
+        return
+    msg = load().slq_last_error().decode(errors="replace")
+    if rc in (SLQ_ERR_VALUE, SLQ_ERR_NONFINITE):
+        raise ValueError(msg)
+    if rc == SLQ_ERR_EIGEN:
+        raise TridiagonalEigenError(msg, alpha=alpha, beta=beta)
+    if rc == SLQ_ERR_ALLOC:
+        raise MemoryError(msg)
+    raise SlqLibraryError(msg)
+
+
+def ptr(t) -> int | None:
+    """Device/host pointer of a torch tensor or numpy array (None for None)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise SlqLibraryError("no CUDA device visible: the SLQ engine runs only on the GPU (no CPU fallback)")
+    load()
+    return torch
+
+
+def launch_count() -> int:
+    return int(load().slq_launch_count())
+
+
+def profile_begin() -> None:
+    load().slq_profile_begin()
+
+
+def profile_end() -> dict:
+    n = len(KERNEL_CLASSES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    load().slq_profile_end(ms, cnt, n)
+    return {k: {"ms": float(ms[i]), "launches": int(cnt[i])} for i, k in enumerate(KERNEL_CLASSES)}

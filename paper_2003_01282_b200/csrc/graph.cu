@@ -1,0 +1,289 @@
+// Device graph preparation: the work of operators.py:52-62 (_adjacency, degrees) and the
+// per-operator set-up of make_operator (operators.py:65-102), done once per graph on the GPU:
+//   * int64 -> int32 column narrowing (+ range check),
+//   * unit-weight detection (weights dropped when all are 1.0: implicit CSR values),
+//   * degrees d = A.1 as sequential in-row sums (bit-identical to scipy csr_matvec),
+//   * dinv = 1/sqrt(d) with IEEE sqrt then divide (operators.py:85-86), 0 for isolated rows,
+//   * tr L = sum d, max degree and isolated count (deterministic fixed-order reductions),
+//   * the fixed SpMM row-tile partition (depends on the graph only, never on probe counts).
+#include <algorithm>
+#include <vector>
+
+#include "slq_common.cuh"
+
+namespace slq {
+
+constexpr int kMaxTiles = 148 * 16;   // SpMM tiles: <= 16 per SM
+constexpr int64_t kMinTileCost = 2048;
+constexpr int64_t kRowCost = 2;       // per-row overhead in nonzero-equivalents
+constexpr int64_t kMinStreamRows = 64;
+
+__global__ void narrow_cols_kernel(const int64_t* __restrict__ cols, int32_t* __restrict__ out,
+                                   int64_t nnz, int64_t n, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = cols[i];
+    if (c < 0 || c >= n) *bad = 1;
+    out[i] = static_cast<int32_t>(c);
+  }
+}
+
+__global__ void unit_weight_kernel(const double* __restrict__ w, int64_t nnz, int* __restrict__ nonunit) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (w[i] != 1.0) *nonunit = 1;
+}
+
+// One thread per row: sequential sum in stored order (scipy csr_matvec with x = ones).
+__global__ void degree_kernel(const int64_t* __restrict__ off, const double* __restrict__ w,
+                              int64_t n, double* __restrict__ deg, double* __restrict__ dinv) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = off[r], e = off[r + 1];
+    double s = 0.0;
+    if (w) {
+      for (int64_t k = b; k < e; ++k) s = __dadd_rn(s, __dmul_rn(w[k], 1.0));
+    } else {
+      s = static_cast<double>(e - b);   // exact: sum of ones, < 2^53
+    }
+    deg[r] = s;
+    dinv[r] = s > 0.0 ? __ddiv_rn(1.0, __dsqrt_rn(s)) : 0.0;
+  }
+}
+
+// Fixed-order block partials of (sum d, max d, #isolated); final pass in one block.
+constexpr int kScalBlock = 256;
+__global__ void degree_stats_kernel(const double* __restrict__ deg, int64_t n, int64_t per_block,
+                                    double* __restrict__ psum, double* __restrict__ pmax,
+                                    long long* __restrict__ piso) {
+  __shared__ double ss[kScalBlock], sm[kScalBlock];
+  __shared__ long long si[kScalBlock];
+  const int64_t b = blockIdx.x * per_block, e = min(n, b + per_block);
+  double s = 0.0, mx = 0.0;
+  long long iso = 0;
+  for (int64_t r = b + threadIdx.x; r < e; r += blockDim.x) {
+    const double d = deg[r];
+    s += d;
+    mx = fmax(mx, d);
+    iso += (d == 0.0);
+  }
+  ss[threadIdx.x] = s; sm[threadIdx.x] = mx; si[threadIdx.x] = iso;
+  __syncthreads();
+  for (int h = kScalBlock / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      ss[threadIdx.x] += ss[threadIdx.x + h];
+      sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + h]);
+      si[threadIdx.x] += si[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { psum[blockIdx.x] = ss[0]; pmax[blockIdx.x] = sm[0]; piso[blockIdx.x] = si[0]; }
+}
+
+__global__ void degree_stats_final(const double* psum, const double* pmax, const long long* piso,
+                                   int nb, double* out3) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0, mx = 0.0;
+    long long iso = 0;
+    for (int i = 0; i < nb; ++i) { s += psum[i]; mx = fmax(mx, pmax[i]); iso += piso[i]; }
+    out3[0] = s; out3[1] = mx; out3[2] = static_cast<double>(iso);
+  }
+}
+
+// tile_rows[t] = first row r with offsets[r] + kRowCost*r >= t*target (lower bound), t <= ntiles.
+__global__ void tile_kernel(const int64_t* __restrict__ off, int64_t n, int64_t target, int ntiles,
+                            int64_t* __restrict__ tile_rows) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > ntiles) return;
+  if (t == ntiles) { tile_rows[t] = n; return; }
+  const int64_t key = static_cast<int64_t>(t) * target;
+  int64_t lo = 0, hi = n;   // search in [0, n]
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] + kRowCost * mid >= key) hi = mid; else lo = mid + 1;
+  }
+  tile_rows[t] = lo;
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
+}
+
+static void* track(slq_graph* g, void* p) {
+  g->owned[g->n_owned++] = p;
+  return p;
+}
+
+static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols, const double* weights,
+                       cudaStream_t st) {
+  const int64_t n = g->n, nnz = g->nnz;
+  void* p = nullptr;
+  SLQ_CUDA(cudaMalloc(&p, sizeof(int64_t) * (n + 1)));
+  g->offsets = static_cast<int64_t*>(track(g, p));
+  SLQ_CUDA(cudaMemcpyAsync(const_cast<int64_t*>(g->offsets), offsets, sizeof(int64_t) * (n + 1),
+                           cudaMemcpyDefault, st));
+  SLQ_CUDA(cudaMalloc(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  g->cols = static_cast<int32_t*>(track(g, p));
+  SLQ_CUDA(cudaMalloc(&p, sizeof(double) * std::max<int64_t>(n, 1) * 2));
+  track(g, p);
+  g->degree = static_cast<double*>(p);
+  g->dinv = g->degree + std::max<int64_t>(n, 1);
+  int* flags = nullptr;   // [0] bad column, [1] non-unit weight
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), 2 * sizeof(int), st));
+  SLQ_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+
+  if (nnz > 0) {
+    {
+      LaunchScope ls(K_PREPARE, st);
+      narrow_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, const_cast<int32_t*>(g->cols), nnz, n, flags);
+    }
+    if (weights) {
+      LaunchScope ls(K_PREPARE, st);
+      unit_weight_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(weights, nnz, flags + 1);
+    }
+  }
+  int hflags[2] = {0, 0};
+  SLQ_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  SLQ_CUDA(cudaFreeAsync(flags, st));
+  if (hflags[0]) return fail(SLQ_ERR_VALUE, "column index out of range [0, n)");
+  g->unit_weights = hflags[1] ? 0 : 1;
+  if (!g->unit_weights) {
+    SLQ_CUDA(cudaMalloc(&p, sizeof(double) * nnz));
+    g->weights = static_cast<double*>(track(g, p));
+    SLQ_CUDA(cudaMemcpyAsync(const_cast<double*>(g->weights), weights, sizeof(double) * nnz,
+                             cudaMemcpyDefault, st));
+  }
+  if (n > 0) {
+    LaunchScope ls(K_PREPARE, st);
+    degree_kernel<<<grid_for(n, 256), 256, 0, st>>>(g->offsets, g->weights, n, g->degree, g->dinv);
+  }
+  // degree statistics
+  const int64_t per_block = std::max<int64_t>(4096, (n + 1023) / 1024);
+  const int nb = std::max(1, ceil_div(n, per_block));
+  double* scratch = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * (3 * nb + 3), st));
+  if (n > 0) {
+    {
+      LaunchScope ls(K_PREPARE, st);
+      degree_stats_kernel<<<nb, kScalBlock, 0, st>>>(g->degree, n, per_block, scratch, scratch + nb,
+                                                     reinterpret_cast<long long*>(scratch + 2 * nb));
+    }
+    LaunchScope ls(K_PREPARE, st);
+    degree_stats_final<<<1, 32, 0, st>>>(scratch, scratch + nb, reinterpret_cast<long long*>(scratch + 2 * nb),
+                                         nb, scratch + 3 * nb);
+  } else {
+    SLQ_CUDA(cudaMemsetAsync(scratch + 3 * nb, 0, 3 * sizeof(double), st));
+  }
+  double stats[3];
+  SLQ_CUDA(cudaMemcpyAsync(stats, scratch + 3 * nb, sizeof(stats), cudaMemcpyDeviceToHost, st));
+  // tiles
+  const int64_t total = nnz + kRowCost * n;
+  int64_t target = std::max<int64_t>(kMinTileCost, (total + kMaxTiles - 1) / kMaxTiles);
+  g->ntiles = std::max(1, ceil_div(total, target));
+  SLQ_CUDA(cudaMalloc(&p, sizeof(int64_t) * (g->ntiles + 1)));
+  g->tile_rows = static_cast<int64_t*>(track(g, p));
+  {
+    LaunchScope ls(K_PREPARE, st);
+    tile_kernel<<<ceil_div(g->ntiles + 1, 256), 256, 0, st>>>(g->offsets, n, target, g->ntiles, g->tile_rows);
+  }
+  g->rows_per_stream_tile = std::max<int64_t>(kMinStreamRows, (n + kMaxTiles - 1) / kMaxTiles);
+  g->ntiles_stream = std::max(1, ceil_div(n, g->rows_per_stream_tile));
+  SLQ_CUDA(cudaGetLastError());
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  SLQ_CUDA(cudaFreeAsync(scratch, st));
+  g->trace_l = stats[0];
+  g->max_degree = stats[1];
+  g->isolated = static_cast<int64_t>(stats[2]);
+  g->m = nnz / 2;
+  return SLQ_OK;
+}
+
+}  // namespace slq
+
+using namespace slq;
+
+extern "C" int slq_graph_create(int64_t n, int64_t nnz, const int64_t* offsets, const int64_t* cols,
+                                const double* weights, void* stream, slq_graph** out) {
+  if (!out) return fail(SLQ_ERR_VALUE, "out must not be NULL");
+  *out = nullptr;
+  if (n < 0 || nnz < 0) return fail(SLQ_ERR_VALUE, "negative n or nnz");
+  if (n >= (int64_t(1) << 31)) return fail(SLQ_ERR_VALUE, "n >= 2^31 is not supported (int32 columns)");
+  if (!offsets || (nnz > 0 && !cols)) return fail(SLQ_ERR_VALUE, "NULL CSR array");
+  slq_graph* g = new slq_graph();
+  g->n = n;
+  g->nnz = nnz;
+  cudaGetDevice(&g->device);
+  int rc = graph_build(g, offsets, cols, weights, static_cast<cudaStream_t>(stream));
+  if (rc != SLQ_OK) {
+    slq_graph_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return SLQ_OK;
+}
+
+extern "C" int slq_graph_create_host(int64_t n, int64_t nnz, const int64_t* offsets_host,
+                                     const int64_t* cols_host, const double* weights_host, void* stream,
+                                     slq_graph** out) {
+  // H2D staging of the canonical CSR, then the device build.
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t* d_off = nullptr;
+  int64_t* d_cols = nullptr;
+  double* d_w = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_off), sizeof(int64_t) * (n + 1), st));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_cols), sizeof(int64_t) * std::max<int64_t>(nnz, 1), st));
+  SLQ_CUDA(cudaMemcpyAsync(d_off, offsets_host, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+  if (nnz > 0) SLQ_CUDA(cudaMemcpyAsync(d_cols, cols_host, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+  if (weights_host && nnz > 0) {
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_w), sizeof(double) * nnz, st));
+    SLQ_CUDA(cudaMemcpyAsync(d_w, weights_host, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  }
+  int rc = slq_graph_create(n, nnz, d_off, d_cols, d_w, stream, out);
+  cudaFreeAsync(d_off, st);
+  cudaFreeAsync(d_cols, st);
+  if (d_w) cudaFreeAsync(d_w, st);
+  return rc;
+}
+
+extern "C" int slq_graph_info(const slq_graph* g, slq_graph_info_t* out) {
+  if (!g || !out) return fail(SLQ_ERR_VALUE, "NULL argument");
+  out->n = g->n;
+  out->nnz = g->nnz;
+  out->trace_l = g->trace_l;
+  out->max_degree = g->max_degree;
+  out->isolated = g->isolated;
+  out->unit_weights = g->unit_weights;
+  out->ntiles = g->ntiles;
+  return SLQ_OK;
+}
+
+extern "C" void slq_graph_destroy(slq_graph* g) {
+  if (!g) return;
+  for (int i = 0; i < g->n_owned; ++i) cudaFree(g->owned[i]);
+  delete g;
+}
+
+extern "C" int slq_operator_interval(const slq_graph* g, int kind, double* lo, double* hi) {
+  if (!g || !lo || !hi) return fail(SLQ_ERR_VALUE, "NULL argument");
+  *lo = 0.0;
+  switch (kind) {
+    case SLQ_LAPLACIAN: *hi = 2.0 * g->max_degree; return SLQ_OK;
+    case SLQ_NORMALIZED_LAPLACIAN: *hi = 2.0; return SLQ_OK;
+    case SLQ_DENSITY:
+      if (g->nnz == 0 || g->trace_l <= 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
+      *hi = 1.0;
+      return SLQ_OK;
+  }
+  return fail(SLQ_ERR_VALUE, "unknown operator kind");
+}
+
+extern "C" int slq_graph_degrees(const slq_graph* g, double* degree, double* dinv, void* stream) {
+  if (!g) return fail(SLQ_ERR_VALUE, "NULL graph");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (g->n == 0) return SLQ_OK;
+  if (degree) SLQ_CUDA(cudaMemcpyAsync(degree, g->degree, sizeof(double) * g->n, cudaMemcpyDeviceToDevice, st));
+  if (dinv) SLQ_CUDA(cudaMemcpyAsync(dinv, g->dinv, sizeof(double) * g->n, cudaMemcpyDeviceToDevice, st));
+  return SLQ_OK;
+}

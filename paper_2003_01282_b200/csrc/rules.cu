@@ -1,0 +1,228 @@
+// Gauss quadrature rules, grid quadrature and the probe aggregate.
+//   slq_gauss_rules  <- quadrature_rule (lanczos.py:148-163) + np.clip (slq.py:76-77)
+//                      batched symmetric tridiagonal implicit QL (Wilkinson shift), one thread per
+//                      probe, accumulating only the FIRST ROW of the eigenvector matrix
+//                      (weights = Z[0,:]^2), ascending nodes.
+//   slq_quadrature   <- _apply_rule over the whole t grid (slq.py:89-95, 153-168)
+//   slq_estimate     <- _estimate_from (slq.py:98-105)
+#include <cfloat>
+#include <cmath>
+
+#include "slq_common.cuh"
+
+namespace slq {
+
+// Implicit QL on (d, e) of order m; z holds the first row of the accumulated rotations.
+// Returns 0 on convergence, 1 if an eigenvalue needed more than 60 sweeps.
+__device__ int tridiag_ql_first_row(double* d, double* e, double* z, int m) {
+  for (int l = 0; l < m; ++l) {
+    int sweeps = 0;
+    for (;;) {
+      int mm = l;
+      for (; mm < m - 1; ++mm) {
+        const double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+        if (fabs(e[mm]) <= DBL_EPSILON * dd || fabs(e[mm]) < DBL_MIN) break;
+      }
+      if (mm == l) break;
+      if (++sweeps > 60) return 1;
+      // Wilkinson-type shift from the leading 2x2 block
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0;
+      bool deflated = false;
+      for (int i = mm - 1; i >= l; --i) {
+        double f = s * e[i];
+        const double b = c * e[i];
+        r = hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {          // underflow: split the matrix here and restart
+          d[i + 1] -= p;
+          e[mm] = 0.0;
+          deflated = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0 * c * b;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - b;
+        f = z[i + 1];
+        z[i + 1] = s * z[i] + c * f;
+        z[i] = c * z[i] - s * f;
+      }
+      if (deflated) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+  return 0;
+}
+
+__global__ void gauss_rules_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                                   const int32_t* __restrict__ steps, int64_t count, int ld, double lo,
+                                   double hi, double* __restrict__ nodes, double* __restrict__ weights,
+                                   int32_t* __restrict__ info, int* __restrict__ status) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= count) return;
+  double d[kMaxSteps], e[kMaxSteps], z[kMaxSteps];
+  const int m = steps[p];
+  const double* a = alpha + p * ld;
+  const double* b = beta + p * ld;
+  bool finite = true;
+  for (int k = 0; k < m; ++k) {
+    d[k] = a[k];
+    e[k] = k + 1 < m ? b[k] : 0.0;
+    z[k] = k == 0 ? 1.0 : 0.0;
+    finite = finite && isfinite(d[k]) && isfinite(e[k]);
+  }
+  int rc = 0;
+  if (!finite) rc = -1;                       // scipy check_finite -> ValueError
+  else rc = tridiag_ql_first_row(d, e, z, m);
+  info[p] = rc;
+  if (rc) {
+    atomicMax(status, rc < 0 ? 2 : 1);
+    for (int k = 0; k < ld; ++k) { nodes[p * ld + k] = 0.0; weights[p * ld + k] = 0.0; }
+    return;
+  }
+  // ascending sort of (node, weight) pairs
+  for (int k = 0; k < m; ++k) z[k] = z[k] * z[k];
+  for (int i = 1; i < m; ++i) {
+    const double dv = d[i], zv = z[i];
+    int j = i - 1;
+    while (j >= 0 && d[j] > dv) { d[j + 1] = d[j]; z[j + 1] = z[j]; --j; }
+    d[j + 1] = dv;
+    z[j + 1] = zv;
+  }
+  for (int k = 0; k < ld; ++k) {
+    nodes[p * ld + k] = k < m ? fmin(fmax(d[k], lo), hi) : 0.0;
+    weights[p * ld + k] = k < m ? z[k] : 0.0;
+  }
+}
+
+template <int FN>
+__device__ __forceinline__ double integrand(double t, double x) {
+  if (FN == SLQ_FN_HEAT) return exp(-t * x);
+  if (FN == SLQ_FN_WAVE_RE) return cos(t * x);
+  if (FN == SLQ_FN_WAVE_IM) return -sin(t * x);
+  if (FN == SLQ_FN_XLOGX) return x > 0.0 ? x * log(x) : 0.0;
+  return x;
+}
+
+template <int FN>
+__global__ void quadrature_kernel(const double* __restrict__ nodes, const double* __restrict__ weights,
+                                  const int32_t* __restrict__ steps, int64_t count, int ld,
+                                  const double* __restrict__ tgrid, int64_t T, double* __restrict__ pv,
+                                  int* __restrict__ nonfinite) {
+  const int64_t total = T * count;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ti = idx / count, p = idx - ti * count;
+    const double t = tgrid ? tgrid[ti] : 0.0;
+    const int m = steps[p];
+    double acc = 0.0;
+    bool ok = true;
+    for (int k = 0; k < m; ++k) {
+      const double f = integrand<FN>(t, nodes[p * ld + k]);
+      ok = ok && isfinite(f);
+      acc = fma(weights[p * ld + k], f, acc);
+    }
+    if (!ok) *nonfinite = 1;
+    pv[ti * count + p] = acc;
+  }
+}
+
+__global__ void estimate_kernel(const double* __restrict__ pv, int64_t T, int64_t count, double n,
+                                double* __restrict__ value, double* __restrict__ std_error) {
+  const int64_t ti = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (ti >= T) return;
+  const double* row = pv + ti * count;
+  double s = 0.0, sx = 0.0;
+  for (int64_t p = 0; p < count; ++p) { s += row[p]; sx += n * row[p]; }
+  value[ti] = n * (s / static_cast<double>(count));
+  if (count > 1) {
+    const double mean = sx / static_cast<double>(count);
+    double ss = 0.0;
+    for (int64_t p = 0; p < count; ++p) {
+      const double dlt = n * row[p] - mean;
+      ss += dlt * dlt;
+    }
+    std_error[ti] = sqrt(ss / static_cast<double>(count - 1)) / sqrt(static_cast<double>(count));
+  } else {
+    std_error[ti] = 0.0;
+  }
+}
+
+}  // namespace slq
+
+using namespace slq;
+
+extern "C" int slq_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count,
+                               int ld, double lo, double hi, double* nodes, double* weights, int32_t* info,
+                               void* stream) {
+  if (count < 0 || ld < 1 || ld > kMaxSteps) return fail(SLQ_ERR_VALUE, "bad rule shape (ld must be in [1,128])");
+  if (count == 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* status = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(int), st));
+  SLQ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+  {
+    LaunchScope ls(K_EIG, st);
+    gauss_rules_kernel<<<ceil_div(count, 64), 64, 0, st>>>(alpha, beta, steps, count, ld, lo, hi, nodes, weights,
+                                                             info, status);
+  }
+  int h = 0;
+  SLQ_CUDA(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(status, st);
+  SLQ_CUDA(cudaGetLastError());
+  if (h == 2) return fail(SLQ_ERR_VALUE, "array must not contain infs or NaNs");
+  if (h == 1) return fail(SLQ_ERR_EIGEN, "tridiagonal eigensolver failed: no convergence");
+  return SLQ_OK;
+}
+
+extern "C" int slq_quadrature(const double* nodes, const double* weights, const int32_t* steps, int64_t count,
+                              int ld, const double* t, int64_t T, int fn, double* per_vector, void* stream) {
+  if (count < 0 || T < 0) return fail(SLQ_ERR_VALUE, "negative size");
+  if (count == 0 || T == 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* flag = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), st));
+  SLQ_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  const int64_t total = T * count;
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  {
+    LaunchScope ls(K_QUAD, st);
+    switch (fn) {
+      case SLQ_FN_HEAT: quadrature_kernel<SLQ_FN_HEAT><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, per_vector, flag); break;
+      case SLQ_FN_WAVE_RE: quadrature_kernel<SLQ_FN_WAVE_RE><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, per_vector, flag); break;
+      case SLQ_FN_WAVE_IM: quadrature_kernel<SLQ_FN_WAVE_IM><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, per_vector, flag); break;
+      case SLQ_FN_XLOGX: quadrature_kernel<SLQ_FN_XLOGX><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, per_vector, flag); break;
+      case SLQ_FN_IDENTITY: quadrature_kernel<SLQ_FN_IDENTITY><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, per_vector, flag); break;
+      default: cudaFreeAsync(flag, st); return fail(SLQ_ERR_VALUE, "unknown integrand");
+    }
+  }
+  int h = 0;
+  SLQ_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(flag, st);
+  SLQ_CUDA(cudaGetLastError());
+  if (h) return fail(SLQ_ERR_NONFINITE, "f returned a non-finite value at quadrature nodes");
+  return SLQ_OK;
+}
+
+extern "C" int slq_estimate(const double* per_vector, int64_t T, int64_t count, double n, double* value,
+                            double* std_error, void* stream) {
+  if (count < 1 || T < 0) return fail(SLQ_ERR_VALUE, "need at least one probe");
+  if (T == 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  {
+    LaunchScope ls(K_ESTIMATE, st);
+    estimate_kernel<<<ceil_div(T, 128), 128, 0, st>>>(per_vector, T, count, n, value, std_error);
+  }
+  SLQ_CUDA(cudaGetLastError());
+  return SLQ_OK;
+}

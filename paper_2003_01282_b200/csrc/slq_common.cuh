@@ -1,0 +1,92 @@
+// Shared definitions for the sm_100a SLQ engine (libslq_b200.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/slq_b200.h"
+
+namespace slq {
+
+constexpr int kWarp = 32;
+constexpr int kMaxSteps = 128;     // largest Lanczos step count a rule can carry
+constexpr int kCgsBlock = 16;      // basis vectors handled per CGS sweep (register accumulators)
+
+// --- error state (thread local, see slq_last_error) -------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define SLQ_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::slq::cuda_fail(_e, #call); \
+  } while (0)
+
+// --- launch accounting + optional per-class CUDA-event timing ----------------
+enum KernelClass {
+  K_PREPARE = 0,
+  K_PROBE,
+  K_SPMM,
+  K_CGS_DOT,
+  K_CGS_UPDATE,
+  K_REDUCE,
+  K_EIG,
+  K_QUAD,
+  K_ESTIMATE,
+  K_BATCHED,
+  K_NUM_CLASSES
+};
+
+void launch_begin(KernelClass k, cudaStream_t s);
+void launch_end(KernelClass k, cudaStream_t s);
+
+struct LaunchScope {
+  KernelClass k;
+  cudaStream_t s;
+  LaunchScope(KernelClass k_, cudaStream_t s_) : k(k_), s(s_) { launch_begin(k, s); }
+  ~LaunchScope() { launch_end(k, s); }
+};
+
+// --- device helpers ----------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ double to_f64(T x) { return static_cast<double>(x); }
+
+template <typename T>
+__device__ __forceinline__ T from_f64(double x) { return static_cast<T>(x); }
+
+__device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
+__device__ __forceinline__ double ldg_f64(const float* p) { return static_cast<double>(__ldg(p)); }
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace slq
+
+// Opaque graph handle (definition shared by the .cu files).
+struct slq_graph {
+  int64_t n = 0;
+  int64_t nnz = 0;
+  int64_t m = 0;                 // undirected edges = nnz / 2 for simple graphs
+  int device = 0;
+  const int64_t* offsets = nullptr;  // [n+1] device (owned copy)
+  const int32_t* cols = nullptr;     // [nnz] device, narrowed to int32
+  const double* weights = nullptr;   // [nnz] device, nullptr when every weight is 1.0
+  double* degree = nullptr;          // [n]
+  double* dinv = nullptr;            // [n]  1/sqrt(d) (0 for isolated)
+  // SpMM tiles: contiguous row ranges with bounded (nnz + row) cost, fixed per graph
+  int ntiles = 0;
+  int64_t* tile_rows = nullptr;      // [ntiles+1] device
+  // streaming tiles (pass B): contiguous equal row ranges
+  int ntiles_stream = 0;
+  int64_t rows_per_stream_tile = 0;
+  // host copies of the scalars
+  double trace_l = 0.0;     // sum of degrees (tr L)
+  double max_degree = 0.0;
+  int64_t isolated = 0;
+  int unit_weights = 1;
+  // owned device allocations
+  void* owned[8] = {nullptr};
+  int n_owned = 0;
+};

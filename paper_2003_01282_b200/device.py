@@ -1,0 +1,196 @@
+"""Device-resident graphs and per-probe rules (thin wrappers over the C ABI).
+
+PyTorch is only the container for device buffers and the stream handle; all
+arithmetic happens in libslq_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .graphs import Graph
+
+KIND_CODES = {"laplacian": _lib.LAPLACIAN, "normalized_laplacian": _lib.NORMALIZED_LAPLACIAN,
+              "density": _lib.DENSITY}
+
+
+class DeviceGraph:
+    """Prepared CSR on one GPU: int32 columns, implicit unit weights, degrees, dinv, tiles."""
+
+    def __init__(self, g: Graph, device=None, *, from_device: bool = False):
+        torch = _lib.require_cuda()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.graph = g
+        self.n = int(g.n)
+        self.handle = ctypes.c_void_p()
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            stream = _lib.stream_handle(self.device)
+            w = None if g.is_unweighted() else np.ascontiguousarray(g.weights, dtype=np.float64)
+            if from_device:
+                off = torch.as_tensor(np.asarray(g.row_offsets, dtype=np.int64), device=self.device)
+                cols = torch.as_tensor(np.asarray(g.col_indices, dtype=np.int64), device=self.device)
+                wt = None if w is None else torch.as_tensor(w, device=self.device)
+                rc = lib.slq_graph_create(self.n, g.nnz, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(wt), stream,
+                                          ctypes.byref(self.handle))
+            else:
+                off = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
+                cols = np.ascontiguousarray(g.col_indices, dtype=np.int64)
+                rc = lib.slq_graph_create_host(self.n, g.nnz, off.ctypes.data, cols.ctypes.data,
+                                               None if w is None else w.ctypes.data, stream,
+                                               ctypes.byref(self.handle))
+        _lib.check(rc)
+        info = _lib.GraphInfo()
+        _lib.check(lib.slq_graph_info(self.handle, ctypes.byref(info)))
+        self.info = info
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().slq_graph_destroy(h)
+            except Exception:
+                pass
+            self.handle = ctypes.c_void_p()
+
+    # -- operator set-up -----------------------------------------------------------
+    def interval(self, kind: str) -> tuple[float, float]:
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        _lib.check(_lib.load().slq_operator_interval(self.handle, KIND_CODES[kind], ctypes.byref(lo), ctypes.byref(hi)))
+        return float(lo.value), float(hi.value)
+
+    def degrees(self):
+        import torch
+
+        d = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        dinv = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_degrees(self.handle, _lib.ptr(d), _lib.ptr(dinv),
+                                                      _lib.stream_handle(self.device)))
+        return d, dinv
+
+    def apply(self, kind: str, x):
+        """Y = Op(X) for a [n] or [n, k] float64 block (torch CUDA tensor or numpy array)."""
+        import torch
+
+        host = isinstance(x, np.ndarray)
+        xt = torch.as_tensor(np.asarray(x, dtype=np.float64), device=self.device) if host else x
+        if xt.dtype != torch.float64:
+            raise TypeError("operator apply takes float64 vectors")
+        one = xt.dim() == 1
+        xt = xt.reshape(self.n, -1).contiguous()
+        y = torch.empty_like(xt)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_operator_apply(self.handle, KIND_CODES[kind], _lib.ptr(xt), _lib.ptr(y),
+                                                       xt.shape[1], xt.shape[1], _lib.stream_handle(self.device)))
+        if one:
+            y = y.reshape(-1)
+        return y.cpu().numpy() if host else y
+
+    # -- Lanczos + rules -----------------------------------------------------------
+    def tridiagonals(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *,
+                     reorth: int = -1, dtype: str = "f64", start=None):
+        """alpha/beta [count, s'] and steps [count] on the device."""
+        import torch
+
+        s = min(int(steps), self.n)
+        alpha = torch.zeros((count, s), dtype=torch.float64, device=self.device)
+        beta = torch.zeros((count, s), dtype=torch.float64, device=self.device)
+        st = torch.zeros(count, dtype=torch.int32, device=self.device)
+        code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            stream = _lib.stream_handle(self.device)
+            if start is None:
+                rc = lib.slq_lanczos(self.handle, KIND_CODES[kind], int(seed), int(probe_begin), int(count), int(steps),
+                                     int(reorth), code, _lib.ptr(alpha), _lib.ptr(beta), _lib.ptr(st), stream)
+            else:
+                q0 = start.contiguous()
+                rc = lib.slq_lanczos_start(self.handle, KIND_CODES[kind], _lib.ptr(q0), q0.shape[1], int(count),
+                                           int(steps), int(reorth), code, _lib.ptr(alpha), _lib.ptr(beta),
+                                           _lib.ptr(st), stream)
+        _lib.check(rc)
+        return alpha, beta, st
+
+    def rules(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1,
+              dtype: str = "f64") -> "DeviceRules":
+        alpha, beta, st = self.tridiagonals(kind, seed, probe_begin, count, steps, reorth=reorth, dtype=dtype)
+        return gauss_rules(alpha, beta, st, self.interval(kind), n=self.n)
+
+
+@dataclass
+class DeviceRules:
+    nodes: object      # torch [count, s] float64 (clamped, ascending, zero padded)
+    weights: object    # torch [count, s]
+    steps: object      # torch [count] int32
+    n: int
+    alpha: object = None
+    beta: object = None
+
+    @property
+    def count(self) -> int:
+        return int(self.nodes.shape[0])
+
+    def quadrature(self, t, fn: int):
+        """per_vector [T, count] on the device."""
+        import torch
+
+        dev = self.nodes.device
+        tt = torch.as_tensor(np.asarray(t, dtype=np.float64), device=dev) if t is not None else None
+        T = 1 if tt is None else int(tt.numel())
+        pv = torch.empty((T, self.count), dtype=torch.float64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().slq_quadrature(_lib.ptr(self.nodes), _lib.ptr(self.weights), _lib.ptr(self.steps),
+                                                   self.count, int(self.nodes.shape[1]), _lib.ptr(tt), T, fn,
+                                                   _lib.ptr(pv), _lib.stream_handle(dev)))
+        return pv
+
+    def estimate(self, pv):
+        """(value [T], std_error [T]) on the device."""
+        import torch
+
+        dev = pv.device
+        T = int(pv.shape[0])
+        val = torch.empty(T, dtype=torch.float64, device=dev)
+        std = torch.empty(T, dtype=torch.float64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().slq_estimate(_lib.ptr(pv), T, int(pv.shape[1]), float(self.n), _lib.ptr(val),
+                                                 _lib.ptr(std), _lib.stream_handle(dev)))
+        return val, std
+
+
+def gauss_rules(alpha, beta, steps, interval, n: int) -> DeviceRules:
+    import torch
+
+    count, width = alpha.shape
+    nodes = torch.zeros_like(alpha)
+    weights = torch.zeros_like(alpha)
+    info = torch.zeros(count, dtype=torch.int32, device=alpha.device)
+    if count:
+        with torch.cuda.device(alpha.device):
+            rc = _lib.load().slq_gauss_rules(_lib.ptr(alpha), _lib.ptr(beta), _lib.ptr(steps), count, width,
+                                             float(interval[0]), float(interval[1]), _lib.ptr(nodes),
+                                             _lib.ptr(weights), _lib.ptr(info), _lib.stream_handle(alpha.device))
+        if rc == _lib.SLQ_ERR_EIGEN:
+            bad = int(torch.nonzero(info).flatten()[0])
+            k = int(steps[bad])
+            _lib.check(rc, alpha=alpha[bad, :k].cpu().numpy(), beta=beta[bad, :k - 1].cpu().numpy())
+        _lib.check(rc)
+    return DeviceRules(nodes, weights, steps, n, alpha, beta)
+
+
+def device_graph(g: Graph, device=None) -> DeviceGraph:
+    """Cached DeviceGraph for a Graph (Graph arrays are read-only, so the cache stays valid)."""
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = str(dev)
+    cache = g._device_cache
+    dg = cache.get(key)
+    if dg is None:
+        dg = DeviceGraph(g, dev)
+        cache[key] = dg
+    return dg

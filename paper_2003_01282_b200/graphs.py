@@ -30,6 +30,7 @@ class Graph:
     weights: np.ndarray
     m: int
     _hash: list = field(default_factory=list, init=False, repr=False, compare=False)
+    _device_cache: dict = field(default_factory=dict, init=False, repr=False, compare=False)
 
     def __post_init__(self):
         for arr in (self.row_offsets, self.col_indices, self.weights):

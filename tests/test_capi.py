@@ -1,0 +1,48 @@
+"""The C-ABI library loads and exports every symbol include/slq_b200.h declares (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from oracle import pcg64
+from paper_2003_01282_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "slq_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(slq_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = declared_symbols()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_lib.exported_symbols())
+
+
+def test_build_info_names_sm100a():
+    assert b"sm_100a" in _lib.load().slq_build_info()
+
+
+@pytest.mark.parametrize("seed,index", [(0, 0), (0, 1), (7, 5), (123, 99), (2**40 + 3, 17), (5, 2**33 + 1)])
+def test_host_probe_state_matches_seedsequence(seed, index):
+    out = (ctypes.c_uint64 * 4)()
+    assert _lib.load().slq_probe_state(seed, index, out) == 0
+    state, inc = pcg64.pcg64_initial_state(seed, index)
+    assert (out[0] << 64) | out[1] == state
+    assert (out[2] << 64) | out[3] == inc
+
+
+def test_sm100a_cubin_embedded():
+    import subprocess
+
+    r = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in r.stdout

@@ -1,0 +1,300 @@
+"""GPU parity ladder: the CUDA path through the C ABI vs the golden
+fixtures made by the real reference and vs the oracle.
+
+Tolerances (north star): fp64 descriptors within 1e-9 relative (rel-l2, the
+reference's relative_error); fp32 vector storage within 1e-4.  Integer/bit work
+(probes, degrees, the operator apply) is bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import golden
+from oracle import pcg64, slq_oracle as O
+from paper_2003_01282_b200 import _lib
+from paper_2003_01282_b200.descriptors import (TimeGrid, netlsd_heat_wave_slq, netlsd_slq, vnge_slq)
+from paper_2003_01282_b200.device import DeviceGraph
+from paper_2003_01282_b200.graphs import csr_from_edges
+from paper_2003_01282_b200.slq import SlqConfig
+
+pytestmark = pytest.mark.gpu
+
+KIND = {"L": "laplacian", "NL": "normalized_laplacian", "P": "density"}
+FP64_TOL = 1e-9
+FP32_TOL = 1e-4
+GRID = TimeGrid(1e-2, 1e2, 250)
+
+
+@pytest.fixture(scope="module")
+def small():
+    return golden.load("small.npz")
+
+
+def names(z):
+    return [str(x) for x in z["names"]]
+
+
+def test_library_runs_on_device(cuda_device):
+    before = _lib.launch_count()
+    g = csr_from_edges(3, [0, 1], [1, 2])
+    DeviceGraph(g, cuda_device).apply("normalized_laplacian", np.eye(3))
+    assert _lib.launch_count() > before
+
+
+# 1. probes: device bits == reference stream (slq.py:63-72)
+@pytest.mark.parametrize("seed,begin,count,n", [(0, 0, 5, 1), (0, 0, 33, 2), (3, 7, 40, 129), (123, 90, 10, 1001),
+                                                (2**40 + 3, 17, 3, 4097)])
+def test_probes_bit_exact(cuda_device, seed, begin, count, n):
+    out = torch.zeros((n, count), dtype=torch.float64, device=cuda_device)
+    _lib.check(_lib.load().slq_probes(seed, begin, count, n, out.data_ptr(), count, _lib.stream_handle()))
+    got = out.cpu().numpy()
+    for j in range(count):
+        i = begin + j
+        if n <= 300:
+            ref = np.array(pcg64.rademacher(seed, i, n))
+        else:
+            rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(i,)))
+            ref = rng.integers(0, 2, size=n).astype(np.float64) * 2.0 - 1.0
+        assert np.array_equal(got[:, j], ref), (seed, i, n)
+
+
+def test_probes_golden(cuda_device):
+    z = golden.load("probes.npz")
+    k = 0
+    while f"probe{k}_case" in z:
+        seed, i, n = (int(x) for x in z[f"probe{k}_case"])
+        out = torch.zeros((n, 1), dtype=torch.float64, device=cuda_device)
+        _lib.check(_lib.load().slq_probes(seed, i, 1, n, out.data_ptr(), 1, _lib.stream_handle()))
+        assert np.array_equal(out[:, 0].cpu().numpy(), z[f"probe{k}_v"].astype(np.float64))
+        k += 1
+
+
+# 2. degrees / dinv / trL exact (operators.py:58-62, 84-86, 93)
+def test_degrees_exact(cuda_device, small):
+    for name in names(small):
+        g = golden.graph(small, f"{name}/")
+        if g.n == 0:
+            continue
+        dg = DeviceGraph(g, cuda_device)
+        d, dinv = dg.degrees()
+        ref_d = O.degrees(g)
+        assert np.array_equal(d.cpu().numpy(), ref_d), name
+        pos = ref_d > 0
+        ref_dinv = np.zeros(g.n)
+        ref_dinv[pos] = 1.0 / np.sqrt(ref_d[pos])
+        assert np.array_equal(dinv.cpu().numpy(), ref_dinv), name
+        assert dg.info.trace_l == float(ref_d.sum())
+        assert dg.info.isolated == int((ref_d == 0).sum())
+
+
+# 3. operator apply: bit-identical to the reference closure (golden apply_* arrays)
+def test_operator_apply_bit_exact(cuda_device, small):
+    for name in names(small):
+        g = golden.graph(small, f"{name}/")
+        dg = DeviceGraph(g, cuda_device)
+        x = small[f"{name}/x"]
+        for kname, kind in KIND.items():
+            key = f"{name}/apply_{kname}"
+            if key not in small:
+                with pytest.raises(ValueError, match="without edges"):
+                    dg.apply(kind, x)
+                continue
+            got = dg.apply(kind, x)
+            assert np.array_equal(got, small[key]), (name, kname, np.max(np.abs(got - small[key])))
+
+
+def test_operator_apply_many_columns_bit_exact(cuda_device):
+    z = golden.load("rmat12.npz")
+    g = golden.graph(z)
+    x = np.random.default_rng(0).standard_normal((g.n, 70))
+    for kind, okind in (("normalized_laplacian", O.NORMALIZED_LAPLACIAN), ("density", O.DENSITY),
+                        ("laplacian", O.LAPLACIAN)):
+        got = DeviceGraph(g, cuda_device).apply(kind, x)
+        assert np.array_equal(got, O.make_block_operator(g, okind).apply(x)), kind
+
+
+# 4./5. per-probe tridiagonals and rules vs the reference
+def check_rules(dg, kind, z, prefix, n_v, s, seed, hi):
+    alpha, beta, st = dg.tridiagonals(kind, seed, 0, n_v, s)
+    rules = dg.rules(kind, seed, 0, n_v, s)
+    steps = z[f"{prefix}/steps"]
+    assert np.array_equal(st.cpu().numpy(), steps), prefix
+    a, b = alpha.cpu().numpy(), beta.cpu().numpy()
+    nodes, weights = rules.nodes.cpu().numpy(), rules.weights.cpu().numpy()
+    for p in range(n_v):
+        k = int(steps[p])
+        assert np.allclose(a[p, :k], z[f"{prefix}/alpha"][p, :k], rtol=1e-11, atol=1e-13 * hi), (prefix, p)
+        assert np.allclose(b[p, :k - 1], z[f"{prefix}/beta"][p, :k - 1], rtol=1e-11, atol=1e-13 * hi), (prefix, p)
+        assert np.max(np.abs(nodes[p, :k] - z[f"{prefix}/nodes"][p, :k]), initial=0) <= 1e-11 * hi, (prefix, p)
+        assert np.allclose(weights[p, :k], z[f"{prefix}/weights"][p, :k], rtol=1e-8, atol=1e-12), (prefix, p)
+
+
+def test_small_graph_rules_match_reference(cuda_device, small):
+    for name in names(small):
+        g = golden.graph(small, f"{name}/")
+        dg = DeviceGraph(g, cuda_device)
+        for kname, kind in KIND.items():
+            for s in (4, 10):
+                prefix = f"{name}/{kname}_s{s}"
+                if f"{prefix}/steps" not in small:
+                    continue
+                hi = float(small[f"{prefix}/interval"][1])
+                check_rules(dg, kind, small, prefix, 8, s, 3, hi)
+
+
+@pytest.mark.parametrize("fname", ["c1_ba1000.npz", "sbm5k.npz", "rmat12.npz"])
+def test_medium_graph_rules_match_reference(cuda_device, fname):
+    z = golden.load(fname)
+    g = golden.graph(z)
+    dg = DeviceGraph(g, cuda_device)
+    n_v, s = z["NL/alpha"].shape
+    check_rules(dg, "normalized_laplacian", z, "NL", n_v, s, 0, 2.0)
+    check_rules(dg, "density", z, "P", n_v, s, 0, 1.0)
+
+
+# 6. descriptors vs the reference (rel-l2, the reference's relative_error)
+def test_small_graph_descriptors(cuda_device, small):
+    for name in names(small):
+        g = golden.graph(small, f"{name}/")
+        cfg = SlqConfig(n_v=8, s=10, seed=3)
+        heat, wave = netlsd_heat_wave_slq(g, GRID, cfg)
+        assert golden.rel_l2(heat.values, small[f"{name}/desc/heat"]) <= FP64_TOL, name
+        assert np.allclose(heat.std_errors, small[f"{name}/desc/heat_std"], rtol=1e-7, atol=1e-10), name
+        ref_w = small[f"{name}/desc/wave_re"] + 1j * small[f"{name}/desc/wave_im"]
+        assert golden.rel_l2(wave.values, ref_w) <= FP64_TOL, name
+        assert heat.graph_hash == str(small[f"{name}/desc/graph_hash"])
+        if f"{name}/desc/vnge" in small:
+            v = vnge_slq(g, cfg)
+            ref = float(small[f"{name}/desc/vnge"])
+            assert abs(v.value - ref) <= FP64_TOL * max(abs(ref), 1e-300) or abs(v.value - ref) <= 1e-13, name
+        else:
+            with pytest.raises(ValueError, match="without edges"):
+                vnge_slq(g, cfg)
+
+
+@pytest.mark.parametrize("fname", ["c1_ba1000.npz", "sbm5k.npz", "rmat12.npz"])
+def test_medium_graph_descriptors(cuda_device, fname):
+    z = golden.load(fname)
+    g = golden.graph(z)
+    n_v, s = z["NL/alpha"].shape
+    cfg = SlqConfig(n_v=n_v, s=s, seed=0)
+    heat, wave = netlsd_heat_wave_slq(g, GRID, cfg)
+    assert golden.rel_l2(heat.values, z["heat"]) <= FP64_TOL
+    assert golden.max_rel(heat.values, z["heat"]) <= FP64_TOL
+    assert golden.rel_l2(wave.values, z["wave_re"] + 1j * z["wave_im"]) <= FP64_TOL
+    v = vnge_slq(g, cfg)
+    assert abs(v.value - float(z["vnge"])) <= FP64_TOL * abs(float(z["vnge"]))
+    # fp32 vector storage (fp64 reductions): 1e-4
+    h32, w32 = netlsd_heat_wave_slq(g, GRID, cfg, dtype="f32")
+    assert golden.rel_l2(h32.values, z["heat"]) <= FP32_TOL
+    assert golden.rel_l2(w32.values, z["wave_re"] + 1j * z["wave_im"]) <= FP32_TOL
+    v32 = vnge_slq(g, cfg, dtype="f32")
+    assert abs(v32.value - float(z["vnge"])) <= FP32_TOL * abs(float(z["vnge"]))
+
+
+def test_er_batch_sample_descriptors(cuda_device):
+    z = golden.load("erbatch40.npz")
+    cfg = SlqConfig(n_v=20, s=10, seed=0)
+    for k in range(int(z["count"])):
+        g = golden.graph(z, f"{k}/")
+        h = netlsd_slq(g, GRID, cfg)
+        assert golden.rel_l2(h.values, z[f"{k}/heat"]) <= FP64_TOL, k
+
+
+# determinism: per-probe rules independent of chunk width / probe range (reference prefix property)
+def test_rules_independent_of_chunking(cuda_device):
+    z = golden.load("sbm5k.npz")
+    dg = DeviceGraph(golden.graph(z), cuda_device)
+    a_full, b_full, s_full = dg.tridiagonals("normalized_laplacian", 0, 0, 70, 15)
+    a1, b1, s1 = dg.tridiagonals("normalized_laplacian", 0, 0, 33, 15)
+    a2, b2, s2 = dg.tridiagonals("normalized_laplacian", 0, 33, 37, 15)
+    assert torch.equal(a_full, torch.cat([a1, a2]))
+    assert torch.equal(b_full, torch.cat([b1, b2]))
+    assert torch.equal(s_full, torch.cat([s1, s2]))
+    a3, _, _ = dg.tridiagonals("normalized_laplacian", 0, 0, 70, 15)
+    assert torch.equal(a_full, a3)
+
+
+# edge cases the reference tests
+def test_empty_graph_heat_is_exactly_n(cuda_device):
+    g = csr_from_edges(7, [], [])
+    h = netlsd_slq(g, TimeGrid(1e-2, 1e2, 16), SlqConfig(n_v=12, s=4, seed=1))
+    assert np.all(h.values == 7.0)
+
+
+def test_single_vertex_and_steps_beyond_n(cuda_device):
+    g = csr_from_edges(1, [], [])
+    h = netlsd_slq(g, TimeGrid(1e-2, 1e2, 8), SlqConfig(n_v=3, s=10, seed=0))
+    assert np.all(h.values == 1.0)
+    g2 = csr_from_edges(3, [0, 1], [1, 2])
+    h2 = netlsd_slq(g2, GRID, SlqConfig(n_v=5, s=10, seed=0))
+    ref, _ = O.heat_trace(g2, GRID.values, 5, 10, 0)
+    assert golden.rel_l2(h2.values, ref) <= FP64_TOL
+
+
+def test_k2_vnge_is_zero(cuda_device):
+    v = vnge_slq(csr_from_edges(2, [0], [1]), SlqConfig(n_v=8, s=5, seed=2))
+    assert abs(v.value) <= 1e-10
+
+
+def test_nonfinite_f_raises(cuda_device):
+    from paper_2003_01282_b200.operators import OperatorKind, make_operator
+    from paper_2003_01282_b200.slq import slq_trace
+
+    op = make_operator(csr_from_edges(3, [0, 1], [1, 2]), OperatorKind.NORMALIZED_LAPLACIAN)
+    with pytest.raises(ValueError, match="non-finite"):
+        slq_trace(op, lambda x: np.full_like(x, np.nan), SlqConfig(n_v=4, s=4, seed=0))
+
+
+def test_weighted_graph_matches_oracle(cuda_device):
+    rng = np.random.default_rng(9)
+    n = 300
+    iu, ju = np.triu_indices(n, 1)
+    keep = rng.random(iu.size) < 0.05
+    g = csr_from_edges(n, iu[keep], ju[keep], rng.uniform(0.5, 1.5, int(keep.sum())))
+    cfg = SlqConfig(n_v=40, s=12, seed=4)
+    heat, wave = netlsd_heat_wave_slq(g, GRID, cfg)
+    ref, _ = O.heat_trace(g, GRID.values, 40, 12, 4)
+    assert golden.rel_l2(heat.values, ref) <= FP64_TOL
+    v = vnge_slq(g, cfg)
+    ref_v, _ = O.vnge(g, 40, 12, 4)
+    assert abs(v.value - ref_v) <= FP64_TOL * abs(ref_v)
+
+
+def test_lanczos_from_start_vector_matches_oracle(cuda_device):
+    from paper_2003_01282_b200.lanczos import lanczos_tridiagonalize, quadrature_rule
+    from paper_2003_01282_b200.operators import OperatorKind, make_operator
+
+    z = golden.load("c1_ba1000.npz")
+    g = golden.graph(z)
+    op = make_operator(g, OperatorKind.NORMALIZED_LAPLACIAN)
+    q0 = O.draw_probes(g.n, 0, [0])[:, 0]
+    tri = lanczos_tridiagonalize(op, q0, 10)
+    assert tri.steps == int(z["NL/steps"][0])
+    assert np.allclose(tri.alpha, z["NL/alpha"][0], rtol=1e-12)
+    rule = quadrature_rule(tri)
+    assert np.allclose(rule.weights, z["NL/weights"][0], rtol=1e-8, atol=1e-13)
+    with pytest.raises(ValueError, match="unit norm"):
+        lanczos_tridiagonalize(op, 2 * q0, 10)
+
+
+# full-size configs through size-independent properties + oracle on a probe subset
+def test_c2_sbm100k_heat_wave_vs_oracle(cuda_device):
+    from paper_2003_01282_b200 import synth
+
+    g = synth.sbm(100_000, 10, 1e-3, 1e-5, seed=0)
+    cfg = SlqConfig(n_v=100, s=15, seed=0)
+    heat, wave = netlsd_heat_wave_slq(g, GRID, cfg)
+    # oracle on the first 12 probes; prefix property makes this a per-probe check
+    op = O.make_block_operator(g, O.NORMALIZED_LAPLACIAN)
+    rules = O.slq_rules(op, 12, 15, 0, threads=4)
+    dg = DeviceGraph(g, cuda_device)
+    dr = dg.rules("normalized_laplacian", 0, 0, 12, 15)
+    assert np.max(np.abs(dr.nodes.cpu().numpy() - rules.nodes)) <= 1e-11 * 2.0
+    assert np.allclose(dr.weights.cpu().numpy(), rules.weights, rtol=1e-8, atol=1e-12)
+    h12, _ = O.heat_from_rules(rules, g.n, GRID.values)
+    got12 = netlsd_slq(g, GRID, SlqConfig(n_v=12, s=15, seed=0))
+    assert golden.rel_l2(got12.values, h12) <= FP64_TOL
+    # t -> 0 limit: every rule integrates 1, so h_t -> n (a size-independent check)
+    assert abs(heat.values[0] - g.n) / g.n < 0.03
+    assert np.all(np.isfinite(wave.values))
