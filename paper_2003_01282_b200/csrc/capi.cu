@@ -31,16 +31,26 @@ struct Rec {
 static std::mutex g_mu;
 static bool g_prof = false;
 static std::vector<Rec> g_recs;
+static std::vector<cudaEvent_t> g_pool;   // events are created once and recycled
 static int64_t g_class_launches[K_NUM_CLASSES] = {0};
+
+static cudaEvent_t pooled_event() {
+  if (g_pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = g_pool.back();
+  g_pool.pop_back();
+  return e;
+}
 
 void launch_begin(KernelClass k, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   std::lock_guard<std::mutex> lk(g_mu);
   g_class_launches[k] += 1;
   if (!g_prof) return;
-  Rec r{static_cast<int>(k), nullptr, nullptr};
-  cudaEventCreate(&r.a);
-  cudaEventCreate(&r.b);
+  Rec r{static_cast<int>(k), pooled_event(), pooled_event()};
   cudaEventRecord(r.a, s);
   g_recs.push_back(r);
 }
@@ -66,8 +76,13 @@ extern "C" uint64_t slq_launch_count(void) { return g_launches.load(); }
 
 extern "C" void slq_profile_begin(void) {
   std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& r : g_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto& r : g_recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
   g_recs.clear();
+  while (g_pool.size() < 4096) {   // pre-create so recording stays cheap inside timed regions
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    g_pool.push_back(e);
+  }
   for (auto& c : g_class_launches) c = 0;
   g_prof = true;
 }
@@ -86,8 +101,10 @@ extern "C" int slq_profile_end(double* ms, int64_t* launches, int n) {
     cudaEventSynchronize(r.b);
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) acc[r.cls] += t;
-    cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& r : recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
   }
   const int m = n < K_NUM_CLASSES ? n : K_NUM_CLASSES;
   for (int i = 0; i < m; ++i) {

@@ -16,7 +16,7 @@ namespace slq {
 constexpr int kMaxTiles = 148 * 16;   // SpMM tiles: <= 16 per SM
 constexpr int64_t kMinTileCost = 2048;
 constexpr int64_t kRowCost = 2;       // per-row overhead in nonzero-equivalents
-constexpr int64_t kMinStreamRows = 64;
+constexpr int64_t kMinStreamRows = 128;
 
 __global__ void narrow_cols_kernel(const int64_t* __restrict__ cols, int32_t* __restrict__ out,
                                    int64_t nnz, int64_t n, int* __restrict__ bad) {
@@ -119,13 +119,13 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
                        cudaStream_t st) {
   const int64_t n = g->n, nnz = g->nnz;
   void* p = nullptr;
-  SLQ_CUDA(cudaMalloc(&p, sizeof(int64_t) * (n + 1)));
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), st));
   g->offsets = static_cast<int64_t*>(track(g, p));
   SLQ_CUDA(cudaMemcpyAsync(const_cast<int64_t*>(g->offsets), offsets, sizeof(int64_t) * (n + 1),
                            cudaMemcpyDefault, st));
-  SLQ_CUDA(cudaMalloc(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), st));
   g->cols = static_cast<int32_t*>(track(g, p));
-  SLQ_CUDA(cudaMalloc(&p, sizeof(double) * std::max<int64_t>(n, 1) * 2));
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * std::max<int64_t>(n, 1) * 2, st));
   track(g, p);
   g->degree = static_cast<double*>(p);
   g->dinv = g->degree + std::max<int64_t>(n, 1);
@@ -150,7 +150,7 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   if (hflags[0]) return fail(SLQ_ERR_VALUE, "column index out of range [0, n)");
   g->unit_weights = hflags[1] ? 0 : 1;
   if (!g->unit_weights) {
-    SLQ_CUDA(cudaMalloc(&p, sizeof(double) * nnz));
+    SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * nnz, st));
     g->weights = static_cast<double*>(track(g, p));
     SLQ_CUDA(cudaMemcpyAsync(const_cast<double*>(g->weights), weights, sizeof(double) * nnz,
                              cudaMemcpyDefault, st));
@@ -182,7 +182,7 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   const int64_t total = nnz + kRowCost * n;
   int64_t target = std::max<int64_t>(kMinTileCost, (total + kMaxTiles - 1) / kMaxTiles);
   g->ntiles = std::max(1, ceil_div(total, target));
-  SLQ_CUDA(cudaMalloc(&p, sizeof(int64_t) * (g->ntiles + 1)));
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (g->ntiles + 1), st));
   g->tile_rows = static_cast<int64_t*>(track(g, p));
   {
     LaunchScope ls(K_PREPARE, st);
@@ -214,7 +214,9 @@ extern "C" int slq_graph_create(int64_t n, int64_t nnz, const int64_t* offsets, 
   slq_graph* g = new slq_graph();
   g->n = n;
   g->nnz = nnz;
+  g->stream = stream;
   cudaGetDevice(&g->device);
+  ensure_pool(g->device);
   int rc = graph_build(g, offsets, cols, weights, static_cast<cudaStream_t>(stream));
   if (rc != SLQ_OK) {
     slq_graph_destroy(g);
@@ -261,7 +263,8 @@ extern "C" int slq_graph_info(const slq_graph* g, slq_graph_info_t* out) {
 
 extern "C" void slq_graph_destroy(slq_graph* g) {
   if (!g) return;
-  for (int i = 0; i < g->n_owned; ++i) cudaFree(g->owned[i]);
+  // stream-ordered frees on the creation stream (it must outlive the graph)
+  for (int i = 0; i < g->n_owned; ++i) cudaFreeAsync(g->owned[i], static_cast<cudaStream_t>(g->stream));
   delete g;
 }
 

@@ -21,19 +21,18 @@
 // bitwise independent of the chunk width, probe range and GPU count (reference prefix property).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
+#include "bulk_pipe.cuh"
 #include "pcg64.cuh"
 #include "slq_common.cuh"
 
 namespace slq {
 
-constexpr int kSpmmWarps = 4;
-constexpr int kStreamWarps = 4;
-constexpr int kReduceWarps = 32;
 constexpr int kProbeRun = 32;        // 64-bit PCG outputs per thread in probe_init (64 rows)
 constexpr int kSecondPassGrid = 148 * 4;
-constexpr int kMaxChunk = 512;       // probes per chunk (16 probe groups)
+constexpr int kMaxChunk = 256;       // probes per chunk (flat CGS CTAs of <= 512 threads)
 
 // ----------------------------------------------------------------------------- probes
 template <typename VT>
@@ -106,6 +105,16 @@ __global__ void state_init_kernel(ChunkState s, int64_t n, int given_start) {
   if (p == 0) *s.any_again = 0;
 }
 
+// ----------------------------------------------------------------------------- launch geometry
+// A CTA covers one block of up to kBlk = 128 probes; lane l owns probes l, l+32, l+64, l+96 of the
+// block (PPL = probes per lane), so one shuffled column index feeds PPL coalesced 256-byte gathers.
+// Which thread owns a probe never changes its arithmetic: every per-probe sum runs in a fixed order
+// set by the graph's tiles and the warp count, never by c.
+constexpr int kBlk = 128;
+constexpr int kSpmmWarps = 8;
+
+__device__ __forceinline__ bool probe_ok(int p, int c) { return p < c; }
+
 // ----------------------------------------------------------------------------- pass A: SpMM
 struct SpmmArgs {
   const int64_t* offsets;
@@ -139,16 +148,30 @@ __device__ __forceinline__ double op_epilogue(double x, double acc, double d, do
   }
 }
 
-template <typename VT, int KIND, bool WEIGHTED>
+// One term of the in-row sum: A_jk * (dinv_k * x_k) with x_k = u_k * r (operators.py:89 order).
+template <int KIND, bool WEIGHTED>
+__device__ __forceinline__ double gather_term(double xraw, double r, double sk, double wk) {
+  double t = __dmul_rn(xraw, r);
+  if (KIND == SLQ_NORMALIZED_LAPLACIAN) t = __dmul_rn(sk, t);
+  if (WEIGHTED) t = __dmul_rn(wk, t);
+  return t;
+}
+
+template <typename VT, int KIND, bool WEIGHTED, int PPL>
 __global__ void __launch_bounds__(kSpmmWarps * 32)
 spmm_kernel(SpmmArgs a) {
-  __shared__ double red[kSpmmWarps][32];
+  __shared__ double red[kSpmmWarps][kBlk];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int p = blockIdx.y * 32 + lane;
-  const bool pv = p < a.c;
-  const double r = (a.r && pv) ? a.r[p] : 1.0;
-  const VT* __restrict__ u = static_cast<const VT*>(a.u);
-  VT* __restrict__ w = static_cast<VT*>(a.w);
+  const int pbase = blockIdx.y * kBlk + lane;
+  bool pv[PPL];
+  double r[PPL];
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    pv[j] = probe_ok(pbase + 32 * j, a.c);
+    r[j] = (a.r && pv[j]) ? a.r[pbase + 32 * j] : 1.0;
+  }
+  const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
+  VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
   const int64_t* __restrict__ off = a.offsets;
   const int32_t* __restrict__ cols = a.cols;
   const double* __restrict__ dinv = a.dinv;
@@ -157,10 +180,14 @@ spmm_kernel(SpmmArgs a) {
 
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int64_t rb = a.tile_rows[tile], re = a.tile_rows[tile + 1];
-    double dot = 0.0;
+    double dot[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) dot[j] = 0.0;
     for (int64_t row = rb + warp; row < re; row += kSpmmWarps) {
       const int64_t beg = off[row], end = off[row + 1];
-      double acc = 0.0;
+      double acc[PPL];
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
       for (int64_t base = beg; base < end; base += 32) {
         const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
         int mycol = 0;
@@ -171,63 +198,89 @@ spmm_kernel(SpmmArgs a) {
           if (WEIGHTED) myw = __ldg(wts + base + lane);
         }
         int k = 0;
-        for (; k + 8 <= cnt; k += 8) {
-          double xv[8];
+        for (; k + 4 <= cnt; k += 4) {
+          double xv[4][PPL];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int cc = __shfl_sync(0xffffffffu, mycol, k + j);
-            xv[j] = pv ? ldg_f64(u + static_cast<int64_t>(cc) * ldi + p) : 0.0;
+          for (int q = 0; q < 4; ++q) {
+            const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q)) * ldi;
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            double t = __dmul_rn(xv[j], r);
-            if (KIND == SLQ_NORMALIZED_LAPLACIAN) t = __dmul_rn(__shfl_sync(0xffffffffu, mys, k + j), t);
-            if (WEIGHTED) t = __dmul_rn(__shfl_sync(0xffffffffu, myw, k + j), t);
-            acc = __dadd_rn(acc, t);
+          for (int q = 0; q < 4; ++q) {
+            const double sk = __shfl_sync(0xffffffffu, mys, k + q);
+            const double wk = __shfl_sync(0xffffffffu, myw, k + q);
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xv[q][j], r[j], sk, wk));
           }
         }
         for (; k < cnt; ++k) {
-          const int cc = __shfl_sync(0xffffffffu, mycol, k);
+          const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k)) * ldi;
           const double sk = __shfl_sync(0xffffffffu, mys, k);
           const double wk = __shfl_sync(0xffffffffu, myw, k);
-          double t = __dmul_rn(pv ? ldg_f64(u + static_cast<int64_t>(cc) * ldi + p) : 0.0, r);
-          if (KIND == SLQ_NORMALIZED_LAPLACIAN) t = __dmul_rn(sk, t);
-          if (WEIGHTED) t = __dmul_rn(wk, t);
-          acc = __dadd_rn(acc, t);
+#pragma unroll
+          for (int j = 0; j < PPL; ++j) {
+            const double xr = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+            acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr, r[j], sk, wk));
+          }
         }
       }
-      if (pv) {
-        const double x = __dmul_rn(ldg_f64(u + row * ldi + p), r);
-        const double y = op_epilogue<KIND>(x, acc, __ldg(a.degree + row),
-                                           KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0, a.scale);
-        w[row * a.ldc_out + p] = from_f64<VT>(y);
-        dot = fma(x, y, dot);
+      const double d = __ldg(a.degree + row);
+      const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        if (!pv[j]) continue;
+        const double x = __dmul_rn(ldg_f64(u + row * ldi + 32 * j), r[j]);
+        const double y = op_epilogue<KIND>(x, acc[j], d, dis, a.scale);
+        w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
+        dot[j] = fma(x, y, dot[j]);
       }
     }
     if (a.partial) {
-      red[warp][lane] = dot;
-      __syncthreads();
-      if (warp == 0) {
-        double s = red[0][lane];
 #pragma unroll
-        for (int j = 1; j < kSpmmWarps; ++j) s += red[j][lane];
-        a.partial[static_cast<int64_t>(tile) * a.cpad + blockIdx.y * 32 + lane] = s;
+      for (int j = 0; j < PPL; ++j) red[warp][lane + 32 * j] = dot[j];
+      __syncthreads();
+      for (int pl = threadIdx.x; pl < PPL * 32; pl += blockDim.x) {
+        const int p = blockIdx.y * kBlk + pl;
+        double s = red[0][pl];
+#pragma unroll
+        for (int v = 1; v < kSpmmWarps; ++v) s += red[v][pl];
+        if (p < a.cpad) a.partial[static_cast<int64_t>(tile) * a.cpad + p] = s;
       }
       __syncthreads();
     }
   }
 }
 
+static int ppl_for(int c) {
+  const int cb = c < kBlk ? c : kBlk;
+  return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
+}
+
+template <typename VT, int KIND, bool W>
+static void spmm_dispatch(SpmmArgs a, dim3 grid, cudaStream_t st) {
+  switch (ppl_for(a.c)) {
+    case 1: spmm_kernel<VT, KIND, W, 1><<<grid, kSpmmWarps * 32, 0, st>>>(a); break;
+    case 2: spmm_kernel<VT, KIND, W, 2><<<grid, kSpmmWarps * 32, 0, st>>>(a); break;
+    default: spmm_kernel<VT, KIND, W, 4><<<grid, kSpmmWarps * 32, 0, st>>>(a); break;
+  }
+}
+
 template <typename VT>
-static void launch_spmm(int kind, const slq_graph* g, SpmmArgs a, int ngroups, cudaStream_t st) {
-  dim3 grid(a.ntiles, ngroups);
+static void launch_spmm(int kind, SpmmArgs a, cudaStream_t st) {
+  dim3 grid(a.ntiles, ceil_div(a.c, kBlk));
   LaunchScope ls(K_SPMM, st);
   const bool wt = a.weights != nullptr;
-#define SLQ_SPMM(K, W) spmm_kernel<VT, K, W><<<grid, kSpmmWarps * 32, 0, st>>>(a)
-  if (kind == SLQ_NORMALIZED_LAPLACIAN) { if (wt) SLQ_SPMM(SLQ_NORMALIZED_LAPLACIAN, true); else SLQ_SPMM(SLQ_NORMALIZED_LAPLACIAN, false); }
-  else if (kind == SLQ_DENSITY) { if (wt) SLQ_SPMM(SLQ_DENSITY, true); else SLQ_SPMM(SLQ_DENSITY, false); }
-  else { if (wt) SLQ_SPMM(SLQ_LAPLACIAN, true); else SLQ_SPMM(SLQ_LAPLACIAN, false); }
-#undef SLQ_SPMM
+  if (kind == SLQ_NORMALIZED_LAPLACIAN) {
+    if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, grid, st);
+    else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, grid, st);
+  } else if (kind == SLQ_DENSITY) {
+    if (wt) spmm_dispatch<VT, SLQ_DENSITY, true>(a, grid, st);
+    else spmm_dispatch<VT, SLQ_DENSITY, false>(a, grid, st);
+  } else {
+    if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, grid, st);
+    else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, grid, st);
+  }
 }
 
 // ----------------------------------------------------------------------------- pass B: CGS
@@ -237,137 +290,442 @@ struct CgsArgs {
   int ntiles;
   int c, cpad;
   int i;                           // current Lanczos step
-  int k0, nk;                      // basis block [k0, k0+nk) handled by this launch
+  int k0, nk;                      // basis block [k0, k0+nk) handled by this launch (dot kernel)
   int second;                      // 1: second CGS pass on u_{i+1}
   int reorth;
-  const void* basis;               // u_0 .. u_S (S+1 vectors; u_{i+1} is the output slot)
+  const void* basis;               // u_0 .. u_S
   const void* w;                   // Op(q_i)
   ChunkState s;
   double* partial;                 // [ntiles][nq][cpad]
 };
 
-template <typename VT>
-__device__ __forceinline__ double qval(const VT* basis, int64_t vs, int k, int64_t idx, double rk) {
-  return __dmul_rn(ldg_f64(basis + k * vs + idx), rk);
-}
-
 // w' = (w - alpha q_i) - beta_{i-1} q_{i-1}    (lanczos.py:129, numpy left-to-right evaluation)
-template <typename VT>
-__device__ __forceinline__ double three_term(const CgsArgs& a, const VT* basis, const VT* w, int64_t idx,
-                                             double al, double bp, double ri, double rim1) {
-  const double wv = ldg_f64(w + idx);
-  const double qi = qval(basis, a.vec_stride, a.i, idx, ri);
-  const double qp = a.i > 0 ? qval(basis, a.vec_stride, a.i - 1, idx, rim1) : 0.0;
+__device__ __forceinline__ double three_term(double wv, double ui, double uim1, double al, double bp, double ri,
+                                             double rim1) {
+  const double qi = __dmul_rn(ui, ri);
+  const double qp = __dmul_rn(uim1, rim1);
   return __dsub_rn(__dsub_rn(wv, __dmul_rn(al, qi)), __dmul_rn(bp, qp));
 }
 
+// Streaming CGS kernels use a flat layout: thread t of a CTA owns ONE probe column p = t % ldc and
+// one of kRowSlots row slots, for a group of tiles; a warp reads 256 contiguous bytes per load and
+// every per-probe scalar (alpha, beta, r, CGS coefficients) lives in registers.  The row slot of a
+// row is its index mod kRowSlots, so per-probe sums never depend on the chunk width.
+constexpr int kRowSlots = 2;
+constexpr int kStreamThreads = 256;
+
+struct FlatGeom {
+  int ldc, G;    // tiles per CTA
+};
+
+static FlatGeom flat_geom(int64_t ldc) {
+  FlatGeom f;
+  f.ldc = static_cast<int>(ldc);
+  f.G = std::max(1, static_cast<int>(kStreamThreads / (kRowSlots * ldc)));
+  return f;
+}
+
+// Partials of sum_rows u_k . w' (CGS coefficient before the r_k scale, lanczos.py:73) for k in
+// [k0, k0+nk) and of ||w'||^2 (lanczos.py:72).
 template <typename VT>
-__global__ void __launch_bounds__(kStreamWarps * 32)
-cgs_dot_kernel(CgsArgs a) {
-  __shared__ double red[kStreamWarps][kCgsBlock + 1][32];
+__global__ void __launch_bounds__(512)
+cgs_dot_kernel(CgsArgs a, int ldc_i, int G) {
+  extern __shared__ double part[];   // [G][kRowSlots][nq][ldc]
   if (a.second && *a.s.any_again == 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int p = blockIdx.y * 32 + lane;
+  const int t = threadIdx.x;
+  const int p = t % ldc_i;
+  const int slot = (t / ldc_i) % kRowSlots;
+  const int gt = t / (ldc_i * kRowSlots);
   const bool pv = p < a.c;
-  const VT* basis = static_cast<const VT*>(a.basis);
-  const VT* w = static_cast<const VT*>(a.w);
   const int cp = a.cpad;
+  const int nq = a.nk + 1;
   const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
   const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
   const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
   const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
-  double rk[kCgsBlock];
-#pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) rk[kk] = (pv && kk < a.nk) ? a.s.rsc[(a.k0 + kk) * cp + p] : 0.0;
-  const int nq = a.nk + 1;
+  const VT* basis = static_cast<const VT*>(a.basis) + p;
+  const VT* w = static_cast<const VT*>(a.w) + p;
+  const int64_t vs = a.vec_stride;
+  const VT* ui = basis + static_cast<int64_t>(a.i) * vs;
+  const VT* uim1 = basis + static_cast<int64_t>(a.i > 0 ? a.i - 1 : 0) * vs;
+  const VT* unext = basis + static_cast<int64_t>(a.i + 1) * vs;
+  const VT* uk0 = basis + static_cast<int64_t>(a.k0) * vs;
 
-  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    const int64_t rb = static_cast<int64_t>(tile) * a.rows_per_tile;
-    const int64_t re = min(a.n, rb + a.rows_per_tile);
+  for (int tb = blockIdx.x * G; tb < a.ntiles; tb += gridDim.x * G) {
+    const int tile = tb + gt;
     double acc[kCgsBlock];
 #pragma unroll
     for (int kk = 0; kk < kCgsBlock; ++kk) acc[kk] = 0.0;
     double nb = 0.0;
-    if (pv) {
-      for (int64_t row = rb + warp; row < re; row += kStreamWarps) {
-        const int64_t idx = row * a.ldc + p;
-        const double wp = a.second ? ldg_f64(basis + (a.i + 1) * a.vec_stride + idx)
-                                   : three_term(a, basis, w, idx, al, bp, ri, rim1);
+    if (pv && tile < a.ntiles) {
+      const int64_t rb = static_cast<int64_t>(tile) * a.rows_per_tile;
+      const int64_t re = min(a.n, rb + a.rows_per_tile);
+      for (int64_t row = rb + slot; row < re; row += kRowSlots) {
+        const int64_t idx = row * a.ldc;
+        const double wp = a.second ? ldg_f64(unext + idx)
+                                   : three_term(ldg_f64(w + idx), ldg_f64(ui + idx),
+                                                a.i > 0 ? ldg_f64(uim1 + idx) : 0.0, al, bp, ri, rim1);
         nb = fma(wp, wp, nb);
 #pragma unroll
         for (int kk = 0; kk < kCgsBlock; ++kk)
-          if (kk < a.nk) acc[kk] = fma(qval(basis, a.vec_stride, a.k0 + kk, idx, rk[kk]), wp, acc[kk]);
+          if (kk < a.nk) acc[kk] = fma(ldg_f64(uk0 + kk * vs + idx), wp, acc[kk]);
       }
     }
+    double* my = part + (static_cast<int64_t>(gt) * kRowSlots + slot) * nq * ldc_i + p;
 #pragma unroll
-    for (int kk = 0; kk < kCgsBlock; ++kk) red[warp][kk][lane] = acc[kk];
-    red[warp][kCgsBlock][lane] = nb;
+    for (int kk = 0; kk < kCgsBlock; ++kk)
+      if (kk < a.nk) my[kk * ldc_i] = acc[kk];
+    my[a.nk * ldc_i] = nb;
     __syncthreads();
-    for (int q = warp; q < nq; q += kStreamWarps) {
-      const int slot = q < a.nk ? q : kCgsBlock;
-      double s = red[0][slot][lane];
+    // fixed-order combine of the row slots
+    const int per_tile = nq * ldc_i;
+    for (int e = t; e < G * per_tile; e += blockDim.x) {
+      const int g2 = e / per_tile, rem = e - g2 * per_tile;
+      const int q = rem / ldc_i, pp = rem - q * ldc_i;
+      const int tl = tb + g2;
+      if (tl >= a.ntiles || pp >= cp) continue;
+      const double* src = part + static_cast<int64_t>(g2) * kRowSlots * per_tile + rem;
+      double s = src[0];
 #pragma unroll
-      for (int j = 1; j < kStreamWarps; ++j) s += red[j][slot][lane];
-      a.partial[(static_cast<int64_t>(tile) * nq + q) * cp + blockIdx.y * 32 + lane] = s;
+      for (int rs = 1; rs < kRowSlots; ++rs) s += src[rs * per_tile];
+      a.partial[(static_cast<int64_t>(tl) * nq + q) * cp + pp] = s;
     }
     __syncthreads();
   }
 }
 
+// u_{i+1} = w' - sum_k coef_k u_k (coef_k = h_k r_k, i.e. basis.T @ h with q_k = u_k r_k, lanczos.py:73);
+// partials of ||u_{i+1}||^2.  Second pass: u_{i+1} -= sum_k coef2_k u_k for flagged probes only.
 template <typename VT>
-__global__ void __launch_bounds__(kStreamWarps * 32)
-cgs_update_kernel(CgsArgs a) {
-  extern __shared__ double dyn[];          // [nk][32] h, then [nk][32] r
-  __shared__ double red[kStreamWarps][32];
+__global__ void __launch_bounds__(512)
+cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
+  extern __shared__ double part[];   // [G][kRowSlots][ldc]
   if (a.second && *a.s.any_again == 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int p = blockIdx.y * 32 + lane;
+  const int t = threadIdx.x;
+  const int p = t % ldc_i;
+  const int slot = (t / ldc_i) % kRowSlots;
+  const int gt = t / (ldc_i * kRowSlots);
   const int cp = a.cpad;
   const bool pv = p < a.c && (!a.second || a.s.again[p]);
-  const VT* basis = static_cast<const VT*>(a.basis);
-  VT* out = const_cast<VT*>(basis) + (a.i + 1) * a.vec_stride;
-  const VT* w = static_cast<const VT*>(a.w);
   const int nk = a.reorth ? a.i + 1 : 0;
-  double* hs = dyn;
-  double* rs = dyn + nk * 32;
-  for (int k = warp; k < nk; k += kStreamWarps) {
-    hs[k * 32 + lane] = pv ? a.s.h[k * cp + p] : 0.0;
-    rs[k * 32 + lane] = pv ? a.s.rsc[k * cp + p] : 0.0;
-  }
-  __syncthreads();
+  double cf[kCgsBlock];
+#pragma unroll
+  for (int kk = 0; kk < kCgsBlock; ++kk) cf[kk] = (pv && kk < nk) ? a.s.h[kk * cp + p] * a.s.rsc[kk * cp + p] : 0.0;
   const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
   const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
   const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
   const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
+  VT* basis = const_cast<VT*>(static_cast<const VT*>(a.basis)) + p;
+  const VT* w = static_cast<const VT*>(a.w) + p;
+  const int64_t vs = a.vec_stride;
+  VT* out = basis + static_cast<int64_t>(a.i + 1) * vs;
+  const VT* ui = basis + static_cast<int64_t>(a.i) * vs;
+  const VT* uim1 = basis + static_cast<int64_t>(a.i > 0 ? a.i - 1 : 0) * vs;
 
-  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    const int64_t rb = static_cast<int64_t>(tile) * a.rows_per_tile;
-    const int64_t re = min(a.n, rb + a.rows_per_tile);
+  for (int tb = blockIdx.x * G; tb < a.ntiles; tb += gridDim.x * G) {
+    const int tile = tb + gt;
     double nrm = 0.0;
-    if (pv) {
-      for (int64_t row = rb + warp; row < re; row += kStreamWarps) {
-        const int64_t idx = row * a.ldc + p;
-        const double wp = a.second ? ldg_f64(out + idx) : three_term(a, basis, w, idx, al, bp, ri, rim1);
-        // basis.T @ h, accumulated over k in order, then one subtraction (lanczos.py:73)
+    if (pv && tile < a.ntiles) {
+      const int64_t rb = static_cast<int64_t>(tile) * a.rows_per_tile;
+      const int64_t re = min(a.n, rb + a.rows_per_tile);
+      for (int64_t row = rb + slot; row < re; row += kRowSlots) {
+        const int64_t idx = row * a.ldc;
+        const double wp = a.second ? ldg_f64(out + idx)
+                                   : three_term(ldg_f64(w + idx), ldg_f64(ui + idx),
+                                                a.i > 0 ? ldg_f64(uim1 + idx) : 0.0, al, bp, ri, rim1);
         double proj = 0.0;
-        for (int k = 0; k < nk; ++k)
-          proj = __dadd_rn(proj, __dmul_rn(qval(basis, a.vec_stride, k, idx, rs[k * 32 + lane]), hs[k * 32 + lane]));
+#pragma unroll
+        for (int kk = 0; kk < kCgsBlock; ++kk)
+          if (kk < nk) proj = fma(ldg_f64(basis + kk * vs + idx), cf[kk], proj);
+        for (int k = kCgsBlock; k < nk; ++k)   // s > 17 only
+          proj = fma(ldg_f64(basis + k * vs + idx), a.s.h[k * cp + p] * a.s.rsc[k * cp + p], proj);
         const VT v = from_f64<VT>(nk ? __dsub_rn(wp, proj) : wp);
         out[idx] = v;
         const double vd = to_f64(v);
         nrm = fma(vd, vd, nrm);
       }
     }
-    red[warp][lane] = nrm;
+    part[(gt * kRowSlots + slot) * ldc_i + p] = nrm;
     __syncthreads();
-    if (warp == 0) {
-      double s = red[0][lane];
+    for (int e = t; e < G * ldc_i; e += blockDim.x) {
+      const int g2 = e / ldc_i, pp = e - g2 * ldc_i;
+      const int tl = tb + g2;
+      if (tl >= a.ntiles || pp >= cp) continue;
+      double s = part[(g2 * kRowSlots) * ldc_i + pp];
 #pragma unroll
-      for (int j = 1; j < kStreamWarps; ++j) s += red[j][lane];
-      a.partial[static_cast<int64_t>(tile) * cp + blockIdx.y * 32 + lane] = s;
+      for (int rs = 1; rs < kRowSlots; ++rs) s += part[(g2 * kRowSlots + rs) * ldc_i + pp];
+      a.partial[static_cast<int64_t>(tl) * cp + pp] = s;
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------- staged (TMA bulk) CGS kernels
+// Persistent: kPersist CTAs, CTA b owns the contiguous rows [n*b/G, n*(b+1)/G).  Warp 0 is the
+// producer: one elected lane streams row chunks of every needed vector into a kStages-deep shared
+// memory ring with cp.async.bulk (completion on a "full" mbarrier).  Consumer thread p owns probe
+// column p, walks its CTA's rows in ascending order from shared memory and releases each stage on
+// an "empty" mbarrier.  Bytes in flight per SM = the whole ring (no register cost), and every
+// per-probe sum runs in row order inside a fixed row range: independent of c and of the chunking.
+constexpr int kPersist = 148;
+constexpr int kStages = 3;
+constexpr int kMaxStaged = kCgsBlock + 4;
+constexpr size_t kStagedSmem = 220 * 1024;
+
+struct StagedArgs {
+  CgsArgs a;
+  int nvec;                       // vectors staged per chunk
+  const void* vec[kMaxStaged];    // global base of each staged vector
+  int slot_src, slot_ui, slot_uim1;
+  int slot_k[kCgsBlock];          // slot of basis vector k0 + kk
+  int rt;                         // rows per chunk
+};
+
+template <typename VT>
+struct StageRing {
+  uint64_t* full;
+  uint64_t* empty;
+  VT* buf;
+  __device__ StageRing(unsigned char* smem) {
+    full = reinterpret_cast<uint64_t*>(smem);
+    empty = full + kStages;
+    buf = reinterpret_cast<VT*>(smem + 128);
+  }
+};
+
+// Producer loop (one lane): chunk ch of the CTA's rows into stage ch % kStages.
+template <typename VT>
+__device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int64_t lo, int64_t hi) {
+  const int64_t ldc = sa.a.ldc;
+  const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * sa.rt * ldc;
+  int ch = 0;
+  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+    const int s = ch % kStages;
+    if (ch >= kStages) mbar_wait(&ring.empty[s], ((ch / kStages) - 1) & 1);
+    const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
+    const uint32_t bytes = static_cast<uint32_t>(rows * ldc * sizeof(VT));
+    mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec);
+    VT* dst = ring.buf + s * stage_elems;
+    for (int v = 0; v < sa.nvec; ++v)
+      bulk_g2s(dst + static_cast<int64_t>(v) * sa.rt * ldc, static_cast<const VT*>(sa.vec[v]) + r0 * ldc, bytes,
+               &ring.full[s]);
+  }
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(32 + 256, 1)
+cgs_dot_staged(StagedArgs sa) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const CgsArgs& a = sa.a;
+  if (a.second && *a.s.any_again == 0) return;
+  StageRing<VT> ring(smem);
+  const int nwc = (blockDim.x - 32) / 32;   // consumer warps
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) staged_produce<VT>(sa, ring, lo, hi);
+    return;
+  }
+  const int p = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const bool pv = p < a.c;
+  const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
+  const int nq = a.nk + 1;
+  const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
+  const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
+  const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
+  const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
+  const int64_t vstride = static_cast<int64_t>(sa.rt) * ldc;
+  const int64_t stage_elems = sa.nvec * vstride;
+  int koff[kCgsBlock];
+#pragma unroll
+  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * static_cast<int>(vstride);
+  const int osrc = sa.slot_src * static_cast<int>(vstride), oui = sa.slot_ui * static_cast<int>(vstride),
+            ouim1 = sa.slot_uim1 * static_cast<int>(vstride);
+  double acc[kCgsBlock];
+#pragma unroll
+  for (int kk = 0; kk < kCgsBlock; ++kk) acc[kk] = 0.0;
+  double nb = 0.0;
+  int ch = 0;
+  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+    const int s = ch % kStages;
+    mbar_wait(&ring.full[s], (ch / kStages) & 1);
+    const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
+    const VT* base = ring.buf + s * stage_elems + p;
+    if (pv) {
+      for (int r = 0; r < rows; ++r) {
+        const VT* e = base + r * ldc;
+        const double wp = a.second ? to_f64(e[osrc])
+                                   : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
+                                                al, bp, ri, rim1);
+        nb = fma(wp, wp, nb);
+#pragma unroll
+        for (int kk = 0; kk < kCgsBlock; ++kk)
+          if (kk < a.nk) acc[kk] = fma(to_f64(e[koff[kk]]), wp, acc[kk]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[s]);
+  }
+  if (p < cp) {
+    double* dst = a.partial + static_cast<int64_t>(blockIdx.x) * nq * cp + p;
+#pragma unroll
+    for (int kk = 0; kk < kCgsBlock; ++kk)
+      if (kk < a.nk) dst[kk * cp] = acc[kk];
+    dst[a.nk * cp] = nb;
+  }
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(32 + 256, 1)
+cgs_update_staged(StagedArgs sa) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const CgsArgs& a = sa.a;
+  if (a.second && *a.s.any_again == 0) return;
+  StageRing<VT> ring(smem);
+  const int nwc = (blockDim.x - 32) / 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) staged_produce<VT>(sa, ring, lo, hi);
+    return;
+  }
+  const int p = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
+  const bool pv = p < a.c && (!a.second || a.s.again[p]);
+  const int nk = a.reorth ? a.i + 1 : 0;
+  double cf[kCgsBlock];
+#pragma unroll
+  for (int kk = 0; kk < kCgsBlock; ++kk) cf[kk] = (pv && kk < nk) ? a.s.h[kk * cp + p] * a.s.rsc[kk * cp + p] : 0.0;
+  const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
+  const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
+  const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
+  const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
+  const int64_t vstride = static_cast<int64_t>(sa.rt) * ldc;
+  const int64_t stage_elems = sa.nvec * vstride;
+  int koff[kCgsBlock];
+#pragma unroll
+  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * static_cast<int>(vstride);
+  const int osrc = sa.slot_src * static_cast<int>(vstride), oui = sa.slot_ui * static_cast<int>(vstride),
+            ouim1 = sa.slot_uim1 * static_cast<int>(vstride);
+  VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(a.i + 1) * a.vec_stride + p;
+  double nrm = 0.0;
+  int ch = 0;
+  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+    const int s = ch % kStages;
+    mbar_wait(&ring.full[s], (ch / kStages) & 1);
+    const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
+    const VT* base = ring.buf + s * stage_elems + p;
+    if (pv) {
+      for (int r = 0; r < rows; ++r) {
+        const VT* e = base + r * ldc;
+        const double wp = a.second ? to_f64(e[osrc])
+                                   : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
+                                                al, bp, ri, rim1);
+        double proj = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kCgsBlock; ++kk)
+          if (kk < nk) proj = fma(to_f64(e[koff[kk]]), cf[kk], proj);
+        const VT v = from_f64<VT>(nk ? __dsub_rn(wp, proj) : wp);
+        out[(r0 + r) * a.ldc] = v;
+        const double vd = to_f64(v);
+        nrm = fma(vd, vd, nrm);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[s]);
+  }
+  if (p < cp) a.partial[static_cast<int64_t>(blockIdx.x) * cp + p] = nrm;
+}
+
+// Build the staged-vector list; returns false when the geometry does not fit (caller falls back).
+template <typename VT>
+static bool staged_setup(const CgsArgs& a, bool update, StagedArgs* sa, size_t* smem) {
+  StagedArgs s{};
+  s.a = a;
+  const VT* basis = static_cast<const VT*>(a.basis);
+  int nv = 0;
+  s.slot_src = nv;
+  s.vec[nv++] = a.second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
+  const int kfirst = update ? 0 : a.k0;
+  const int kcount = update ? (a.reorth ? a.i + 1 : 0) : a.nk;
+  if (kcount > kCgsBlock) return false;
+  for (int kk = 0; kk < kCgsBlock; ++kk) s.slot_k[kk] = 0;
+  for (int kk = 0; kk < kcount; ++kk) {
+    s.slot_k[kk] = nv;
+    s.vec[nv++] = basis + static_cast<int64_t>(kfirst + kk) * a.vec_stride;
+  }
+  auto slot_of = [&](int k) {
+    if (k >= kfirst && k < kfirst + kcount) return s.slot_k[k - kfirst];
+    s.vec[nv] = basis + static_cast<int64_t>(k) * a.vec_stride;
+    return nv++;
+  };
+  s.slot_ui = 0;
+  s.slot_uim1 = 0;
+  if (!a.second) {
+    s.slot_ui = slot_of(a.i);
+    if (a.i > 0) s.slot_uim1 = slot_of(a.i - 1);
+  }
+  s.nvec = nv;
+  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT);
+  const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
+  int64_t rt = static_cast<int64_t>((kStagedSmem - 128) / (kStages * row_bytes));
+  rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
+  const int consumers = ((static_cast<int>(a.ldc) + 31) / 32) * 32;
+  if (rt < 1 || consumers > 256) return false;
+  s.rt = static_cast<int>(rt);
+  *smem = 128 + kStages * rt * row_bytes;
+  *sa = s;
+  return true;
+}
+
+template <typename VT>
+static bool launch_staged(const CgsArgs& a, bool update, cudaStream_t st) {
+  StagedArgs sa;
+  size_t smem = 0;
+  if (!staged_setup<VT>(a, update, &sa, &smem)) return false;
+  const int threads = 32 + ((static_cast<int>(a.ldc) + 31) / 32) * 32;
+  if (update) {
+    LaunchScope ls(K_CGS_UPDATE, st);
+    cudaFuncSetAttribute(cgs_update_staged<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStagedSmem));
+    cgs_update_staged<VT><<<kPersist, threads, smem, st>>>(sa);
+  } else {
+    LaunchScope ls(K_CGS_DOT, st);
+    cudaFuncSetAttribute(cgs_dot_staged<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStagedSmem));
+    cgs_dot_staged<VT><<<kPersist, threads, smem, st>>>(sa);
+  }
+  return true;
+}
+
+template <typename VT>
+static int launch_cgs_dot(CgsArgs a, int max_ctas, cudaStream_t st) {
+  const FlatGeom f = flat_geom(a.ldc);
+  const int threads = f.G * kRowSlots * f.ldc;
+  const int ctas = std::max(1, std::min(ceil_div(a.ntiles, f.G), max_ctas));
+  const size_t smem = sizeof(double) * threads * (a.nk + 1);
+  LaunchScope ls(K_CGS_DOT, st);
+  if (smem > 48 * 1024)
+    SLQ_CUDA(cudaFuncSetAttribute(cgs_dot_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cgs_dot_kernel<VT><<<ctas, threads, smem, st>>>(a, f.ldc, f.G);
+  return SLQ_OK;
+}
+
+template <typename VT>
+static int launch_cgs_update(CgsArgs a, int max_ctas, cudaStream_t st) {
+  const FlatGeom f = flat_geom(a.ldc);
+  const int threads = f.G * kRowSlots * f.ldc;
+  const int ctas = std::max(1, std::min(ceil_div(a.ntiles, f.G), max_ctas));
+  const size_t smem = sizeof(double) * threads;
+  LaunchScope ls(K_CGS_UPDATE, st);
+  cgs_update_kernel<VT><<<ctas, threads, smem, st>>>(a, f.ldc, f.G);
+  return SLQ_OK;
 }
 
 // ----------------------------------------------------------------------------- reductions
@@ -383,6 +741,9 @@ struct ReduceArgs {
   ChunkState s;
 };
 
+constexpr int kReduceWarps = 16;
+
+// Fixed-order tree over tiles (deterministic; no atomics), then the per-probe scalar logic.
 __global__ void __launch_bounds__(kReduceWarps * 32)
 reduce_kernel(ReduceArgs a) {
   __shared__ double red[kReduceWarps][32];
@@ -406,7 +767,7 @@ reduce_kernel(ReduceArgs a) {
       if (blockIdx.y == 0 && lane == 0) *a.s.any_again = 0;
       break;
     case RED_CGS:
-      if (q < a.nk) a.s.h[(a.k0 + q) * cp + p] = tot;
+      if (q < a.nk) a.s.h[(a.k0 + q) * cp + p] = tot * a.s.rsc[(a.k0 + q) * cp + p];
       else if (!a.second) a.s.nb2[p] = tot;
       break;
     case RED_NORM:
@@ -436,8 +797,8 @@ reduce_kernel(ReduceArgs a) {
   }
 }
 
-static void launch_reduce(ReduceArgs a, int ngroups, cudaStream_t st) {
-  dim3 grid(a.nq, ngroups);
+static void launch_reduce(ReduceArgs a, cudaStream_t st) {
+  dim3 grid(a.nq, a.cpad / 32);
   LaunchScope ls(K_REDUCE, st);
   reduce_kernel<<<grid, kReduceWarps * 32, 0, st>>>(a);
 }
@@ -457,7 +818,16 @@ __global__ void scatter_out_kernel(ChunkState s, int64_t col0, int S, double* al
 }
 
 // ----------------------------------------------------------------------------- engine
-static void ensure_pool(int dev) {
+static bool staged_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SLQ_STAGED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+void ensure_pool(int dev) {
   static bool done[64] = {false};
   if (dev < 0 || dev >= 64 || done[dev]) return;
   cudaMemPool_t pool;
@@ -486,25 +856,25 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const int vb = sizeof(VT);
   // ldc: probes padded to a 32-byte sector multiple
   const int64_t ldc = ((c * vb + 31) / 32) * 32 / vb;
-  const int ngroups = ceil_div(c, 32);
-  const int cpad = ngroups * 32;
+  const int cpad = ceil_div(c, 32) * 32;
   const int64_t vs = n * ldc;
   double lo = 0, hi = 0;
   int rc = slq_operator_interval(g, kind, &lo, &hi);
   if (rc) return rc;
   const double tol = 1e-12 * hi;                           // lanczos.py:36,109-110
 
-  // workspace: S+1 basis slots + w, state arrays, partials
-  const int nq_max = std::max(kCgsBlock + 1, 1);
-  const int64_t ptiles = std::max(g->ntiles, g->ntiles_stream);
-  size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
-  size_t bytes_state = sizeof(double) * cpad * (4 * (S + 1) + 2) + sizeof(int) * (3 * cpad + 4);
-  size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
+  const int nq_max = kCgsBlock + 1;
+  const int64_t ptiles = std::max<int64_t>({g->ntiles, g->ntiles_stream, kPersist});
+  const size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
+  const size_t bytes_state = sizeof(double) * cpad * (4 * (S + 1) + 2) + sizeof(int) * (3 * cpad + 4);
+  const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
+  const size_t off_state = ((bytes_vec + 255) / 256) * 256;
+  const size_t off_part = off_state + ((bytes_state + 255) / 256) * 256;
   char* ws = nullptr;
-  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes_vec + bytes_state + bytes_part + 256, st));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_part + bytes_part, st));
   VT* basis = reinterpret_cast<VT*>(ws);
   VT* wv = basis + (S + 1) * vs;
-  double* dstate = reinterpret_cast<double*>(ws + ((bytes_vec + 127) / 128) * 128);
+  double* dstate = reinterpret_cast<double*>(ws + off_state);
   ChunkState s;
   s.c = c; s.cpad = cpad; s.S = S;
   s.rsc = dstate;
@@ -517,7 +887,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   s.alive = istate + cpad;
   s.again = istate + 2 * cpad;
   s.any_again = istate + 3 * cpad;
-  double* partial = reinterpret_cast<double*>(ws + ((bytes_vec + 127) / 128) * 128 + ((bytes_state + 127) / 128) * 128);
+  double* partial = reinterpret_cast<double*>(ws + off_part);
 
   {
     LaunchScope ls(K_PROBE, st);
@@ -544,59 +914,52 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   ReduceArgs ra{};
   ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.tol = tol; ra.reorth = reorth;
 
-  const dim3 sgrid(g->ntiles_stream, ngroups);
-  const size_t upd_smem = reorth ? sizeof(double) * 2 * 32 * S : 0;
-  if (upd_smem > 48 * 1024)
-    SLQ_CUDA(cudaFuncSetAttribute(cgs_update_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(upd_smem)));
-  const dim3 sgrid2(std::min(g->ntiles_stream, kSecondPassGrid), ngroups);
+  const int gx = 1 << 30;                 // one CTA per tile group
+  const bool use_staged = staged_enabled();
+  const int gx2 = kSecondPassGrid;        // second pass: small grid-stride launch
+
+  auto dot_pass = [&](int i, int second, int grid_x) {
+    for (int k0 = 0; k0 <= i; k0 += kCgsBlock) {
+      ca.k0 = k0;
+      ca.nk = std::min(kCgsBlock, i + 1 - k0);
+      ca.second = second;
+      const bool staged = use_staged && launch_staged<VT>(ca, false, st);
+      if (!staged) launch_cgs_dot<VT>(ca, grid_x, st);
+      ra.mode = RED_CGS; ra.ntiles = staged ? kPersist : g->ntiles_stream; ra.nq = ca.nk + 1; ra.k0 = k0; ra.nk = ca.nk;
+      ra.second = second;
+      launch_reduce(ra, st);
+    }
+  };
 
   for (int i = 0; i < S; ++i) {
     sa.u = basis + i * vs;
     sa.r = s.rsc + i * cpad;
-    launch_spmm<VT>(kind, g, sa, ngroups, st);
-    ra.mode = RED_ALPHA; ra.ntiles = g->ntiles; ra.nq = 1; ra.i = i;
-    launch_reduce(ra, ngroups, st);
+    launch_spmm<VT>(kind, sa, st);
+    ra.mode = RED_ALPHA; ra.ntiles = g->ntiles; ra.nq = 1; ra.i = i; ra.second = 0;
+    launch_reduce(ra, st);
     if (i == S - 1) break;
     ca.i = i;
+    if (reorth) dot_pass(i, 0, gx);
     ca.second = 0;
-    if (reorth) {
-      for (int k0 = 0; k0 <= i; k0 += kCgsBlock) {
-        ca.k0 = k0; ca.nk = std::min(kCgsBlock, i + 1 - k0);
-        {
-          LaunchScope ls(K_CGS_DOT, st);
-          cgs_dot_kernel<VT><<<sgrid, kStreamWarps * 32, 0, st>>>(ca);
-        }
-        ra.mode = RED_CGS; ra.ntiles = g->ntiles_stream; ra.nq = ca.nk + 1; ra.k0 = k0; ra.nk = ca.nk;
-        launch_reduce(ra, ngroups, st);
-      }
+    bool staged_upd = use_staged && launch_staged<VT>(ca, true, st);
+    if (!staged_upd) {
+      rc = launch_cgs_update<VT>(ca, gx, st);
+      if (rc) return rc;
     }
-    {
-      LaunchScope ls(K_CGS_UPDATE, st);
-      cgs_update_kernel<VT><<<sgrid, kStreamWarps * 32, upd_smem, st>>>(ca);
-    }
-    ra.mode = RED_NORM; ra.ntiles = g->ntiles_stream; ra.nq = 1;
-    launch_reduce(ra, ngroups, st);
+    ra.mode = RED_NORM; ra.ntiles = staged_upd ? kPersist : g->ntiles_stream; ra.nq = 1; ra.second = 0;
+    launch_reduce(ra, st);
     if (reorth) {
       // conditional second CGS pass (lanczos.py:75-76); kernels exit unless a probe asked for it
+      dot_pass(i, 1, gx2);
       ca.second = 1;
-      ra.second = 1;
-      for (int k0 = 0; k0 <= i; k0 += kCgsBlock) {
-        ca.k0 = k0; ca.nk = std::min(kCgsBlock, i + 1 - k0);
-        {
-          LaunchScope ls(K_CGS_DOT, st);
-          cgs_dot_kernel<VT><<<sgrid2, kStreamWarps * 32, 0, st>>>(ca);
-        }
-        ra.mode = RED_CGS; ra.ntiles = g->ntiles_stream; ra.nq = ca.nk + 1; ra.k0 = k0; ra.nk = ca.nk;
-        launch_reduce(ra, ngroups, st);
+      staged_upd = use_staged && launch_staged<VT>(ca, true, st);
+      if (!staged_upd) {
+        rc = launch_cgs_update<VT>(ca, gx2, st);
+        if (rc) return rc;
       }
-      {
-        LaunchScope ls(K_CGS_UPDATE, st);
-        cgs_update_kernel<VT><<<sgrid2, kStreamWarps * 32, upd_smem, st>>>(ca);
-      }
-      ra.mode = RED_NORM2; ra.ntiles = g->ntiles_stream; ra.nq = 1;
-      launch_reduce(ra, ngroups, st);
       ca.second = 0;
+      ra.mode = RED_NORM2; ra.ntiles = staged_upd ? kPersist : g->ntiles_stream; ra.nq = 1; ra.second = 1;
+      launch_reduce(ra, st);
       ra.second = 0;
     }
   }
@@ -676,7 +1039,7 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
   sa.scale = kind == SLQ_DENSITY ? 1.0 / g->trace_l : 0.0;
   sa.u = x; sa.r = nullptr; sa.w = y; sa.ldc_in = ld; sa.ldc_out = ld;
   sa.c = static_cast<int>(ncols); sa.cpad = ceil_div(ncols, 32) * 32; sa.partial = nullptr;
-  launch_spmm<double>(kind, g, sa, ceil_div(ncols, 32), st);
+  launch_spmm<double>(kind, sa, st);
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
 }

@@ -40,6 +40,8 @@ enum KernelClass {
   K_NUM_CLASSES
 };
 
+void ensure_pool(int dev);   // keep the stream-ordered allocator's memory cached
+
 void launch_begin(KernelClass k, cudaStream_t s);
 void launch_end(KernelClass k, cudaStream_t s);
 
@@ -70,6 +72,7 @@ struct slq_graph {
   int64_t nnz = 0;
   int64_t m = 0;                 // undirected edges = nnz / 2 for simple graphs
   int device = 0;
+  void* stream = nullptr;            // creation stream: owned buffers are freed on it
   const int64_t* offsets = nullptr;  // [n+1] device (owned copy)
   const int32_t* cols = nullptr;     // [nnz] device, narrowed to int32
   const double* weights = nullptr;   // [nnz] device, nullptr when every weight is 1.0

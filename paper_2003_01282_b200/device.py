@@ -139,7 +139,12 @@ class DeviceRules:
         import torch
 
         dev = self.nodes.device
-        tt = torch.as_tensor(np.asarray(t, dtype=np.float64), device=dev) if t is not None else None
+        if t is None:
+            tt = None
+        elif isinstance(t, torch.Tensor):
+            tt = t.to(device=dev, dtype=torch.float64).contiguous()
+        else:
+            tt = torch.tensor(np.asarray(t, dtype=np.float64), device=dev)
         T = 1 if tt is None else int(tt.numel())
         pv = torch.empty((T, self.count), dtype=torch.float64, device=dev)
         with torch.cuda.device(dev):
