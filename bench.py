@@ -223,7 +223,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = ClockSampler(local) if (rank == 0 and not os.environ.get("BENCH_NO_CLOCKS")) else None
     if sampler:
         sampler.start()
     launches0 = _lib.launch_count()
@@ -309,6 +309,7 @@ def run_ours(args):
                      "frac": (ach / peak) if ach else None, "traffic": args.traffic, "peak_source": peak_src},
         "kernels": per_class,
         "ms_per_step_profiled": float(np.mean(ptimes)),
+        "ms_steps": [round(t, 3) for t in times],
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": UNIT, "seconds_per_signature": e2e_s,

@@ -48,4 +48,22 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
+// Grid-wide barrier for persistent kernels whose CTAs are all co-resident (one CTA per SM, grid <= SMs).
+// `counter` is zeroed before the launch; barrier number k (1-based) completes when counter >= k*G.
+__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int target = k * gridDim.x * gridDim.y;
+    __threadfence();
+    atomicAdd(counter, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if (v < target) __nanosleep(32);
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 }  // namespace slq

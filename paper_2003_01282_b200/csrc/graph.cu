@@ -14,7 +14,7 @@
 namespace slq {
 
 constexpr int kMaxTiles = 148 * 16;   // SpMM tiles: <= 16 per SM
-constexpr int64_t kMinTileCost = 2048;
+constexpr int64_t kMinTileCost = 512;
 constexpr int64_t kRowCost = 2;       // per-row overhead in nonzero-equivalents
 constexpr int64_t kMinStreamRows = 128;
 

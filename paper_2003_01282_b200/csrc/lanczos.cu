@@ -21,14 +21,20 @@
 // bitwise independent of the chunk width, probe range and GPU count (reference prefix property).
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "bulk_pipe.cuh"
 #include "pcg64.cuh"
 #include "slq_common.cuh"
 
 namespace slq {
+
+namespace cg = cooperative_groups;
 
 constexpr int kProbeRun = 32;        // 64-bit PCG outputs per thread in probe_init (64 rows)
 constexpr int kSecondPassGrid = 148 * 4;
@@ -89,10 +95,12 @@ struct ChunkState {
   int* alive = nullptr;     // [cpad]
   int* again = nullptr;     // [cpad]
   int* any_again = nullptr; // [1]
+  unsigned int* barrier = nullptr;   // [S] grid-barrier counters of the persistent step kernels
 };
 
 __global__ void state_init_kernel(ChunkState s, int64_t n, int given_start) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < s.S) s.barrier[p] = 0u;
   if (p >= s.cpad) return;
   const bool pv = p < s.c;
   // r_0: the probe +-1 block is scaled by 1/fl(sqrt(n)) (= 1/||v||); a caller-given unit start
@@ -103,6 +111,99 @@ __global__ void state_init_kernel(ChunkState s, int64_t n, int given_start) {
   s.again[p] = 0;
   for (int k = 0; k < s.S; ++k) { s.alpha[k * s.cpad + p] = 0.0; s.beta[k * s.cpad + p] = 0.0; }
   if (p == 0) *s.any_again = 0;
+}
+
+// ----------------------------------------------------------------------------- reductions
+enum ReduceMode { RED_ALPHA = 0, RED_CGS = 1, RED_NORM = 2, RED_NORM2 = 3 };
+
+struct ReduceArgs {
+  const double* partial;   // [ntiles][nq][cpad]
+  int ntiles, nq, cpad, c;
+  int mode;
+  int i, k0, nk, reorth;
+  int second;              // 1: reduction of the conditional second CGS pass
+  double tol;              // breakdown tolerance 1e-12 * interval_hi
+  ChunkState s;
+};
+
+constexpr int kReduceWarps = 16;
+constexpr int kStripes = 16;   // fixed partition of the partial rows: the sum order never depends on
+                               // the CTA shape that runs the reduction
+
+// Per-probe scalar logic applied to a fully reduced quantity (lanczos.py:123-137).
+__device__ void apply_reduced(const ReduceArgs& a, int q, int p, double tot, bool first_slice) {
+  const int cp = a.cpad;
+  const bool pv = p < a.c;
+  switch (a.mode) {
+    case RED_ALPHA:
+      if (pv && a.s.alive[p]) a.s.alpha[a.i * cp + p] = tot;
+      if (first_slice && p == 0) *a.s.any_again = 0;
+      break;
+    case RED_CGS:
+      if (q < a.nk) a.s.h[(a.k0 + q) * cp + p] = tot * a.s.rsc[(a.k0 + q) * cp + p];
+      else if (!a.second) a.s.nb2[p] = tot;
+      break;
+    case RED_NORM:
+    case RED_NORM2: {
+      if (!pv || !a.s.alive[p]) break;
+      const double b = sqrt(tot);
+      if (a.mode == RED_NORM) {
+        if (a.reorth && b < 0.5 * sqrt(a.s.nb2[p])) {    // lanczos.py:75
+          a.s.again[p] = 1;
+          *a.s.any_again = 1;
+          break;
+        }
+      } else {
+        if (!a.s.again[p]) break;
+        a.s.again[p] = 0;
+      }
+      if (b <= a.tol) {                                  // lanczos.py:133-134
+        a.s.steps[p] = a.i + 1;
+        a.s.alive[p] = 0;
+        a.s.rsc[(a.i + 1) * cp + p] = 0.0;
+      } else {
+        a.s.beta[a.i * cp + p] = b;
+        a.s.rsc[(a.i + 1) * cp + p] = __ddiv_rn(1.0, b);
+      }
+      break;
+    }
+  }
+}
+
+// Reduce quantity q for the 32 probes of `group` over a.ntiles partial rows, with any number of
+// warps (>= 1).  All threads of the CTA must call it.  red: kStripes*32 doubles of shared memory.
+__device__ void reduce_slice(const ReduceArgs& a, int q, int group, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int p = group * 32 + lane;
+  const int64_t stride = static_cast<int64_t>(a.nq) * a.cpad;
+  const double* src = a.partial + static_cast<int64_t>(q) * a.cpad + p;
+  for (int sidx = warp; sidx < kStripes; sidx += nw) {
+    double s = 0.0;
+    int t = sidx;
+    for (; t + 3 * kStripes < a.ntiles; t += 4 * kStripes) {
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = src[(t + j * kStripes) * stride];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s += v[j];
+    }
+    for (; t < a.ntiles; t += kStripes) s += src[t * stride];
+    red[sidx * 32 + lane] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double tot = red[lane];
+    for (int j = 1; j < kStripes; ++j) tot += red[j * 32 + lane];
+    apply_reduced(a, q, p, tot, group == 0 && q == 0);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kReduceWarps * 32)
+reduce_kernel(ReduceArgs a) {
+  __shared__ double red[kStripes * 32];
+  if (a.second && *a.s.any_again == 0) return;
+  reduce_slice(a, blockIdx.x, blockIdx.y, red);
 }
 
 // ----------------------------------------------------------------------------- launch geometry
@@ -131,6 +232,7 @@ struct SpmmArgs {
   int64_t ldc_in, ldc_out;
   int c, cpad;
   double* partial;         // [ntiles][cpad] alpha partials (nullptr = none)
+  ReduceArgs red;          // cooperative launches: alpha reduced in-kernel after a grid barrier
 };
 
 template <int KIND>
@@ -157,8 +259,8 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
   return t;
 }
 
-template <typename VT, int KIND, bool WEIGHTED, int PPL>
-__global__ void __launch_bounds__(kSpmmWarps * 32)
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool COOP>
+__global__ void __launch_bounds__(kSpmmWarps * 32, 4)
 spmm_kernel(SpmmArgs a) {
   __shared__ double red[kSpmmWarps][kBlk];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -197,17 +299,18 @@ spmm_kernel(SpmmArgs a) {
           if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + mycol);
           if (WEIGHTED) myw = __ldg(wts + base + lane);
         }
+        constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane
         int k = 0;
-        for (; k + 4 <= cnt; k += 4) {
-          double xv[4][PPL];
+        for (; k + UNR <= cnt; k += UNR) {
+          double xv[UNR][PPL];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < UNR; ++q) {
             const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q)) * ldi;
 #pragma unroll
             for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < UNR; ++q) {
             const double sk = __shfl_sync(0xffffffffu, mys, k + q);
             const double wk = __shfl_sync(0xffffffffu, myw, k + q);
 #pragma unroll
@@ -250,6 +353,12 @@ spmm_kernel(SpmmArgs a) {
       __syncthreads();
     }
   }
+  if (COOP) {
+    // alpha_i = q_i . w over all tiles (fixed-order stripes), by the first cpad/32 CTAs
+    cg::this_grid().sync();
+    const int nblk = gridDim.x * gridDim.y, lb = blockIdx.y * gridDim.x + blockIdx.x;
+    for (int sl = lb; sl < a.cpad / 32; sl += nblk) reduce_slice(a.red, 0, sl, &red[0][0]);
+  }
 }
 
 static int ppl_for(int c) {
@@ -257,29 +366,50 @@ static int ppl_for(int c) {
   return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
 }
 
-template <typename VT, int KIND, bool W>
-static void spmm_dispatch(SpmmArgs a, dim3 grid, cudaStream_t st) {
-  switch (ppl_for(a.c)) {
-    case 1: spmm_kernel<VT, KIND, W, 1><<<grid, kSpmmWarps * 32, 0, st>>>(a); break;
-    case 2: spmm_kernel<VT, KIND, W, 2><<<grid, kSpmmWarps * 32, 0, st>>>(a); break;
-    default: spmm_kernel<VT, KIND, W, 4><<<grid, kSpmmWarps * 32, 0, st>>>(a); break;
+template <typename VT, int KIND, bool W, int PPL>
+static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
+  if (coop) {
+    static int max_ctas[64] = {0};   // co-resident CTAs per device for this instantiation
+    if (max_ctas[dev] == 0) {
+      int per_sm = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<VT, KIND, W, PPL, true>, kSpmmWarps * 32, 0);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      max_ctas[dev] = std::max(1, per_sm * sms);
+    }
+    const int gx = std::max(1, std::min(a.ntiles, max_ctas[dev] / gy));
+    void* args[] = {&a};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(spmm_kernel<VT, KIND, W, PPL, true>), dim3(gx, gy),
+                                dim3(kSpmmWarps * 32), args, 0, st);
+  } else {
+    dim3 grid(std::min(a.ntiles, 148 * 4), gy);
+    spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   }
 }
 
+template <typename VT, int KIND, bool W>
+static void spmm_dispatch(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
+  switch (ppl_for(a.c)) {
+    case 1: spmm_launch_one<VT, KIND, W, 1>(a, gy, coop, dev, st); break;
+    case 2: spmm_launch_one<VT, KIND, W, 2>(a, gy, coop, dev, st); break;
+    default: spmm_launch_one<VT, KIND, W, 4>(a, gy, coop, dev, st); break;
+  }
+}
+
+// coop: alpha is reduced in-kernel (cooperative launch); else the caller runs reduce_kernel.
 template <typename VT>
-static void launch_spmm(int kind, SpmmArgs a, cudaStream_t st) {
-  dim3 grid(a.ntiles, ceil_div(a.c, kBlk));
+static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st) {
+  const int gy = ceil_div(a.c, kBlk);
   LaunchScope ls(K_SPMM, st);
   const bool wt = a.weights != nullptr;
   if (kind == SLQ_NORMALIZED_LAPLACIAN) {
-    if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, grid, st);
-    else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, grid, st);
+    if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, gy, coop, dev, st);
+    else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, gy, coop, dev, st);
   } else if (kind == SLQ_DENSITY) {
-    if (wt) spmm_dispatch<VT, SLQ_DENSITY, true>(a, grid, st);
-    else spmm_dispatch<VT, SLQ_DENSITY, false>(a, grid, st);
+    if (wt) spmm_dispatch<VT, SLQ_DENSITY, true>(a, gy, coop, dev, st);
+    else spmm_dispatch<VT, SLQ_DENSITY, false>(a, gy, coop, dev, st);
   } else {
-    if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, grid, st);
-    else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, grid, st);
+    if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, gy, coop, dev, st);
+    else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, gy, coop, dev, st);
   }
 }
 
@@ -460,13 +590,19 @@ cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
   }
 }
 
-// ---------------------------------------------------------------- staged (TMA bulk) CGS kernels
-// Persistent: kPersist CTAs, CTA b owns the contiguous rows [n*b/G, n*(b+1)/G).  Warp 0 is the
-// producer: one elected lane streams row chunks of every needed vector into a kStages-deep shared
-// memory ring with cp.async.bulk (completion on a "full" mbarrier).  Consumer thread p owns probe
-// column p, walks its CTA's rows in ascending order from shared memory and releases each stage on
-// an "empty" mbarrier.  Bytes in flight per SM = the whole ring (no register cost), and every
-// per-probe sum runs in row order inside a fixed row range: independent of c and of the chunking.
+// ---------------------------------------------------------------- staged (TMA bulk) CGS step kernel
+// One cooperative persistent launch per Lanczos step does all of pass B: kPersist CTAs, CTA b owns
+// the contiguous rows [n*b/G, n*(b+1)/G).  Warp 0 lane 0 is the producer: it streams row chunks of
+// every needed vector into a kStages-deep shared-memory ring with cp.async.bulk (completion on a
+// "full" mbarrier).  Consumer thread p owns probe column p, walks its CTA's rows in ascending
+// order from shared memory and releases each stage on an "empty" mbarrier.  Bytes in flight per SM
+// = the whole ring (no register cost).  Phases, separated by grid-wide barriers:
+//   A  dots   partials of u_k . w' (k <= i) and ||w'||^2                       (lanczos.py:72-73)
+//   B  reduce CGS coefficients h_k (fixed-order stripes)
+//   C  update u_{i+1} = w' - sum_k h_k q_k, partials of ||u_{i+1}||^2          (lanczos.py:73)
+//   D  finalize beta_i, breakdown, second-pass flag                             (lanczos.py:75,132-134)
+//   A'-D' the conditional second CGS pass, only if some probe asked for it     (lanczos.py:75-76)
+// Every per-probe sum runs in row order inside a fixed row range: independent of c and chunking.
 constexpr int kPersist = 148;
 constexpr int kStages = 3;
 constexpr int kMaxStaged = kCgsBlock + 4;
@@ -477,8 +613,13 @@ struct StagedArgs {
   int nvec;                       // vectors staged per chunk
   const void* vec[kMaxStaged];    // global base of each staged vector
   int slot_src, slot_ui, slot_uim1;
-  int slot_k[kCgsBlock];          // slot of basis vector k0 + kk
+  int slot_k[kCgsBlock];          // slot of basis vector k
   int rt;                         // rows per chunk
+};
+
+struct StepArgs {
+  StagedArgs pass[2];             // [0]: src = w, [1]: src = u_{i+1} (second CGS pass)
+  ReduceArgs red;
 };
 
 template <typename VT>
@@ -486,19 +627,23 @@ struct StageRing {
   uint64_t* full;
   uint64_t* empty;
   VT* buf;
-  __device__ StageRing(unsigned char* smem) {
+  __device__ explicit StageRing(unsigned char* smem) {
     full = reinterpret_cast<uint64_t*>(smem);
     empty = full + kStages;
     buf = reinterpret_cast<VT*>(smem + 128);
   }
 };
 
-// Producer loop (one lane): chunk ch of the CTA's rows into stage ch % kStages.
+__device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
+  return hi > lo ? static_cast<int>((hi - lo + rt - 1) / rt) : 0;
+}
+
+// Producer (one lane): chunk j of [lo, hi) goes to ring slot (ch0 + j) % kStages.
 template <typename VT>
-__device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int64_t lo, int64_t hi) {
+__device__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
   const int64_t ldc = sa.a.ldc;
   const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * sa.rt * ldc;
-  int ch = 0;
+  int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
     const int s = ch % kStages;
     if (ch >= kStages) mbar_wait(&ring.empty[s], ((ch / kStages) - 1) & 1);
@@ -512,44 +657,38 @@ __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<V
   }
 }
 
+struct ProbeScalars {
+  double al, bp, ri, rim1;
+  __device__ ProbeScalars(const CgsArgs& a, int p, bool pv) {
+    const int cp = a.cpad;
+    al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
+    bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
+    ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
+    rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
+  }
+};
+
+// Phase A (consumer side): partials [cta][nk+1][cpad] of u_k . w' and ||w'||^2.
 template <typename VT>
-__global__ void __launch_bounds__(32 + 256, 1)
-cgs_dot_staged(StagedArgs sa) {
-  extern __shared__ __align__(128) unsigned char smem[];
+__device__ void staged_dot_consume(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi,
+                                   bool second) {
   const CgsArgs& a = sa.a;
-  if (a.second && *a.s.any_again == 0) return;
-  StageRing<VT> ring(smem);
-  const int nwc = (blockDim.x - 32) / 32;   // consumer warps
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) staged_produce<VT>(sa, ring, lo, hi);
-    return;
-  }
   const int p = threadIdx.x - 32, lane = threadIdx.x & 31;
   const bool pv = p < a.c;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
-  const int nq = a.nk + 1;
-  const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
-  const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
-  const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
-  const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
-  const int64_t vstride = static_cast<int64_t>(sa.rt) * ldc;
-  const int64_t stage_elems = sa.nvec * vstride;
+  const int nk = a.i + 1;
+  const ProbeScalars ps(a, p, pv);
+  const int vstride = sa.rt * ldc;
+  const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * vstride;
   int koff[kCgsBlock];
 #pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * static_cast<int>(vstride);
-  const int osrc = sa.slot_src * static_cast<int>(vstride), oui = sa.slot_ui * static_cast<int>(vstride),
-            ouim1 = sa.slot_uim1 * static_cast<int>(vstride);
+  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * vstride;
+  const int osrc = sa.slot_src * vstride, oui = sa.slot_ui * vstride, ouim1 = sa.slot_uim1 * vstride;
   double acc[kCgsBlock];
 #pragma unroll
   for (int kk = 0; kk < kCgsBlock; ++kk) acc[kk] = 0.0;
   double nb = 0.0;
-  int ch = 0;
+  int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
@@ -558,66 +697,49 @@ cgs_dot_staged(StagedArgs sa) {
     if (pv) {
       for (int r = 0; r < rows; ++r) {
         const VT* e = base + r * ldc;
-        const double wp = a.second ? to_f64(e[osrc])
-                                   : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
-                                                al, bp, ri, rim1);
+        const double wp = second ? to_f64(e[osrc])
+                                 : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
+                                              ps.al, ps.bp, ps.ri, ps.rim1);
         nb = fma(wp, wp, nb);
 #pragma unroll
         for (int kk = 0; kk < kCgsBlock; ++kk)
-          if (kk < a.nk) acc[kk] = fma(to_f64(e[koff[kk]]), wp, acc[kk]);
+          if (kk < nk) acc[kk] = fma(to_f64(e[koff[kk]]), wp, acc[kk]);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
   if (p < cp) {
-    double* dst = a.partial + static_cast<int64_t>(blockIdx.x) * nq * cp + p;
+    double* dst = a.partial + static_cast<int64_t>(blockIdx.x) * (nk + 1) * cp + p;
 #pragma unroll
     for (int kk = 0; kk < kCgsBlock; ++kk)
-      if (kk < a.nk) dst[kk * cp] = acc[kk];
-    dst[a.nk * cp] = nb;
+      if (kk < nk) dst[kk * cp] = acc[kk];
+    dst[nk * cp] = nb;
   }
 }
 
+// Phase C (consumer side): u_{i+1} and partials [cta][cpad] of ||u_{i+1}||^2.
 template <typename VT>
-__global__ void __launch_bounds__(32 + 256, 1)
-cgs_update_staged(StagedArgs sa) {
-  extern __shared__ __align__(128) unsigned char smem[];
+__device__ void staged_update_consume(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi,
+                                      bool second) {
   const CgsArgs& a = sa.a;
-  if (a.second && *a.s.any_again == 0) return;
-  StageRing<VT> ring(smem);
-  const int nwc = (blockDim.x - 32) / 32;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) staged_produce<VT>(sa, ring, lo, hi);
-    return;
-  }
   const int p = threadIdx.x - 32, lane = threadIdx.x & 31;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
-  const bool pv = p < a.c && (!a.second || a.s.again[p]);
+  const bool pv = p < a.c && (!second || a.s.again[p]);
   const int nk = a.reorth ? a.i + 1 : 0;
   double cf[kCgsBlock];
 #pragma unroll
   for (int kk = 0; kk < kCgsBlock; ++kk) cf[kk] = (pv && kk < nk) ? a.s.h[kk * cp + p] * a.s.rsc[kk * cp + p] : 0.0;
-  const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
-  const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
-  const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
-  const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
-  const int64_t vstride = static_cast<int64_t>(sa.rt) * ldc;
-  const int64_t stage_elems = sa.nvec * vstride;
+  const ProbeScalars ps(a, p, pv);
+  const int vstride = sa.rt * ldc;
+  const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * vstride;
   int koff[kCgsBlock];
 #pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * static_cast<int>(vstride);
-  const int osrc = sa.slot_src * static_cast<int>(vstride), oui = sa.slot_ui * static_cast<int>(vstride),
-            ouim1 = sa.slot_uim1 * static_cast<int>(vstride);
+  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * vstride;
+  const int osrc = sa.slot_src * vstride, oui = sa.slot_ui * vstride, ouim1 = sa.slot_uim1 * vstride;
   VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(a.i + 1) * a.vec_stride + p;
   double nrm = 0.0;
-  int ch = 0;
+  int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
@@ -626,9 +748,9 @@ cgs_update_staged(StagedArgs sa) {
     if (pv) {
       for (int r = 0; r < rows; ++r) {
         const VT* e = base + r * ldc;
-        const double wp = a.second ? to_f64(e[osrc])
-                                   : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
-                                                al, bp, ri, rim1);
+        const double wp = second ? to_f64(e[osrc])
+                                 : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
+                                              ps.al, ps.bp, ps.ri, ps.rim1);
         double proj = 0.0;
 #pragma unroll
         for (int kk = 0; kk < kCgsBlock; ++kk)
@@ -645,31 +767,88 @@ cgs_update_staged(StagedArgs sa) {
   if (p < cp) a.partial[static_cast<int64_t>(blockIdx.x) * cp + p] = nrm;
 }
 
-// Build the staged-vector list; returns false when the geometry does not fit (caller falls back).
 template <typename VT>
-static bool staged_setup(const CgsArgs& a, bool update, StagedArgs* sa, size_t* smem) {
+__global__ void __launch_bounds__(32 + 256, 1)
+cgs_step_kernel(StepArgs sa) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double red[kStripes * 32];
+  StageRing<VT> ring(smem);
+  const CgsArgs& a = sa.pass[0].a;
+  unsigned int* bar = a.s.barrier + a.i;
+  unsigned int nbar = 0;
+  auto sync_grid = [&]() { grid_barrier(bar, ++nbar); };
+  const int nwc = (blockDim.x - 32) / 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
+  const int ngroups = a.cpad / 32;
+  const int nk = a.i + 1;
+  int ch = 0;
+  for (int pass = 0; pass < (a.reorth ? 2 : 1); ++pass) {
+    const StagedArgs& st = sa.pass[pass];
+    const bool second = pass == 1;
+    if (second && *a.s.any_again == 0) break;   // uniform: read after a grid barrier
+    const int nch = chunk_count(lo, hi, st.rt);
+    ReduceArgs r = sa.red;
+    r.second = pass;
+    r.ntiles = gridDim.x;
+    if (a.reorth) {
+      // A: dots
+      if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
+      } else {
+        staged_dot_consume<VT>(st, ring, ch, lo, hi, second);
+      }
+      ch += nch;
+      sync_grid();
+      // B: CGS coefficients (+ ||w'||^2 on the first pass)
+      r.mode = RED_CGS; r.nq = nk + 1; r.k0 = 0; r.nk = nk;
+      for (int sl = blockIdx.x; sl < r.nq * ngroups; sl += gridDim.x) reduce_slice(r, sl % r.nq, sl / r.nq, red);
+      sync_grid();
+    }
+    // C: update
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
+    } else {
+      staged_update_consume<VT>(st, ring, ch, lo, hi, second);
+    }
+    ch += nch;
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // u_{i+1} is bulk-read by a second pass
+    sync_grid();
+    // D: beta, breakdown, second-pass flag
+    r.mode = second ? RED_NORM2 : RED_NORM; r.nq = 1;
+    for (int sl = blockIdx.x; sl < ngroups; sl += gridDim.x) reduce_slice(r, 0, sl, red);
+    sync_grid();
+  }
+}
+
+// Build the staged-vector list of one pass; false when the geometry does not fit.
+template <typename VT>
+static bool staged_setup(const CgsArgs& a, bool second, StagedArgs* out) {
   StagedArgs s{};
   s.a = a;
   const VT* basis = static_cast<const VT*>(a.basis);
   int nv = 0;
   s.slot_src = nv;
-  s.vec[nv++] = a.second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
-  const int kfirst = update ? 0 : a.k0;
-  const int kcount = update ? (a.reorth ? a.i + 1 : 0) : a.nk;
+  s.vec[nv++] = second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
+  const int kcount = a.reorth ? a.i + 1 : 0;
   if (kcount > kCgsBlock) return false;
   for (int kk = 0; kk < kCgsBlock; ++kk) s.slot_k[kk] = 0;
   for (int kk = 0; kk < kcount; ++kk) {
     s.slot_k[kk] = nv;
-    s.vec[nv++] = basis + static_cast<int64_t>(kfirst + kk) * a.vec_stride;
+    s.vec[nv++] = basis + static_cast<int64_t>(kk) * a.vec_stride;
   }
   auto slot_of = [&](int k) {
-    if (k >= kfirst && k < kfirst + kcount) return s.slot_k[k - kfirst];
+    if (k < kcount) return s.slot_k[k];
     s.vec[nv] = basis + static_cast<int64_t>(k) * a.vec_stride;
     return nv++;
   };
   s.slot_ui = 0;
   s.slot_uim1 = 0;
-  if (!a.second) {
+  if (!second) {
     s.slot_ui = slot_of(a.i);
     if (a.i > 0) s.slot_uim1 = slot_of(a.i - 1);
   }
@@ -678,28 +857,50 @@ static bool staged_setup(const CgsArgs& a, bool update, StagedArgs* sa, size_t* 
   const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
   int64_t rt = static_cast<int64_t>((kStagedSmem - 128) / (kStages * row_bytes));
   rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
-  const int consumers = ((static_cast<int>(a.ldc) + 31) / 32) * 32;
-  if (rt < 1 || consumers > 256) return false;
+  if (rt < 1 || a.ldc > 256) return false;
   s.rt = static_cast<int>(rt);
-  *smem = 128 + kStages * rt * row_bytes;
-  *sa = s;
+  *out = s;
   return true;
 }
 
+static int coop_supported(int dev) {
+  static int v[64] = {0};
+  if (dev < 0 || dev >= 64) return 0;
+  if (v[dev] == 0) {
+    int coop = 0, sms = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    v[dev] = (coop && sms >= kPersist) ? 1 : 2;
+  }
+  return v[dev] == 1;
+}
+
+// Launch pass B of step i as one cooperative kernel; false when the staged path does not apply.
 template <typename VT>
-static bool launch_staged(const CgsArgs& a, bool update, cudaStream_t st) {
-  StagedArgs sa;
-  size_t smem = 0;
-  if (!staged_setup<VT>(a, update, &sa, &smem)) return false;
+static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, int dev, cudaStream_t st, int* rc) {
+  *rc = SLQ_OK;
+  if (!coop_supported(dev)) return false;
+  StepArgs sa{};
+  if (!staged_setup<VT>(a, false, &sa.pass[0]) || !staged_setup<VT>(a, true, &sa.pass[1])) return false;
+  sa.red = red;
+  const size_t smem = 128 + kStages * std::max(static_cast<size_t>(sa.pass[0].nvec) * sa.pass[0].rt,
+                                               static_cast<size_t>(sa.pass[1].nvec) * sa.pass[1].rt) *
+                                a.ldc * sizeof(VT);
   const int threads = 32 + ((static_cast<int>(a.ldc) + 31) / 32) * 32;
-  if (update) {
-    LaunchScope ls(K_CGS_UPDATE, st);
-    cudaFuncSetAttribute(cgs_update_staged<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStagedSmem));
-    cgs_update_staged<VT><<<kPersist, threads, smem, st>>>(sa);
-  } else {
-    LaunchScope ls(K_CGS_DOT, st);
-    cudaFuncSetAttribute(cgs_dot_staged<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStagedSmem));
-    cgs_dot_staged<VT><<<kPersist, threads, smem, st>>>(sa);
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[sizeof(VT) == 8]) {
+    cudaFuncSetAttribute(cgs_step_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kStagedSmem));
+    attr_set[sizeof(VT) == 8] = true;
+  }
+  LaunchScope ls(K_CGS_UPDATE, st);
+  // kPersist = 148 CTAs with > half of an SM's shared memory each: one per SM, all co-resident, so
+  // the software grid barrier is safe (coop_supported() checked the SM count).
+  cgs_step_kernel<VT><<<kPersist, threads, smem, st>>>(sa);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *rc = cuda_fail(e, "cudaLaunchCooperativeKernel(cgs_step_kernel)");
+    return true;
   }
   return true;
 }
@@ -728,75 +929,6 @@ static int launch_cgs_update(CgsArgs a, int max_ctas, cudaStream_t st) {
   return SLQ_OK;
 }
 
-// ----------------------------------------------------------------------------- reductions
-enum ReduceMode { RED_ALPHA = 0, RED_CGS = 1, RED_NORM = 2, RED_NORM2 = 3 };
-
-struct ReduceArgs {
-  const double* partial;   // [ntiles][nq][cpad]
-  int ntiles, nq, cpad, c;
-  int mode;
-  int i, k0, nk, reorth;
-  int second;              // 1: reduction of the conditional second CGS pass
-  double tol;              // breakdown tolerance 1e-12 * interval_hi
-  ChunkState s;
-};
-
-constexpr int kReduceWarps = 16;
-
-// Fixed-order tree over tiles (deterministic; no atomics), then the per-probe scalar logic.
-__global__ void __launch_bounds__(kReduceWarps * 32)
-reduce_kernel(ReduceArgs a) {
-  __shared__ double red[kReduceWarps][32];
-  if (a.second && *a.s.any_again == 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = blockIdx.x;
-  const int p = blockIdx.y * 32 + lane;
-  double s = 0.0;
-  for (int t = warp; t < a.ntiles; t += kReduceWarps)
-    s += a.partial[(static_cast<int64_t>(t) * a.nq + q) * a.cpad + p];
-  red[warp][lane] = s;
-  __syncthreads();
-  if (warp != 0) return;
-  double tot = red[0][lane];
-  for (int j = 1; j < kReduceWarps; ++j) tot += red[j][lane];
-  const int cp = a.cpad;
-  const bool pv = p < a.c;
-  switch (a.mode) {
-    case RED_ALPHA:
-      if (pv && a.s.alive[p]) a.s.alpha[a.i * cp + p] = tot;
-      if (blockIdx.y == 0 && lane == 0) *a.s.any_again = 0;
-      break;
-    case RED_CGS:
-      if (q < a.nk) a.s.h[(a.k0 + q) * cp + p] = tot * a.s.rsc[(a.k0 + q) * cp + p];
-      else if (!a.second) a.s.nb2[p] = tot;
-      break;
-    case RED_NORM:
-    case RED_NORM2: {
-      if (!pv || !a.s.alive[p]) break;
-      const double b = sqrt(tot);
-      if (a.mode == RED_NORM) {
-        if (a.reorth && b < 0.5 * sqrt(a.s.nb2[p])) {    // lanczos.py:75
-          a.s.again[p] = 1;
-          *a.s.any_again = 1;
-          break;
-        }
-      } else {
-        if (!a.s.again[p]) break;
-        a.s.again[p] = 0;
-      }
-      if (b <= a.tol) {                                  // lanczos.py:133-134
-        a.s.steps[p] = a.i + 1;
-        a.s.alive[p] = 0;
-        a.s.rsc[(a.i + 1) * cp + p] = 0.0;
-      } else {
-        a.s.beta[a.i * cp + p] = b;
-        a.s.rsc[(a.i + 1) * cp + p] = __ddiv_rn(1.0, b);
-      }
-      break;
-    }
-  }
-}
-
 static void launch_reduce(ReduceArgs a, cudaStream_t st) {
   dim3 grid(a.nq, a.cpad / 32);
   LaunchScope ls(K_REDUCE, st);
@@ -818,6 +950,22 @@ __global__ void scatter_out_kernel(ChunkState s, int64_t col0, int S, double* al
 }
 
 // ----------------------------------------------------------------------------- engine
+static double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static bool trace_host() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("SLQ_TRACE_HOST"); v = (e && e[0] == '1') ? 1 : 0; }
+  return v == 1;
+}
+#define SLQ_TRACE(label) do { if (trace_host()) fprintf(stderr, "[slq host] %-28s %9.3f ms\n", label, host_ms() - t_host0); } while (0)
+
+static bool env_flag(const char* name, bool dflt) {
+  const char* e = getenv(name);
+  if (!e || !e[0]) return dflt;
+  return e[0] != '0';
+}
+
 static bool staged_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -852,6 +1000,7 @@ template <typename VT>
 static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0, const double* q0, int64_t ldq,
                      int c, int S, int reorth, double* alpha_out, double* beta_out, int32_t* steps_out, int64_t col0,
                      cudaStream_t st) {
+  const double t_host0 = host_ms();
   const int64_t n = g->n;
   const int vb = sizeof(VT);
   // ldc: probes padded to a 32-byte sector multiple
@@ -866,12 +1015,14 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const int nq_max = kCgsBlock + 1;
   const int64_t ptiles = std::max<int64_t>({g->ntiles, g->ntiles_stream, kPersist});
   const size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
-  const size_t bytes_state = sizeof(double) * cpad * (4 * (S + 1) + 2) + sizeof(int) * (3 * cpad + 4);
+  const size_t bytes_state = sizeof(double) * cpad * (4 * (S + 1) + 2) + sizeof(int) * (3 * cpad + 4 + S + 4);
   const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
   const size_t off_state = ((bytes_vec + 255) / 256) * 256;
   const size_t off_part = off_state + ((bytes_state + 255) / 256) * 256;
   char* ws = nullptr;
+  SLQ_TRACE("before malloc");
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_part + bytes_part, st));
+  SLQ_TRACE("after malloc");
   VT* basis = reinterpret_cast<VT*>(ws);
   VT* wv = basis + (S + 1) * vs;
   double* dstate = reinterpret_cast<double*>(ws + off_state);
@@ -887,11 +1038,12 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   s.alive = istate + cpad;
   s.again = istate + 2 * cpad;
   s.any_again = istate + 3 * cpad;
+  s.barrier = reinterpret_cast<unsigned int*>(istate + 3 * cpad + 4);
   double* partial = reinterpret_cast<double*>(ws + off_part);
 
   {
     LaunchScope ls(K_PROBE, st);
-    state_init_kernel<<<ceil_div(cpad, 128), 128, 0, st>>>(s, n, q0 != nullptr);
+    state_init_kernel<<<ceil_div(std::max(cpad, S), 128), 128, 0, st>>>(s, n, q0 != nullptr);
   }
   if (q0) {
     LaunchScope ls(K_PROBE, st);
@@ -916,16 +1068,18 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
 
   const int gx = 1 << 30;                 // one CTA per tile group
   const bool use_staged = staged_enabled();
+  const bool coop = use_staged && coop_supported(g->device);
+  const bool coop_spmm = coop && env_flag("SLQ_COOP_SPMM", false);
   const int gx2 = kSecondPassGrid;        // second pass: small grid-stride launch
 
+  // Non-staged path (s > 17, SLQ_STAGED=0 or no cooperative launch): separate kernels + reductions.
   auto dot_pass = [&](int i, int second, int grid_x) {
     for (int k0 = 0; k0 <= i; k0 += kCgsBlock) {
       ca.k0 = k0;
       ca.nk = std::min(kCgsBlock, i + 1 - k0);
       ca.second = second;
-      const bool staged = use_staged && launch_staged<VT>(ca, false, st);
-      if (!staged) launch_cgs_dot<VT>(ca, grid_x, st);
-      ra.mode = RED_CGS; ra.ntiles = staged ? kPersist : g->ntiles_stream; ra.nq = ca.nk + 1; ra.k0 = k0; ra.nk = ca.nk;
+      launch_cgs_dot<VT>(ca, grid_x, st);
+      ra.mode = RED_CGS; ra.ntiles = g->ntiles_stream; ra.nq = ca.nk + 1; ra.k0 = k0; ra.nk = ca.nk;
       ra.second = second;
       launch_reduce(ra, st);
     }
@@ -934,31 +1088,36 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   for (int i = 0; i < S; ++i) {
     sa.u = basis + i * vs;
     sa.r = s.rsc + i * cpad;
-    launch_spmm<VT>(kind, sa, st);
-    ra.mode = RED_ALPHA; ra.ntiles = g->ntiles; ra.nq = 1; ra.i = i; ra.second = 0;
-    launch_reduce(ra, st);
+    ra.mode = RED_ALPHA; ra.ntiles = g->ntiles; ra.nq = 1; ra.i = i; ra.second = 0; ra.k0 = 0; ra.nk = 0;
+    sa.red = ra;
+    SLQ_TRACE("spmm launch");
+    launch_spmm<VT>(kind, sa, coop_spmm, g->device, st);
+    SLQ_TRACE("spmm launched");
+    if (!coop_spmm) launch_reduce(ra, st);
     if (i == S - 1) break;
     ca.i = i;
-    if (reorth) dot_pass(i, 0, gx);
     ca.second = 0;
-    bool staged_upd = use_staged && launch_staged<VT>(ca, true, st);
-    if (!staged_upd) {
-      rc = launch_cgs_update<VT>(ca, gx, st);
+    bool done = false;
+    if (coop) {
+      done = launch_cgs_step<VT>(ca, ra, g->device, st, &rc);
+      SLQ_TRACE("step launched");
       if (rc) return rc;
     }
-    ra.mode = RED_NORM; ra.ntiles = staged_upd ? kPersist : g->ntiles_stream; ra.nq = 1; ra.second = 0;
+    if (done) continue;
+    if (reorth) dot_pass(i, 0, gx);
+    ca.second = 0;
+    rc = launch_cgs_update<VT>(ca, gx, st);
+    if (rc) return rc;
+    ra.mode = RED_NORM; ra.ntiles = g->ntiles_stream; ra.nq = 1; ra.second = 0;
     launch_reduce(ra, st);
     if (reorth) {
       // conditional second CGS pass (lanczos.py:75-76); kernels exit unless a probe asked for it
       dot_pass(i, 1, gx2);
       ca.second = 1;
-      staged_upd = use_staged && launch_staged<VT>(ca, true, st);
-      if (!staged_upd) {
-        rc = launch_cgs_update<VT>(ca, gx2, st);
-        if (rc) return rc;
-      }
+      rc = launch_cgs_update<VT>(ca, gx2, st);
+      if (rc) return rc;
       ca.second = 0;
-      ra.mode = RED_NORM2; ra.ntiles = staged_upd ? kPersist : g->ntiles_stream; ra.nq = 1; ra.second = 1;
+      ra.mode = RED_NORM2; ra.ntiles = g->ntiles_stream; ra.nq = 1; ra.second = 1;
       launch_reduce(ra, st);
       ra.second = 0;
     }
@@ -969,6 +1128,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   }
   SLQ_CUDA(cudaGetLastError());
   SLQ_CUDA(cudaFreeAsync(ws, st));
+  SLQ_TRACE("chunk done");
   return SLQ_OK;
 }
 
@@ -996,7 +1156,9 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ensure_pool(g->device);
   const int vb = dtype == SLQ_F64 ? 8 : 4;
+  const double t_host0 = host_ms();
   const int cmax = choose_chunk(g, count, S, vb);
+  SLQ_TRACE("choose_chunk");
   for (int64_t done = 0; done < count;) {
     const int c = static_cast<int>(std::min<int64_t>(cmax, count - done));
     const double* qc = q0 ? q0 + done : nullptr;
@@ -1039,7 +1201,7 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
   sa.scale = kind == SLQ_DENSITY ? 1.0 / g->trace_l : 0.0;
   sa.u = x; sa.r = nullptr; sa.w = y; sa.ldc_in = ld; sa.ldc_out = ld;
   sa.c = static_cast<int>(ncols); sa.cpad = ceil_div(ncols, 32) * 32; sa.partial = nullptr;
-  launch_spmm<double>(kind, sa, st);
+  launch_spmm<double>(kind, sa, false, g->device, st);
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
 }

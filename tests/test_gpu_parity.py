@@ -307,3 +307,32 @@ def test_c2_sbm100k_heat_wave_vs_oracle(cuda_device):
     # t -> 0 limit: every rule integrates 1, so h_t -> n (a size-independent check)
     assert abs(heat.values[0] - g.n) / g.n < 0.03
     assert np.all(np.isfinite(wave.values))
+
+
+def test_long_runs_use_fallback_kernels_and_match_oracle(cuda_device):
+    # s = 24 > 17: CGS blocks beyond 16 basis vectors take the non-staged kernels
+    z = golden.load("sbm5k.npz")
+    g = golden.graph(z)
+    ref, _ = O.heat_trace(g, GRID.values, 6, 24, 0)
+    h = netlsd_slq(g, GRID, SlqConfig(n_v=6, s=24, seed=0))
+    assert golden.rel_l2(h.values, ref) <= FP64_TOL
+    ref_v, _ = O.vnge(g, 6, 24, 0)
+    assert abs(vnge_slq(g, SlqConfig(n_v=6, s=24, seed=0)).value - ref_v) <= FP64_TOL * abs(ref_v)
+
+
+def test_flat_kernels_match_staged(cuda_device):
+    # the non-staged streaming kernels (SLQ_STAGED=0) give the same rules within fp64 rounding
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests'); import numpy as np, golden; "
+            "from paper_2003_01282_b200.device import DeviceGraph; "
+            "g = golden.graph(golden.load('rmat12.npz')); r = DeviceGraph(g).rules('density', 0, 0, 16, 15); "
+            "np.save('/tmp/slq_flat_nodes.npy', r.nodes.cpu().numpy())")
+    env = dict(__import__('os').environ, SLQ_STAGED="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env,
+                   cwd=__import__('os').path.dirname(__import__('os').path.dirname(__file__)))
+    flat = np.load("/tmp/slq_flat_nodes.npy")
+    g = golden.graph(golden.load("rmat12.npz"))
+    staged = DeviceGraph(g, cuda_device).rules("density", 0, 0, 16, 15).nodes.cpu().numpy()
+    assert np.max(np.abs(flat - staged)) <= 1e-14
