@@ -177,7 +177,7 @@ def run_ours(args):
 
     from paper_2003_01282_b200 import _lib
     from paper_2003_01282_b200.descriptors import TimeGrid, netlsd_heat_wave_slq
-    from paper_2003_01282_b200.device import DeviceGraph, gauss_rules
+    from paper_2003_01282_b200.device import DeviceGraph
     from paper_2003_01282_b200.dist import gather_rules_arrays
     from paper_2003_01282_b200.graphs import Graph
     from paper_2003_01282_b200.slq import SlqConfig
@@ -199,27 +199,28 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    fns = [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM]
+
     def step():
-        # device-resident input: prepare + probes + Lanczos + rules + quadrature + aggregate
-        dg = DeviceGraph.__new__(DeviceGraph)
+        # device-resident input: prepare + probes + Lanczos + rules + quadrature + aggregate (no host sync)
         import ctypes
 
-        dg.device, dg.graph, dg.n = dev, g, g.n
+        dg = DeviceGraph.__new__(DeviceGraph)
+        dg.device, dg.graph, dg.n, dg._info = dev, g, g.n, None
         dg.handle = ctypes.c_void_p()
         _lib.check(_lib.load().slq_graph_create(g.n, g.nnz, off_d.data_ptr(), cols_d.data_ptr(), None,
                                                 stream.cuda_stream, ctypes.byref(dg.handle)))
         rules = dg.rules("normalized_laplacian", 0, rank * n_v, n_v, s, dtype=dtype)
         if world > 1:
             nodes, weights, steps = gather_rules_arrays(rules.nodes, rules.weights, rules.steps, total_probes)
-            rules = type(rules)(nodes, weights, steps, g.n)
-        out = []
-        for fn in (_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM):
-            out.append(rules.estimate(rules.quadrature(tgrid, fn)))
+            rules = type(rules)(nodes, weights, steps, g.n, status=rules.status)
+        out = rules.integrate(tgrid, fns)
         del dg
-        return out
+        return out, rules.status
 
     for _ in range(args.warmup):
-        step()
+        _, status = step()
+    _lib.check_status(int(status.item()))   # the device reported no error on the warm-up steps
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

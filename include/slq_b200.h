@@ -76,7 +76,10 @@ typedef struct slq_graph_info_t {
 
 /* Build the device graph from DEVICE CSR arrays (canonical layout of graphs.py:110-132):
  * int64 offsets[n+1], int64 cols[nnz] (sorted per row), float64 weights[nnz] or NULL
- * (NULL = every weight 1.0).  The arrays are copied/narrowed; the caller keeps ownership. */
+ * (NULL = every weight 1.0).  The arrays are copied/narrowed; the caller keeps ownership.
+ * Stream-ordered and asynchronous: input errors (out-of-range columns) surface in
+ * slq_graph_info() and in the status word of the asynchronous calls.  `stream` must outlive
+ * the graph (its buffers are freed on it). */
 int slq_graph_create(int64_t n, int64_t nnz, const int64_t* offsets, const int64_t* cols,
                      const double* weights, void* stream, slq_graph** out);
 /* Same from HOST arrays (the end-to-end plugin entry: H2D copies happen inside). */
@@ -129,6 +132,28 @@ int slq_quadrature(const double* nodes, const double* weights, const int32_t* st
 /* value[t] = n * mean_p per_vector[t][p]; std_error[t] = std(n*pv, ddof=1)/sqrt(count). */
 int slq_estimate(const double* per_vector, int64_t T, int64_t count, double n, double* value,
                  double* std_error, void* stream);
+
+/* ---- asynchronous composite entry points (no host synchronisation; errors are OR-ed into a
+ * device int32 *status: 1 eigensolver failed, 2 non-finite tridiagonal, 4 non-finite integrand,
+ * 8 out-of-range column index).  The caller reads *status with the results. ---- */
+
+/* Gauss rules of probes [probe_begin, +count): slq_lanczos + slq_gauss_rules with the operator's
+ * clamp interval taken from the device graph scalars.  nodes/weights [count][s'], s' = min(steps, n). */
+int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
+              int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
+              void* stream);
+
+/* For each integrand fns_host[f] (host array of SLQ_FN_*): quadrature over t[T] and the probe
+ * aggregate: values[f][T], std_errors[f][T]; per_vector[f][T][count] if not NULL (slq.py:89-105). */
+int slq_integrate(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,
+                  const double* t, int64_t T, const int* fns_host, int nfn, double n, double* values,
+                  double* std_errors, double* per_vector, int32_t* status, void* stream);
+
+/* The whole signature (netlsd_slq / vnge_slq / wave): rules of probes 0..count-1, then every
+ * integrand over the grid.  values/std_errors [nfn][T] on the device.  descriptors.py:124-149, 227-243. */
+int slq_signature(const slq_graph* g, int kind, uint64_t seed, int64_t count, int steps, int reorth,
+                  int dtype, const double* t, int64_t T, const int* fns_host, int nfn, double* values,
+                  double* std_errors, int32_t* status, void* stream);
 
 /* Rademacher probes as +-1.0 into out[n][ld] (column j = probe probe_begin+j). */
 int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int64_t n, double* out,

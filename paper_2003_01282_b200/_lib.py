@@ -50,6 +50,9 @@ _SIGS = {
     "slq_estimate": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp]),
     "slq_probes": (_int, [_u64, _i64, _i64, _i64, _vp, _i64, _vp]),
     "slq_probe_state": (_int, [_u64, _u64, ctypes.POINTER(_u64)]),
+    "slq_rules": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "slq_integrate": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _dbl, _vp, _vp, _vp, _vp, _vp]),
+    "slq_signature": (_int, [_vp, _int, _u64, _i64, _int, _int, _int, _vp, _i64, _vp, _int, _vp, _vp, _vp, _vp]),
     "slq_lanczos_batched": (_int, [_vp, _vp, _i64, _int, _u64, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "slq_last_error": (ctypes.c_char_p, []),
     "slq_launch_count": (_u64, []),
@@ -94,6 +97,30 @@ def check(rc: int, alpha=None, beta=None) -> None:
     if rc == SLQ_ERR_ALLOC:
         raise MemoryError(msg)
     raise SlqLibraryError(msg)
+
+
+ST_EIGEN, ST_NAN_TRI, ST_NAN_F, ST_BAD_COL = 1, 2, 4, 8
+
+
+def check_status(status: int, alpha=None, beta=None) -> None:
+    """Raise the reference's exception for a device status word of the asynchronous calls."""
+    status = int(status)
+    if status == 0:
+        return
+    if status & ST_BAD_COL:
+        raise ValueError("column index out of range [0, n)")
+    if status & ST_NAN_TRI:
+        raise ValueError("array must not contain infs or NaNs")
+    if status & ST_EIGEN:
+        raise TridiagonalEigenError("tridiagonal eigensolver failed: no convergence", alpha=alpha, beta=beta)
+    if status & ST_NAN_F:
+        raise ValueError("f returned a non-finite value at quadrature nodes")
+    raise SlqLibraryError(f"unknown device status {status}")
+
+
+def int_array(values) -> ctypes.Array:
+    arr = (ctypes.c_int * len(values))(*[int(v) for v in values])
+    return arr
 
 
 def ptr(t) -> int | None:

@@ -23,8 +23,9 @@ __global__ void narrow_cols_kernel(const int64_t* __restrict__ cols, int32_t* __
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = cols[i];
-    if (c < 0 || c >= n) *bad = 1;
-    out[i] = static_cast<int32_t>(c);
+    const bool ok = c >= 0 && c < n;
+    if (!ok) *bad = 1;
+    out[i] = ok ? static_cast<int32_t>(c) : 0;   // clamped: no out-of-range gather ever happens
   }
 }
 
@@ -87,6 +88,8 @@ __global__ void degree_stats_final(const double* psum, const double* pmax, const
     long long iso = 0;
     for (int i = 0; i < nb; ++i) { s += psum[i]; mx = fmax(mx, pmax[i]); iso += piso[i]; }
     out3[0] = s; out3[1] = mx; out3[2] = static_cast<double>(iso);
+    out3[3] = s > 0.0 ? 1.0 / s : 0.0;    // density scale 1/tr L (operators.py:96)
+    out3[4] = 2.0 * mx;                   // Laplacian interval hi (operators.py:79)
   }
 }
 
@@ -117,6 +120,8 @@ static void* track(slq_graph* g, void* p) {
 
 static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols, const double* weights,
                        cudaStream_t st) {
+  // Fully stream-ordered: no host synchronisation.  Scalars stay on the device (g->dscal); the host
+  // mirror is fetched lazily by fetch_host_scalars() (slq_graph_info, Laplacian interval).
   const int64_t n = g->n, nnz = g->nnz;
   void* p = nullptr;
   SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), st));
@@ -129,37 +134,28 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   track(g, p);
   g->degree = static_cast<double*>(p);
   g->dinv = g->degree + std::max<int64_t>(n, 1);
-  int* flags = nullptr;   // [0] bad column, [1] non-unit weight
-  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), 2 * sizeof(int), st));
-  SLQ_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
-
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * 8 + sizeof(int) * 4, st));
+  track(g, p);
+  g->dscal = static_cast<double*>(p);
+  g->dflags = reinterpret_cast<int*>(g->dscal + 8);
+  SLQ_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * 8 + sizeof(int) * 4, st));
   if (nnz > 0) {
-    {
-      LaunchScope ls(K_PREPARE, st);
-      narrow_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, const_cast<int32_t*>(g->cols), nnz, n, flags);
-    }
-    if (weights) {
-      LaunchScope ls(K_PREPARE, st);
-      unit_weight_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(weights, nnz, flags + 1);
-    }
+    LaunchScope ls(K_PREPARE, st);
+    narrow_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, const_cast<int32_t*>(g->cols), nnz, n, g->dflags);
   }
-  int hflags[2] = {0, 0};
-  SLQ_CUDA(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-  SLQ_CUDA(cudaStreamSynchronize(st));
-  SLQ_CUDA(cudaFreeAsync(flags, st));
-  if (hflags[0]) return fail(SLQ_ERR_VALUE, "column index out of range [0, n)");
-  g->unit_weights = hflags[1] ? 0 : 1;
-  if (!g->unit_weights) {
+  if (weights && nnz > 0) {
+    // explicit weights are kept even if all are 1.0 (w * t == t exactly, so results are identical)
     SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * nnz, st));
     g->weights = static_cast<double*>(track(g, p));
-    SLQ_CUDA(cudaMemcpyAsync(const_cast<double*>(g->weights), weights, sizeof(double) * nnz,
-                             cudaMemcpyDefault, st));
+    SLQ_CUDA(cudaMemcpyAsync(const_cast<double*>(g->weights), weights, sizeof(double) * nnz, cudaMemcpyDefault, st));
+    LaunchScope ls(K_PREPARE, st);
+    unit_weight_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(g->weights, nnz, g->dflags + 1);
   }
   if (n > 0) {
     LaunchScope ls(K_PREPARE, st);
     degree_kernel<<<grid_for(n, 256), 256, 0, st>>>(g->offsets, g->weights, n, g->degree, g->dinv);
   }
-  // degree statistics
+  // degree statistics -> dscal
   const int64_t per_block = std::max<int64_t>(4096, (n + 1023) / 1024);
   const int nb = std::max(1, ceil_div(n, per_block));
   double* scratch = nullptr;
@@ -172,12 +168,9 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
     }
     LaunchScope ls(K_PREPARE, st);
     degree_stats_final<<<1, 32, 0, st>>>(scratch, scratch + nb, reinterpret_cast<long long*>(scratch + 2 * nb),
-                                         nb, scratch + 3 * nb);
-  } else {
-    SLQ_CUDA(cudaMemsetAsync(scratch + 3 * nb, 0, 3 * sizeof(double), st));
+                                         nb, g->dscal);
   }
-  double stats[3];
-  SLQ_CUDA(cudaMemcpyAsync(stats, scratch + 3 * nb, sizeof(stats), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaFreeAsync(scratch, st));
   // tiles
   const int64_t total = nnz + kRowCost * n;
   int64_t target = std::max<int64_t>(kMinTileCost, (total + kMaxTiles - 1) / kMaxTiles);
@@ -190,13 +183,26 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   }
   g->rows_per_stream_tile = std::max<int64_t>(kMinStreamRows, (n + kMaxTiles - 1) / kMaxTiles);
   g->ntiles_stream = std::max(1, ceil_div(n, g->rows_per_stream_tile));
-  SLQ_CUDA(cudaGetLastError());
-  SLQ_CUDA(cudaStreamSynchronize(st));
-  SLQ_CUDA(cudaFreeAsync(scratch, st));
-  g->trace_l = stats[0];
-  g->max_degree = stats[1];
-  g->isolated = static_cast<int64_t>(stats[2]);
   g->m = nnz / 2;
+  SLQ_CUDA(cudaGetLastError());
+  return SLQ_OK;
+}
+
+// Host mirror of the device scalars (synchronises the creation stream once).
+int fetch_host_scalars(slq_graph* g) {
+  if (g->host_valid) return SLQ_OK;
+  double sc[8];
+  int fl[4];
+  cudaStream_t st = static_cast<cudaStream_t>(g->stream);
+  SLQ_CUDA(cudaMemcpyAsync(sc, g->dscal, sizeof(sc), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaMemcpyAsync(fl, g->dflags, sizeof(fl), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  g->trace_l = sc[0];
+  g->max_degree = sc[1];
+  g->isolated = static_cast<int64_t>(sc[2]);
+  g->bad_columns = fl[0];
+  g->unit_weights = fl[1] ? 0 : 1;
+  g->host_valid = 1;
   return SLQ_OK;
 }
 
@@ -251,6 +257,9 @@ extern "C" int slq_graph_create_host(int64_t n, int64_t nnz, const int64_t* offs
 
 extern "C" int slq_graph_info(const slq_graph* g, slq_graph_info_t* out) {
   if (!g || !out) return fail(SLQ_ERR_VALUE, "NULL argument");
+  int rc = fetch_host_scalars(const_cast<slq_graph*>(g));
+  if (rc) return rc;
+  if (g->bad_columns) return fail(SLQ_ERR_VALUE, "column index out of range [0, n)");
   out->n = g->n;
   out->nnz = g->nnz;
   out->trace_l = g->trace_l;
@@ -272,10 +281,16 @@ extern "C" int slq_operator_interval(const slq_graph* g, int kind, double* lo, d
   if (!g || !lo || !hi) return fail(SLQ_ERR_VALUE, "NULL argument");
   *lo = 0.0;
   switch (kind) {
-    case SLQ_LAPLACIAN: *hi = 2.0 * g->max_degree; return SLQ_OK;
+    case SLQ_LAPLACIAN: {
+      int rc = fetch_host_scalars(const_cast<slq_graph*>(g));
+      if (rc) return rc;
+      *hi = 2.0 * g->max_degree;
+      return SLQ_OK;
+    }
     case SLQ_NORMALIZED_LAPLACIAN: *hi = 2.0; return SLQ_OK;
     case SLQ_DENSITY:
-      if (g->nnz == 0 || g->trace_l <= 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
+      // weights are strictly positive, so tr L > 0 exactly when there is an edge
+      if (g->nnz == 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
       *hi = 1.0;
       return SLQ_OK;
   }

@@ -122,7 +122,8 @@ struct ReduceArgs {
   int mode;
   int i, k0, nk, reorth;
   int second;              // 1: reduction of the conditional second CGS pass
-  double tol;              // breakdown tolerance 1e-12 * interval_hi
+  int kind;                // operator kind: breakdown tolerance 1e-12 * interval_hi (lanczos.py:36,110)
+  const double* dscal;     // device graph scalars (Laplacian interval_hi = dscal[4])
   ChunkState s;
 };
 
@@ -157,7 +158,8 @@ __device__ void apply_reduced(const ReduceArgs& a, int q, int p, double tot, boo
         if (!a.s.again[p]) break;
         a.s.again[p] = 0;
       }
-      if (b <= a.tol) {                                  // lanczos.py:133-134
+      const double hi = a.kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (a.kind == SLQ_DENSITY ? 1.0 : a.dscal[4]);
+      if (b <= 1e-12 * hi) {                             // lanczos.py:133-134
         a.s.steps[p] = a.i + 1;
         a.s.alive[p] = 0;
         a.s.rsc[(a.i + 1) * cp + p] = 0.0;
@@ -225,7 +227,7 @@ struct SpmmArgs {
   const double* dinv;
   const int64_t* tile_rows;
   int ntiles;
-  double scale;            // density: 1/trL
+  const double* dscal;     // device graph scalars; density scale 1/tr L = dscal[3]
   const void* u;           // [n][ldc] input (unnormalised)
   const double* r;         // [cpad] per-probe scale (nullptr = 1.0)
   void* w;                 // [n][ldc] output
@@ -279,6 +281,7 @@ spmm_kernel(SpmmArgs a) {
   const double* __restrict__ dinv = a.dinv;
   const double* __restrict__ wts = a.weights;
   const int64_t ldi = a.ldc_in;
+  const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
 
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int64_t rb = a.tile_rows[tile], re = a.tile_rows[tile + 1];
@@ -334,7 +337,7 @@ spmm_kernel(SpmmArgs a) {
       for (int j = 0; j < PPL; ++j) {
         if (!pv[j]) continue;
         const double x = __dmul_rn(ldg_f64(u + row * ldi + 32 * j), r[j]);
-        const double y = op_epilogue<KIND>(x, acc[j], d, dis, a.scale);
+        const double y = op_epilogue<KIND>(x, acc[j], d, dis, scale);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
         dot[j] = fma(x, y, dot[j]);
       }
@@ -1007,10 +1010,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const int64_t ldc = ((c * vb + 31) / 32) * 32 / vb;
   const int cpad = ceil_div(c, 32) * 32;
   const int64_t vs = n * ldc;
-  double lo = 0, hi = 0;
-  int rc = slq_operator_interval(g, kind, &lo, &hi);
-  if (rc) return rc;
-  const double tol = 1e-12 * hi;                           // lanczos.py:36,109-110
+  int rc = SLQ_OK;
 
   const int nq_max = kCgsBlock + 1;
   const int64_t ptiles = std::max<int64_t>({g->ntiles, g->ntiles_stream, kPersist});
@@ -1055,7 +1055,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   SpmmArgs sa{};
   sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
-  sa.scale = kind == SLQ_DENSITY ? 1.0 / g->trace_l : 0.0;
+  sa.dscal = g->dscal;
   sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad; sa.partial = partial;
 
   CgsArgs ca{};
@@ -1064,7 +1064,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   ca.partial = partial; ca.reorth = reorth;
 
   ReduceArgs ra{};
-  ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.tol = tol; ra.reorth = reorth;
+  ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.kind = kind; ra.dscal = g->dscal; ra.reorth = reorth;
 
   const int gx = 1 << 30;                 // one CTA per tile group
   const bool use_staged = staged_enabled();
@@ -1145,9 +1145,8 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   if (kind < 0 || kind > 2) return fail(SLQ_ERR_VALUE, "unknown operator kind");
   if (dtype != SLQ_F64 && dtype != SLQ_F32) return fail(SLQ_ERR_VALUE, "dtype must be SLQ_F64 or SLQ_F32");
   if (g->n == 0) return fail(SLQ_ERR_VALUE, "start vector must have unit norm");
-  double lo, hi;
-  int rc = slq_operator_interval(g, kind, &lo, &hi);
-  if (rc) return rc;
+  if (kind == SLQ_DENSITY && g->nnz == 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
+  int rc = SLQ_OK;
   const int S = static_cast<int>(std::min<int64_t>(steps, g->n));   // lanczos.py:105
   if (S > kMaxSteps) return fail(SLQ_ERR_VALUE, "steps > 128 not supported");
   if (reorth < 0) reorth = S <= 100 ? 1 : 0;                          // lanczos.py:106-107
@@ -1189,16 +1188,14 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
                                   int64_t ld, void* stream) {
   if (!g || (!x && g->n) || (!y && g->n)) return fail(SLQ_ERR_VALUE, "NULL argument");
   if (kind < 0 || kind > 2) return fail(SLQ_ERR_VALUE, "unknown operator kind");
-  double lo, hi;
-  int rc = slq_operator_interval(g, kind, &lo, &hi);
-  if (rc) return rc;
+  if (kind == SLQ_DENSITY && g->nnz == 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
   if (ncols <= 0 || g->n == 0) return SLQ_OK;
   if (ld < ncols) return fail(SLQ_ERR_VALUE, "ld < ncols");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SpmmArgs sa{};
   sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
-  sa.scale = kind == SLQ_DENSITY ? 1.0 / g->trace_l : 0.0;
+  sa.dscal = g->dscal;
   sa.u = x; sa.r = nullptr; sa.w = y; sa.ldc_in = ld; sa.ldc_out = ld;
   sa.c = static_cast<int>(ncols); sa.cpad = ceil_div(ncols, 32) * 32; sa.partial = nullptr;
   launch_spmm<double>(kind, sa, false, g->device, st);

@@ -6,6 +6,7 @@
 //   slq_quadrature   <- _apply_rule over the whole t grid (slq.py:89-95, 153-168)
 //   slq_estimate     <- _estimate_from (slq.py:98-105)
 #include <cfloat>
+#include <algorithm>
 #include <cmath>
 
 #include "slq_common.cuh"
@@ -62,12 +63,20 @@ __device__ int tridiag_ql_first_row(double* d, double* e, double* z, int m) {
   return 0;
 }
 
+// status bits (device int, OR-ed): 1 eigensolver failed, 2 non-finite tridiagonal, 4 non-finite integrand,
+// 8 out-of-range column index in the graph.
+constexpr int kStEigen = 1, kStNanTri = 2, kStNanF = 4, kStBadCol = 8;
+
+// hi_kind >= 0: the clamp interval comes from the device graph scalars (no host round trip).
 __global__ void gauss_rules_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
                                    const int32_t* __restrict__ steps, int64_t count, int ld, double lo,
                                    double hi, double* __restrict__ nodes, double* __restrict__ weights,
-                                   int32_t* __restrict__ info, int* __restrict__ status) {
+                                   int32_t* __restrict__ info, int* __restrict__ status, const double* dscal,
+                                   int hi_kind, const int* gflags) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p == 0 && gflags && gflags[0]) atomicOr(status, kStBadCol);
   if (p >= count) return;
+  if (hi_kind >= 0) hi = hi_kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (hi_kind == SLQ_DENSITY ? 1.0 : dscal[4]);
   double d[kMaxSteps], e[kMaxSteps], z[kMaxSteps];
   const int m = steps[p];
   const double* a = alpha + p * ld;
@@ -82,9 +91,9 @@ __global__ void gauss_rules_kernel(const double* __restrict__ alpha, const doubl
   int rc = 0;
   if (!finite) rc = -1;                       // scipy check_finite -> ValueError
   else rc = tridiag_ql_first_row(d, e, z, m);
-  info[p] = rc;
+  if (info) info[p] = rc;
   if (rc) {
-    atomicMax(status, rc < 0 ? 2 : 1);
+    atomicOr(status, rc < 0 ? kStNanTri : kStEigen);
     for (int k = 0; k < ld; ++k) { nodes[p * ld + k] = 0.0; weights[p * ld + k] = 0.0; }
     return;
   }
@@ -130,7 +139,7 @@ __global__ void quadrature_kernel(const double* __restrict__ nodes, const double
       ok = ok && isfinite(f);
       acc = fma(weights[p * ld + k], f, acc);
     }
-    if (!ok) *nonfinite = 1;
+    if (!ok) atomicOr(nonfinite, kStNanF);
     pv[ti * count + p] = acc;
   }
 }
@@ -172,15 +181,15 @@ extern "C" int slq_gauss_rules(const double* alpha, const double* beta, const in
   {
     LaunchScope ls(K_EIG, st);
     gauss_rules_kernel<<<ceil_div(count, 64), 64, 0, st>>>(alpha, beta, steps, count, ld, lo, hi, nodes, weights,
-                                                             info, status);
+                                                             info, status, nullptr, -1, nullptr);
   }
   int h = 0;
   SLQ_CUDA(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
   SLQ_CUDA(cudaStreamSynchronize(st));
   cudaFreeAsync(status, st);
   SLQ_CUDA(cudaGetLastError());
-  if (h == 2) return fail(SLQ_ERR_VALUE, "array must not contain infs or NaNs");
-  if (h == 1) return fail(SLQ_ERR_EIGEN, "tridiagonal eigensolver failed: no convergence");
+  if (h & kStNanTri) return fail(SLQ_ERR_VALUE, "array must not contain infs or NaNs");
+  if (h & kStEigen) return fail(SLQ_ERR_EIGEN, "tridiagonal eigensolver failed: no convergence");
   return SLQ_OK;
 }
 
@@ -225,4 +234,80 @@ extern "C" int slq_estimate(const double* per_vector, int64_t T, int64_t count, 
   }
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
+}
+
+// ------------------------------------------------------------------ asynchronous composite entry points
+static void launch_quadrature(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,
+                              const double* t, int64_t T, int fn, double* pv, int* status, cudaStream_t st) {
+  const int64_t total = T * count;
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  LaunchScope ls(K_QUAD, st);
+  switch (fn) {
+    case SLQ_FN_HEAT: quadrature_kernel<SLQ_FN_HEAT><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
+    case SLQ_FN_WAVE_RE: quadrature_kernel<SLQ_FN_WAVE_RE><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
+    case SLQ_FN_WAVE_IM: quadrature_kernel<SLQ_FN_WAVE_IM><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
+    case SLQ_FN_XLOGX: quadrature_kernel<SLQ_FN_XLOGX><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
+    default: quadrature_kernel<SLQ_FN_IDENTITY><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
+  }
+}
+
+extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
+                         int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
+                         void* stream) {
+  if (!g || !status) return fail(SLQ_ERR_VALUE, "NULL argument");
+  if (count == 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int S = static_cast<int>(std::min<int64_t>(steps, std::max<int64_t>(g->n, 1)));
+  double* ab = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ab), sizeof(double) * 2 * count * S, st));
+  int rc = slq_lanczos(g, kind, seed, probe_begin, count, steps, reorth, dtype, ab, ab + count * S, steps_out, stream);
+  if (rc == SLQ_OK) {
+    LaunchScope ls(K_EIG, st);
+    gauss_rules_kernel<<<ceil_div(count, 64), 64, 0, st>>>(ab, ab + count * S, steps_out, count, S, 0.0, 0.0, nodes,
+                                                             weights, nullptr, status, g->dscal, kind, g->dflags);
+  }
+  cudaFreeAsync(ab, st);
+  if (rc) return rc;
+  SLQ_CUDA(cudaGetLastError());
+  return SLQ_OK;
+}
+
+extern "C" int slq_integrate(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,
+                             const double* t, int64_t T, const int* fns_host, int nfn, double n, double* values,
+                             double* std_errors, double* per_vector, int32_t* status, void* stream) {
+  if (count < 1 || T < 0 || nfn < 0 || !status) return fail(SLQ_ERR_VALUE, "bad integrate arguments");
+  if (T == 0 || nfn == 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* pv = per_vector;
+  if (!pv) SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pv), sizeof(double) * nfn * T * count, st));
+  for (int f = 0; f < nfn; ++f) {
+    double* pvf = pv + static_cast<int64_t>(f) * T * count;
+    launch_quadrature(nodes, weights, steps, count, ld, t, T, fns_host[f], pvf, status, st);
+    LaunchScope ls(K_ESTIMATE, st);
+    estimate_kernel<<<ceil_div(T, 128), 128, 0, st>>>(pvf, T, count, n, values + static_cast<int64_t>(f) * T,
+                                                      std_errors + static_cast<int64_t>(f) * T);
+  }
+  if (!per_vector) cudaFreeAsync(pv, st);
+  SLQ_CUDA(cudaGetLastError());
+  return SLQ_OK;
+}
+
+extern "C" int slq_signature(const slq_graph* g, int kind, uint64_t seed, int64_t count, int steps, int reorth,
+                             int dtype, const double* t, int64_t T, const int* fns_host, int nfn, double* values,
+                             double* std_errors, int32_t* status, void* stream) {
+  if (!g || !status) return fail(SLQ_ERR_VALUE, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int S = static_cast<int>(std::min<int64_t>(steps, std::max<int64_t>(g->n, 1)));
+  char* buf = nullptr;
+  const size_t bn = sizeof(double) * count * S;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * bn + sizeof(int32_t) * count + 16, st));
+  double* nodes = reinterpret_cast<double*>(buf);
+  double* weights = nodes + count * S;
+  int32_t* stp = reinterpret_cast<int32_t*>(buf + 2 * bn);
+  int rc = slq_rules(g, kind, seed, 0, count, steps, reorth, dtype, nodes, weights, stp, status, stream);
+  if (rc == SLQ_OK)
+    rc = slq_integrate(nodes, weights, stp, count, S, t, T, fns_host, nfn, static_cast<double>(g->n), values,
+                       std_errors, nullptr, status, stream);
+  cudaFreeAsync(buf, st);
+  return rc;
 }

@@ -41,6 +41,10 @@ enum KernelClass {
 };
 
 void ensure_pool(int dev);   // keep the stream-ordered allocator's memory cached
+}  // namespace slq
+struct slq_graph;
+namespace slq {
+int fetch_host_scalars(slq_graph* g);
 
 void launch_begin(KernelClass k, cudaStream_t s);
 void launch_end(KernelClass k, cudaStream_t s);
@@ -84,7 +88,12 @@ struct slq_graph {
   // streaming tiles (pass B): contiguous equal row ranges
   int ntiles_stream = 0;
   int64_t rows_per_stream_tile = 0;
-  // host copies of the scalars
+  // device scalars: [0] tr L, [1] max degree, [2] #isolated, [3] 1/tr L, [4] 2*max degree
+  double* dscal = nullptr;
+  int* dflags = nullptr;    // [0] out-of-range column seen, [1] a weight != 1.0
+  // host copies of the scalars (filled lazily by fetch_host_scalars)
+  int host_valid = 0;
+  int bad_columns = 0;
   double trace_l = 0.0;     // sum of degrees (tr L)
   double max_degree = 0.0;
   int64_t isolated = 0;

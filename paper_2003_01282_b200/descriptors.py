@@ -86,10 +86,16 @@ def _params(cfg: SlqConfig) -> dict:
     return {"n_v": cfg.n_v, "s": cfg.s, "distribution": cfg.distribution, "seed": cfg.seed}
 
 
-def _grid_estimates(rules, t: np.ndarray, code: int):
-    pv = rules.quadrature(t, code)
-    val, std = rules.estimate(pv)
-    return val.cpu().numpy(), std.cpu().numpy()
+def _integrate_host(rules, t, codes):
+    """Device quadrature + aggregate for every integrand, ONE device->host copy, then the status check."""
+    import torch
+
+    vals, stds = rules.integrate(t, codes)
+    packed = torch.cat([vals.reshape(-1), stds.reshape(-1), rules.status.to(torch.float64)]).cpu().numpy()
+    _lib.check_status(int(packed[-1]))
+    k = vals.numel()
+    shape = tuple(vals.shape)
+    return packed[:k].reshape(shape), packed[k:2 * k].reshape(shape)
 
 
 def _hash(g: Graph, with_hash: bool) -> str:
@@ -106,16 +112,15 @@ def netlsd_heat_wave_slq(g: Graph, grid: TimeGrid | None = None, cfg: SlqConfig 
     op = make_operator(g, OperatorKind.NORMALIZED_LAPLACIAN)
     rules = slq_rules(op, cfg, dtype=dtype, shard=shard)
     t = np.asarray(grid.values, dtype=np.float64)
-    hv, hs = _grid_estimates(rules, t, _lib.FN_HEAT)
+    codes = [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM] if wave else [_lib.FN_HEAT]
+    vals, stds = _integrate_host(rules, t, codes)
     gh = _hash(g, with_hash)
-    heat = HeatTraceDescriptor(grid=grid, values=hv, method="slq", params=_params(cfg), graph_hash=gh,
-                               std_errors=hs)
+    heat = HeatTraceDescriptor(grid=grid, values=vals[0], method="slq", params=_params(cfg), graph_hash=gh,
+                               std_errors=stds[0])
     if not wave:
         return heat, None
-    rv, rs = _grid_estimates(rules, t, _lib.FN_WAVE_RE)
-    iv, is_ = _grid_estimates(rules, t, _lib.FN_WAVE_IM)
-    wav = WaveTraceDescriptor(grid=grid, values=rv + 1j * iv, method="slq", params=_params(cfg), graph_hash=gh,
-                              std_errors=rs + 1j * is_)
+    wav = WaveTraceDescriptor(grid=grid, values=vals[1] + 1j * vals[2], method="slq", params=_params(cfg),
+                              graph_hash=gh, std_errors=stds[1] + 1j * stds[2])
     return heat, wav
 
 
@@ -138,9 +143,9 @@ def vnge_slq(g: Graph, cfg: SlqConfig | None = None, *, threads: int = 1, dtype:
     cfg = cfg or SlqConfig()
     op = make_operator(g, OperatorKind.DENSITY)
     rules = slq_rules(op, cfg, dtype=dtype, shard=shard)
-    val, std = _grid_estimates(rules, None, _lib.FN_XLOGX)
-    return EntropyValue(value=-float(val[0]), method="slq", params=_params(cfg), graph_hash=_hash(g, with_hash),
-                        std_error=float(std[0]))
+    val, std = _integrate_host(rules, None, [_lib.FN_XLOGX])
+    return EntropyValue(value=-float(val[0, 0]), method="slq", params=_params(cfg), graph_hash=_hash(g, with_hash),
+                        std_error=float(std[0, 0]))
 
 
 def _grid_from_timescales(timescales) -> TimeGrid:

@@ -43,9 +43,16 @@ class DeviceGraph:
                                                None if w is None else w.ctypes.data, stream,
                                                ctypes.byref(self.handle))
         _lib.check(rc)
-        info = _lib.GraphInfo()
-        _lib.check(lib.slq_graph_info(self.handle, ctypes.byref(info)))
-        self.info = info
+        self._info = None
+
+    @property
+    def info(self):
+        """Graph scalars (tr L, max degree, ...); the first access synchronises the stream."""
+        if self._info is None:
+            info = _lib.GraphInfo()
+            _lib.check(_lib.load().slq_graph_info(self.handle, ctypes.byref(info)))
+            self._info = info
+        return self._info
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -116,9 +123,24 @@ class DeviceGraph:
         return alpha, beta, st
 
     def rules(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1,
-              dtype: str = "f64") -> "DeviceRules":
-        alpha, beta, st = self.tridiagonals(kind, seed, probe_begin, count, steps, reorth=reorth, dtype=dtype)
-        return gauss_rules(alpha, beta, st, self.interval(kind), n=self.n)
+              dtype: str = "f64", status=None) -> "DeviceRules":
+        """Gauss rules of probes [probe_begin, +count), asynchronously (errors land in ``status``)."""
+        import torch
+
+        s = min(int(steps), self.n)
+        nodes = torch.zeros((count, s), dtype=torch.float64, device=self.device)
+        weights = torch.zeros_like(nodes)
+        st = torch.zeros(count, dtype=torch.int32, device=self.device)
+        if status is None:
+            status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if KIND_CODES[kind] == _lib.DENSITY and self.graph.nnz == 0:
+            raise ValueError("density matrix undefined for a graph without edges")
+        code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_rules(self.handle, KIND_CODES[kind], int(seed), int(probe_begin), int(count),
+                                             int(steps), int(reorth), code, _lib.ptr(nodes), _lib.ptr(weights),
+                                             _lib.ptr(st), _lib.ptr(status), _lib.stream_handle(self.device)))
+        return DeviceRules(nodes, weights, st, self.n, status=status)
 
 
 @dataclass
@@ -129,6 +151,34 @@ class DeviceRules:
     n: int
     alpha: object = None
     beta: object = None
+    status: object = None    # device int32[1]: OR of the asynchronous error bits
+
+    def check(self) -> None:
+        if self.status is not None:
+            _lib.check_status(int(self.status.item()))
+
+    def integrate(self, t, fns):
+        """values [nfn, T] and std_errors [nfn, T] on the device (no host synchronisation)."""
+        import torch
+
+        dev = self.nodes.device
+        if self.status is None:
+            self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        if t is None:
+            tt, T = None, 1
+        else:
+            tt = t.to(device=dev, dtype=torch.float64).contiguous() if isinstance(t, torch.Tensor) \
+                else torch.tensor(np.asarray(t, dtype=np.float64), device=dev)
+            T = int(tt.numel())
+        vals = torch.empty((len(fns), T), dtype=torch.float64, device=dev)
+        stds = torch.empty_like(vals)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().slq_integrate(_lib.ptr(self.nodes), _lib.ptr(self.weights), _lib.ptr(self.steps),
+                                                  self.count, int(self.nodes.shape[1]), _lib.ptr(tt), T,
+                                                  _lib.int_array(fns), len(fns), float(self.n), _lib.ptr(vals),
+                                                  _lib.ptr(stds), None, _lib.ptr(self.status),
+                                                  _lib.stream_handle(dev)))
+        return vals, stds
 
     @property
     def count(self) -> int:

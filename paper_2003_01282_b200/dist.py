@@ -65,5 +65,7 @@ def sharded_rules(dg, kind: str, cfg, *, dtype: str = "f64", reorth: int = -1, g
         nodes = torch.zeros((0, width), dtype=torch.float64, device=dg.device)
         weights = torch.zeros_like(nodes)
         steps = torch.zeros(0, dtype=torch.int32, device=dg.device)
+    if e > b:
+        local.check()   # one rank's eigensolver failure must not be gathered silently
     nodes, weights, steps = gather_rules_arrays(nodes, weights, steps, cfg.n_v, group)
     return DeviceRules(nodes, weights, steps, dg.n)

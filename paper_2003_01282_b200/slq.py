@@ -152,8 +152,10 @@ def _finish(rules: DeviceRules, fs: Sequence, n: int, control_variate=None) -> l
         ts = None if fs[0].t is None else np.array([f.t for f in fs], dtype=np.float64)
         pv = rules.quadrature(ts, code)
         val, std = rules.estimate(pv)
+        rules.check()
         pv_h, val_h, std_h = pv.cpu().numpy(), val.cpu().numpy(), std.cpu().numpy()
         return [SlqEstimate(float(val_h[k]), pv_h[k], float(std_h[k])) for k in range(len(fs))]
+    rules.check()
     host = _host_rules(rules)
     out = []
     for f in fs:
