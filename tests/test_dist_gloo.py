@@ -1,0 +1,71 @@
+"""Multi-rank host logic of the probe sharding (world_size 2, gloo, CPU): balanced probe ranges,
+the all-gather of per-rank rule blocks in probe order, and that the assembled rules — and so the
+descriptors — equal the single-rank result bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2003_01282_b200.dist import gather_rules_arrays, probe_ranges
+
+
+def test_probe_ranges_balanced():
+    assert probe_ranges(100, 8) == [(0, 13), (13, 26), (26, 39), (39, 52), (52, 64), (64, 76), (76, 88), (88, 100)]
+    assert probe_ranges(3, 4) == [(0, 1), (1, 2), (2, 3), (3, 3)]
+    for n_v in (1, 7, 128):
+        for w in (1, 2, 3, 8):
+            r = probe_ranges(n_v, w)
+            assert r[0][0] == 0 and r[-1][1] == n_v
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            sizes = [e - b for b, e in r]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rules_for(probes, width):
+    # deterministic stand-in for per-probe rules: a pure function of the probe index
+    rng = [np.random.default_rng(1000 + p) for p in probes]
+    nodes = np.stack([np.sort(r.uniform(0, 2, width)) for r in rng]) if probes else np.zeros((0, width))
+    weights = np.stack([r.dirichlet(np.ones(width)) for r in rng]) if probes else np.zeros((0, width))
+    steps = np.array([width - (p % 3 == 0) for p in probes], dtype=np.int32)
+    return nodes, weights, steps
+
+
+def _worker(rank, world, port, n_v, width, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = probe_ranges(n_v, world)[rank]
+    nodes, weights, steps = _rules_for(list(range(b, e)), width)
+    gn, gw, gs = gather_rules_arrays(torch.tensor(nodes), torch.tensor(weights), torch.tensor(steps), n_v)
+    if rank == 0:
+        out.put((gn.numpy(), gw.numpy(), gs.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_v,world", [(10, 2), (3, 2), (1, 2)])
+def test_gather_rules_world2_matches_single(n_v, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_v, 6, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = _rules_for(list(range(n_v)), 6)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
