@@ -19,7 +19,9 @@ LAPLACIAN, NORMALIZED_LAPLACIAN, DENSITY = 0, 1, 2
 F64, F32 = 0, 1
 FN_HEAT, FN_WAVE_RE, FN_WAVE_IM, FN_XLOGX, FN_IDENTITY = range(5)
 
-KERNEL_CLASSES = ("prepare", "probe", "spmm", "cgs_dot", "cgs_update", "reduce", "eig", "quad",
+# kernel classes as counted by the library (cgs_step = the persistent per-step CGS kernel, or the
+# separate update kernels on the fallback path)
+KERNEL_CLASSES = ("prepare", "probe", "spmm", "cgs_dot", "cgs_step", "reduce", "eig", "quad",
                   "estimate", "batched")
 
 _vp = ctypes.c_void_p

@@ -48,6 +48,11 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
+// Named barrier over `count` threads (multiple of 32); id 0 is __syncthreads.
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // Grid-wide barrier for persistent kernels whose CTAs are all co-resident (one CTA per SM, grid <= SMs).
 // `counter` is zeroed before the launch; barrier number k (1-based) completes when counter >= k*G.
 __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int k) {

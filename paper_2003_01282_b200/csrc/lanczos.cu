@@ -91,6 +91,11 @@ struct ChunkState {
   double* beta = nullptr;   // [S][cpad]
   double* h = nullptr;      // [S][cpad]    CGS coefficients of the current step
   double* nb2 = nullptr;    // [cpad]       ||w'||^2
+  // staged path (Gram form of CGS): raw sums and the Gram matrix of the stored basis
+  double* cdot = nullptr;   // [S+1][cpad]  sum_rows u_k . w            (k <= i)
+  double* gram = nullptr;   // [S+1][cpad]  sum_rows u_k . u_{i+1}      (k <= i), row of the new vector
+  double* nrm2 = nullptr;   // [cpad]       ||u_{i+1}||^2
+  double* G = nullptr;      // [(S+1)*(S+1)][cpad]  G(k,j) = q_k . q_j
   int* steps = nullptr;     // [cpad]
   int* alive = nullptr;     // [cpad]
   int* again = nullptr;     // [cpad]
@@ -371,22 +376,10 @@ static int ppl_for(int c) {
 
 template <typename VT, int KIND, bool W, int PPL>
 static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
-  if (coop) {
-    static int max_ctas[64] = {0};   // co-resident CTAs per device for this instantiation
-    if (max_ctas[dev] == 0) {
-      int per_sm = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_kernel<VT, KIND, W, PPL, true>, kSpmmWarps * 32, 0);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      max_ctas[dev] = std::max(1, per_sm * sms);
-    }
-    const int gx = std::max(1, std::min(a.ntiles, max_ctas[dev] / gy));
-    void* args[] = {&a};
-    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(spmm_kernel<VT, KIND, W, PPL, true>), dim3(gx, gy),
-                                dim3(kSpmmWarps * 32), args, 0, st);
-  } else {
-    dim3 grid(std::min(a.ntiles, 148 * 4), gy);
-    spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
-  }
+  (void)coop;
+  (void)dev;
+  dim3 grid(std::min(a.ntiles, 148 * 4), gy);
+  spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
 }
 
 template <typename VT, int KIND, bool W>
@@ -594,22 +587,28 @@ cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
 }
 
 // ---------------------------------------------------------------- staged (TMA bulk) CGS step kernel
-// One cooperative persistent launch per Lanczos step does all of pass B: kPersist CTAs, CTA b owns
+// One persistent launch per Lanczos step does everything after the SpMM: kPersist CTAs, CTA b owns
 // the contiguous rows [n*b/G, n*(b+1)/G).  Warp 0 lane 0 is the producer: it streams row chunks of
 // every needed vector into a kStages-deep shared-memory ring with cp.async.bulk (completion on a
 // "full" mbarrier).  Consumer thread p owns probe column p, walks its CTA's rows in ascending
-// order from shared memory and releases each stage on an "empty" mbarrier.  Bytes in flight per SM
-// = the whole ring (no register cost).  Phases, separated by grid-wide barriers:
-//   A  dots   partials of u_k . w' (k <= i) and ||w'||^2                       (lanczos.py:72-73)
-//   B  reduce CGS coefficients h_k (fixed-order stripes)
-//   C  update u_{i+1} = w' - sum_k h_k q_k, partials of ||u_{i+1}||^2          (lanczos.py:73)
-//   D  finalize beta_i, breakdown, second-pass flag                             (lanczos.py:75,132-134)
-//   A'-D' the conditional second CGS pass, only if some probe asked for it     (lanczos.py:75-76)
-// Every per-probe sum runs in row order inside a fixed row range: independent of c and chunking.
+// order from shared memory and releases each stage on an "empty" mbarrier (bytes in flight per SM
+// = the whole ring, no register cost).
+//
+// CGS in Gram form.  With q_k = r_k u_k and G(k,j) = q_k . q_j (kept per probe), the reference's
+// coefficient h_k = q_k . w' with w' = (w - alpha q_i) - beta q_{i-1} (lanczos.py:72-73,129) is
+//     h_k = r_k (u_k . w) - alpha G(k,i) - beta G(k,i-1),   alpha = r_i (u_i . w),
+// so one streaming phase (A) yields alpha and every h_k; the update phase (C) forms w' exactly as
+// the reference, subtracts sum_k h_k q_k, and accumulates ||w'||^2, ||u_{i+1}||^2 and the Gram row
+// u_k . u_{i+1} of the new vector.  The Gram row is also the second CGS pass's coefficients
+// (lanczos.py:75-76), so that pass is a single update phase (C').  Phases are separated by a
+// software grid barrier (all CTAs co-resident: one per SM).  Every per-probe sum runs in row order
+// inside a fixed row range, reduced in fixed stripes: independent of c and of chunking.
 constexpr int kPersist = 148;
+constexpr int kStageSlots = 3;          // consumer threads per probe column: rows (row - lo) % 3; 32+3*128 = 416 threads -> 128 regs
+constexpr int kStagedMaxLdc = 128;     // consumers = kStageSlots * round_up(ldc, 32) <= 512
 constexpr int kStages = 3;
 constexpr int kMaxStaged = kCgsBlock + 4;
-constexpr size_t kStagedSmem = 220 * 1024;
+constexpr size_t kStagedSmem = 200 * 1024;   // + 20 KB static: within the 227 KB per CTA
 
 struct StagedArgs {
   CgsArgs a;
@@ -621,7 +620,7 @@ struct StagedArgs {
 };
 
 struct StepArgs {
-  StagedArgs pass[2];             // [0]: src = w, [1]: src = u_{i+1} (second CGS pass)
+  StagedArgs pass[2];             // [0]: src = w (phases A, C), [1]: src = u_{i+1} (phase C')
   ReduceArgs red;
 };
 
@@ -643,7 +642,7 @@ __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
 
 // Producer (one lane): chunk j of [lo, hi) goes to ring slot (ch0 + j) % kStages.
 template <typename VT>
-__device__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
+__device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
   const int64_t ldc = sa.a.ldc;
   const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * sa.rt * ldc;
   int ch = ch0;
@@ -660,171 +659,307 @@ __device__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch
   }
 }
 
-struct ProbeScalars {
-  double al, bp, ri, rim1;
-  __device__ ProbeScalars(const CgsArgs& a, int p, bool pv) {
-    const int cp = a.cpad;
-    al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
-    bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
-    ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
-    rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
-  }
-};
+// Gram-matrix entry G(k, j) of probe p (G is symmetric; stored as [(S+1)*(S+1)][cpad]).
+__device__ __forceinline__ double gram_at(const ChunkState& s, int k, int j, int p) {
+  return s.G[(static_cast<int64_t>(k) * (s.S + 1) + j) * s.cpad + p];
+}
 
-// Phase A (consumer side): partials [cta][nk+1][cpad] of u_k . w' and ||w'||^2.
-template <typename VT>
-__device__ void staged_dot_consume(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi,
-                                   bool second) {
+// Shared-memory stage layout: [slot][row][ldc], slot 0 = source (w or u_{i+1}), slot 1+k = u_k.
+// NK = i + 1 basis vectors is a compile-time constant, so every loop below is fully unrolled with
+// no predicates and the per-vector offsets stay in registers.
+
+// Phase A (consumer side): partials [cta*slots+slot][nq][cpad] of u_k . w (k < NK); at i == 0 also
+// u_0 . u_0 (q = 1) for G(0,0).
+template <typename VT, int NK>
+__device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo,
+                                           int64_t hi, int nq, int cols_pad) {
   const CgsArgs& a = sa.a;
-  const int p = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const int t = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const int p = t % cols_pad, slot = t / cols_pad;
   const bool pv = p < a.c;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
-  const int nk = a.i + 1;
-  const ProbeScalars ps(a, p, pv);
-  const int vstride = sa.rt * ldc;
-  const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * vstride;
-  int koff[kCgsBlock];
+  const int rt = sa.rt;
+  const int vstride = rt * ldc;
+  const int64_t stage_elems = static_cast<int64_t>(NK + 1) * vstride;
+  double acc[NK];
 #pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * vstride;
-  const int osrc = sa.slot_src * vstride, oui = sa.slot_ui * vstride, ouim1 = sa.slot_uim1 * vstride;
-  double acc[kCgsBlock];
-#pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) acc[kk] = 0.0;
-  double nb = 0.0;
+  for (int kk = 0; kk < NK; ++kk) acc[kk] = 0.0;
+  double g00 = 0.0;
   int ch = ch0;
-  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+  for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
-    const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
-    const VT* base = ring.buf + s * stage_elems + p;
+    const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
     if (pv) {
-      for (int r = 0; r < rows; ++r) {
+      const VT* base = ring.buf + s * stage_elems + p;
+      // this thread's rows: (row - lo) % kStageSlots == slot, ascending
+      int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
+      for (; r < rows; r += kStageSlots) {
         const VT* e = base + r * ldc;
-        const double wp = second ? to_f64(e[osrc])
-                                 : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
-                                              ps.al, ps.bp, ps.ri, ps.rim1);
-        nb = fma(wp, wp, nb);
+        const double wv = to_f64(e[0]);
+        const VT* uk = e + vstride;
 #pragma unroll
-        for (int kk = 0; kk < kCgsBlock; ++kk)
-          if (kk < nk) acc[kk] = fma(to_f64(e[koff[kk]]), wp, acc[kk]);
+        for (int kk = 0; kk < NK; ++kk) acc[kk] = fma(to_f64(uk[kk * vstride]), wv, acc[kk]);
+        if (NK == 1) {
+          const double u0 = to_f64(uk[0]);
+          g00 = fma(u0, u0, g00);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
   if (p < cp) {
-    double* dst = a.partial + static_cast<int64_t>(blockIdx.x) * (nk + 1) * cp + p;
+    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * kStageSlots + slot) * nq * cp + p;
 #pragma unroll
-    for (int kk = 0; kk < kCgsBlock; ++kk)
-      if (kk < nk) dst[kk * cp] = acc[kk];
-    dst[nk * cp] = nb;
+    for (int kk = 0; kk < NK; ++kk) dst[kk * cp] = acc[kk];
+    if (NK == 1) dst[NK * cp] = g00;
   }
 }
 
-// Phase C (consumer side): u_{i+1} and partials [cta][cpad] of ||u_{i+1}||^2.
-template <typename VT>
-__device__ void staged_update_consume(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi,
-                                      bool second) {
+// Phase C / C' (consumer side).  First pass: w' = three-term, u_{i+1} = w' - sum_k coef_k u_k.
+// Second pass (flagged probes): u_{i+1} -= sum_k coef_k u_k.  Partials [cta*slots+slot][nq][cpad]:
+// q=0 ||w'||^2, q=1 ||u_{i+1}||^2, q=2+k  u_k . u_{i+1}.
+template <typename VT, int NK, bool SECOND>
+__device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo,
+                                             int64_t hi, int cols_pad, double* cf_sm) {
   const CgsArgs& a = sa.a;
-  const int p = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const ChunkState& S = a.s;
+  const int t = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const int p = t % cols_pad, slot = t / cols_pad;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
-  const bool pv = p < a.c && (!second || a.s.again[p]);
-  const int nk = a.reorth ? a.i + 1 : 0;
-  double cf[kCgsBlock];
+  const bool pv = p < a.c && (!SECOND || S.again[p]);
+  constexpr int nq = NK + 2;
+  const int i = NK - 1;
+  double al = 0.0, bp = 0.0, ri = 0.0, rim1 = 0.0;
+  if (pv) {
+    ri = S.rsc[i * cp + p];
+    rim1 = i > 0 ? S.rsc[(i - 1) * cp + p] : 0.0;
+    bp = i > 0 ? S.beta[(i - 1) * cp + p] : 0.0;
+    al = ri * S.cdot[i * cp + p];
+  }
+  // CGS coefficients coef_k = h_k r_k into shared memory [NK][cols_pad] (slot 0 computes)
+  if (slot == 0) {
 #pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) cf[kk] = (pv && kk < nk) ? a.s.h[kk * cp + p] * a.s.rsc[kk * cp + p] : 0.0;
-  const ProbeScalars ps(a, p, pv);
-  const int vstride = sa.rt * ldc;
-  const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * vstride;
-  int koff[kCgsBlock];
+    for (int kk = 0; kk < NK; ++kk) {
+      double c = 0.0;
+      if (pv) {
+        const double rk = S.rsc[kk * cp + p];
+        double h;
+        if (SECOND) {
+          h = rk * S.gram[kk * cp + p];                                           // q_k . w''
+        } else {
+          h = rk * S.cdot[kk * cp + p] - al * gram_at(S, kk, i, p);
+          if (i > 0) h -= bp * gram_at(S, kk, i - 1, p);
+        }
+        c = h * rk;
+      }
+      cf_sm[kk * cols_pad + p] = c;
+    }
+  }
+  named_barrier_sync(1, blockDim.x - 32);   // consumers only
+  double cf[NK];
 #pragma unroll
-  for (int kk = 0; kk < kCgsBlock; ++kk) koff[kk] = sa.slot_k[kk] * vstride;
-  const int osrc = sa.slot_src * vstride, oui = sa.slot_ui * vstride, ouim1 = sa.slot_uim1 * vstride;
-  VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(a.i + 1) * a.vec_stride + p;
-  double nrm = 0.0;
+  for (int kk = 0; kk < NK; ++kk) cf[kk] = cf_sm[kk * cols_pad + p];
+  const int rt = sa.rt;
+  const int vstride = rt * ldc;
+  const int64_t stage_elems = static_cast<int64_t>(NK + 1) * vstride;
+  VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
+  double nb = 0.0, nrm = 0.0;
+  double gr[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) gr[kk] = 0.0;
   int ch = ch0;
-  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+  for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
-    const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
-    const VT* base = ring.buf + s * stage_elems + p;
+    const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
     if (pv) {
-      for (int r = 0; r < rows; ++r) {
+      const VT* base = ring.buf + s * stage_elems + p;
+      int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
+      for (; r < rows; r += kStageSlots) {
         const VT* e = base + r * ldc;
-        const double wp = second ? to_f64(e[osrc])
-                                 : three_term(to_f64(e[osrc]), to_f64(e[oui]), a.i > 0 ? to_f64(e[ouim1]) : 0.0,
-                                              ps.al, ps.bp, ps.ri, ps.rim1);
-        double proj = 0.0;
+        const VT* uk = e + vstride;
+        double wp;
+        if (SECOND) {
+          wp = to_f64(e[0]);
+        } else {
+          wp = three_term(to_f64(e[0]), to_f64(uk[i * vstride]), i > 0 ? to_f64(uk[(i > 0 ? i - 1 : 0) * vstride]) : 0.0,
+                          al, bp, ri, rim1);
+          nb = fma(wp, wp, nb);
+        }
+        // basis.T @ h as two interleaved partial sums (shorter dependency chain), then one subtraction
+        double pe = 0.0, po = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < kCgsBlock; ++kk)
-          if (kk < nk) proj = fma(to_f64(e[koff[kk]]), cf[kk], proj);
-        const VT v = from_f64<VT>(nk ? __dsub_rn(wp, proj) : wp);
+        for (int kk = 0; kk < NK; ++kk) {
+          if (kk & 1) po = fma(to_f64(uk[kk * vstride]), cf[kk], po);
+          else pe = fma(to_f64(uk[kk * vstride]), cf[kk], pe);
+        }
+        const VT v = from_f64<VT>(__dsub_rn(wp, pe + po));
         out[(r0 + r) * a.ldc] = v;
         const double vd = to_f64(v);
         nrm = fma(vd, vd, nrm);
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) gr[kk] = fma(to_f64(uk[kk * vstride]), vd, gr[kk]);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
-  if (p < cp) a.partial[static_cast<int64_t>(blockIdx.x) * cp + p] = nrm;
+  if (p < cp) {
+    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * kStageSlots + slot) * nq * cp + p;
+    dst[0] = nb;
+    dst[cp] = nrm;
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) dst[(2 + kk) * cp] = gr[kk];
+  }
 }
 
-template <typename VT>
-__global__ void __launch_bounds__(32 + 256, 1)
+// Fixed-order stripe reduction of quantity q for 32 probes; returns the total in warp 0's lanes.
+__device__ double stripe_sum(const double* partial, int ntiles, int nq, int cpad, int q, int group, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int p = group * 32 + lane;
+  const int64_t stride = static_cast<int64_t>(nq) * cpad;
+  const double* src = partial + static_cast<int64_t>(q) * cpad + p;
+  for (int sidx = warp; sidx < kStripes; sidx += nw) {
+    double s = 0.0;
+    for (int t = sidx; t < ntiles; t += kStripes) s += src[t * stride];
+    red[sidx * 32 + lane] = s;
+  }
+  __syncthreads();
+  double tot = 0.0;
+  if (warp == 0) {
+    tot = red[lane];
+    for (int j = 1; j < kStripes; ++j) tot += red[j * 32 + lane];
+  }
+  __syncthreads();
+  return tot;
+}
+
+// Phases C (or C'), D, E of one CGS pass (SECOND: the conditional second pass, lanczos.py:75-76).
+template <typename VT, int NK, bool SECOND, typename Sync>
+__device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs& st, StageRing<VT>& ring, int& ch,
+                                            int64_t lo, int64_t hi, int cols_pad, int nrows_partial, double* cf_sm,
+                                            double* red, Sync& sync_grid) {
+  const CgsArgs& a = sa.pass[0].a;
+  const ChunkState& S = a.s;
+  const int ngroups = a.cpad / 32, cp = a.cpad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nk = a.i + 1, nq = nk + 2, nslot = S.S + 1;
+  // C / C': update
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
+  } else {
+    phase_update<VT, NK, SECOND>(st, ring, ch, lo, hi, cols_pad, cf_sm);
+  }
+  ch += chunk_count(lo, hi, st.rt);
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // u_{i+1} is bulk-read by a second pass
+  sync_grid();
+  // D: reduce ||w'||^2, ||u_{i+1}||^2 and the Gram row
+  for (int sl = blockIdx.x; sl < nq * ngroups; sl += gridDim.x) {
+    const int q = sl % nq, gidx = sl / nq, p = gidx * 32 + lane;
+    const double tot = stripe_sum(a.partial, nrows_partial, nq, cp, q, gidx, red);
+    if (warp == 0 && p < a.c) {
+      if (q == 0) { if (!SECOND) S.nb2[p] = tot; }
+      else if (q == 1) S.nrm2[p] = tot;
+      else S.gram[(q - 2) * cp + p] = tot;
+    }
+  }
+  sync_grid();
+  // E: beta, breakdown, second-pass flag, Gram column of q_{i+1} (lanczos.py:75,132-137)
+  for (int gidx = blockIdx.x; gidx < ngroups; gidx += gridDim.x) {
+    const int p = gidx * 32 + lane;
+    if (warp != 0 || p >= a.c || !S.alive[p]) continue;
+    if (SECOND && !S.again[p]) continue;
+    const double b = sqrt(S.nrm2[p]);
+    if (!SECOND && b < 0.5 * sqrt(S.nb2[p])) {
+      S.again[p] = 1;
+      *S.any_again = 1;
+      continue;
+    }
+    if (SECOND) S.again[p] = 0;
+    const double hi_int = sa.red.kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0
+                          : (sa.red.kind == SLQ_DENSITY ? 1.0 : sa.red.dscal[4]);   // interval_hi
+    if (b <= 1e-12 * hi_int) {
+      S.steps[p] = a.i + 1;
+      S.alive[p] = 0;
+      S.rsc[(a.i + 1) * cp + p] = 0.0;
+    } else {
+      const double rn = __ddiv_rn(1.0, b);
+      S.beta[a.i * cp + p] = b;
+      S.rsc[(a.i + 1) * cp + p] = rn;
+      const int j = a.i + 1;
+      for (int k = 0; k <= a.i; ++k) {
+        const double gkj = S.rsc[k * cp + p] * rn * S.gram[k * cp + p];
+        S.G[(static_cast<int64_t>(k) * nslot + j) * cp + p] = gkj;
+        S.G[(static_cast<int64_t>(j) * nslot + k) * cp + p] = gkj;
+      }
+      S.G[(static_cast<int64_t>(j) * nslot + j) * cp + p] = rn * rn * S.nrm2[p];
+    }
+  }
+  sync_grid();
+}
+
+template <typename VT, int NK>
+__global__ void __launch_bounds__(32 + kStageSlots * kStagedMaxLdc, 1)
 cgs_step_kernel(StepArgs sa) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double red[kStripes * 32];
+  __shared__ double cf_sm[kCgsBlock * kStagedMaxLdc];
   StageRing<VT> ring(smem);
   const CgsArgs& a = sa.pass[0].a;
-  unsigned int* bar = a.s.barrier + a.i;
+  const ChunkState& S = a.s;
+  unsigned int* bar = S.barrier + a.i;
   unsigned int nbar = 0;
   auto sync_grid = [&]() { grid_barrier(bar, ++nbar); };
   const int nwc = (blockDim.x - 32) / 32;
+  const int cols_pad = (blockDim.x - 32) / kStageSlots;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
     mbar_fence_init();
   }
   __syncthreads();
   const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
-  const int ngroups = a.cpad / 32;
+  const int ngroups = a.cpad / 32, cp = a.cpad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nk = a.i + 1;
+  const int nslot = S.S + 1;
+  const int nrows_partial = gridDim.x * kStageSlots;
   int ch = 0;
-  for (int pass = 0; pass < (a.reorth ? 2 : 1); ++pass) {
-    const StagedArgs& st = sa.pass[pass];
-    const bool second = pass == 1;
-    if (second && *a.s.any_again == 0) break;   // uniform: read after a grid barrier
-    const int nch = chunk_count(lo, hi, st.rt);
-    ReduceArgs r = sa.red;
-    r.second = pass;
-    r.ntiles = gridDim.x;
-    if (a.reorth) {
-      // A: dots
-      if (threadIdx.x < 32) {
-        if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
+  const StagedArgs& st0 = sa.pass[0];
+  const int nch0 = chunk_count(lo, hi, st0.rt);
+
+  // A: u_k . w for k <= i (and u_0 . u_0 at i == 0)
+  const int nqa = nk + (a.i == 0 ? 1 : 0);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) staged_produce<VT>(st0, ring, ch, lo, hi);
+  } else {
+    phase_dots<VT, NK>(st0, ring, ch, lo, hi, nqa, cols_pad);
+  }
+  ch += nch0;
+  sync_grid();
+  // B: reduce them (fixed stripes); G(0,0) at the first step
+  for (int sl = blockIdx.x; sl < nqa * ngroups; sl += gridDim.x) {
+    const int q = sl % nqa, gidx = sl / nqa, p = gidx * 32 + lane;
+    const double tot = stripe_sum(a.partial, nrows_partial, nqa, cp, q, gidx, red);
+    if (warp == 0 && p < a.c) {
+      if (q < nk) {
+        S.cdot[q * cp + p] = tot;
+        if (q == a.i && S.alive[p]) S.alpha[a.i * cp + p] = S.rsc[a.i * cp + p] * tot;   // alpha = q_i . w
       } else {
-        staged_dot_consume<VT>(st, ring, ch, lo, hi, second);
+        const double r0 = S.rsc[p];
+        S.G[p] = r0 * r0 * tot;                                                       // G(0,0)
       }
-      ch += nch;
-      sync_grid();
-      // B: CGS coefficients (+ ||w'||^2 on the first pass)
-      r.mode = RED_CGS; r.nq = nk + 1; r.k0 = 0; r.nk = nk;
-      for (int sl = blockIdx.x; sl < r.nq * ngroups; sl += gridDim.x) reduce_slice(r, sl % r.nq, sl / r.nq, red);
-      sync_grid();
     }
-    // C: update
-    if (threadIdx.x < 32) {
-      if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
-    } else {
-      staged_update_consume<VT>(st, ring, ch, lo, hi, second);
-    }
-    ch += nch;
-    asm volatile("fence.proxy.async.global;" ::: "memory");   // u_{i+1} is bulk-read by a second pass
-    sync_grid();
-    // D: beta, breakdown, second-pass flag
-    r.mode = second ? RED_NORM2 : RED_NORM; r.nq = 1;
-    for (int sl = blockIdx.x; sl < ngroups; sl += gridDim.x) reduce_slice(r, 0, sl, red);
-    sync_grid();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *S.any_again = 0;
+  sync_grid();
+  update_pass<VT, NK, false>(sa, sa.pass[0], ring, ch, lo, hi, cols_pad, nrows_partial, cf_sm, red, sync_grid);
+  if (*S.any_again) {   // uniform: read after a grid barrier
+#ifdef SLQ_DEBUG_SECOND
+    if (blockIdx.x == 0 && threadIdx.x == 0) printf("second pass at step %d\n", a.i);
+#endif
+    update_pass<VT, NK, true>(sa, sa.pass[1], ring, ch, lo, hi, cols_pad, nrows_partial, cf_sm, red, sync_grid);
   }
 }
 
@@ -837,30 +972,21 @@ static bool staged_setup(const CgsArgs& a, bool second, StagedArgs* out) {
   int nv = 0;
   s.slot_src = nv;
   s.vec[nv++] = second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
-  const int kcount = a.reorth ? a.i + 1 : 0;
-  if (kcount > kCgsBlock) return false;
+  const int kcount = a.i + 1;
+  if (!a.reorth || kcount > kCgsBlock) return false;
   for (int kk = 0; kk < kCgsBlock; ++kk) s.slot_k[kk] = 0;
   for (int kk = 0; kk < kcount; ++kk) {
     s.slot_k[kk] = nv;
     s.vec[nv++] = basis + static_cast<int64_t>(kk) * a.vec_stride;
   }
-  auto slot_of = [&](int k) {
-    if (k < kcount) return s.slot_k[k];
-    s.vec[nv] = basis + static_cast<int64_t>(k) * a.vec_stride;
-    return nv++;
-  };
-  s.slot_ui = 0;
-  s.slot_uim1 = 0;
-  if (!second) {
-    s.slot_ui = slot_of(a.i);
-    if (a.i > 0) s.slot_uim1 = slot_of(a.i - 1);
-  }
+  s.slot_ui = s.slot_k[a.i];
+  s.slot_uim1 = a.i > 0 ? s.slot_k[a.i - 1] : 0;
   s.nvec = nv;
   const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT);
   const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
   int64_t rt = static_cast<int64_t>((kStagedSmem - 128) / (kStages * row_bytes));
   rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
-  if (rt < 1 || a.ldc > 256) return false;
+  if (rt < 1 || a.ldc > kStagedMaxLdc) return false;
   s.rt = static_cast<int>(rt);
   *out = s;
   return true;
@@ -870,15 +996,15 @@ static int coop_supported(int dev) {
   static int v[64] = {0};
   if (dev < 0 || dev >= 64) return 0;
   if (v[dev] == 0) {
-    int coop = 0, sms = 0;
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    v[dev] = (coop && sms >= kPersist) ? 1 : 2;
+    v[dev] = sms >= kPersist ? 1 : 2;
   }
   return v[dev] == 1;
 }
 
-// Launch pass B of step i as one cooperative kernel; false when the staged path does not apply.
+// Launch everything after the SpMM of step i as one persistent kernel; false when the staged path
+// does not apply (the caller then runs the separate kernels).
 template <typename VT>
 static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, int dev, cudaStream_t st, int* rc) {
   *rc = SLQ_OK;
@@ -889,20 +1015,31 @@ static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, int dev, cu
   const size_t smem = 128 + kStages * std::max(static_cast<size_t>(sa.pass[0].nvec) * sa.pass[0].rt,
                                                static_cast<size_t>(sa.pass[1].nvec) * sa.pass[1].rt) *
                                 a.ldc * sizeof(VT);
-  const int threads = 32 + ((static_cast<int>(a.ldc) + 31) / 32) * 32;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[sizeof(VT) == 8]) {
-    cudaFuncSetAttribute(cgs_step_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kStagedSmem));
-    attr_set[sizeof(VT) == 8] = true;
-  }
+  const int threads = 32 + kStageSlots * (((static_cast<int>(a.ldc) + 31) / 32) * 32);
   LaunchScope ls(K_CGS_UPDATE, st);
-  // kPersist = 148 CTAs with > half of an SM's shared memory each: one per SM, all co-resident, so
-  // the software grid barrier is safe (coop_supported() checked the SM count).
-  cgs_step_kernel<VT><<<kPersist, threads, smem, st>>>(sa);
+  // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
+  // so the software grid barrier is safe (coop_supported() checked the SM count).
+  switch (a.i + 1) {
+#define SLQ_STEP_CASE(K)                                                                                  \
+    case K: {                                                                                              \
+      static bool attr = false;                                                                            \
+      if (!attr) {                                                                                         \
+        cudaFuncSetAttribute(cgs_step_kernel<VT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                             static_cast<int>(kStagedSmem));                                               \
+        attr = true;                                                                                       \
+      }                                                                                                    \
+      cgs_step_kernel<VT, K><<<kPersist, threads, smem, st>>>(sa);                                         \
+      break;                                                                                               \
+    }
+    SLQ_STEP_CASE(1) SLQ_STEP_CASE(2) SLQ_STEP_CASE(3) SLQ_STEP_CASE(4) SLQ_STEP_CASE(5) SLQ_STEP_CASE(6)
+    SLQ_STEP_CASE(7) SLQ_STEP_CASE(8) SLQ_STEP_CASE(9) SLQ_STEP_CASE(10) SLQ_STEP_CASE(11) SLQ_STEP_CASE(12)
+    SLQ_STEP_CASE(13) SLQ_STEP_CASE(14) SLQ_STEP_CASE(15) SLQ_STEP_CASE(16)
+#undef SLQ_STEP_CASE
+    default: return false;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    *rc = cuda_fail(e, "cudaLaunchCooperativeKernel(cgs_step_kernel)");
+    *rc = cuda_fail(e, "cgs_step_kernel launch");
     return true;
   }
   return true;
@@ -963,12 +1100,6 @@ static bool trace_host() {
 }
 #define SLQ_TRACE(label) do { if (trace_host()) fprintf(stderr, "[slq host] %-28s %9.3f ms\n", label, host_ms() - t_host0); } while (0)
 
-static bool env_flag(const char* name, bool dflt) {
-  const char* e = getenv(name);
-  if (!e || !e[0]) return dflt;
-  return e[0] != '0';
-}
-
 static bool staged_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1012,10 +1143,11 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const int64_t vs = n * ldc;
   int rc = SLQ_OK;
 
-  const int nq_max = kCgsBlock + 1;
-  const int64_t ptiles = std::max<int64_t>({g->ntiles, g->ntiles_stream, kPersist});
+  const int nq_max = kCgsBlock + 2;
+  const int64_t ptiles = std::max<int64_t>({g->ntiles, g->ntiles_stream, kPersist * kStageSlots});
   const size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
-  const size_t bytes_state = sizeof(double) * cpad * (4 * (S + 1) + 2) + sizeof(int) * (3 * cpad + 4 + S + 4);
+  const size_t bytes_state = sizeof(double) * cpad * (6 * (S + 1) + 3 + (S + 1) * (S + 1)) +
+                             sizeof(int) * (3 * cpad + 4 + S + 4);
   const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
   const size_t off_state = ((bytes_vec + 255) / 256) * 256;
   const size_t off_part = off_state + ((bytes_state + 255) / 256) * 256;
@@ -1033,7 +1165,11 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   s.beta = s.alpha + (S + 1) * cpad;
   s.h = s.beta + (S + 1) * cpad;
   s.nb2 = s.h + (S + 1) * cpad;
-  int* istate = reinterpret_cast<int*>(s.nb2 + cpad);
+  s.cdot = s.nb2 + cpad;
+  s.gram = s.cdot + (S + 1) * cpad;
+  s.nrm2 = s.gram + (S + 1) * cpad;
+  s.G = s.nrm2 + cpad;
+  int* istate = reinterpret_cast<int*>(s.G + (S + 1) * (S + 1) * cpad);
   s.steps = istate;
   s.alive = istate + cpad;
   s.again = istate + 2 * cpad;
@@ -1069,7 +1205,6 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const int gx = 1 << 30;                 // one CTA per tile group
   const bool use_staged = staged_enabled();
   const bool coop = use_staged && coop_supported(g->device);
-  const bool coop_spmm = coop && env_flag("SLQ_COOP_SPMM", false);
   const int gx2 = kSecondPassGrid;        // second pass: small grid-stride launch
 
   // Non-staged path (s > 17, SLQ_STAGED=0 or no cooperative launch): separate kernels + reductions.
@@ -1090,20 +1225,24 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     sa.r = s.rsc + i * cpad;
     ra.mode = RED_ALPHA; ra.ntiles = g->ntiles; ra.nq = 1; ra.i = i; ra.second = 0; ra.k0 = 0; ra.nk = 0;
     sa.red = ra;
-    SLQ_TRACE("spmm launch");
-    launch_spmm<VT>(kind, sa, coop_spmm, g->device, st);
-    SLQ_TRACE("spmm launched");
-    if (!coop_spmm) launch_reduce(ra, st);
-    if (i == S - 1) break;
     ca.i = i;
     ca.second = 0;
-    bool done = false;
-    if (coop) {
-      done = launch_cgs_step<VT>(ca, ra, g->device, st, &rc);
+    // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
+    // writes w; otherwise (last step, s > 17, SLQ_STAGED=0) the SpMM also reduces alpha.
+    const bool staged = coop && reorth && i < S - 1 && i + 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
+    sa.partial = staged ? nullptr : partial;
+    SLQ_TRACE("spmm launch");
+    launch_spmm<VT>(kind, sa, false, g->device, st);
+    SLQ_TRACE("spmm launched");
+    if (!staged) launch_reduce(ra, st);
+    if (i == S - 1) break;
+    if (staged) {
+      const bool done = launch_cgs_step<VT>(ca, ra, g->device, st, &rc);
       SLQ_TRACE("step launched");
       if (rc) return rc;
+      if (done) continue;
+      return fail(SLQ_ERR_CUDA, "staged step kernel unavailable after the SpMM skipped alpha");
     }
-    if (done) continue;
     if (reorth) dot_pass(i, 0, gx);
     ca.second = 0;
     rc = launch_cgs_update<VT>(ca, gx, st);
