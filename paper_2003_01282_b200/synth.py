@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .graphs import Graph, block_diagonal, csr_from_edges
+from .graphs import Graph, block_diagonal, csr_from_edges, unique_sorted
 
 __all__ = ["barabasi_albert", "sbm", "erdos_renyi", "er_batch", "rmat"]
 
@@ -116,6 +116,6 @@ def rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c:
             v |= np.where(right, bit, 0)
         keep = u != v
         u, v = u[keep], v[keep]
-        keys.append(np.unique(np.minimum(u, v) * n + np.maximum(u, v)))
-    key = np.unique(np.concatenate(keys))
+        keys.append(unique_sorted(np.minimum(u, v) * n + np.maximum(u, v)))
+    key = unique_sorted(np.concatenate(keys))
     return csr_from_edges(n, key // n, key % n)
