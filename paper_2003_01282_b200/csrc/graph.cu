@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "slq_common.cuh"
 
 namespace slq {
@@ -90,6 +92,44 @@ __global__ void degree_stats_final(const double* psum, const double* pmax, const
     out3[0] = s; out3[1] = mx; out3[2] = static_cast<double>(iso);
     out3[3] = s > 0.0 ? 1.0 / s : 0.0;    // density scale 1/tr L (operators.py:96)
     out3[4] = 2.0 * mx;                   // Laplacian interval hi (operators.py:79)
+  }
+}
+
+// Long rows (degree > kLongRow) are split into kSeg-nonzero segments processed by separate warps
+// (R-MAT hubs reach 64k nonzeros at scale 20).  Per-row segment counts, then exclusive scans.
+__global__ void long_row_count_kernel(const int64_t* __restrict__ off, int64_t n, int64_t* __restrict__ nseg_row,
+                                      int64_t* __restrict__ is_long) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = r < n ? off[r + 1] - off[r] : 0;
+    const bool lng = d > kLongRow;
+    nseg_row[r] = lng ? (d + kSeg - 1) / kSeg : 0;
+    is_long[r] = lng ? 1 : 0;
+  }
+}
+
+__global__ void long_row_fill_kernel(const int64_t* __restrict__ off, int64_t n, const int64_t* __restrict__ seg_first,
+                                     const int64_t* __restrict__ long_idx, int32_t* __restrict__ long_rows,
+                                     int64_t* __restrict__ long_seg_first, int32_t* __restrict__ seg_row,
+                                     int64_t* __restrict__ seg_begin, int64_t* __restrict__ counts) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (r == n) {
+      counts[0] = long_idx[n];
+      counts[1] = seg_first[n];
+      long_seg_first[long_idx[n]] = seg_first[n];
+      continue;
+    }
+    const int64_t d = off[r + 1] - off[r];
+    if (d <= kLongRow) continue;
+    const int64_t lr = long_idx[r], sf = seg_first[r];
+    long_rows[lr] = static_cast<int32_t>(r);
+    long_seg_first[lr] = sf;
+    const int64_t ns = (d + kSeg - 1) / kSeg;
+    for (int64_t k = 0; k < ns; ++k) {
+      seg_row[sf + k] = static_cast<int32_t>(r);
+      seg_begin[sf + k] = off[r] + k * kSeg;
+    }
   }
 }
 
@@ -184,6 +224,40 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   g->rows_per_stream_tile = std::max<int64_t>(kMinStreamRows, (n + kMaxTiles - 1) / kMaxTiles);
   g->ntiles_stream = std::max(1, ceil_div(n, g->rows_per_stream_tile));
   g->m = nnz / 2;
+  // long-row segments (device-side counts; host-side upper bounds size the buffers)
+  g->max_long = nnz / (kLongRow + 1) + 1;
+  g->max_seg = nnz / kSeg + g->max_long + 1;
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (2 + (g->max_long + 1) + g->max_seg) +
+                                   sizeof(int32_t) * (g->max_long + g->max_seg) + 64, st));
+  track(g, p);
+  g->long_counts = static_cast<int64_t*>(p);
+  g->long_seg_first = g->long_counts + 2;
+  g->seg_begin = g->long_seg_first + g->max_long + 1;
+  g->long_rows = reinterpret_cast<int32_t*>(g->seg_begin + g->max_seg);
+  g->seg_row = g->long_rows + g->max_long;
+  SLQ_CUDA(cudaMemsetAsync(g->long_counts, 0, 2 * sizeof(int64_t), st));
+  if (n > 0 && nnz > kLongRow) {
+    int64_t* tmp = nullptr;   // [n+1] nseg_row, [n+1] is_long, [n+1] seg_first, [n+1] long_idx
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(int64_t) * 4 * (n + 1), st));
+    {
+      LaunchScope ls(K_PREPARE, st);
+      long_row_count_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(g->offsets, n, tmp, tmp + (n + 1));
+    }
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp, tmp + 2 * (n + 1), static_cast<int>(n + 1), st);
+    void* cubtmp = nullptr;
+    SLQ_CUDA(cudaMallocAsync(&cubtmp, tb + 16, st));
+    SLQ_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, tmp, tmp + 2 * (n + 1), static_cast<int>(n + 1), st));
+    SLQ_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, tmp + (n + 1), tmp + 3 * (n + 1), static_cast<int>(n + 1), st));
+    {
+      LaunchScope ls(K_PREPARE, st);
+      long_row_fill_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(g->offsets, n, tmp + 2 * (n + 1), tmp + 3 * (n + 1),
+                                                                g->long_rows, g->long_seg_first, g->seg_row,
+                                                                g->seg_begin, g->long_counts);
+    }
+    SLQ_CUDA(cudaFreeAsync(cubtmp, st));
+    SLQ_CUDA(cudaFreeAsync(tmp, st));
+  }
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
 }

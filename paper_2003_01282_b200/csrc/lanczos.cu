@@ -238,8 +238,16 @@ struct SpmmArgs {
   void* w;                 // [n][ldc] output
   int64_t ldc_in, ldc_out;
   int c, cpad;
-  double* partial;         // [ntiles][cpad] alpha partials (nullptr = none)
+  double* partial;         // [ntiles + max_long][cpad] alpha partials (nullptr = none)
   ReduceArgs red;          // cooperative launches: alpha reduced in-kernel after a grid barrier
+  // long rows (graph.cu): device counts, segment table, per-segment partial sums [max_seg][cpad]
+  const int64_t* long_counts;
+  const int32_t* long_rows;
+  const int64_t* long_seg_first;
+  const int32_t* seg_row;
+  const int64_t* seg_begin;
+  int64_t max_long;
+  double* segpart;
 };
 
 template <int KIND>
@@ -266,6 +274,57 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
   return t;
 }
 
+// acc[j] += sum over nonzeros [beg, end) of one row, in stored order (sequential, unfused: the
+// reference's csr_matvec order).  Columns are loaded 32 at a time and broadcast by shuffles; UNR
+// gathers are in flight per lane.
+template <typename VT, int KIND, bool WEIGHTED, int PPL>
+__device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
+                                             const double* __restrict__ wts, const VT* __restrict__ u, int64_t ldi,
+                                             const bool* pv, const double* r, int64_t beg, int64_t end, double* acc) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = beg; base < end; base += 32) {
+    const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
+    int mycol = 0;
+    double mys = 1.0, myw = 1.0;
+    if (lane < cnt) {
+      mycol = __ldg(cols + base + lane);
+      if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + mycol);
+      if (WEIGHTED) myw = __ldg(wts + base + lane);
+    }
+    constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane
+    int k = 0;
+    for (; k + UNR <= cnt; k += UNR) {
+      double xv[UNR][PPL];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q)) * ldi;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const double sk = __shfl_sync(0xffffffffu, mys, k + q);
+        const double wk = __shfl_sync(0xffffffffu, myw, k + q);
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xv[q][j], r[j], sk, wk));
+      }
+    }
+    for (; k < cnt; ++k) {
+      const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k)) * ldi;
+      const double sk = __shfl_sync(0xffffffffu, mys, k);
+      const double wk = __shfl_sync(0xffffffffu, myw, k);
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        const double xr = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+        acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr, r[j], sk, wk));
+      }
+    }
+  }
+}
+
+// Pass A.  Work items: first the long-row segments (one warp each, partial sums to a.segpart),
+// then the graph-fixed row tiles (one warp per short row; alpha partials per tile).  Long rows are
+// finished by spmm_long_finish_kernel (segment partials summed in segment order).
 template <typename VT, int KIND, bool WEIGHTED, int PPL, bool COOP>
 __global__ void __launch_bounds__(kSpmmWarps * 32, 4)
 spmm_kernel(SpmmArgs a) {
@@ -282,11 +341,29 @@ spmm_kernel(SpmmArgs a) {
   const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
   VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
   const int64_t* __restrict__ off = a.offsets;
-  const int32_t* __restrict__ cols = a.cols;
   const double* __restrict__ dinv = a.dinv;
-  const double* __restrict__ wts = a.weights;
   const int64_t ldi = a.ldc_in;
   const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
+
+  // long-row segments
+  const int64_t nseg = a.long_counts ? a.long_counts[1] : 0;
+  for (int64_t sb = static_cast<int64_t>(blockIdx.x) * kSpmmWarps; sb < nseg;
+       sb += static_cast<int64_t>(gridDim.x) * kSpmmWarps) {
+    const int64_t sgi = sb + warp;
+    if (sgi >= nseg) continue;
+    const int64_t row = a.seg_row[sgi];
+    const int64_t beg = a.seg_begin[sgi];
+    const int64_t rend = off[row + 1];
+    const int64_t end = beg + kSeg < rend ? beg + kSeg : rend;
+    double acc[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
+    gather_range<VT, KIND, WEIGHTED, PPL>(a.cols, dinv, a.weights, u, ldi, pv, r, beg, end, acc);
+    double* dst = a.segpart + sgi * a.cpad + pbase;
+#pragma unroll
+    for (int j = 0; j < PPL; ++j)
+      if (pv[j]) dst[32 * j] = acc[j];
+  }
 
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int64_t rb = a.tile_rows[tile], re = a.tile_rows[tile + 1];
@@ -295,47 +372,11 @@ spmm_kernel(SpmmArgs a) {
     for (int j = 0; j < PPL; ++j) dot[j] = 0.0;
     for (int64_t row = rb + warp; row < re; row += kSpmmWarps) {
       const int64_t beg = off[row], end = off[row + 1];
+      if (a.long_counts && end - beg > kLongRow) continue;   // finished from its segments
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      for (int64_t base = beg; base < end; base += 32) {
-        const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
-        int mycol = 0;
-        double mys = 1.0, myw = 1.0;
-        if (lane < cnt) {
-          mycol = __ldg(cols + base + lane);
-          if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + mycol);
-          if (WEIGHTED) myw = __ldg(wts + base + lane);
-        }
-        constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane
-        int k = 0;
-        for (; k + UNR <= cnt; k += UNR) {
-          double xv[UNR][PPL];
-#pragma unroll
-          for (int q = 0; q < UNR; ++q) {
-            const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q)) * ldi;
-#pragma unroll
-            for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < UNR; ++q) {
-            const double sk = __shfl_sync(0xffffffffu, mys, k + q);
-            const double wk = __shfl_sync(0xffffffffu, myw, k + q);
-#pragma unroll
-            for (int j = 0; j < PPL; ++j) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xv[q][j], r[j], sk, wk));
-          }
-        }
-        for (; k < cnt; ++k) {
-          const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k)) * ldi;
-          const double sk = __shfl_sync(0xffffffffu, mys, k);
-          const double wk = __shfl_sync(0xffffffffu, myw, k);
-#pragma unroll
-          for (int j = 0; j < PPL; ++j) {
-            const double xr = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
-            acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr, r[j], sk, wk));
-          }
-        }
-      }
+      gather_range<VT, KIND, WEIGHTED, PPL>(a.cols, dinv, a.weights, u, ldi, pv, r, beg, end, acc);
       const double d = __ldg(a.degree + row);
       const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
 #pragma unroll
@@ -369,6 +410,50 @@ spmm_kernel(SpmmArgs a) {
   }
 }
 
+// Long rows: sum the segment partials in segment order, then the operator epilogue.  alpha
+// partials go to partial rows [ntiles, ntiles + max_long) (zero for unused rows).
+template <typename VT, int KIND, int PPL>
+__global__ void __launch_bounds__(kSpmmWarps * 32)
+spmm_long_finish_kernel(SpmmArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pbase = blockIdx.y * kBlk + lane;
+  const int64_t nlong = a.long_counts[0];
+  const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
+  VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
+  const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
+  for (int64_t lr = static_cast<int64_t>(blockIdx.x) * kSpmmWarps + warp; lr < a.max_long;
+       lr += static_cast<int64_t>(gridDim.x) * kSpmmWarps) {
+    double dot[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) dot[j] = 0.0;
+    if (lr < nlong) {
+      const int64_t row = a.long_rows[lr];
+      const int64_t s0 = a.long_seg_first[lr], s1 = a.long_seg_first[lr + 1];
+      const double d = __ldg(a.degree + row);
+      const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(a.dinv + row) : 0.0;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        const int p = pbase + 32 * j;
+        if (p >= a.c) continue;
+        double acc = 0.0;
+        for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, a.segpart[sg * a.cpad + p]);
+        const double rj = a.r ? a.r[p] : 1.0;
+        const double x = __dmul_rn(ldg_f64(u + row * a.ldc_in + 32 * j), rj);
+        const double y = op_epilogue<KIND>(x, acc, d, dis, scale);
+        w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
+        dot[j] = fma(x, y, dot[j]);
+      }
+    }
+    if (a.partial) {
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        const int p = pbase + 32 * j;
+        if (p < a.cpad) a.partial[(static_cast<int64_t>(a.ntiles) + lr) * a.cpad + p] = dot[j];
+      }
+    }
+  }
+}
+
 static int ppl_for(int c) {
   const int cb = c < kBlk ? c : kBlk;
   return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
@@ -382,6 +467,16 @@ static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_
   spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
 }
 
+template <typename VT, int KIND>
+static void long_finish_dispatch(SpmmArgs& a, int gy, cudaStream_t st) {
+  dim3 g2(static_cast<unsigned>(std::min<int64_t>((a.max_long + kSpmmWarps - 1) / kSpmmWarps, 148 * 8)), gy);
+  switch (ppl_for(a.c)) {
+    case 1: spmm_long_finish_kernel<VT, KIND, 1><<<g2, kSpmmWarps * 32, 0, st>>>(a); break;
+    case 2: spmm_long_finish_kernel<VT, KIND, 2><<<g2, kSpmmWarps * 32, 0, st>>>(a); break;
+    default: spmm_long_finish_kernel<VT, KIND, 4><<<g2, kSpmmWarps * 32, 0, st>>>(a); break;
+  }
+}
+
 template <typename VT, int KIND, bool W>
 static void spmm_dispatch(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
   switch (ppl_for(a.c)) {
@@ -391,10 +486,8 @@ static void spmm_dispatch(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t 
   }
 }
 
-// coop: alpha is reduced in-kernel (cooperative launch); else the caller runs reduce_kernel.
 template <typename VT>
-static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st) {
-  const int gy = ceil_div(a.c, kBlk);
+static void launch_spmm_main(int kind, SpmmArgs& a, bool coop, int dev, int gy, cudaStream_t st) {
   LaunchScope ls(K_SPMM, st);
   const bool wt = a.weights != nullptr;
   if (kind == SLQ_NORMALIZED_LAPLACIAN) {
@@ -406,6 +499,19 @@ static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t s
   } else {
     if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, gy, coop, dev, st);
     else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, gy, coop, dev, st);
+  }
+}
+
+// The SpMM pass (short rows + long-row segments), then the long-row finish when the graph has any.
+template <typename VT>
+static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st) {
+  const int gy = ceil_div(a.c, kBlk);
+  launch_spmm_main<VT>(kind, a, coop, dev, gy, st);
+  if (a.long_counts && a.max_long > 0) {
+    LaunchScope ls(K_SPMM, st);
+    if (kind == SLQ_NORMALIZED_LAPLACIAN) long_finish_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN>(a, gy, st);
+    else if (kind == SLQ_DENSITY) long_finish_dispatch<VT, SLQ_DENSITY>(a, gy, st);
+    else long_finish_dispatch<VT, SLQ_LAPLACIAN>(a, gy, st);
   }
 }
 
@@ -1090,6 +1196,16 @@ __global__ void scatter_out_kernel(ChunkState s, int64_t col0, int S, double* al
 }
 
 // ----------------------------------------------------------------------------- engine
+static void set_long_rows(SpmmArgs& sa, const slq_graph* g, double* segpart) {
+  sa.long_counts = g->long_counts;
+  sa.long_rows = g->long_rows;
+  sa.long_seg_first = g->long_seg_first;
+  sa.seg_row = g->seg_row;
+  sa.seg_begin = g->seg_begin;
+  sa.max_long = g->max_long;
+  sa.segpart = segpart;
+}
+
 static double host_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -1144,16 +1260,18 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   int rc = SLQ_OK;
 
   const int nq_max = kCgsBlock + 2;
-  const int64_t ptiles = std::max<int64_t>({g->ntiles, g->ntiles_stream, kPersist * kStageSlots});
+  const int64_t ptiles = std::max<int64_t>({g->ntiles + g->max_long, g->ntiles_stream, kPersist * kStageSlots});
   const size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
   const size_t bytes_state = sizeof(double) * cpad * (6 * (S + 1) + 3 + (S + 1) * (S + 1)) +
                              sizeof(int) * (3 * cpad + 4 + S + 4);
   const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
+  const size_t bytes_seg = sizeof(double) * g->max_seg * cpad;
   const size_t off_state = ((bytes_vec + 255) / 256) * 256;
   const size_t off_part = off_state + ((bytes_state + 255) / 256) * 256;
   char* ws = nullptr;
   SLQ_TRACE("before malloc");
-  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_part + bytes_part, st));
+  const size_t off_seg = off_part + ((bytes_part + 255) / 256) * 256;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_seg + bytes_seg, st));
   SLQ_TRACE("after malloc");
   VT* basis = reinterpret_cast<VT*>(ws);
   VT* wv = basis + (S + 1) * vs;
@@ -1193,6 +1311,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
   sa.dscal = g->dscal;
   sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad; sa.partial = partial;
+  set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));
 
   CgsArgs ca{};
   ca.n = n; ca.ldc = ldc; ca.vec_stride = vs; ca.rows_per_tile = g->rows_per_stream_tile;
@@ -1223,7 +1342,8 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   for (int i = 0; i < S; ++i) {
     sa.u = basis + i * vs;
     sa.r = s.rsc + i * cpad;
-    ra.mode = RED_ALPHA; ra.ntiles = g->ntiles; ra.nq = 1; ra.i = i; ra.second = 0; ra.k0 = 0; ra.nk = 0;
+    ra.mode = RED_ALPHA; ra.ntiles = static_cast<int>(g->ntiles + g->max_long); ra.nq = 1; ra.i = i; ra.second = 0;
+    ra.k0 = 0; ra.nk = 0;
     sa.red = ra;
     ca.i = i;
     ca.second = 0;
@@ -1337,7 +1457,11 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
   sa.dscal = g->dscal;
   sa.u = x; sa.r = nullptr; sa.w = y; sa.ldc_in = ld; sa.ldc_out = ld;
   sa.c = static_cast<int>(ncols); sa.cpad = ceil_div(ncols, 32) * 32; sa.partial = nullptr;
+  double* segpart = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&segpart), sizeof(double) * g->max_seg * sa.cpad + 64, st));
+  set_long_rows(sa, g, segpart);
   launch_spmm<double>(kind, sa, false, g->device, st);
+  SLQ_CUDA(cudaFreeAsync(segpart, st));
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
 }

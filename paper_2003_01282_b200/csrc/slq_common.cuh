@@ -13,6 +13,8 @@ namespace slq {
 constexpr int kWarp = 32;
 constexpr int kMaxSteps = 128;     // largest Lanczos step count a rule can carry
 constexpr int kCgsBlock = 16;      // basis vectors handled per CGS sweep (register accumulators)
+constexpr int64_t kLongRow = 1024;  // rows with more nonzeros are split into segments ...
+constexpr int64_t kSeg = 1024;      // ... of this many nonzeros, one warp each
 
 // --- error state (thread local, see slq_last_error) -------------------------
 void set_error(const std::string& msg);
@@ -98,7 +100,14 @@ struct slq_graph {
   double max_degree = 0.0;
   int64_t isolated = 0;
   int unit_weights = 1;
+  // long rows split into kSeg-nonzero segments (device counts: [0] long rows, [1] segments)
+  int64_t max_long = 0, max_seg = 0;   // host upper bounds
+  int64_t* long_counts = nullptr;
+  int32_t* long_rows = nullptr;        // [max_long]
+  int64_t* long_seg_first = nullptr;   // [max_long+1] first segment of each long row
+  int32_t* seg_row = nullptr;          // [max_seg]
+  int64_t* seg_begin = nullptr;        // [max_seg] first nonzero of each segment
   // owned device allocations
-  void* owned[8] = {nullptr};
+  void* owned[12] = {nullptr};
   int n_owned = 0;
 };
