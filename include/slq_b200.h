@@ -161,13 +161,22 @@ int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int64_t n, dou
 /* Host: PCG64 (state_hi, state_lo, inc_hi, inc_lo) of SeedSequence(seed, spawn_key=(index,)). */
 int slq_probe_state(uint64_t seed, uint64_t index, uint64_t out_host[4]);
 
-/* Batched block-diagonal path (C3): per-graph heat signatures of many small graphs stacked
- * in one block-diagonal CSR.  vertex_offsets[G+1] (device int64) delimit the graphs; each
- * graph uses probes 0..n_v-1 restricted to its own n_g vertices (stream prefixes, q0 = v/sqrt(n_g)).
- * Outputs: nodes/weights [G][n_v][steps], steps_out [G][n_v]. */
+/* Batched block-diagonal path (C3): many small graphs stacked in one block-diagonal CSR, one CTA
+ * per graph.  vertex_offsets[G+1] (device int64) delimit the graphs; graph g uses probes
+ * 0..n_v-1 restricted to its own n_g vertices (stream prefixes, q0 = v/sqrt(n_g)) exactly as
+ * netlsd_slq / vnge_slq on that graph alone (descriptors.py:124-149, 227-243).  kind: SLQ_NORMALIZED_LAPLACIAN
+ * or SLQ_DENSITY; n_v <= 64.  Outputs: nodes/weights [G][n_v][steps] (clamped, ascending),
+ * steps_out [G][n_v]; errors OR-ed into the device *status. */
 int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs,
                         int kind, uint64_t seed, int n_v, int steps, int dtype, double* nodes,
-                        double* weights, int32_t* steps_out, void* stream);
+                        double* weights, int32_t* steps_out, int32_t* status, void* stream);
+
+/* Per-graph quadrature + probe aggregate of batched rules: values/std_errors [G][T]
+ * (value = n_g * mean over the graph's probes). */
+int slq_integrate_batched(const double* nodes, const double* weights, const int32_t* steps,
+                          int64_t num_graphs, int n_v, int ld, const int64_t* vertex_offsets,
+                          const double* t, int64_t T, int fn, double* values, double* std_errors,
+                          int32_t* status, void* stream);
 
 /* Diagnostics */
 const char* slq_last_error(void);

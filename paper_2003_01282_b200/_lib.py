@@ -55,7 +55,8 @@ _SIGS = {
     "slq_rules": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "slq_integrate": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _int, _dbl, _vp, _vp, _vp, _vp, _vp]),
     "slq_signature": (_int, [_vp, _int, _u64, _i64, _int, _int, _int, _vp, _i64, _vp, _int, _vp, _vp, _vp, _vp]),
-    "slq_lanczos_batched": (_int, [_vp, _vp, _i64, _int, _u64, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "slq_lanczos_batched": (_int, [_vp, _vp, _i64, _int, _u64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "slq_integrate_batched": (_int, [_vp, _vp, _vp, _i64, _int, _int, _vp, _vp, _i64, _int, _vp, _vp, _vp, _vp]),
     "slq_last_error": (ctypes.c_char_p, []),
     "slq_launch_count": (_u64, []),
     "slq_profile_begin": (None, []),

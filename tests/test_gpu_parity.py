@@ -372,3 +372,37 @@ def test_long_rows_split_into_segments(cuda_device):
     v = vnge_slq(g, cfg)
     rv, _ = O.vnge(g, 24, 15, 2)
     assert abs(v.value - rv) <= FP64_TOL * abs(rv)
+
+
+# batched block-diagonal path (C3)
+def test_batched_er_sample_matches_reference(cuda_device):
+    from paper_2003_01282_b200.batched import netlsd_slq_batch
+
+    z = golden.load("erbatch40.npz")
+    graphs = [golden.graph(z, f"{k}/") for k in range(int(z["count"]))]
+    cfg = SlqConfig(n_v=20, s=10, seed=0)
+    vals, stds = netlsd_slq_batch(graphs, GRID, cfg)
+    vals32, _ = netlsd_slq_batch(graphs, GRID, cfg, dtype="f32")
+    for k in range(len(graphs)):
+        ref = z[f"{k}/heat"]
+        assert golden.rel_l2(vals[k], ref) <= FP64_TOL, k
+        assert np.allclose(stds[k], z[f"{k}/heat_std"], rtol=1e-6, atol=1e-10), k
+        assert golden.rel_l2(vals32[k], ref) <= FP32_TOL, k
+
+
+def test_batched_matches_single_graph_path_and_vnge(cuda_device):
+    from paper_2003_01282_b200 import synth
+    from paper_2003_01282_b200.batched import netlsd_slq_batch, vnge_slq_batch
+
+    graphs = synth.er_batch(30, seed=7) + [csr_from_edges(5, [0, 1, 2, 3], [1, 2, 3, 4]),
+                                          csr_from_edges(3, [0, 1], [1, 2])]   # n < s: steps clamp
+    cfg = SlqConfig(n_v=16, s=12, seed=4)
+    vals, _ = netlsd_slq_batch(graphs, GRID, cfg)
+    ents, _ = vnge_slq_batch(graphs, cfg)
+    for k, g in enumerate(graphs):
+        single = netlsd_slq(g, GRID, cfg).values
+        assert golden.rel_l2(vals[k], single) <= 1e-12, k
+        rv, _ = O.vnge(g, 16, 12, 4)
+        assert abs(ents[k] - rv) <= FP64_TOL * max(abs(rv), 1e-12), k
+    with pytest.raises(ValueError, match="without edges"):
+        vnge_slq_batch(graphs + [csr_from_edges(4, [], [])], cfg)

@@ -26,13 +26,60 @@ CONFIGS = {
 KIND = {"nl": "normalized_laplacian", "p": "density"}
 
 
+def run_c3(args):
+    """10,000 ER graphs (n ~ U{20..200}, p ~ U[0.05,0.3]) stacked block-diagonally, n_v=20, s=10,
+    per-graph heat on 250 t; fp32 per BASELINE (fp64 also reported)."""
+    from paper_2003_01282_b200.batched import BatchedGraphs, netlsd_slq_batch
+    from paper_2003_01282_b200.slq import SlqConfig
+
+    t0 = time.perf_counter()
+    graphs = synth.er_batch(args.graphs, seed=0)
+    batch = BatchedGraphs(graphs)
+    gen_s = time.perf_counter() - t0
+    grid = TimeGrid(1e-2, 1e2, 250)
+    cfg = SlqConfig(n_v=20, s=10, seed=0)
+    out = {"config": "c3", "graphs": len(graphs), "n": batch.stacked.n, "nnz": batch.stacked.nnz, "gen_s": gen_s}
+    for dtype in ("f32", "f64"):
+        times = []
+        for _ in range(args.reps + 1):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rules = batch.rules("normalized_laplacian", cfg, dtype)
+            vals, stds = batch.integrate(rules, grid.values, _lib.FN_HEAT)
+            e1.record()
+            torch.cuda.synchronize()
+            _lib.check_status(int(rules[3].item()))
+            times.append(e0.elapsed_time(e1))
+        ms = float(np.median(times[1:]))
+        units = batch.stacked.nnz * cfg.n_v * cfg.s
+        out[dtype] = {"ms": ms, "units_per_s": units / (ms * 1e-3), "graphs_per_s": len(graphs) / (ms * 1e-3),
+                      "times": times}
+    if args.check_probes:
+        from oracle import slq_oracle as O
+
+        k = min(50, len(graphs))
+        t1 = time.perf_counter()
+        ref = [O.heat_trace(graphs[j], grid.values, 20, 10, 0)[0] for j in range(k)]
+        cpu_s = time.perf_counter() - t1
+        for dtype in ("f64", "f32"):
+            vals, _ = netlsd_slq_batch(batch, grid, cfg, dtype=dtype)
+            errs = [float(np.linalg.norm(vals[j] - ref[j]) / np.linalg.norm(ref[j])) for j in range(k)]
+            out[dtype]["parity_max_rel_l2_first50"] = max(errs)
+        out["cpu_oracle_s_per_graph"] = cpu_s / k
+    print(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--check-probes", type=int, default=8)
     ap.add_argument("--dtype", default="f64")
+    ap.add_argument("--graphs", type=int, default=10_000)
     args = ap.parse_args()
+    if args.config == "c3":
+        return run_c3(args)
     cfg = CONFIGS[args.config]
     t0 = time.perf_counter()
     g = cfg["make"]()
