@@ -504,10 +504,10 @@ static void launch_spmm_main(int kind, SpmmArgs& a, bool coop, int dev, int gy, 
 
 // The SpMM pass (short rows + long-row segments), then the long-row finish when the graph has any.
 template <typename VT>
-static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st) {
+static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st, bool finish = true) {
   const int gy = ceil_div(a.c, kBlk);
   launch_spmm_main<VT>(kind, a, coop, dev, gy, st);
-  if (a.long_counts && a.max_long > 0) {
+  if (finish && a.long_counts && a.max_long > 0) {
     LaunchScope ls(K_SPMM, st);
     if (kind == SLQ_NORMALIZED_LAPLACIAN) long_finish_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN>(a, gy, st);
     else if (kind == SLQ_DENSITY) long_finish_dispatch<VT, SLQ_DENSITY>(a, gy, st);
@@ -728,6 +728,7 @@ struct StagedArgs {
 struct StepArgs {
   StagedArgs pass[2];             // [0]: src = w (phases A, C), [1]: src = u_{i+1} (phase C')
   ReduceArgs red;
+  SpmmArgs spmm;                  // long rows of the preceding SpMM are finished in phase 0
 };
 
 template <typename VT>
@@ -1035,6 +1036,33 @@ cgs_step_kernel(StepArgs sa) {
   const StagedArgs& st0 = sa.pass[0];
   const int nch0 = chunk_count(lo, hi, st0.rt);
 
+  // 0: finish the SpMM's long rows (segment partials in order + epilogue); skipped when none
+  const SpmmArgs& sp = sa.spmm;
+  const int64_t nlong = sp.long_counts ? sp.long_counts[0] : 0;
+  if (nlong > 0) {
+    const int nw = blockDim.x >> 5;
+    const VT* uu = static_cast<const VT*>(sp.u);
+    VT* ww = static_cast<VT*>(sp.w);
+    const double scale = sp.dscal[3];
+    for (int64_t lr = static_cast<int64_t>(blockIdx.x) * nw + warp; lr < nlong;
+         lr += static_cast<int64_t>(gridDim.x) * nw) {
+      const int64_t row = sp.long_rows[lr];
+      const int64_t s0 = sp.long_seg_first[lr], s1 = sp.long_seg_first[lr + 1];
+      const double d = sp.degree[row], dis = sp.dinv[row];
+      for (int p = lane; p < sp.c; p += 32) {
+        double acc = 0.0;
+        for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, sp.segpart[sg * sp.cpad + p]);
+        const double x = __dmul_rn(to_f64(uu[row * sp.ldc_in + p]), sp.r[p]);
+        double y;
+        if (sa.red.kind == SLQ_NORMALIZED_LAPLACIAN) y = op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, acc, d, dis, scale);
+        else if (sa.red.kind == SLQ_DENSITY) y = op_epilogue<SLQ_DENSITY>(x, acc, d, dis, scale);
+        else y = op_epilogue<SLQ_LAPLACIAN>(x, acc, d, dis, scale);
+        ww[row * sp.ldc_out + p] = from_f64<VT>(y);
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // w is bulk-read in phase A
+    sync_grid();
+  }
   // A: u_k . w for k <= i (and u_0 . u_0 at i == 0)
   const int nqa = nk + (a.i == 0 ? 1 : 0);
   if (threadIdx.x < 32) {
@@ -1112,12 +1140,14 @@ static int coop_supported(int dev) {
 // Launch everything after the SpMM of step i as one persistent kernel; false when the staged path
 // does not apply (the caller then runs the separate kernels).
 template <typename VT>
-static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, int dev, cudaStream_t st, int* rc) {
+static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, int dev,
+                            cudaStream_t st, int* rc) {
   *rc = SLQ_OK;
   if (!coop_supported(dev)) return false;
   StepArgs sa{};
   if (!staged_setup<VT>(a, false, &sa.pass[0]) || !staged_setup<VT>(a, true, &sa.pass[1])) return false;
   sa.red = red;
+  sa.spmm = spmm;
   const size_t smem = 128 + kStages * std::max(static_cast<size_t>(sa.pass[0].nvec) * sa.pass[0].rt,
                                                static_cast<size_t>(sa.pass[1].nvec) * sa.pass[1].rt) *
                                 a.ldc * sizeof(VT);
@@ -1352,12 +1382,12 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     const bool staged = coop && reorth && i < S - 1 && i + 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
     sa.partial = staged ? nullptr : partial;
     SLQ_TRACE("spmm launch");
-    launch_spmm<VT>(kind, sa, false, g->device, st);
+    launch_spmm<VT>(kind, sa, false, g->device, st, /*finish=*/!staged);   // staged: phase 0 finishes
     SLQ_TRACE("spmm launched");
     if (!staged) launch_reduce(ra, st);
     if (i == S - 1) break;
     if (staged) {
-      const bool done = launch_cgs_step<VT>(ca, ra, g->device, st, &rc);
+      const bool done = launch_cgs_step<VT>(ca, ra, sa, g->device, st, &rc);
       SLQ_TRACE("step launched");
       if (rc) return rc;
       if (done) continue;
