@@ -15,8 +15,9 @@
 
 namespace slq {
 
-constexpr int kMaxTiles = 148 * 16;   // SpMM tiles: <= 16 per SM
-constexpr int64_t kMinTileCost = 512;
+constexpr int kMaxTiles = 148 * 256;  // SpMM warp tiles (dynamically scheduled): ~8 per resident warp
+constexpr int kMaxStreamTiles = 148 * 16;
+constexpr int64_t kMinTileCost = 64;
 constexpr int64_t kRowCost = 2;       // per-row overhead in nonzero-equivalents
 constexpr int64_t kMinStreamRows = 128;
 
@@ -221,7 +222,7 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
     LaunchScope ls(K_PREPARE, st);
     tile_kernel<<<ceil_div(g->ntiles + 1, 256), 256, 0, st>>>(g->offsets, n, target, g->ntiles, g->tile_rows);
   }
-  g->rows_per_stream_tile = std::max<int64_t>(kMinStreamRows, (n + kMaxTiles - 1) / kMaxTiles);
+  g->rows_per_stream_tile = std::max<int64_t>(kMinStreamRows, (n + kMaxStreamTiles - 1) / kMaxStreamTiles);
   g->ntiles_stream = std::max(1, ceil_div(n, g->rows_per_stream_tile));
   g->m = nnz / 2;
   // long-row segments (device-side counts; host-side upper bounds size the buffers)

@@ -101,11 +101,13 @@ struct ChunkState {
   int* again = nullptr;     // [cpad]
   int* any_again = nullptr; // [1]
   unsigned int* barrier = nullptr;   // [S] grid-barrier counters of the persistent step kernels
+  unsigned long long* work = nullptr;   // [S][4] SpMM work counters
 };
 
 __global__ void state_init_kernel(ChunkState s, int64_t n, int given_start) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < s.S) s.barrier[p] = 0u;
+  if (p < 4 * s.S) s.work[p] = 0ull;
   if (p >= s.cpad) return;
   const bool pv = p < s.c;
   // r_0: the probe +-1 block is scaled by 1/fl(sqrt(n)) (= 1/||v||); a caller-given unit start
@@ -248,6 +250,7 @@ struct SpmmArgs {
   const int64_t* seg_begin;
   int64_t max_long;
   double* segpart;
+  unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
 };
 
 template <int KIND>
@@ -322,14 +325,15 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
   }
 }
 
-// Pass A.  Work items: first the long-row segments (one warp each, partial sums to a.segpart),
-// then the graph-fixed row tiles (one warp per short row; alpha partials per tile).  Long rows are
-// finished by spmm_long_finish_kernel (segment partials summed in segment order).
+// Pass A.  Warp-level work items taken from an atomic counter: first the long-row segments (partial
+// sums to a.segpart), then the graph-fixed row tiles (one warp per tile: rows in order, alpha
+// partial per tile).  Which warp runs an item never changes its arithmetic, so results are
+// deterministic; dynamic scheduling removes the tail left by hub rows.  Long rows are finished by
+// spmm_long_finish_kernel or the step kernel's phase 0.
 template <typename VT, int KIND, bool WEIGHTED, int PPL, bool COOP>
 __global__ void __launch_bounds__(kSpmmWarps * 32, 4)
 spmm_kernel(SpmmArgs a) {
-  __shared__ double red[kSpmmWarps][kBlk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int pbase = blockIdx.y * kBlk + lane;
   bool pv[PPL];
   double r[PPL];
@@ -344,33 +348,40 @@ spmm_kernel(SpmmArgs a) {
   const double* __restrict__ dinv = a.dinv;
   const int64_t ldi = a.ldc_in;
   const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
-
-  // long-row segments
   const int64_t nseg = a.long_counts ? a.long_counts[1] : 0;
-  for (int64_t sb = static_cast<int64_t>(blockIdx.x) * kSpmmWarps; sb < nseg;
-       sb += static_cast<int64_t>(gridDim.x) * kSpmmWarps) {
-    const int64_t sgi = sb + warp;
-    if (sgi >= nseg) continue;
-    const int64_t row = a.seg_row[sgi];
-    const int64_t beg = a.seg_begin[sgi];
+  unsigned long long* counter = a.work + blockIdx.y;   // [0..1] segments, [2..3] tiles (per probe block)
+
+  // phase 1: long-row segments, one warp each (dynamic)
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = static_cast<long long>(atomicAdd(counter, 1ull));
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= nseg) break;
+    const int64_t row = a.seg_row[item];
+    const int64_t beg = a.seg_begin[item];
     const int64_t rend = off[row + 1];
     const int64_t end = beg + kSeg < rend ? beg + kSeg : rend;
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
     gather_range<VT, KIND, WEIGHTED, PPL>(a.cols, dinv, a.weights, u, ldi, pv, r, beg, end, acc);
-    double* dst = a.segpart + sgi * a.cpad + pbase;
+    double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
     for (int j = 0; j < PPL; ++j)
       if (pv[j]) dst[32 * j] = acc[j];
   }
-
-  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+  // phase 2: row tiles, one warp each (dynamic); rows in order, alpha partial per tile
+  unsigned long long* tcounter = counter + 2;
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = static_cast<long long>(atomicAdd(tcounter, 1ull));
+    const int tile = static_cast<int>(__shfl_sync(0xffffffffu, item, 0));
+    if (tile >= a.ntiles) break;
     const int64_t rb = a.tile_rows[tile], re = a.tile_rows[tile + 1];
     double dot[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) dot[j] = 0.0;
-    for (int64_t row = rb + warp; row < re; row += kSpmmWarps) {
+    for (int64_t row = rb; row < re; ++row) {
       const int64_t beg = off[row], end = off[row + 1];
       if (a.long_counts && end - beg > kLongRow) continue;   // finished from its segments
       double acc[PPL];
@@ -390,23 +401,9 @@ spmm_kernel(SpmmArgs a) {
     }
     if (a.partial) {
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) red[warp][lane + 32 * j] = dot[j];
-      __syncthreads();
-      for (int pl = threadIdx.x; pl < PPL * 32; pl += blockDim.x) {
-        const int p = blockIdx.y * kBlk + pl;
-        double s = red[0][pl];
-#pragma unroll
-        for (int v = 1; v < kSpmmWarps; ++v) s += red[v][pl];
-        if (p < a.cpad) a.partial[static_cast<int64_t>(tile) * a.cpad + p] = s;
-      }
-      __syncthreads();
+      for (int j = 0; j < PPL; ++j)
+        if (pbase + 32 * j < a.cpad) a.partial[static_cast<int64_t>(tile) * a.cpad + pbase + 32 * j] = dot[j];
     }
-  }
-  if (COOP) {
-    // alpha_i = q_i . w over all tiles (fixed-order stripes), by the first cpad/32 CTAs
-    cg::this_grid().sync();
-    const int nblk = gridDim.x * gridDim.y, lb = blockIdx.y * gridDim.x + blockIdx.x;
-    for (int sl = lb; sl < a.cpad / 32; sl += nblk) reduce_slice(a.red, 0, sl, &red[0][0]);
   }
 }
 
@@ -1293,7 +1290,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const int64_t ptiles = std::max<int64_t>({g->ntiles + g->max_long, g->ntiles_stream, kPersist * kStageSlots});
   const size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
   const size_t bytes_state = sizeof(double) * cpad * (6 * (S + 1) + 3 + (S + 1) * (S + 1)) +
-                             sizeof(int) * (3 * cpad + 4 + S + 4);
+                             sizeof(int) * (3 * cpad + 4 + S + 4) + sizeof(unsigned long long) * (4 * S + 2);
   const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
   const size_t bytes_seg = sizeof(double) * g->max_seg * cpad;
   const size_t off_state = ((bytes_vec + 255) / 256) * 256;
@@ -1323,11 +1320,13 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   s.again = istate + 2 * cpad;
   s.any_again = istate + 3 * cpad;
   s.barrier = reinterpret_cast<unsigned int*>(istate + 3 * cpad + 4);
+  s.work = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(s.barrier + S) + 15) & ~static_cast<uintptr_t>(15));
   double* partial = reinterpret_cast<double*>(ws + off_part);
 
   {
     LaunchScope ls(K_PROBE, st);
-    state_init_kernel<<<ceil_div(std::max(cpad, S), 128), 128, 0, st>>>(s, n, q0 != nullptr);
+    state_init_kernel<<<ceil_div(std::max(cpad, 4 * S), 128), 128, 0, st>>>(s, n, q0 != nullptr);
   }
   if (q0) {
     LaunchScope ls(K_PROBE, st);
@@ -1375,6 +1374,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     ra.mode = RED_ALPHA; ra.ntiles = static_cast<int>(g->ntiles + g->max_long); ra.nq = 1; ra.i = i; ra.second = 0;
     ra.k0 = 0; ra.nk = 0;
     sa.red = ra;
+    sa.work = s.work + 4 * i;
     ca.i = i;
     ca.second = 0;
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
@@ -1481,17 +1481,28 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
   if (ncols <= 0 || g->n == 0) return SLQ_OK;
   if (ld < ncols) return fail(SLQ_ERR_VALUE, "ld < ncols");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SpmmArgs sa{};
-  sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
-  sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
-  sa.dscal = g->dscal;
-  sa.u = x; sa.r = nullptr; sa.w = y; sa.ldc_in = ld; sa.ldc_out = ld;
-  sa.c = static_cast<int>(ncols); sa.cpad = ceil_div(ncols, 32) * 32; sa.partial = nullptr;
+  constexpr int64_t kCols = 2 * kBlk;   // columns per pass (two 128-probe blocks)
+  const int64_t passes = (ncols + kCols - 1) / kCols;
   double* segpart = nullptr;
-  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&segpart), sizeof(double) * g->max_seg * sa.cpad + 64, st));
-  set_long_rows(sa, g, segpart);
-  launch_spmm<double>(kind, sa, false, g->device, st);
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&segpart), sizeof(double) * g->max_seg * kCols + 64, st));
+  unsigned long long* work = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work), sizeof(unsigned long long) * 4 * passes, st));
+  SLQ_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) * 4 * passes, st));
+  for (int64_t pi = 0; pi < passes; ++pi) {
+    const int64_t j0 = pi * kCols;
+    SpmmArgs sa{};
+    sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
+    sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
+    sa.dscal = g->dscal;
+    sa.u = x + j0; sa.r = nullptr; sa.w = y + j0; sa.ldc_in = ld; sa.ldc_out = ld;
+    sa.c = static_cast<int>(std::min<int64_t>(kCols, ncols - j0));
+    sa.cpad = ceil_div(sa.c, 32) * 32; sa.partial = nullptr;
+    sa.work = work + 4 * pi;
+    set_long_rows(sa, g, segpart);
+    launch_spmm<double>(kind, sa, false, g->device, st);
+  }
   SLQ_CUDA(cudaFreeAsync(segpart, st));
+  SLQ_CUDA(cudaFreeAsync(work, st));
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
 }
