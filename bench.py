@@ -175,8 +175,9 @@ def algorithmic_bytes(g, c, s, vb):
     n, nnz = g.n, g.nnz
     row = c * vb
     spmm = s * (nnz * (row + 4) + n * (2 * row + 24))
-    # CGS step kernel, step i: phase A streams w,u_0..u_i; phase C streams them again and writes u_{i+1}
-    step = sum(n * row * (2 * (i + 2) + 1) for i in range(s - 1))
+    # CGS step kernel, step i: phase A streams w, u_1..u_i and the probe bitmask (u_0, 16 B/row);
+    # phase C streams them again and writes u_{i+1}
+    step = sum(n * row * (2 * (i + 1) + 1) + 2 * n * 16 for i in range(s - 1))
     return {"spmm": spmm, "cgs_step": step}
 
 

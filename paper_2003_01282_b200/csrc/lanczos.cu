@@ -41,34 +41,56 @@ constexpr int kSecondPassGrid = 148 * 4;
 constexpr int kMaxChunk = 256;       // probes per chunk (flat CGS CTAs of <= 512 threads)
 
 // ----------------------------------------------------------------------------- probes
+// Rademacher probes: u (if not null) gets +-1 values; bits (if not null) gets one bit per probe,
+// bits[row][kBitWords] with word g = probes 32g..32g+31 (bit set = +1).  A warp = 32 probes of one
+// group over a run of 2*kProbeRun rows.
+constexpr int kBitWords = 4;   // bitmask row stride in 32-bit words (16 B: bulk-copy aligned; c <= 128)
+
 template <typename VT>
 __global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* __restrict__ u,
-                                  int64_t ldc) {
+                                  int64_t ldc, uint32_t* __restrict__ bits) {
   const int lane = threadIdx.x & 31;
   const int64_t run = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int p = blockIdx.y * 32 + lane;
   const int64_t row0 = run * (2 * kProbeRun);
-  if (p >= c || row0 >= n) return;
-  u128 st, inc;
-  pcg64_seed_state(seed, static_cast<uint64_t>(probe_begin + p), &st, &inc);
-  st = pcg_advance(st, inc, static_cast<uint64_t>(run) * kProbeRun);
+  if (row0 >= n) return;                       // warp-uniform
+  const bool pv = p < c;
+  u128 st = 0, inc = 0;
+  if (pv) {
+    pcg64_seed_state(seed, static_cast<uint64_t>(probe_begin + p), &st, &inc);
+    st = pcg_advance(st, inc, static_cast<uint64_t>(run) * kProbeRun);
+  }
   const u128 mult = pcg_mult();
   for (int m = 0; m < kProbeRun; ++m) {
-    st = st * mult + inc;
-    const uint64_t out = pcg_output(st);
+    uint64_t out = 0;
+    if (pv) {
+      st = st * mult + inc;
+      out = pcg_output(st);
+    }
     const int64_t r = row0 + 2 * m;
-    if (r < n) u[r * ldc + p] = from_f64<VT>(((out >> 31) & 1u) ? 1.0 : -1.0);
-    if (r + 1 < n) u[(r + 1) * ldc + p] = from_f64<VT>(((out >> 63) & 1u) ? 1.0 : -1.0);
+    const bool b0 = (out >> 31) & 1u, b1 = (out >> 63) & 1u;
+    if (u && pv) {
+      if (r < n) u[r * ldc + p] = from_f64<VT>(b0 ? 1.0 : -1.0);
+      if (r + 1 < n) u[(r + 1) * ldc + p] = from_f64<VT>(b1 ? 1.0 : -1.0);
+    }
+    if (bits) {
+      const uint32_t w0 = __ballot_sync(0xffffffffu, pv && b0);
+      const uint32_t w1 = __ballot_sync(0xffffffffu, pv && b1);
+      if (lane == 0) {
+        if (r < n) bits[r * kBitWords + blockIdx.y] = w0;
+        if (r + 1 < n) bits[(r + 1) * kBitWords + blockIdx.y] = w1;
+      }
+    }
   }
 }
 
 template <typename VT>
 static void launch_probes(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* u, int64_t ldc,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint32_t* bits = nullptr) {
   const int64_t runs = (n + 2 * kProbeRun - 1) / (2 * kProbeRun);
   dim3 grid(ceil_div(runs, 4), ceil_div(c, 32));
   LaunchScope ls(K_PROBE, st);
-  probe_init_kernel<VT><<<grid, 128, 0, st>>>(seed, probe_begin, c, n, u, ldc);
+  probe_init_kernel<VT><<<grid, 128, 0, st>>>(seed, probe_begin, c, n, u, ldc, bits);
 }
 
 template <typename VT>
@@ -251,6 +273,7 @@ struct SpmmArgs {
   int64_t max_long;
   double* segpart;
   unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
+  const uint32_t* bits;      // first step: u_0 as a probe bitmask [n][kBitWords] (nullptr = use u)
 };
 
 template <int KIND>
@@ -280,10 +303,11 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
 // acc[j] += sum over nonzeros [beg, end) of one row, in stored order (sequential, unfused: the
 // reference's csr_matvec order).  Columns are loaded 32 at a time and broadcast by shuffles; UNR
 // gathers are in flight per lane.
-template <typename VT, int KIND, bool WEIGHTED, int PPL>
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS>
 __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
                                              const double* __restrict__ wts, const VT* __restrict__ u, int64_t ldi,
-                                             const bool* pv, const double* r, int64_t beg, int64_t end, double* acc) {
+                                             const uint32_t* __restrict__ bits, const bool* pv, const double* r,
+                                             int64_t beg, int64_t end, double* acc) {
   const int lane = threadIdx.x & 31;
   for (int64_t base = beg; base < end; base += 32) {
     const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
@@ -300,9 +324,18 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       double xv[UNR][PPL];
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q)) * ldi;
+        const int64_t cq = static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q));
+        if (BITS) {
+          // u_0 = +-1 from the probe bitmask: one uniform 16-byte load covers 128 probes
+          const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + cq * kBitWords));
+          const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+          for (int j = 0; j < PPL; ++j) xv[q][j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
+        } else {
+          const VT* src = u + cq * ldi;
+#pragma unroll
+          for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+        }
       }
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
@@ -313,16 +346,34 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       }
     }
     for (; k < cnt; ++k) {
-      const VT* src = u + static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k)) * ldi;
+      const int64_t cq = static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k));
       const double sk = __shfl_sync(0xffffffffu, mys, k);
       const double wk = __shfl_sync(0xffffffffu, myw, k);
+      double xr[PPL];
+      if (BITS) {
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + cq * kBitWords));
+        const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) {
-        const double xr = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
-        acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr, r[j], sk, wk));
+        for (int j = 0; j < PPL; ++j) xr[j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
+      } else {
+        const VT* src = u + cq * ldi;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) xr[j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
       }
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr[j], r[j], sk, wk));
     }
   }
+}
+
+// own-row value u[row][probe j] (from the bitmask on the first step)
+template <typename VT, int PPL, bool BITS>
+__device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint32_t* bits, int64_t row, int j) {
+  if (BITS) {
+    const uint32_t wd = __ldg(bits + row * kBitWords + j);
+    return ((wd >> (threadIdx.x & 31)) & 1u) ? 1.0 : -1.0;
+  }
+  return ldg_f64(u + row * ldi + 32 * j);
 }
 
 // Pass A.  Warp-level work items taken from an atomic counter: first the long-row segments (partial
@@ -330,7 +381,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
 // partial per tile).  Which warp runs an item never changes its arithmetic, so results are
 // deterministic; dynamic scheduling removes the tail left by hub rows.  Long rows are finished by
 // spmm_long_finish_kernel or the step kernel's phase 0.
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool COOP>
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS>
 __global__ void __launch_bounds__(kSpmmWarps * 32, 4)
 spmm_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
@@ -364,7 +415,7 @@ spmm_kernel(SpmmArgs a) {
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-    gather_range<VT, KIND, WEIGHTED, PPL>(a.cols, dinv, a.weights, u, ldi, pv, r, beg, end, acc);
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS>(a.cols, dinv, a.weights, u, ldi, a.bits, pv, r, beg, end, acc);
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
     for (int j = 0; j < PPL; ++j)
@@ -387,13 +438,13 @@ spmm_kernel(SpmmArgs a) {
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      gather_range<VT, KIND, WEIGHTED, PPL>(a.cols, dinv, a.weights, u, ldi, pv, r, beg, end, acc);
+      gather_range<VT, KIND, WEIGHTED, PPL, BITS>(a.cols, dinv, a.weights, u, ldi, a.bits, pv, r, beg, end, acc);
       const double d = __ldg(a.degree + row);
       const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         if (!pv[j]) continue;
-        const double x = __dmul_rn(ldg_f64(u + row * ldi + 32 * j), r[j]);
+        const double x = __dmul_rn(own_value<VT, PPL, BITS>(u, ldi, a.bits, row, j), r[j]);
         const double y = op_epilogue<KIND>(x, acc[j], d, dis, scale);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
         dot[j] = fma(x, y, dot[j]);
@@ -435,7 +486,9 @@ spmm_long_finish_kernel(SpmmArgs a) {
         double acc = 0.0;
         for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, a.segpart[sg * a.cpad + p]);
         const double rj = a.r ? a.r[p] : 1.0;
-        const double x = __dmul_rn(ldg_f64(u + row * a.ldc_in + 32 * j), rj);
+        const double own = a.bits ? (((a.bits[row * kBitWords + j] >> lane) & 1u) ? 1.0 : -1.0)
+                                  : ldg_f64(u + row * a.ldc_in + 32 * j);
+        const double x = __dmul_rn(own, rj);
         const double y = op_epilogue<KIND>(x, acc, d, dis, scale);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
         dot[j] = fma(x, y, dot[j]);
@@ -460,8 +513,9 @@ template <typename VT, int KIND, bool W, int PPL>
 static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
   (void)coop;
   (void)dev;
-  dim3 grid(std::min(a.ntiles, 148 * 4), gy);
-  spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  dim3 grid(148 * 4, gy);   // persistent: work is taken from the atomic counters
+  if (a.bits) spmm_kernel<VT, KIND, W, PPL, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  else spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
 }
 
 template <typename VT, int KIND>
@@ -715,8 +769,9 @@ constexpr size_t kStagedSmem = 200 * 1024;   // + 20 KB static: within the 227 K
 
 struct StagedArgs {
   CgsArgs a;
-  int nvec;                       // vectors staged per chunk
+  int nvec;                       // VT vectors staged per chunk (source + u_1..u_{NK-1})
   const void* vec[kMaxStaged];    // global base of each staged vector
+  const uint32_t* bits;           // u_0 as the probe bitmask [n][kBitWords], staged after the vectors
   int slot_src, slot_ui, slot_uim1;
   int slot_k[kCgsBlock];          // slot of basis vector k
   int rt;                         // rows per chunk
@@ -740,6 +795,16 @@ struct StageRing {
   }
 };
 
+// One ring stage: nvec VT row blocks [rt][ldc], then the bitmask rows [rt][kBitWords] (in VT units).
+template <typename VT>
+__host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int64_t ldc) {
+  return static_cast<int64_t>(nvec) * rt * ldc + (static_cast<int64_t>(rt) * kBitWords * 4 + sizeof(VT) - 1) / sizeof(VT);
+}
+
+__device__ __forceinline__ double bit_value(const uint32_t* brow, int p) {
+  return ((brow[p >> 5] >> (p & 31)) & 1u) ? 1.0 : -1.0;
+}
+
 __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
   return hi > lo ? static_cast<int>((hi - lo + rt - 1) / rt) : 0;
 }
@@ -748,18 +813,20 @@ __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
 template <typename VT>
 __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
   const int64_t ldc = sa.a.ldc;
-  const int64_t stage_elems = static_cast<int64_t>(sa.nvec) * sa.rt * ldc;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, ldc);
   int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
     const int s = ch % kStages;
     if (ch >= kStages) mbar_wait(&ring.empty[s], ((ch / kStages) - 1) & 1);
     const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
     const uint32_t bytes = static_cast<uint32_t>(rows * ldc * sizeof(VT));
-    mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec);
+    const uint32_t bbytes = static_cast<uint32_t>(rows * kBitWords * sizeof(uint32_t));
+    mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec + bbytes);
     VT* dst = ring.buf + s * stage_elems;
     for (int v = 0; v < sa.nvec; ++v)
       bulk_g2s(dst + static_cast<int64_t>(v) * sa.rt * ldc, static_cast<const VT*>(sa.vec[v]) + r0 * ldc, bytes,
                &ring.full[s]);
+    bulk_g2s(dst + static_cast<int64_t>(sa.nvec) * sa.rt * ldc, sa.bits + r0 * kBitWords, bbytes, &ring.full[s]);
   }
 }
 
@@ -768,9 +835,20 @@ __device__ __forceinline__ double gram_at(const ChunkState& s, int k, int j, int
   return s.G[(static_cast<int64_t>(k) * (s.S + 1) + j) * s.cpad + p];
 }
 
-// Shared-memory stage layout: [slot][row][ldc], slot 0 = source (w or u_{i+1}), slot 1+k = u_k.
-// NK = i + 1 basis vectors is a compile-time constant, so every loop below is fully unrolled with
-// no predicates and the per-vector offsets stay in registers.
+// Shared-memory stage layout: [slot][row][ldc] with slot 0 = source (w or u_{i+1}) and slot k = u_k
+// for k >= 1, then the probe bitmask rows (u_0 = +-1).  NK = i + 1 basis vectors is a compile-time
+// constant, so every loop below is fully unrolled with no predicates.
+
+template <typename VT, int NK>
+struct StageView {
+  const VT* e;             // this thread's element of row r in slot 0
+  const uint32_t* brow;    // bitmask row r
+  int vstride, p;
+  __device__ __forceinline__ double src() const { return to_f64(e[0]); }
+  __device__ __forceinline__ double u(int k) const {   // k is a compile-time constant after unrolling
+    return k == 0 ? bit_value(brow, p) : to_f64(e[k * vstride]);
+  }
+};
 
 // Phase A (consumer side): partials [cta*slots+slot][nq][cpad] of u_k . w (k < NK); at i == 0 also
 // u_0 . u_0 (q = 1) for G(0,0).
@@ -784,7 +862,7 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
   const int rt = sa.rt;
   const int vstride = rt * ldc;
-  const int64_t stage_elems = static_cast<int64_t>(NK + 1) * vstride;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, ldc);
   double acc[NK];
 #pragma unroll
   for (int kk = 0; kk < NK; ++kk) acc[kk] = 0.0;
@@ -795,19 +873,16 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
     const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
     if (pv) {
-      const VT* base = ring.buf + s * stage_elems + p;
+      const VT* stage = ring.buf + s * stage_elems;
+      const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
       // this thread's rows: (row - lo) % kStageSlots == slot, ascending
       int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
       for (; r < rows; r += kStageSlots) {
-        const VT* e = base + r * ldc;
-        const double wv = to_f64(e[0]);
-        const VT* uk = e + vstride;
+        const StageView<VT, NK> v{stage + p + r * ldc, sbits + r * kBitWords, vstride, p};
+        const double wv = v.src();
 #pragma unroll
-        for (int kk = 0; kk < NK; ++kk) acc[kk] = fma(to_f64(uk[kk * vstride]), wv, acc[kk]);
-        if (NK == 1) {
-          const double u0 = to_f64(uk[0]);
-          g00 = fma(u0, u0, g00);
-        }
+        for (int kk = 0; kk < NK; ++kk) acc[kk] = fma(v.u(kk), wv, acc[kk]);
+        if (NK == 1) g00 += 1.0;   // u_0 . u_0 = number of rows (+-1 entries)
       }
     }
     __syncwarp();
@@ -834,7 +909,7 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
   const bool pv = p < a.c && (!SECOND || S.again[p]);
   constexpr int nq = NK + 2;
-  const int i = NK - 1;
+  constexpr int i = NK - 1;
   double al = 0.0, bp = 0.0, ri = 0.0, rim1 = 0.0;
   if (pv) {
     ri = S.rsc[i * cp + p];
@@ -867,7 +942,7 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
   for (int kk = 0; kk < NK; ++kk) cf[kk] = cf_sm[kk * cols_pad + p];
   const int rt = sa.rt;
   const int vstride = rt * ldc;
-  const int64_t stage_elems = static_cast<int64_t>(NK + 1) * vstride;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, ldc);
   VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
   double nb = 0.0, nrm = 0.0;
   double gr[NK];
@@ -879,32 +954,31 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
     const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
     if (pv) {
-      const VT* base = ring.buf + s * stage_elems + p;
+      const VT* stage = ring.buf + s * stage_elems;
+      const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
       int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
       for (; r < rows; r += kStageSlots) {
-        const VT* e = base + r * ldc;
-        const VT* uk = e + vstride;
+        const StageView<VT, NK> v{stage + p + r * ldc, sbits + r * kBitWords, vstride, p};
         double wp;
         if (SECOND) {
-          wp = to_f64(e[0]);
+          wp = v.src();
         } else {
-          wp = three_term(to_f64(e[0]), to_f64(uk[i * vstride]), i > 0 ? to_f64(uk[(i > 0 ? i - 1 : 0) * vstride]) : 0.0,
-                          al, bp, ri, rim1);
+          wp = three_term(v.src(), v.u(i), i > 0 ? v.u(i > 0 ? i - 1 : 0) : 0.0, al, bp, ri, rim1);
           nb = fma(wp, wp, nb);
         }
         // basis.T @ h as two interleaved partial sums (shorter dependency chain), then one subtraction
         double pe = 0.0, po = 0.0;
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk) {
-          if (kk & 1) po = fma(to_f64(uk[kk * vstride]), cf[kk], po);
-          else pe = fma(to_f64(uk[kk * vstride]), cf[kk], pe);
+          if (kk & 1) po = fma(v.u(kk), cf[kk], po);
+          else pe = fma(v.u(kk), cf[kk], pe);
         }
-        const VT v = from_f64<VT>(__dsub_rn(wp, pe + po));
-        out[(r0 + r) * a.ldc] = v;
-        const double vd = to_f64(v);
+        const VT vv = from_f64<VT>(__dsub_rn(wp, pe + po));
+        out[(r0 + r) * a.ldc] = vv;
+        const double vd = to_f64(vv);
         nrm = fma(vd, vd, nrm);
 #pragma unroll
-        for (int kk = 0; kk < NK; ++kk) gr[kk] = fma(to_f64(uk[kk * vstride]), vd, gr[kk]);
+        for (int kk = 0; kk < NK; ++kk) gr[kk] = fma(v.u(kk), vd, gr[kk]);
       }
     }
     __syncwarp();
@@ -1049,7 +1123,9 @@ cgs_step_kernel(StepArgs sa) {
       for (int p = lane; p < sp.c; p += 32) {
         double acc = 0.0;
         for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, sp.segpart[sg * sp.cpad + p]);
-        const double x = __dmul_rn(to_f64(uu[row * sp.ldc_in + p]), sp.r[p]);
+        const double own = sp.bits ? (((sp.bits[row * kBitWords + (p >> 5)] >> (p & 31)) & 1u) ? 1.0 : -1.0)
+                                   : to_f64(uu[row * sp.ldc_in + p]);
+        const double x = __dmul_rn(own, sp.r[p]);
         double y;
         if (sa.red.kind == SLQ_NORMALIZED_LAPLACIAN) y = op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, acc, d, dis, scale);
         else if (sa.red.kind == SLQ_DENSITY) y = op_epilogue<SLQ_DENSITY>(x, acc, d, dis, scale);
@@ -1096,26 +1172,25 @@ cgs_step_kernel(StepArgs sa) {
 
 // Build the staged-vector list of one pass; false when the geometry does not fit.
 template <typename VT>
-static bool staged_setup(const CgsArgs& a, bool second, StagedArgs* out) {
+static bool staged_setup(const CgsArgs& a, bool second, const uint32_t* bits, StagedArgs* out) {
   StagedArgs s{};
   s.a = a;
   const VT* basis = static_cast<const VT*>(a.basis);
+  const int nk = a.i + 1;
+  if (!a.reorth || nk > kCgsBlock || !bits) return false;
   int nv = 0;
   s.slot_src = nv;
   s.vec[nv++] = second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
-  const int kcount = a.i + 1;
-  if (!a.reorth || kcount > kCgsBlock) return false;
   for (int kk = 0; kk < kCgsBlock; ++kk) s.slot_k[kk] = 0;
-  for (int kk = 0; kk < kcount; ++kk) {
+  for (int kk = 1; kk < nk; ++kk) {       // u_0 comes from the bitmask
     s.slot_k[kk] = nv;
     s.vec[nv++] = basis + static_cast<int64_t>(kk) * a.vec_stride;
   }
-  s.slot_ui = s.slot_k[a.i];
-  s.slot_uim1 = a.i > 0 ? s.slot_k[a.i - 1] : 0;
+  s.bits = bits;
   s.nvec = nv;
-  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT);
+  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t);
   const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
-  int64_t rt = static_cast<int64_t>((kStagedSmem - 128) / (kStages * row_bytes));
+  int64_t rt = static_cast<int64_t>((kStagedSmem - 256) / (kStages * row_bytes));
   rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
   if (rt < 1 || a.ldc > kStagedMaxLdc) return false;
   s.rt = static_cast<int>(rt);
@@ -1137,17 +1212,17 @@ static int coop_supported(int dev) {
 // Launch everything after the SpMM of step i as one persistent kernel; false when the staged path
 // does not apply (the caller then runs the separate kernels).
 template <typename VT>
-static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, int dev,
-                            cudaStream_t st, int* rc) {
+static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
+                            int dev, cudaStream_t st, int* rc) {
   *rc = SLQ_OK;
   if (!coop_supported(dev)) return false;
   StepArgs sa{};
-  if (!staged_setup<VT>(a, false, &sa.pass[0]) || !staged_setup<VT>(a, true, &sa.pass[1])) return false;
+  if (!staged_setup<VT>(a, false, bits, &sa.pass[0]) || !staged_setup<VT>(a, true, bits, &sa.pass[1])) return false;
   sa.red = red;
   sa.spmm = spmm;
-  const size_t smem = 128 + kStages * std::max(static_cast<size_t>(sa.pass[0].nvec) * sa.pass[0].rt,
-                                               static_cast<size_t>(sa.pass[1].nvec) * sa.pass[1].rt) *
-                                a.ldc * sizeof(VT);
+  const size_t smem = 128 + kStages * sizeof(VT) *
+                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, a.ldc),
+                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, a.ldc));
   const int threads = 32 + kStageSlots * (((static_cast<int>(a.ldc) + 31) / 32) * 32);
   LaunchScope ls(K_CGS_UPDATE, st);
   // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
@@ -1298,7 +1373,9 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   char* ws = nullptr;
   SLQ_TRACE("before malloc");
   const size_t off_seg = off_part + ((bytes_part + 255) / 256) * 256;
-  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_seg + bytes_seg, st));
+  const size_t off_bits = off_seg + ((bytes_seg + 255) / 256) * 256;
+  const size_t bytes_bits = sizeof(uint32_t) * kBitWords * static_cast<size_t>(std::max<int64_t>(n, 1));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_bits + bytes_bits, st));
   SLQ_TRACE("after malloc");
   VT* basis = reinterpret_cast<VT*>(ws);
   VT* wv = basis + (S + 1) * vs;
@@ -1328,11 +1405,16 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     LaunchScope ls(K_PROBE, st);
     state_init_kernel<<<ceil_div(std::max(cpad, 4 * S), 128), 128, 0, st>>>(s, n, q0 != nullptr);
   }
+  // u_0 as a probe bitmask (c <= 128): the first SpMM gathers bits and the staged step kernels
+  // stream bits instead of u_0; the +-1 values are materialised only for the non-staged kernels.
+  const bool coop_ok = staged_enabled() && coop_supported(g->device);
+  uint32_t* bits = (!q0 && c <= kBlk) ? reinterpret_cast<uint32_t*>(ws + off_bits) : nullptr;
+  const bool all_staged = bits && coop_ok && reorth && S - 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
   if (q0) {
     LaunchScope ls(K_PROBE, st);
     copy_start_kernel<VT><<<std::max(1, std::min(ceil_div(n * c, 256), 148 * 16)), 256, 0, st>>>(q0, ldq, c, n, basis, ldc);
   } else {
-    launch_probes<VT>(seed, probe0, c, n, basis, ldc, st);
+    launch_probes<VT>(seed, probe0, c, n, all_staged ? nullptr : basis, ldc, st, bits);
   }
 
   SpmmArgs sa{};
@@ -1351,8 +1433,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.kind = kind; ra.dscal = g->dscal; ra.reorth = reorth;
 
   const int gx = 1 << 30;                 // one CTA per tile group
-  const bool use_staged = staged_enabled();
-  const bool coop = use_staged && coop_supported(g->device);
+  const bool coop = coop_ok && bits != nullptr;
   const int gx2 = kSecondPassGrid;        // second pass: small grid-stride launch
 
   // Non-staged path (s > 17, SLQ_STAGED=0 or no cooperative launch): separate kernels + reductions.
@@ -1375,6 +1456,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     ra.k0 = 0; ra.nk = 0;
     sa.red = ra;
     sa.work = s.work + 4 * i;
+    sa.bits = (i == 0) ? bits : nullptr;
     ca.i = i;
     ca.second = 0;
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
@@ -1387,7 +1469,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     if (!staged) launch_reduce(ra, st);
     if (i == S - 1) break;
     if (staged) {
-      const bool done = launch_cgs_step<VT>(ca, ra, sa, g->device, st, &rc);
+      const bool done = launch_cgs_step<VT>(ca, ra, sa, bits, g->device, st, &rc);
       SLQ_TRACE("step launched");
       if (rc) return rc;
       if (done) continue;
