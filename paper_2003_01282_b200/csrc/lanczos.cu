@@ -27,6 +27,7 @@
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "bulk_pipe.cuh"
 #include "pcg64.cuh"
@@ -303,20 +304,30 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
 // acc[j] += sum over nonzeros [beg, end) of one row, in stored order (sequential, unfused: the
 // reference's csr_matvec order).  Columns are loaded 32 at a time and broadcast by shuffles; UNR
 // gathers are in flight per lane.
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS>
+// acc[j] += sum over nonzeros [beg, end) of one row, in stored order.
+//  EXACT (operator apply, r == 1): t = fl(dinv_c * u_c) [* w], acc = fl(acc + t): the reference's
+//        csr_matvec order and rounding, bit for bit.
+//  !EXACT (Lanczos): acc = fma(s_c, u_c, acc) with s_c = dinv_c [* w]; the caller multiplies the
+//        sum by the probe scale r afterwards (q = r u is never formed per gathered value).
+// Columns are loaded 32 at a time; each lane turns its column into an element offset once and the
+// warp broadcasts offsets with one shuffle per nonzero.  Probe slots beyond c are clamped to a valid
+// column (loaded, never stored), so the loads need no predicates.
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT>
 __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
                                              const double* __restrict__ wts, const VT* __restrict__ u, int64_t ldi,
-                                             const uint32_t* __restrict__ bits, const bool* pv, const double* r,
+                                             const uint32_t* __restrict__ bits, const int* pidx, const double* r,
                                              int64_t beg, int64_t end, double* acc) {
   const int lane = threadIdx.x & 31;
   for (int64_t base = beg; base < end; base += 32) {
     const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
-    int mycol = 0;
+    int64_t myoff = 0;
     double mys = 1.0, myw = 1.0;
     if (lane < cnt) {
-      mycol = __ldg(cols + base + lane);
-      if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + mycol);
+      const int64_t col = __ldg(cols + base + lane);
+      myoff = BITS ? col * kBitWords : col * ldi;
+      if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + col);
       if (WEIGHTED) myw = __ldg(wts + base + lane);
+      if (!EXACT && WEIGHTED) mys *= myw;   // s_c = dinv_c * w (or w)
     }
     constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane
     int k = 0;
@@ -324,44 +335,53 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       double xv[UNR][PPL];
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const int64_t cq = static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k + q));
+        const int64_t o = __shfl_sync(0xffffffffu, myoff, k + q);
         if (BITS) {
           // u_0 = +-1 from the probe bitmask: one uniform 16-byte load covers 128 probes
-          const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + cq * kBitWords));
+          const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
           const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
           for (int j = 0; j < PPL; ++j) xv[q][j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
         } else {
-          const VT* src = u + cq * ldi;
+          const VT* src = u + o;
 #pragma unroll
-          for (int j = 0; j < PPL; ++j) xv[q][j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+          for (int j = 0; j < PPL; ++j) xv[q][j] = ldg_f64(src + pidx[j]);
         }
       }
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const double sk = __shfl_sync(0xffffffffu, mys, k + q);
-        const double wk = __shfl_sync(0xffffffffu, myw, k + q);
+        const double sk = (KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED))
+                              ? __shfl_sync(0xffffffffu, mys, k + q) : 1.0;
+        const double wk = (EXACT && WEIGHTED) ? __shfl_sync(0xffffffffu, myw, k + q) : 1.0;
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xv[q][j], r[j], sk, wk));
+        for (int j = 0; j < PPL; ++j) {
+          if (EXACT) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xv[q][j], r[j], sk, wk));
+          else if (KIND == SLQ_NORMALIZED_LAPLACIAN || WEIGHTED) acc[j] = fma(sk, xv[q][j], acc[j]);
+          else acc[j] += xv[q][j];
+        }
       }
     }
     for (; k < cnt; ++k) {
-      const int64_t cq = static_cast<int64_t>(__shfl_sync(0xffffffffu, mycol, k));
-      const double sk = __shfl_sync(0xffffffffu, mys, k);
-      const double wk = __shfl_sync(0xffffffffu, myw, k);
+      const int64_t o = __shfl_sync(0xffffffffu, myoff, k);
+      const double sk = (KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED)) ? __shfl_sync(0xffffffffu, mys, k) : 1.0;
+      const double wk = (EXACT && WEIGHTED) ? __shfl_sync(0xffffffffu, myw, k) : 1.0;
       double xr[PPL];
       if (BITS) {
-        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + cq * kBitWords));
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
         const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
         for (int j = 0; j < PPL; ++j) xr[j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
       } else {
-        const VT* src = u + cq * ldi;
+        const VT* src = u + o;
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) xr[j] = pv[j] ? ldg_f64(src + 32 * j) : 0.0;
+        for (int j = 0; j < PPL; ++j) xr[j] = ldg_f64(src + pidx[j]);
       }
 #pragma unroll
-      for (int j = 0; j < PPL; ++j) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr[j], r[j], sk, wk));
+      for (int j = 0; j < PPL; ++j) {
+        if (EXACT) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr[j], r[j], sk, wk));
+        else if (KIND == SLQ_NORMALIZED_LAPLACIAN || WEIGHTED) acc[j] = fma(sk, xr[j], acc[j]);
+        else acc[j] += xr[j];
+      }
     }
   }
 }
@@ -381,17 +401,19 @@ __device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint
 // partial per tile).  Which warp runs an item never changes its arithmetic, so results are
 // deterministic; dynamic scheduling removes the tail left by hub rows.  Long rows are finished by
 // spmm_long_finish_kernel or the step kernel's phase 0.
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS>
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT>
 __global__ void __launch_bounds__(kSpmmWarps * 32, 4)
 spmm_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   const int pbase = blockIdx.y * kBlk + lane;
   bool pv[PPL];
   double r[PPL];
+  int pidx[PPL];   // column offsets within a gathered row, clamped to a valid probe
 #pragma unroll
   for (int j = 0; j < PPL; ++j) {
     pv[j] = probe_ok(pbase + 32 * j, a.c);
     r[j] = (a.r && pv[j]) ? a.r[pbase + 32 * j] : 1.0;
+    pidx[j] = pv[j] ? 32 * j : (a.c - 1 - (blockIdx.y * kBlk + lane));
   }
   const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
   VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
@@ -415,7 +437,7 @@ spmm_kernel(SpmmArgs a) {
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-    gather_range<VT, KIND, WEIGHTED, PPL, BITS>(a.cols, dinv, a.weights, u, ldi, a.bits, pv, r, beg, end, acc);
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, r, beg, end, acc);
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
     for (int j = 0; j < PPL; ++j)
@@ -438,14 +460,14 @@ spmm_kernel(SpmmArgs a) {
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      gather_range<VT, KIND, WEIGHTED, PPL, BITS>(a.cols, dinv, a.weights, u, ldi, a.bits, pv, r, beg, end, acc);
+      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, r, beg, end, acc);
       const double d = __ldg(a.degree + row);
       const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         if (!pv[j]) continue;
         const double x = __dmul_rn(own_value<VT, PPL, BITS>(u, ldi, a.bits, row, j), r[j]);
-        const double y = op_epilogue<KIND>(x, acc[j], d, dis, scale);
+        const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * r[j], d, dis, scale);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
         dot[j] = fma(x, y, dot[j]);
       }
@@ -485,6 +507,7 @@ spmm_long_finish_kernel(SpmmArgs a) {
         if (p >= a.c) continue;
         double acc = 0.0;
         for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, a.segpart[sg * a.cpad + p]);
+        if (a.r) acc *= a.r[p];   // Lanczos path: segments hold unscaled sums
         const double rj = a.r ? a.r[p] : 1.0;
         const double own = a.bits ? (((a.bits[row * kBitWords + j] >> lane) & 1u) ? 1.0 : -1.0)
                                   : ldg_f64(u + row * a.ldc_in + 32 * j);
@@ -514,8 +537,14 @@ static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_
   (void)coop;
   (void)dev;
   dim3 grid(148 * 4, gy);   // persistent: work is taken from the atomic counters
-  if (a.bits) spmm_kernel<VT, KIND, W, PPL, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
-  else spmm_kernel<VT, KIND, W, PPL, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  // EXACT (bit-identical operator apply) only for the apply entry (r == nullptr, double)
+  if (!a.r) {
+    if (std::is_same<VT, double>::value) spmm_kernel<VT, KIND, W, PPL, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else if (a.bits) {
+    spmm_kernel<VT, KIND, W, PPL, true, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else {
+    spmm_kernel<VT, KIND, W, PPL, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  }
 }
 
 template <typename VT, int KIND>
@@ -1123,6 +1152,7 @@ cgs_step_kernel(StepArgs sa) {
       for (int p = lane; p < sp.c; p += 32) {
         double acc = 0.0;
         for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, sp.segpart[sg * sp.cpad + p]);
+        acc *= sp.r[p];   // segments hold unscaled sums
         const double own = sp.bits ? (((sp.bits[row * kBitWords + (p >> 5)] >> (p & 31)) & 1u) ? 1.0 : -1.0)
                                    : to_f64(uu[row * sp.ldc_in + p]);
         const double x = __dmul_rn(own, sp.r[p]);
@@ -1297,6 +1327,33 @@ __global__ void scatter_out_kernel(ChunkState s, int64_t col0, int S, double* al
   steps[col0 + p] = st;
 }
 
+// alpha_i = q_i . w for the steps that do not run the staged step kernel (the last step, s > 17,
+// SLQ_STAGED=0): kAlphaCtas CTAs with fixed contiguous row ranges, 2 row slots per probe column,
+// per-CTA partials reduced by reduce_kernel (fixed stripes): deterministic and independent of c.
+constexpr int kAlphaCtas = 148 * 4;
+
+template <typename VT>
+__global__ void __launch_bounds__(256)
+alpha_dot_kernel(const VT* __restrict__ u, const double* __restrict__ r, const VT* __restrict__ w, int64_t n,
+                 int64_t ldc, int c, int cpad, double* __restrict__ partial) {
+  __shared__ double red[2][kBlk];
+  const int cols = (blockDim.x >> 1);
+  const int pl = threadIdx.x % cols, slot = threadIdx.x / cols;
+  const int p = blockIdx.y * kBlk + pl;
+  const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+  double s = 0.0;
+  if (p < c) {
+    const double rp = r[p];
+    for (int64_t row = lo + slot; row < hi; row += 2) {
+      const double x = __dmul_rn(ldg_f64(u + row * ldc + p), rp);
+      s = fma(x, ldg_f64(w + row * ldc + p), s);
+    }
+  }
+  red[slot][pl] = s;
+  __syncthreads();
+  if (slot == 0 && p < cpad) partial[static_cast<int64_t>(blockIdx.x) * cpad + p] = red[0][pl] + red[1][pl];
+}
+
 // ----------------------------------------------------------------------------- engine
 static void set_long_rows(SpmmArgs& sa, const slq_graph* g, double* segpart) {
   sa.long_counts = g->long_counts;
@@ -1409,7 +1466,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   // stream bits instead of u_0; the +-1 values are materialised only for the non-staged kernels.
   const bool coop_ok = staged_enabled() && coop_supported(g->device);
   uint32_t* bits = (!q0 && c <= kBlk) ? reinterpret_cast<uint32_t*>(ws + off_bits) : nullptr;
-  const bool all_staged = bits && coop_ok && reorth && S - 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
+  const bool all_staged = bits && coop_ok && reorth && S >= 2 && S - 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
   if (q0) {
     LaunchScope ls(K_PROBE, st);
     copy_start_kernel<VT><<<std::max(1, std::min(ceil_div(n * c, 256), 148 * 16)), 256, 0, st>>>(q0, ldq, c, n, basis, ldc);
@@ -1462,11 +1519,22 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
     // writes w; otherwise (last step, s > 17, SLQ_STAGED=0) the SpMM also reduces alpha.
     const bool staged = coop && reorth && i < S - 1 && i + 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
-    sa.partial = staged ? nullptr : partial;
+    sa.partial = nullptr;   // alpha: step kernel (staged) or alpha_dot_kernel
     SLQ_TRACE("spmm launch");
     launch_spmm<VT>(kind, sa, false, g->device, st, /*finish=*/!staged);   // staged: phase 0 finishes
     SLQ_TRACE("spmm launched");
-    if (!staged) launch_reduce(ra, st);
+    if (!staged) {
+      // the long rows of w must be complete before alpha: finish kernel ran inside launch_spmm
+      const int colsb = std::min(cpad, kBlk);
+      {
+        LaunchScope ls(K_REDUCE, st);
+        alpha_dot_kernel<VT><<<dim3(kAlphaCtas, ceil_div(c, kBlk)), 2 * colsb, 0, st>>>(
+            basis + i * vs, s.rsc + i * cpad, wv, n, ldc, c, cpad, partial);
+      }
+      ReduceArgs rd = ra;
+      rd.ntiles = kAlphaCtas;
+      launch_reduce(rd, st);
+    }
     if (i == S - 1) break;
     if (staged) {
       const bool done = launch_cgs_step<VT>(ca, ra, sa, bits, g->device, st, &rc);

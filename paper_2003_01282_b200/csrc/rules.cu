@@ -19,6 +19,9 @@ namespace slq {
 constexpr int kStEigen = 1, kStNanTri = 2, kStNanF = 4, kStBadCol = 8;
 
 // hi_kind >= 0: the clamp interval comes from the device graph scalars (no host round trip).
+// MAXS: capacity of the per-thread work arrays (local memory): sized to the rule length so the
+// arrays of a CTA stay L1-resident.
+template <int MAXS>
 __global__ void gauss_rules_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
                                    const int32_t* __restrict__ steps, int64_t count, int ld, double lo,
                                    double hi, double* __restrict__ nodes, double* __restrict__ weights,
@@ -28,7 +31,7 @@ __global__ void gauss_rules_kernel(const double* __restrict__ alpha, const doubl
   if (p == 0 && gflags && gflags[0]) atomicOr(status, kStBadCol);
   if (p >= count) return;
   if (hi_kind >= 0) hi = hi_kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (hi_kind == SLQ_DENSITY ? 1.0 : dscal[4]);
-  double d[kMaxSteps], e[kMaxSteps], z[kMaxSteps];
+  double d[MAXS], e[MAXS], z[MAXS];
   const int m = steps[p];
   const double* a = alpha + p * ld;
   const double* b = beta + p * ld;
@@ -116,6 +119,97 @@ __global__ void estimate_kernel(const double* __restrict__ pv, int64_t T, int64_
   }
 }
 
+// Fused quadrature + aggregate for up to 8 integrands: block (t, f); threads over probes; fixed-tree
+// block sums for the mean and for sum (x - mean)^2 (the two passes of np.std, slq.py:98-105).
+struct FnList {
+  int fn[8];
+  int n;
+};
+
+__device__ __forceinline__ double integrand_rt(int fn, double t, double x) {
+  switch (fn) {
+    case SLQ_FN_HEAT: return exp(-t * x);
+    case SLQ_FN_WAVE_RE: return cos(t * x);
+    case SLQ_FN_WAVE_IM: return -sin(t * x);
+    case SLQ_FN_XLOGX: return x > 0.0 ? x * log(x) : 0.0;
+    default: return x;
+  }
+}
+
+__device__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += sh[w];
+    sh[32] = tot;
+  }
+  __syncthreads();
+  tot = sh[32];
+  __syncthreads();
+  return tot;
+}
+
+__global__ void __launch_bounds__(256)
+integrate_kernel(const double* __restrict__ nodes, const double* __restrict__ weights,
+                 const int32_t* __restrict__ steps, int64_t count, int ld, const double* __restrict__ tgrid, int64_t T,
+                 FnList fl, double n, double* __restrict__ values, double* __restrict__ stds,
+                 double* __restrict__ per_vector, int* __restrict__ status) {
+  __shared__ double sh[33];
+  const int64_t ti = blockIdx.x;
+  const int f = blockIdx.y;
+  const int fn = fl.fn[f];
+  const double t = tgrid ? tgrid[ti] : 0.0;
+  double s = 0.0;
+  bool ok = true;
+  for (int64_t p = threadIdx.x; p < count; p += blockDim.x) {
+    const int m = steps[p];
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k) {
+      const double v = integrand_rt(fn, t, nodes[p * ld + k]);
+      ok = ok && isfinite(v);
+      acc = fma(weights[p * ld + k], v, acc);
+    }
+    if (per_vector) per_vector[(static_cast<int64_t>(f) * T + ti) * count + p] = acc;
+    s += acc;
+  }
+  if (!ok) atomicOr(status, kStNanF);
+  const double sp = block_sum(s, sh);
+  const double value = n * (sp / static_cast<double>(count));   // n * mean(per_vector), slq.py:100
+  const double mean = value;                                     // mean of n * per_vector
+  double ss = 0.0;
+  for (int64_t p = threadIdx.x; p < count; p += blockDim.x) {
+    const int m = steps[p];
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k) acc = fma(weights[p * ld + k], integrand_rt(fn, t, nodes[p * ld + k]), acc);
+    const double dl = n * acc - mean;
+    ss += dl * dl;
+  }
+  const double sq = block_sum(ss, sh);
+  if (threadIdx.x == 0) {
+    values[static_cast<int64_t>(f) * T + ti] = value;
+    stds[static_cast<int64_t>(f) * T + ti] =
+        count > 1 ? sqrt(sq / static_cast<double>(count - 1)) / sqrt(static_cast<double>(count)) : 0.0;
+  }
+}
+
+static void launch_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count, int ld,
+                               double lo, double hi, double* nodes, double* weights, int32_t* info, int* status,
+                               const double* dscal, int hi_kind, const int* gflags, cudaStream_t st) {
+  const int grid = ceil_div(count, 32);
+  LaunchScope ls(K_EIG, st);
+#define SLQ_RULES(M) gauss_rules_kernel<M><<<grid, 32, 0, st>>>(alpha, beta, steps, count, ld, lo, hi, nodes, weights, \
+                                                                 info, status, dscal, hi_kind, gflags)
+  if (ld <= 16) SLQ_RULES(16);
+  else if (ld <= 32) SLQ_RULES(32);
+  else if (ld <= 64) SLQ_RULES(64);
+  else SLQ_RULES(kMaxSteps);
+#undef SLQ_RULES
+}
+
 }  // namespace slq
 
 using namespace slq;
@@ -129,11 +223,7 @@ extern "C" int slq_gauss_rules(const double* alpha, const double* beta, const in
   int* status = nullptr;
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(int), st));
   SLQ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
-  {
-    LaunchScope ls(K_EIG, st);
-    gauss_rules_kernel<<<ceil_div(count, 64), 64, 0, st>>>(alpha, beta, steps, count, ld, lo, hi, nodes, weights,
-                                                             info, status, nullptr, -1, nullptr);
-  }
+  launch_gauss_rules(alpha, beta, steps, count, ld, lo, hi, nodes, weights, info, status, nullptr, -1, nullptr, st);
   int h = 0;
   SLQ_CUDA(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
   SLQ_CUDA(cudaStreamSynchronize(st));
@@ -188,20 +278,6 @@ extern "C" int slq_estimate(const double* per_vector, int64_t T, int64_t count, 
 }
 
 // ------------------------------------------------------------------ asynchronous composite entry points
-static void launch_quadrature(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,
-                              const double* t, int64_t T, int fn, double* pv, int* status, cudaStream_t st) {
-  const int64_t total = T * count;
-  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  LaunchScope ls(K_QUAD, st);
-  switch (fn) {
-    case SLQ_FN_HEAT: quadrature_kernel<SLQ_FN_HEAT><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
-    case SLQ_FN_WAVE_RE: quadrature_kernel<SLQ_FN_WAVE_RE><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
-    case SLQ_FN_WAVE_IM: quadrature_kernel<SLQ_FN_WAVE_IM><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
-    case SLQ_FN_XLOGX: quadrature_kernel<SLQ_FN_XLOGX><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
-    default: quadrature_kernel<SLQ_FN_IDENTITY><<<grid, 256, 0, st>>>(nodes, weights, steps, count, ld, t, T, pv, status); break;
-  }
-}
-
 extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
                          int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
                          void* stream) {
@@ -212,11 +288,9 @@ extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   double* ab = nullptr;
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ab), sizeof(double) * 2 * count * S, st));
   int rc = slq_lanczos(g, kind, seed, probe_begin, count, steps, reorth, dtype, ab, ab + count * S, steps_out, stream);
-  if (rc == SLQ_OK) {
-    LaunchScope ls(K_EIG, st);
-    gauss_rules_kernel<<<ceil_div(count, 64), 64, 0, st>>>(ab, ab + count * S, steps_out, count, S, 0.0, 0.0, nodes,
-                                                             weights, nullptr, status, g->dscal, kind, g->dflags);
-  }
+  if (rc == SLQ_OK)
+    launch_gauss_rules(ab, ab + count * S, steps_out, count, S, 0.0, 0.0, nodes, weights, nullptr, status, g->dscal,
+                       kind, g->dflags, st);
   cudaFreeAsync(ab, st);
   if (rc) return rc;
   SLQ_CUDA(cudaGetLastError());
@@ -229,16 +303,19 @@ extern "C" int slq_integrate(const double* nodes, const double* weights, const i
   if (count < 1 || T < 0 || nfn < 0 || !status) return fail(SLQ_ERR_VALUE, "bad integrate arguments");
   if (T == 0 || nfn == 0) return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double* pv = per_vector;
-  if (!pv) SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pv), sizeof(double) * nfn * T * count, st));
-  for (int f = 0; f < nfn; ++f) {
-    double* pvf = pv + static_cast<int64_t>(f) * T * count;
-    launch_quadrature(nodes, weights, steps, count, ld, t, T, fns_host[f], pvf, status, st);
-    LaunchScope ls(K_ESTIMATE, st);
-    estimate_kernel<<<ceil_div(T, 128), 128, 0, st>>>(pvf, T, count, n, values + static_cast<int64_t>(f) * T,
-                                                      std_errors + static_cast<int64_t>(f) * T);
+  for (int f0 = 0; f0 < nfn; f0 += 8) {
+    FnList fl{};
+    fl.n = std::min(8, nfn - f0);
+    for (int f = 0; f < fl.n; ++f) {
+      if (fns_host[f0 + f] < 0 || fns_host[f0 + f] > SLQ_FN_IDENTITY) return fail(SLQ_ERR_VALUE, "unknown integrand");
+      fl.fn[f] = fns_host[f0 + f];
+    }
+    LaunchScope ls(K_QUAD, st);
+    integrate_kernel<<<dim3(static_cast<unsigned>(T), fl.n), 256, 0, st>>>(
+        nodes, weights, steps, count, ld, t, T, fl, n, values + static_cast<int64_t>(f0) * T,
+        std_errors + static_cast<int64_t>(f0) * T,
+        per_vector ? per_vector + static_cast<int64_t>(f0) * T * count : nullptr, status);
   }
-  if (!per_vector) cudaFreeAsync(pv, st);
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
 }

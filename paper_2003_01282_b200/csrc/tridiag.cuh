@@ -5,6 +5,14 @@
 
 namespace slq {
 
+// sqrt(a^2 + b^2): the plain formula when neither square can overflow or underflow (the usual
+// case: tridiagonal entries of L, P are O(1) .. O(1e-9)), else the library hypot.
+__device__ __forceinline__ double fast_hypot(double a, double b) {
+  const double m = fmax(fabs(a), fabs(b));
+  if (m > 1e-150 && m < 1e150) return sqrt(fma(a, a, b * b));
+  return hypot(a, b);
+}
+
 // Implicit QL on (d, e) of order m; z holds the first row of the accumulated rotations.
 // Returns 0 on convergence, 1 if an eigenvalue needed more than 60 sweeps.
 __device__ __forceinline__ int tridiag_ql_first_row(double* d, double* e, double* z, int m) {
@@ -20,14 +28,14 @@ __device__ __forceinline__ int tridiag_ql_first_row(double* d, double* e, double
       if (++sweeps > 60) return 1;
       // Wilkinson-type shift from the leading 2x2 block
       double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-      double r = hypot(g, 1.0);
+      double r = fast_hypot(g, 1.0);
       g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
       double s = 1.0, c = 1.0, p = 0.0;
       bool deflated = false;
       for (int i = mm - 1; i >= l; --i) {
         double f = s * e[i];
         const double b = c * e[i];
-        r = hypot(f, g);
+        r = fast_hypot(f, g);
         e[i + 1] = r;
         if (r == 0.0) {          // underflow: split the matrix here and restart
           d[i + 1] -= p;
@@ -35,8 +43,9 @@ __device__ __forceinline__ int tridiag_ql_first_row(double* d, double* e, double
           deflated = true;
           break;
         }
-        s = f / r;
-        c = g / r;
+        const double rinv = 1.0 / r;
+        s = f * rinv;
+        c = g * rinv;
         g = d[i + 1] - p;
         r = (d[i] - g) * s + 2.0 * c * b;
         p = s * r;
