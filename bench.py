@@ -194,10 +194,15 @@ def run_ours(args):
     from paper_2003_01282_b200.slq import SlqConfig
 
     world, rank, local = dist_env()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")   # gloo: multi-rank test on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     g = build_graph()
     s, n_v = WORKLOAD["lanczos_steps"], WORKLOAD["n_v_per_gpu"]
     total_probes = n_v * world
@@ -269,7 +274,7 @@ def run_ours(args):
     ptimes = [a.elapsed_time(b) for a, b in pev]
     prof = _lib.profile_end()
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()

@@ -39,8 +39,13 @@ def gather_rules_arrays(nodes, weights, steps, n_v: int, group=None):
     pack[:cnt, :width] = nodes
     pack[:cnt, width:2 * width] = weights
     pack[:cnt, 2 * width] = steps.to(torch.float64)
+    on_host = dist.get_backend(group) == "gloo" and pack.is_cuda   # gloo gathers host tensors
+    if on_host:
+        pack = pack.cpu()
     bufs = [torch.empty_like(pack) for _ in range(world)]
     dist.all_gather(bufs, pack, group=group)
+    if on_host:
+        bufs = [b.to(dev) for b in bufs]
     full = torch.cat([bufs[r][: e - b] for r, (b, e) in enumerate(ranges)], dim=0)
     return (full[:, :width].contiguous(), full[:, width:2 * width].contiguous(),
             full[:, 2 * width].to(torch.int32).contiguous())
