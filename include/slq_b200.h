@@ -89,6 +89,20 @@ int slq_graph_create_host(int64_t n, int64_t nnz, const int64_t* offsets_host,
 int slq_graph_info(const slq_graph* g, slq_graph_info_t* out);
 void slq_graph_destroy(slq_graph* g);
 
+/* Generate an R-MAT graph on the device and build its canonical CSR there (no host arrays; the
+ * C4/C5 workloads of BASELINE.json, whose CSR does not fit a host round trip at scale 27).
+ * n = 2^scale, edge_factor * n samples, quadrant probabilities (a, b, c, 1-a-b-c); both directions,
+ * self-loops dropped, duplicates collapsed, rows/columns ascending (graphs.py canonical form, the
+ * reference's graph ingestion at operators.py:52-62 via scipy.sparse.csr_matrix).  Sample j, level l
+ * draws slq_rmat_uniform_host(seed, j, l).  Synchronises `stream` (the unique-key count). */
+int slq_graph_create_rmat(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                          void* stream, slq_graph** out);
+/* Copy the prepared CSR (int64 offsets [n+1], int32 columns [nnz]) into caller buffers (device or
+ * host; either may be NULL), stream-ordered. */
+int slq_graph_csr(const slq_graph* g, int64_t* offsets, int32_t* cols, void* stream);
+/* The generator's uniform for (seed, sample, level), for host restatements of the generator. */
+int slq_rmat_uniform_host(uint64_t seed, uint64_t sample, int level, double* out);
+
 /* Copy the prepared degree vector d = A.1 and dinv = 1/sqrt(d) (0 if isolated) into [n]
  * device buffers (either may be NULL).  operators.py:58-62, 84-86. */
 int slq_graph_degrees(const slq_graph* g, double* degree, double* dinv, void* stream);

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libslq_b200.so")
-SOURCES = ["capi.cu", "graph.cu", "lanczos.cu", "rules.cu", "batched.cu"]
+SOURCES = ["capi.cu", "graph.cu", "lanczos.cu", "rules.cu", "batched.cu", "rmat.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

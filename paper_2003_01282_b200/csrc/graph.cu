@@ -159,18 +159,25 @@ static void* track(slq_graph* g, void* p) {
   return p;
 }
 
+// Fully stream-ordered: no host synchronisation.  Scalars stay on the device (g->dscal); the host
+// mirror is fetched lazily by fetch_host_scalars() (slq_graph_info, Laplacian interval).
+// Either copies (offsets, int64 cols) or adopts device buffers the caller allocated with
+// cudaMallocAsync (adopt_off, adopt_cols: the graph frees them).
 static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols, const double* weights,
-                       cudaStream_t st) {
-  // Fully stream-ordered: no host synchronisation.  Scalars stay on the device (g->dscal); the host
-  // mirror is fetched lazily by fetch_host_scalars() (slq_graph_info, Laplacian interval).
+                       cudaStream_t st, int64_t* adopt_off = nullptr, int32_t* adopt_cols = nullptr) {
   const int64_t n = g->n, nnz = g->nnz;
   void* p = nullptr;
-  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), st));
-  g->offsets = static_cast<int64_t*>(track(g, p));
-  SLQ_CUDA(cudaMemcpyAsync(const_cast<int64_t*>(g->offsets), offsets, sizeof(int64_t) * (n + 1),
-                           cudaMemcpyDefault, st));
-  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), st));
-  g->cols = static_cast<int32_t*>(track(g, p));
+  if (adopt_off) {
+    g->offsets = static_cast<int64_t*>(track(g, adopt_off));
+    g->cols = static_cast<int32_t*>(track(g, adopt_cols));
+  } else {
+    SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), st));
+    g->offsets = static_cast<int64_t*>(track(g, p));
+    SLQ_CUDA(cudaMemcpyAsync(const_cast<int64_t*>(g->offsets), offsets, sizeof(int64_t) * (n + 1),
+                             cudaMemcpyDefault, st));
+    SLQ_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), st));
+    g->cols = static_cast<int32_t*>(track(g, p));
+  }
   SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * std::max<int64_t>(n, 1) * 2, st));
   track(g, p);
   g->degree = static_cast<double*>(p);
@@ -180,7 +187,7 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   g->dscal = static_cast<double*>(p);
   g->dflags = reinterpret_cast<int*>(g->dscal + 8);
   SLQ_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * 8 + sizeof(int) * 4, st));
-  if (nnz > 0) {
+  if (nnz > 0 && !adopt_cols) {
     LaunchScope ls(K_PREPARE, st);
     narrow_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, const_cast<int32_t*>(g->cols), nnz, n, g->dflags);
   }
@@ -261,6 +268,10 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   }
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
+}
+
+int graph_adopt(slq_graph* g, int64_t* offsets, int32_t* cols, cudaStream_t st) {
+  return graph_build(g, nullptr, nullptr, nullptr, st, offsets, cols);
 }
 
 // Host mirror of the device scalars (synchronises the creation stream once).
@@ -370,6 +381,14 @@ extern "C" int slq_operator_interval(const slq_graph* g, int kind, double* lo, d
       return SLQ_OK;
   }
   return fail(SLQ_ERR_VALUE, "unknown operator kind");
+}
+
+extern "C" int slq_graph_csr(const slq_graph* g, int64_t* offsets, int32_t* cols, void* stream) {
+  if (!g) return fail(SLQ_ERR_VALUE, "NULL graph");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (offsets) SLQ_CUDA(cudaMemcpyAsync(offsets, g->offsets, sizeof(int64_t) * (g->n + 1), cudaMemcpyDefault, st));
+  if (cols && g->nnz > 0) SLQ_CUDA(cudaMemcpyAsync(cols, g->cols, sizeof(int32_t) * g->nnz, cudaMemcpyDefault, st));
+  return SLQ_OK;
 }
 
 extern "C" int slq_graph_degrees(const slq_graph* g, double* degree, double* dinv, void* stream) {

@@ -1395,14 +1395,46 @@ void ensure_pool(int dev) {
   done[dev] = true;
 }
 
-static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes) {
+static int64_t partial_rows(const slq_graph* g);
+
+// The all-staged schedule keeps u_0 as a bitmask and never stores u_S, so a chunk holds S vectors
+// (u_1..u_{S-1} and w) instead of S + 2.
+static bool lean_schedule(const slq_graph* g, bool start_block, int S, int reorth) {
+  return !start_block && staged_enabled() && coop_supported(g->device) && reorth && S >= 2 && S - 1 <= kCgsBlock;
+}
+
+// Probes per chunk: as many as fit in 90% of the memory the device and this device's pool can
+// still hand out (the pool keeps freed blocks), rounded down to a 32-byte sector multiple of
+// columns when more than one sector fits (a narrower chunk gathers whole sectors; the padded
+// tail of a wider chunk would not).  Results do not depend on the chunk width.
+static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bool lean) {
   size_t freeb = 0, total = 0;
   cudaMemGetInfo(&freeb, &total);
-  const double budget = 0.85 * static_cast<double>(freeb);
-  const double per_probe = static_cast<double>(S + 2) * static_cast<double>(std::max<int64_t>(g->n, 1)) * vbytes;
+  double avail = static_cast<double>(freeb);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    if (reserved > used) avail += static_cast<double>(reserved - used);
+  }
+  const double budget = 0.9 * avail - static_cast<double>(1ull << 30);
+  const int nvec = lean ? S : S + 2;
+  const double per_probe = static_cast<double>(nvec) * static_cast<double>(std::max<int64_t>(g->n, 1)) * vbytes +
+                           8.0 * static_cast<double>(g->max_seg) +
+                           8.0 * static_cast<double>(partial_rows(g)) * (kCgsBlock + 2);
   int64_t c = static_cast<int64_t>(budget / std::max(per_probe, 1.0));
   c = std::min<int64_t>({c, count, kMaxChunk});
+  const int sector = 32 / vbytes;
+  if (c < count && c > sector) c -= c % sector;
   return static_cast<int>(std::max<int64_t>(c, 1));
+}
+
+// Rows of reduction partials: flat fallback kernels (one per stream tile), the persistent step
+// kernel (one per row slot) and alpha_dot_kernel (one per CTA).  The SpMM writes none.
+static int64_t partial_rows(const slq_graph* g) {
+  return std::max<int64_t>({static_cast<int64_t>(g->ntiles_stream), static_cast<int64_t>(kPersist) * kStageSlots,
+                            static_cast<int64_t>(kAlphaCtas)});
 }
 
 template <typename VT>
@@ -1419,8 +1451,15 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   int rc = SLQ_OK;
 
   const int nq_max = kCgsBlock + 2;
-  const int64_t ptiles = std::max<int64_t>({g->ntiles + g->max_long, g->ntiles_stream, kPersist * kStageSlots});
-  const size_t bytes_vec = static_cast<size_t>(vs) * vb * (S + 2);
+  const int64_t ptiles = partial_rows(g);
+  // u_0 as a probe bitmask (c <= 128): the first SpMM gathers bits and the staged step kernels
+  // stream bits instead of u_0; the +-1 values are materialised only for the non-staged kernels.
+  const bool coop_ok = staged_enabled() && coop_supported(g->device);
+  const bool use_bits = !q0 && c <= kBlk;
+  const bool all_staged = use_bits && coop_ok && reorth && S >= 2 && S - 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
+  // all_staged: slots u_1..u_{S-1} and w only (lean_schedule); basis[0] is never addressed
+  const int64_t nvec = all_staged ? S : S + 2;
+  const size_t bytes_vec = static_cast<size_t>(vs) * vb * nvec;
   const size_t bytes_state = sizeof(double) * cpad * (6 * (S + 1) + 3 + (S + 1) * (S + 1)) +
                              sizeof(int) * (3 * cpad + 4 + S + 4) + sizeof(unsigned long long) * (4 * S + 2);
   const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
@@ -1434,8 +1473,8 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const size_t bytes_bits = sizeof(uint32_t) * kBitWords * static_cast<size_t>(std::max<int64_t>(n, 1));
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_bits + bytes_bits, st));
   SLQ_TRACE("after malloc");
-  VT* basis = reinterpret_cast<VT*>(ws);
-  VT* wv = basis + (S + 1) * vs;
+  VT* basis = all_staged ? reinterpret_cast<VT*>(ws) - vs : reinterpret_cast<VT*>(ws);
+  VT* wv = basis + (all_staged ? S : S + 1) * vs;
   double* dstate = reinterpret_cast<double*>(ws + off_state);
   ChunkState s;
   s.c = c; s.cpad = cpad; s.S = S;
@@ -1462,11 +1501,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     LaunchScope ls(K_PROBE, st);
     state_init_kernel<<<ceil_div(std::max(cpad, 4 * S), 128), 128, 0, st>>>(s, n, q0 != nullptr);
   }
-  // u_0 as a probe bitmask (c <= 128): the first SpMM gathers bits and the staged step kernels
-  // stream bits instead of u_0; the +-1 values are materialised only for the non-staged kernels.
-  const bool coop_ok = staged_enabled() && coop_supported(g->device);
-  uint32_t* bits = (!q0 && c <= kBlk) ? reinterpret_cast<uint32_t*>(ws + off_bits) : nullptr;
-  const bool all_staged = bits && coop_ok && reorth && S >= 2 && S - 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
+  uint32_t* bits = use_bits ? reinterpret_cast<uint32_t*>(ws + off_bits) : nullptr;
   if (q0) {
     LaunchScope ls(K_PROBE, st);
     copy_start_kernel<VT><<<std::max(1, std::min(ceil_div(n * c, 256), 148 * 16)), 256, 0, st>>>(q0, ldq, c, n, basis, ldc);
@@ -1478,7 +1513,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
   sa.dscal = g->dscal;
-  sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad; sa.partial = partial;
+  sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad; sa.partial = nullptr;
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));
 
   CgsArgs ca{};
@@ -1509,7 +1544,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   for (int i = 0; i < S; ++i) {
     sa.u = basis + i * vs;
     sa.r = s.rsc + i * cpad;
-    ra.mode = RED_ALPHA; ra.ntiles = static_cast<int>(g->ntiles + g->max_long); ra.nq = 1; ra.i = i; ra.second = 0;
+    ra.mode = RED_ALPHA; ra.ntiles = kAlphaCtas; ra.nq = 1; ra.i = i; ra.second = 0;
     ra.k0 = 0; ra.nk = 0;
     sa.red = ra;
     sa.work = s.work + 4 * i;
@@ -1595,7 +1630,7 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   ensure_pool(g->device);
   const int vb = dtype == SLQ_F64 ? 8 : 4;
   const double t_host0 = host_ms();
-  const int cmax = choose_chunk(g, count, S, vb);
+  const int cmax = choose_chunk(g, count, S, vb, lean_schedule(g, q0 != nullptr, S, reorth));
   SLQ_TRACE("choose_chunk");
   for (int64_t done = 0; done < count;) {
     const int c = static_cast<int>(std::min<int64_t>(cmax, count - done));

@@ -25,6 +25,7 @@ class DeviceGraph:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.graph = g
         self.n = int(g.n)
+        self.nnz = int(g.nnz)
         self.handle = ctypes.c_void_p()
         lib = _lib.load()
         with torch.cuda.device(self.device):
@@ -44,6 +45,36 @@ class DeviceGraph:
                                                ctypes.byref(self.handle))
         _lib.check(rc)
         self._info = None
+
+    @classmethod
+    def rmat(cls, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+             seed: int = 0, device=None) -> "DeviceGraph":
+        """An R-MAT graph generated and converted to canonical CSR on the device (no host copy of the
+        edges: the C5 workload's 4e9 directed edges never leave HBM).  ``graph`` is None."""
+        torch = _lib.require_cuda()
+        self = cls.__new__(cls)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.graph = None
+        self.handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_create_rmat(int(scale), int(edge_factor), float(a), float(b), float(c),
+                                                         int(seed), _lib.stream_handle(self.device),
+                                                         ctypes.byref(self.handle)))
+        self._info = None
+        self.n = int(self.info.n)
+        self.nnz = int(self.info.nnz)
+        return self
+
+    def csr(self):
+        """(row_offsets int64 [n+1], col_indices int32 [nnz]) copied from the device (small graphs)."""
+        import torch
+
+        off = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
+        cols = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_csr(self.handle, _lib.ptr(off), _lib.ptr(cols),
+                                                  _lib.stream_handle(self.device)))
+        return off.cpu().numpy(), cols[:self.nnz].cpu().numpy()
 
     @property
     def info(self):
@@ -133,7 +164,7 @@ class DeviceGraph:
         st = torch.zeros(count, dtype=torch.int32, device=self.device)
         if status is None:
             status = torch.zeros(1, dtype=torch.int32, device=self.device)
-        if KIND_CODES[kind] == _lib.DENSITY and self.graph.nnz == 0:
+        if KIND_CODES[kind] == _lib.DENSITY and self.nnz == 0:
             raise ValueError("density matrix undefined for a graph without edges")
         code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
         with torch.cuda.device(self.device):
@@ -249,3 +280,14 @@ def device_graph(g: Graph, device=None) -> DeviceGraph:
         dg = DeviceGraph(g, dev)
         cache[key] = dg
     return dg
+
+
+def device_probes(n: int, seed: int, probe_begin: int, count: int, device=None):
+    """Rademacher probes [n, count] (+-1.0, float64) of the seeded streams, generated on the device."""
+    torch = _lib.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((n, count), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().slq_probes(int(seed), int(probe_begin), int(count), int(n), _lib.ptr(out), int(count),
+                                          _lib.stream_handle(dev)))
+    return out

@@ -16,7 +16,7 @@ import numpy as np
 
 from .graphs import Graph, block_diagonal, csr_from_edges, unique_sorted
 
-__all__ = ["barabasi_albert", "sbm", "erdos_renyi", "er_batch", "rmat"]
+__all__ = ["barabasi_albert", "sbm", "erdos_renyi", "er_batch", "rmat", "rmat_device_reference"]
 
 
 def barabasi_albert(n: int, m: int, seed: int = 0) -> Graph:
@@ -91,6 +91,38 @@ def er_batch_stacked(count: int = 10_000, seed: int = 0):
     graphs = er_batch(count, seed)
     g, voff = block_diagonal(graphs)
     return g, voff, graphs
+
+
+def _splitmix64(x: np.ndarray) -> np.ndarray:
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def rmat_device_reference(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+                          seed: int = 0) -> Graph:
+    """Host restatement of the device R-MAT generator (csrc/rmat.cu, ``DeviceGraph.rmat``): the same
+    counter-based uniforms u(seed, sample, level) = splitmix64(splitmix64(seed ^ K) ^ (64 sample + level))
+    >> 11 / 2^53 and the same quadrant rule as ``rmat``; used to check the device build edge for edge."""
+    n = 1 << scale
+    total = edge_factor * n
+    with np.errstate(over="ignore"):
+        base = _splitmix64(np.array([np.uint64(seed) ^ np.uint64(0xD1B54A32D192ED03)], dtype=np.uint64))[0]
+        j = np.arange(total, dtype=np.uint64)
+        u = np.zeros(total, dtype=np.int64)
+        v = np.zeros(total, dtype=np.int64)
+        ab, abc = a + b, a + b + c
+        for level in range(scale):
+            h = _splitmix64(base ^ (j * np.uint64(64) + np.uint64(level)))
+            r = (h >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+            bit = np.int64(1) << (scale - 1 - level)
+            u |= np.where(r >= ab, bit, 0)
+            v |= np.where(((r >= a) & (r < ab)) | (r >= abc), bit, 0)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    key = unique_sorted(np.minimum(u, v) * n + np.maximum(u, v))
+    return csr_from_edges(n, key // n, key % n)
 
 
 def rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,

@@ -46,3 +46,17 @@ def test_sm100a_cubin_embedded():
     if r.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in r.stdout
+
+
+@pytest.mark.parametrize("seed,sample,level", [(0, 0, 0), (0, 12345, 7), (2**63 + 5, 2**40, 26), (17, 3, 63)])
+def test_host_rmat_uniform_matches_numpy_restatement(seed, sample, level):
+    import numpy as np
+
+    from paper_2003_01282_b200.synth import _splitmix64
+
+    out = ctypes.c_double()
+    assert _lib.load().slq_rmat_uniform_host(seed, sample, level, ctypes.byref(out)) == 0
+    with np.errstate(over="ignore"):
+        base = _splitmix64(np.array([np.uint64(seed) ^ np.uint64(0xD1B54A32D192ED03)], dtype=np.uint64))
+        h = _splitmix64(base ^ (np.uint64(sample) * np.uint64(64) + np.uint64(level)))[0]
+    assert out.value == float(h >> np.uint64(11)) / 2.0**53

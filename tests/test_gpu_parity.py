@@ -406,3 +406,35 @@ def test_batched_matches_single_graph_path_and_vnge(cuda_device):
         assert abs(ents[k] - rv) <= FP64_TOL * max(abs(rv), 1e-12), k
     with pytest.raises(ValueError, match="without edges"):
         vnge_slq_batch(graphs + [csr_from_edges(4, [], [])], cfg)
+
+
+# device R-MAT generator + CSR build (C4/C5 workloads) vs its host restatement and the oracle
+@pytest.mark.parametrize("scale,ef,seed", [(8, 4, 1), (12, 16, 0), (15, 16, 7)])
+def test_device_rmat_csr_matches_host_restatement(cuda_device, scale, ef, seed):
+    from paper_2003_01282_b200 import synth
+
+    dg = DeviceGraph.rmat(scale, ef, seed=seed, device=cuda_device)
+    ref = synth.rmat_device_reference(scale, ef, seed=seed)
+    off, cols = dg.csr()
+    assert dg.n == ref.n and dg.nnz == ref.nnz
+    assert np.array_equal(off, ref.row_offsets)
+    assert np.array_equal(cols.astype(np.int64), ref.col_indices)
+
+
+def test_device_rmat_descriptors_match_oracle(cuda_device):
+    from paper_2003_01282_b200 import synth
+
+    dg = DeviceGraph.rmat(12, 16, seed=2, device=cuda_device)
+    g = synth.rmat_device_reference(12, 16, seed=2)
+    host = DeviceGraph(g, cuda_device)
+    a1, b1, s1 = dg.tridiagonals("normalized_laplacian", 0, 0, 24, 15)
+    a2, b2, s2 = host.tridiagonals("normalized_laplacian", 0, 0, 24, 15)
+    assert torch.equal(a1, a2) and torch.equal(b1, b2) and torch.equal(s1, s2)
+    rules = dg.rules("normalized_laplacian", 0, 0, 8, 15)
+    vals, _ = rules.integrate(np.array(GRID.values), [_lib.FN_HEAT])
+    ref, _ = O.heat_trace(g, GRID.values, 8, 15, 0)
+    assert golden.rel_l2(vals.cpu().numpy()[0], ref) <= FP64_TOL
+    p = dg.rules("density", 0, 0, 8, 15)
+    v, _ = p.integrate(None, [_lib.FN_XLOGX])
+    ref_v, _ = O.vnge(g, 8, 15, 0)
+    assert abs(-float(v.cpu().numpy()[0, 0]) - ref_v) <= FP64_TOL * abs(ref_v)

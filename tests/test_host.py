@@ -100,3 +100,12 @@ def test_generators_shapes():
     rows = np.repeat(np.arange(r.n), np.diff(r.row_offsets))
     assert np.all(rows != r.col_indices)           # no self-loops
     assert r.nnz % 2 == 0 and r.m == r.nnz // 2    # symmetric
+
+
+def test_rmat_device_reference_is_canonical():
+    g = synth.rmat_device_reference(10, 8, seed=3)
+    off, cols = g.row_offsets, g.col_indices
+    assert g.n == 1024 and off[-1] == g.nnz and g.nnz % 2 == 0
+    for r in range(0, g.n, 97):
+        row = cols[off[r]:off[r + 1]]
+        assert np.all(np.diff(row) > 0) and not np.any(row == r)

@@ -19,13 +19,17 @@ ap.add_argument("--graph", default="sbm")
 ap.add_argument("--nv", type=int, default=100)
 ap.add_argument("--s", type=int, default=15)
 args = ap.parse_args()
+dev = torch.device("cuda", 0)
 if args.graph == "sbm":
     g = synth.sbm(100_000, 10, 1e-3, 1e-5, seed=0)
+    dg = DeviceGraph(g, dev)
+elif args.graph.startswith("drmat"):   # generated on the device (C5: drmat27)
+    dg = DeviceGraph.rmat(int(args.graph.replace("drmat", "")), 16, seed=0, device=dev)
+    g = dg
 else:
     g = synth.rmat(int(args.graph.replace("rmat", "")), 16, seed=0)
-dev = torch.device("cuda", 0)
+    dg = DeviceGraph(g, dev)
 grid = torch.tensor(np.array(TimeGrid(1e-2, 1e2, 250).values), device=dev)
-dg = DeviceGraph(g, dev)
 for _ in range(args.steps):
     rules = dg.rules("normalized_laplacian", 0, 0, args.nv, args.s, dtype=args.dtype)
     for fn in (_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM):
