@@ -12,7 +12,7 @@ import numpy as np
 
 from .errors import SlqLibraryError, TridiagonalEigenError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslq_b200.so")
+LIB_PATH = os.environ.get("SLQ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslq_b200.so")
 
 SLQ_OK, SLQ_ERR_VALUE, SLQ_ERR_EIGEN, SLQ_ERR_CUDA, SLQ_ERR_NONFINITE, SLQ_ERR_ALLOC = range(6)
 LAPLACIAN, NORMALIZED_LAPLACIAN, DENSITY = 0, 1, 2

@@ -263,7 +263,6 @@ struct SpmmArgs {
   void* w;                 // [n][ldc] output
   int64_t ldc_in, ldc_out;
   int c, cpad;
-  double* partial;         // [ntiles + max_long][cpad] alpha partials (nullptr = none)
   ReduceArgs red;          // cooperative launches: alpha reduced in-kernel after a grid barrier
   // long rows (graph.cu): device counts, segment table, per-segment partial sums [max_seg][cpad]
   const int64_t* long_counts;
@@ -301,23 +300,37 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
   return t;
 }
 
-// acc[j] += sum over nonzeros [beg, end) of one row, in stored order (sequential, unfused: the
-// reference's csr_matvec order).  Columns are loaded 32 at a time and broadcast by shuffles; UNR
-// gathers are in flight per lane.
-// acc[j] += sum over nonzeros [beg, end) of one row, in stored order.
-//  EXACT (operator apply, r == 1): t = fl(dinv_c * u_c) [* w], acc = fl(acc + t): the reference's
-//        csr_matvec order and rounding, bit for bit.
-//  !EXACT (Lanczos): acc = fma(s_c, u_c, acc) with s_c = dinv_c [* w]; the caller multiplies the
-//        sum by the probe scale r afterwards (q = r u is never formed per gathered value).
+// acc[j] = sum over nonzeros [beg, end) of one row (beg is a row start, or a segment start a
+// multiple of kSeg after it).
+//  EXACT (operator apply, r == 1): t = fl(dinv_c * u_c) [* w], acc = fl(acc + t) in stored order:
+//        the reference's csr_matvec order and rounding, bit for bit.
+//  !EXACT (Lanczos): two FMA chains, s_even over the even positions of the range and s_odd over
+//        the odd ones (s_c = dinv_c [* w]), acc = s_even + s_odd; the caller multiplies by the probe
+//        scale r (q = r u is never formed per gathered value).  This order is the same for the
+//        full-warp mapping (lane = probe, both chains in one lane) and the HALF mapping (c <= 16:
+//        each half-warp gathers every other nonzero, so one warp instruction fetches two rows'
+//        worth of probes), so results do not depend on the chunk width.
 // Columns are loaded 32 at a time; each lane turns its column into an element offset once and the
 // warp broadcasts offsets with one shuffle per nonzero.  Probe slots beyond c are clamped to a valid
 // column (loaded, never stored), so the loads need no predicates.
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT>
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF>
 __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
                                              const double* __restrict__ wts, const VT* __restrict__ u, int64_t ldi,
-                                             const uint32_t* __restrict__ bits, const int* pidx, const double* r,
-                                             int64_t beg, int64_t end, double* acc) {
+                                             const uint32_t* __restrict__ bits, const int* pidx, int64_t beg,
+                                             int64_t end, double* acc) {
+  // EXACT runs only for the operator apply (probe scale r == 1: fl(x * 1) == x)
+  constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const int plane = HALF ? (lane & 15) : lane;   // probe lane
+  const int sub = HALF ? (lane >> 4) : 0;        // HALF: chain (position parity) of this half
+  constexpr bool SK = KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED);
+  double a0[PPL], a1[PPL];
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) a0[j] = a1[j] = 0.0;
+  auto value = [&](const VT* src, const uint32_t* brow, int j) -> double {
+    if (BITS) return ((__ldg(brow + j) >> plane) & 1u) ? 1.0 : -1.0;
+    return ldg_f64(src + pidx[j]);
+  };
   for (int64_t base = beg; base < end; base += 32) {
     const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
     int64_t myoff = 0;
@@ -329,13 +342,41 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       if (WEIGHTED) myw = __ldg(wts + base + lane);
       if (!EXACT && WEIGHTED) mys *= myw;   // s_c = dinv_c * w (or w)
     }
-    constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane
+    if (HALF) {
+      // pair m: this half takes position 2m + sub; U pairs in flight
+      constexpr int U = 8;
+      const int npairs = (cnt + 1) >> 1;
+      int m = 0;
+      for (; m + U <= npairs; m += U) {
+        double xv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int64_t o = __shfl_sync(FULL, myoff, 2 * (m + q) + sub);
+          xv[q] = value(u + o, bits + o, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int kk = 2 * (m + q) + sub;
+          const double sk = SK ? __shfl_sync(FULL, mys, kk) : 1.0;
+          if (kk < cnt) a0[0] = SK ? fma(sk, xv[q], a0[0]) : a0[0] + xv[q];
+        }
+      }
+      for (; m < npairs; ++m) {
+        const int kk = 2 * m + sub;
+        const int64_t o = __shfl_sync(FULL, myoff, kk);
+        const double sk = SK ? __shfl_sync(FULL, mys, kk) : 1.0;
+        const double x = value(u + o, bits + o, 0);
+        if (kk < cnt) a0[0] = SK ? fma(sk, x, a0[0]) : a0[0] + x;
+      }
+      continue;
+    }
+    constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane (even: chain = q & 1)
     int k = 0;
     for (; k + UNR <= cnt; k += UNR) {
       double xv[UNR][PPL];
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const int64_t o = __shfl_sync(0xffffffffu, myoff, k + q);
+        const int64_t o = __shfl_sync(FULL, myoff, k + q);
         if (BITS) {
           // u_0 = +-1 from the probe bitmask: one uniform 16-byte load covers 128 probes
           const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
@@ -350,21 +391,20 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       }
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const double sk = (KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED))
-                              ? __shfl_sync(0xffffffffu, mys, k + q) : 1.0;
-        const double wk = (EXACT && WEIGHTED) ? __shfl_sync(0xffffffffu, myw, k + q) : 1.0;
+        const double sk = SK ? __shfl_sync(FULL, mys, k + q) : 1.0;
+        const double wk = (EXACT && WEIGHTED) ? __shfl_sync(FULL, myw, k + q) : 1.0;
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
-          if (EXACT) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xv[q][j], r[j], sk, wk));
-          else if (KIND == SLQ_NORMALIZED_LAPLACIAN || WEIGHTED) acc[j] = fma(sk, xv[q][j], acc[j]);
-          else acc[j] += xv[q][j];
+          if (EXACT) a0[j] = __dadd_rn(a0[j], gather_term<KIND, WEIGHTED>(xv[q][j], 1.0, sk, wk));
+          else if (q & 1) a1[j] = SK ? fma(sk, xv[q][j], a1[j]) : a1[j] + xv[q][j];
+          else a0[j] = SK ? fma(sk, xv[q][j], a0[j]) : a0[j] + xv[q][j];
         }
       }
     }
     for (; k < cnt; ++k) {
-      const int64_t o = __shfl_sync(0xffffffffu, myoff, k);
-      const double sk = (KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED)) ? __shfl_sync(0xffffffffu, mys, k) : 1.0;
-      const double wk = (EXACT && WEIGHTED) ? __shfl_sync(0xffffffffu, myw, k) : 1.0;
+      const int64_t o = __shfl_sync(FULL, myoff, k);
+      const double sk = SK ? __shfl_sync(FULL, mys, k) : 1.0;
+      const double wk = (EXACT && WEIGHTED) ? __shfl_sync(FULL, myw, k) : 1.0;
       double xr[PPL];
       if (BITS) {
         const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
@@ -378,20 +418,27 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       }
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
-        if (EXACT) acc[j] = __dadd_rn(acc[j], gather_term<KIND, WEIGHTED>(xr[j], r[j], sk, wk));
-        else if (KIND == SLQ_NORMALIZED_LAPLACIAN || WEIGHTED) acc[j] = fma(sk, xr[j], acc[j]);
-        else acc[j] += xr[j];
+        if (EXACT) a0[j] = __dadd_rn(a0[j], gather_term<KIND, WEIGHTED>(xr[j], 1.0, sk, wk));
+        else if (k & 1) a1[j] = SK ? fma(sk, xr[j], a1[j]) : a1[j] + xr[j];
+        else a0[j] = SK ? fma(sk, xr[j], a0[j]) : a0[j] + xr[j];
       }
     }
   }
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    if (EXACT) acc[j] = a0[j];
+    else if (HALF) acc[j] = a0[j] + __shfl_xor_sync(FULL, a0[j], 16);   // s_even + s_odd in both halves
+    else acc[j] = a0[j] + a1[j];
+  }
 }
 
-// own-row value u[row][probe j] (from the bitmask on the first step)
+// own-row value u[row][probe j] (from the bitmask on the first step); plane = probe lane
 template <typename VT, int PPL, bool BITS>
-__device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint32_t* bits, int64_t row, int j) {
+__device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint32_t* bits, int64_t row, int j,
+                                            int plane) {
   if (BITS) {
     const uint32_t wd = __ldg(bits + row * kBitWords + j);
-    return ((wd >> (threadIdx.x & 31)) & 1u) ? 1.0 : -1.0;
+    return ((wd >> plane) & 1u) ? 1.0 : -1.0;
   }
   return ldg_f64(u + row * ldi + 32 * j);
 }
@@ -401,19 +448,22 @@ __device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint
 // partial per tile).  Which warp runs an item never changes its arithmetic, so results are
 // deterministic; dynamic scheduling removes the tail left by hub rows.  Long rows are finished by
 // spmm_long_finish_kernel or the step kernel's phase 0.
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT>
-__global__ void __launch_bounds__(kSpmmWarps * 32, 4)
+#ifndef SLQ_SPMM_MINB4
+#define SLQ_SPMM_MINB4 3   // resident CTAs per SM for PPL = 4 (80 registers: no spills in the 4-probe lanes)
+#endif
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF>
+__global__ void __launch_bounds__(kSpmmWarps * 32, PPL == 4 ? SLQ_SPMM_MINB4 : 4)
 spmm_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
-  const int pbase = blockIdx.y * kBlk + lane;
+  const int plane = HALF ? (lane & 15) : lane;   // HALF: two half-warps share probes 0..15
+  const bool writer = !HALF || lane < 16;
+  const int pbase = blockIdx.y * kBlk + plane;
   bool pv[PPL];
-  double r[PPL];
   int pidx[PPL];   // column offsets within a gathered row, clamped to a valid probe
 #pragma unroll
   for (int j = 0; j < PPL; ++j) {
     pv[j] = probe_ok(pbase + 32 * j, a.c);
-    r[j] = (a.r && pv[j]) ? a.r[pbase + 32 * j] : 1.0;
-    pidx[j] = pv[j] ? 32 * j : (a.c - 1 - (blockIdx.y * kBlk + lane));
+    pidx[j] = pv[j] ? 32 * j : (a.c - 1 - (blockIdx.y * kBlk + plane));
   }
   const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
   VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
@@ -437,13 +487,14 @@ spmm_kernel(SpmmArgs a) {
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, r, beg, end, acc);
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, beg, end,
+                                                            acc);
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
     for (int j = 0; j < PPL; ++j)
-      if (pv[j]) dst[32 * j] = acc[j];
+      if (pv[j] && writer) dst[32 * j] = acc[j];
   }
-  // phase 2: row tiles, one warp each (dynamic); rows in order, alpha partial per tile
+  // phase 2: row tiles, one warp each (dynamic); rows in order
   unsigned long long* tcounter = counter + 2;
   for (;;) {
     long long item = 0;
@@ -451,37 +502,29 @@ spmm_kernel(SpmmArgs a) {
     const int tile = static_cast<int>(__shfl_sync(0xffffffffu, item, 0));
     if (tile >= a.ntiles) break;
     const int64_t rb = a.tile_rows[tile], re = a.tile_rows[tile + 1];
-    double dot[PPL];
-#pragma unroll
-    for (int j = 0; j < PPL; ++j) dot[j] = 0.0;
     for (int64_t row = rb; row < re; ++row) {
       const int64_t beg = off[row], end = off[row + 1];
       if (a.long_counts && end - beg > kLongRow) continue;   // finished from its segments
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, r, beg, end, acc);
+      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, beg, end,
+                                                              acc);
       const double d = __ldg(a.degree + row);
       const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
-        if (!pv[j]) continue;
-        const double x = __dmul_rn(own_value<VT, PPL, BITS>(u, ldi, a.bits, row, j), r[j]);
-        const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * r[j], d, dis, scale);
+        if (!pv[j] || !writer) continue;
+        const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + 32 * j);
+        const double x = __dmul_rn(own_value<VT, PPL, BITS>(u, ldi, a.bits, row, j, plane), rj);
+        const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * rj, d, dis, scale);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
-        dot[j] = fma(x, y, dot[j]);
       }
-    }
-    if (a.partial) {
-#pragma unroll
-      for (int j = 0; j < PPL; ++j)
-        if (pbase + 32 * j < a.cpad) a.partial[static_cast<int64_t>(tile) * a.cpad + pbase + 32 * j] = dot[j];
     }
   }
 }
 
-// Long rows: sum the segment partials in segment order, then the operator epilogue.  alpha
-// partials go to partial rows [ntiles, ntiles + max_long) (zero for unused rows).
+// Long rows: sum the segment partials in segment order, then the operator epilogue.
 template <typename VT, int KIND, int PPL>
 __global__ void __launch_bounds__(kSpmmWarps * 32)
 spmm_long_finish_kernel(SpmmArgs a) {
@@ -493,9 +536,6 @@ spmm_long_finish_kernel(SpmmArgs a) {
   const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
   for (int64_t lr = static_cast<int64_t>(blockIdx.x) * kSpmmWarps + warp; lr < a.max_long;
        lr += static_cast<int64_t>(gridDim.x) * kSpmmWarps) {
-    double dot[PPL];
-#pragma unroll
-    for (int j = 0; j < PPL; ++j) dot[j] = 0.0;
     if (lr < nlong) {
       const int64_t row = a.long_rows[lr];
       const int64_t s0 = a.long_seg_first[lr], s1 = a.long_seg_first[lr + 1];
@@ -514,14 +554,6 @@ spmm_long_finish_kernel(SpmmArgs a) {
         const double x = __dmul_rn(own, rj);
         const double y = op_epilogue<KIND>(x, acc, d, dis, scale);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
-        dot[j] = fma(x, y, dot[j]);
-      }
-    }
-    if (a.partial) {
-#pragma unroll
-      for (int j = 0; j < PPL; ++j) {
-        const int p = pbase + 32 * j;
-        if (p < a.cpad) a.partial[(static_cast<int64_t>(a.ntiles) + lr) * a.cpad + p] = dot[j];
       }
     }
   }
@@ -537,13 +569,19 @@ static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_
   (void)coop;
   (void)dev;
   dim3 grid(148 * 4, gy);   // persistent: work is taken from the atomic counters
-  // EXACT (bit-identical operator apply) only for the apply entry (r == nullptr, double)
+  // EXACT (bit-identical operator apply) only for the apply entry (r == nullptr, double);
+  // HALF (two nonzeros per warp instruction) for Lanczos chunks of <= 16 probes.
+  const bool half = PPL == 1 && a.c <= 16 && a.ldc_in <= 16;
   if (!a.r) {
-    if (std::is_same<VT, double>::value) spmm_kernel<VT, KIND, W, PPL, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    if (std::is_same<VT, double>::value)
+      spmm_kernel<VT, KIND, W, PPL, false, true, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else if (half) {
+    if (a.bits) spmm_kernel<VT, KIND, W, 1, true, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    else spmm_kernel<VT, KIND, W, 1, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   } else if (a.bits) {
-    spmm_kernel<VT, KIND, W, PPL, true, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    spmm_kernel<VT, KIND, W, PPL, true, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   } else {
-    spmm_kernel<VT, KIND, W, PPL, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    spmm_kernel<VT, KIND, W, PPL, false, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   }
 }
 
@@ -1513,7 +1551,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
   sa.dscal = g->dscal;
-  sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad; sa.partial = nullptr;
+  sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad;
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));
 
   CgsArgs ca{};
@@ -1554,7 +1592,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
     // writes w; otherwise (last step, s > 17, SLQ_STAGED=0) the SpMM also reduces alpha.
     const bool staged = coop && reorth && i < S - 1 && i + 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
-    sa.partial = nullptr;   // alpha: step kernel (staged) or alpha_dot_kernel
+    // alpha: step kernel (staged) or alpha_dot_kernel
     SLQ_TRACE("spmm launch");
     launch_spmm<VT>(kind, sa, false, g->device, st, /*finish=*/!staged);   // staged: phase 0 finishes
     SLQ_TRACE("spmm launched");
@@ -1681,7 +1719,7 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
     sa.dscal = g->dscal;
     sa.u = x + j0; sa.r = nullptr; sa.w = y + j0; sa.ldc_in = ld; sa.ldc_out = ld;
     sa.c = static_cast<int>(std::min<int64_t>(kCols, ncols - j0));
-    sa.cpad = ceil_div(sa.c, 32) * 32; sa.partial = nullptr;
+    sa.cpad = ceil_div(sa.c, 32) * 32;
     sa.work = work + 4 * pi;
     set_long_rows(sa, g, segpart);
     launch_spmm<double>(kind, sa, false, g->device, st);

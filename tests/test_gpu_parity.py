@@ -225,6 +225,15 @@ def test_rules_independent_of_chunking(cuda_device):
     assert torch.equal(s_full, torch.cat([s1, s2]))
     a3, _, _ = dg.tridiagonals("normalized_laplacian", 0, 0, 70, 15)
     assert torch.equal(a_full, a3)
+    # narrow chunks (<= 16 probes: half-warp SpMM mapping) follow the same summation order
+    for begin, count in ((0, 16), (16, 9), (40, 1)):
+        a4, b4, s4 = dg.tridiagonals("normalized_laplacian", 0, begin, count, 15)
+        assert torch.equal(a4, a_full[begin:begin + count]) and torch.equal(b4, b_full[begin:begin + count])
+        assert torch.equal(s4, s_full[begin:begin + count])
+    for kind in ("normalized_laplacian", "density"):
+        f_full, _, _ = dg.tridiagonals(kind, 0, 0, 40, 15, dtype="f32")
+        f_narrow, _, _ = dg.tridiagonals(kind, 0, 24, 16, 15, dtype="f32")
+        assert torch.equal(f_narrow, f_full[24:40]), kind
 
 
 # edge cases the reference tests
