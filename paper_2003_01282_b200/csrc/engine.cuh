@@ -1,0 +1,1358 @@
+// Shared engine definitions: chunk state, reductions, the SpMM pass and the staged CGS step
+// kernel (templates).  lanczos.cu runs the engine; spmm_*.cu and step_*.cu instantiate the
+// heavy kernel families per vector type so the library builds in parallel translation units.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cooperative_groups.h>
+#include <type_traits>
+#include "bulk_pipe.cuh"
+#include "pcg64.cuh"
+#include "slq_common.cuh"
+
+namespace slq {
+
+
+namespace cg = cooperative_groups;
+
+constexpr int kProbeRun = 32;        // 64-bit PCG outputs per thread in probe_init (64 rows)
+constexpr int kSecondPassGrid = 148 * 4;
+constexpr int kMaxChunk = 256;       // probes per chunk (flat CGS CTAs of <= 512 threads)
+
+// ----------------------------------------------------------------------------- probes
+// Rademacher probes: u (if not null) gets +-1 values; bits (if not null) gets one bit per probe,
+// bits[row][kBitWords] with word g = probes 32g..32g+31 (bit set = +1).  A warp = 32 probes of one
+// group over a run of 2*kProbeRun rows.
+constexpr int kBitWords = 4;   // bitmask row stride in 32-bit words (16 B: bulk-copy aligned; c <= 128)
+
+template <typename VT>
+__global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* __restrict__ u,
+                                  int64_t ldc, uint32_t* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t run = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int p = blockIdx.y * 32 + lane;
+  const int64_t row0 = run * (2 * kProbeRun);
+  if (row0 >= n) return;                       // warp-uniform
+  const bool pv = p < c;
+  u128 st = 0, inc = 0;
+  if (pv) {
+    pcg64_seed_state(seed, static_cast<uint64_t>(probe_begin + p), &st, &inc);
+    st = pcg_advance(st, inc, static_cast<uint64_t>(run) * kProbeRun);
+  }
+  const u128 mult = pcg_mult();
+  for (int m = 0; m < kProbeRun; ++m) {
+    uint64_t out = 0;
+    if (pv) {
+      st = st * mult + inc;
+      out = pcg_output(st);
+    }
+    const int64_t r = row0 + 2 * m;
+    const bool b0 = (out >> 31) & 1u, b1 = (out >> 63) & 1u;
+    if (u && pv) {
+      if (r < n) u[r * ldc + p] = from_f64<VT>(b0 ? 1.0 : -1.0);
+      if (r + 1 < n) u[(r + 1) * ldc + p] = from_f64<VT>(b1 ? 1.0 : -1.0);
+    }
+    if (bits) {
+      const uint32_t w0 = __ballot_sync(0xffffffffu, pv && b0);
+      const uint32_t w1 = __ballot_sync(0xffffffffu, pv && b1);
+      if (lane == 0) {
+        if (r < n) bits[r * kBitWords + blockIdx.y] = w0;
+        if (r + 1 < n) bits[(r + 1) * kBitWords + blockIdx.y] = w1;
+      }
+    }
+  }
+}
+
+template <typename VT>
+static void launch_probes(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* u, int64_t ldc,
+                          cudaStream_t st, uint32_t* bits = nullptr) {
+  const int64_t runs = (n + 2 * kProbeRun - 1) / (2 * kProbeRun);
+  dim3 grid(ceil_div(runs, 4), ceil_div(c, 32));
+  LaunchScope ls(K_PROBE, st);
+  probe_init_kernel<VT><<<grid, 128, 0, st>>>(seed, probe_begin, c, n, u, ldc, bits);
+}
+
+template <typename VT>
+__global__ void copy_start_kernel(const double* __restrict__ q0, int64_t ldq, int c, int64_t n, VT* __restrict__ u,
+                                  int64_t ldc) {
+  const int64_t total = n * c;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / c;
+    const int p = static_cast<int>(idx - r * c);
+    u[r * ldc + p] = from_f64<VT>(q0[r * ldq + p]);
+  }
+}
+
+// ----------------------------------------------------------------------------- per-probe state
+struct ChunkState {
+  int c = 0, cpad = 0, S = 0;
+  double* rsc = nullptr;    // [S+1][cpad]  r_k = 1/beta_{k-1}, r_0 = 1/sqrt(n)
+  double* alpha = nullptr;  // [S][cpad]
+  double* beta = nullptr;   // [S][cpad]
+  double* h = nullptr;      // [S][cpad]    CGS coefficients of the current step
+  double* nb2 = nullptr;    // [cpad]       ||w'||^2
+  // staged path (Gram form of CGS): raw sums and the Gram matrix of the stored basis
+  double* cdot = nullptr;   // [S+1][cpad]  sum_rows u_k . w            (k <= i)
+  double* gram = nullptr;   // [S+1][cpad]  sum_rows u_k . u_{i+1}      (k <= i), row of the new vector
+  double* nrm2 = nullptr;   // [cpad]       ||u_{i+1}||^2
+  double* G = nullptr;      // [(S+1)*(S+1)][cpad]  G(k,j) = q_k . q_j
+  int* steps = nullptr;     // [cpad]
+  int* alive = nullptr;     // [cpad]
+  int* again = nullptr;     // [cpad]
+  int* any_again = nullptr; // [1]
+  unsigned int* barrier = nullptr;   // [S] grid-barrier counters of the persistent step kernels
+  unsigned long long* work = nullptr;   // [S][4] SpMM work counters
+};
+
+static __global__ void state_init_kernel(ChunkState s, int64_t n, int given_start) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < s.S) s.barrier[p] = 0u;
+  if (p < 4 * s.S) s.work[p] = 0ull;
+  if (p >= s.cpad) return;
+  const bool pv = p < s.c;
+  // r_0: the probe +-1 block is scaled by 1/fl(sqrt(n)) (= 1/||v||); a caller-given unit start
+  // vector is used as is.
+  s.rsc[p] = pv ? (given_start ? 1.0 : __ddiv_rn(1.0, __dsqrt_rn(static_cast<double>(n)))) : 0.0;
+  s.steps[p] = s.S;
+  s.alive[p] = pv ? 1 : 0;
+  s.again[p] = 0;
+  for (int k = 0; k < s.S; ++k) { s.alpha[k * s.cpad + p] = 0.0; s.beta[k * s.cpad + p] = 0.0; }
+  if (p == 0) *s.any_again = 0;
+}
+
+// ----------------------------------------------------------------------------- reductions
+enum ReduceMode { RED_ALPHA = 0, RED_CGS = 1, RED_NORM = 2, RED_NORM2 = 3 };
+
+struct ReduceArgs {
+  const double* partial;   // [ntiles][nq][cpad]
+  int ntiles, nq, cpad, c;
+  int mode;
+  int i, k0, nk, reorth;
+  int second;              // 1: reduction of the conditional second CGS pass
+  int kind;                // operator kind: breakdown tolerance 1e-12 * interval_hi (lanczos.py:36,110)
+  const double* dscal;     // device graph scalars (Laplacian interval_hi = dscal[4])
+  ChunkState s;
+};
+
+constexpr int kReduceWarps = 16;
+constexpr int kStripes = 16;   // fixed partition of the partial rows: the sum order never depends on
+                               // the CTA shape that runs the reduction
+
+// Per-probe scalar logic applied to a fully reduced quantity (lanczos.py:123-137).
+static __device__ void apply_reduced(const ReduceArgs& a, int q, int p, double tot, bool first_slice) {
+  const int cp = a.cpad;
+  const bool pv = p < a.c;
+  switch (a.mode) {
+    case RED_ALPHA:
+      if (pv && a.s.alive[p]) a.s.alpha[a.i * cp + p] = tot;
+      if (first_slice && p == 0) *a.s.any_again = 0;
+      break;
+    case RED_CGS:
+      if (q < a.nk) a.s.h[(a.k0 + q) * cp + p] = tot * a.s.rsc[(a.k0 + q) * cp + p];
+      else if (!a.second) a.s.nb2[p] = tot;
+      break;
+    case RED_NORM:
+    case RED_NORM2: {
+      if (!pv || !a.s.alive[p]) break;
+      const double b = sqrt(tot);
+      if (a.mode == RED_NORM) {
+        if (a.reorth && b < 0.5 * sqrt(a.s.nb2[p])) {    // lanczos.py:75
+          a.s.again[p] = 1;
+          *a.s.any_again = 1;
+          break;
+        }
+      } else {
+        if (!a.s.again[p]) break;
+        a.s.again[p] = 0;
+      }
+      const double hi = a.kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (a.kind == SLQ_DENSITY ? 1.0 : a.dscal[4]);
+      if (b <= 1e-12 * hi) {                             // lanczos.py:133-134
+        a.s.steps[p] = a.i + 1;
+        a.s.alive[p] = 0;
+        a.s.rsc[(a.i + 1) * cp + p] = 0.0;
+      } else {
+        a.s.beta[a.i * cp + p] = b;
+        a.s.rsc[(a.i + 1) * cp + p] = __ddiv_rn(1.0, b);
+      }
+      break;
+    }
+  }
+}
+
+// Reduce quantity q for the 32 probes of `group` over a.ntiles partial rows, with any number of
+// warps (>= 1).  All threads of the CTA must call it.  red: kStripes*32 doubles of shared memory.
+static __device__ void reduce_slice(const ReduceArgs& a, int q, int group, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int p = group * 32 + lane;
+  const int64_t stride = static_cast<int64_t>(a.nq) * a.cpad;
+  const double* src = a.partial + static_cast<int64_t>(q) * a.cpad + p;
+  for (int sidx = warp; sidx < kStripes; sidx += nw) {
+    double s = 0.0;
+    int t = sidx;
+    for (; t + 3 * kStripes < a.ntiles; t += 4 * kStripes) {
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = src[(t + j * kStripes) * stride];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s += v[j];
+    }
+    for (; t < a.ntiles; t += kStripes) s += src[t * stride];
+    red[sidx * 32 + lane] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double tot = red[lane];
+    for (int j = 1; j < kStripes; ++j) tot += red[j * 32 + lane];
+    apply_reduced(a, q, p, tot, group == 0 && q == 0);
+  }
+  __syncthreads();
+}
+
+static __global__ void __launch_bounds__(kReduceWarps * 32)
+reduce_kernel(ReduceArgs a) {
+  __shared__ double red[kStripes * 32];
+  if (a.second && *a.s.any_again == 0) return;
+  reduce_slice(a, blockIdx.x, blockIdx.y, red);
+}
+
+// ----------------------------------------------------------------------------- launch geometry
+// A CTA covers one block of up to kBlk = 128 probes; lane l owns probes l, l+32, l+64, l+96 of the
+// block (PPL = probes per lane), so one shuffled column index feeds PPL coalesced 256-byte gathers.
+// Which thread owns a probe never changes its arithmetic: every per-probe sum runs in a fixed order
+// set by the graph's tiles and the warp count, never by c.
+constexpr int kBlk = 128;
+constexpr int kSpmmWarps = 8;
+
+__device__ __forceinline__ bool probe_ok(int p, int c) { return p < c; }
+
+// ----------------------------------------------------------------------------- pass A: SpMM
+struct SpmmArgs {
+  const int64_t* offsets;
+  const int32_t* cols;
+  const double* weights;   // nullptr = unit
+  const double* degree;
+  const double* dinv;
+  const int64_t* tile_rows;
+  int ntiles;
+  const double* dscal;     // device graph scalars; density scale 1/tr L = dscal[3]
+  const void* u;           // [n][ldc] input (unnormalised)
+  const double* r;         // [cpad] per-probe scale (nullptr = 1.0)
+  void* w;                 // [n][ldc] output
+  int64_t ldc_in, ldc_out;
+  int c, cpad;
+  ReduceArgs red;          // cooperative launches: alpha reduced in-kernel after a grid barrier
+  // long rows (graph.cu): device counts, segment table, per-segment partial sums [max_seg][cpad]
+  const int64_t* long_counts;
+  const int32_t* long_rows;
+  const int64_t* long_seg_first;
+  const int32_t* seg_row;
+  const int64_t* seg_begin;
+  int64_t max_long;
+  double* segpart;
+  unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
+  const uint32_t* bits;      // first step: u_0 as a probe bitmask [n][kBitWords] (nullptr = use u)
+};
+
+template <int KIND>
+__device__ __forceinline__ double op_epilogue(double x, double acc, double d, double dis, double scale) {
+  if (KIND == SLQ_NORMALIZED_LAPLACIAN) {
+    // nonisolated * x - dinv_sqrt * (A @ (dinv_sqrt * x))       operators.py:88-89
+    const double keep = d > 0.0 ? 1.0 : 0.0;
+    return __dsub_rn(__dmul_rn(keep, x), __dmul_rn(dis, acc));
+  } else if (KIND == SLQ_DENSITY) {
+    // scale * (d * x - A @ x)                                   operators.py:98-99
+    return __dmul_rn(scale, __dsub_rn(__dmul_rn(d, x), acc));
+  } else {
+    // d * x - A @ x                                             operators.py:76-78
+    return __dsub_rn(__dmul_rn(d, x), acc);
+  }
+}
+
+// One term of the in-row sum: A_jk * (dinv_k * x_k) with x_k = u_k * r (operators.py:89 order).
+template <int KIND, bool WEIGHTED>
+__device__ __forceinline__ double gather_term(double xraw, double r, double sk, double wk) {
+  double t = __dmul_rn(xraw, r);
+  if (KIND == SLQ_NORMALIZED_LAPLACIAN) t = __dmul_rn(sk, t);
+  if (WEIGHTED) t = __dmul_rn(wk, t);
+  return t;
+}
+
+// acc[j] = sum over nonzeros [beg, end) of one row (beg is a row start, or a segment start a
+// multiple of kSeg after it).
+//  EXACT (operator apply, r == 1): t = fl(dinv_c * u_c) [* w], acc = fl(acc + t) in stored order:
+//        the reference's csr_matvec order and rounding, bit for bit.
+//  !EXACT (Lanczos): two FMA chains, s_even over the even positions of the range and s_odd over
+//        the odd ones (s_c = dinv_c [* w]), acc = s_even + s_odd; the caller multiplies by the probe
+//        scale r (q = r u is never formed per gathered value).  This order is the same for the
+//        full-warp mapping (lane = probe, both chains in one lane) and the HALF mapping (c <= 16:
+//        each half-warp gathers every other nonzero, so one warp instruction fetches two rows'
+//        worth of probes), so results do not depend on the chunk width.
+// Columns are loaded 32 at a time; each lane turns its column into an element offset once and the
+// warp broadcasts offsets with one shuffle per nonzero.  Probe slots beyond c are clamped to a valid
+// column (loaded, never stored), so the loads need no predicates.
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF>
+__device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
+                                             const double* __restrict__ wts, const VT* __restrict__ u, int64_t ldi,
+                                             const uint32_t* __restrict__ bits, const int* pidx, int64_t beg,
+                                             int64_t end, double* acc) {
+  // EXACT runs only for the operator apply (probe scale r == 1: fl(x * 1) == x)
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int plane = HALF ? (lane & 15) : lane;   // probe lane
+  const int sub = HALF ? (lane >> 4) : 0;        // HALF: chain (position parity) of this half
+  constexpr bool SK = KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED);
+  double a0[PPL], a1[PPL];
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) a0[j] = a1[j] = 0.0;
+  auto value = [&](const VT* src, const uint32_t* brow, int j) -> double {
+    if (BITS) return ((__ldg(brow + j) >> plane) & 1u) ? 1.0 : -1.0;
+    return ldg_f64(src + pidx[j]);
+  };
+  for (int64_t base = beg; base < end; base += 32) {
+    const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
+    int64_t myoff = 0;
+    double mys = 1.0, myw = 1.0;
+    if (lane < cnt) {
+      const int64_t col = __ldg(cols + base + lane);
+      myoff = BITS ? col * kBitWords : col * ldi;
+      if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + col);
+      if (WEIGHTED) myw = __ldg(wts + base + lane);
+      if (!EXACT && WEIGHTED) mys *= myw;   // s_c = dinv_c * w (or w)
+    }
+    if (HALF) {
+      // pair m: this half takes position 2m + sub; U pairs in flight
+      constexpr int U = 8;
+      const int npairs = (cnt + 1) >> 1;
+      int m = 0;
+      for (; m + U <= npairs; m += U) {
+        double xv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int64_t o = __shfl_sync(FULL, myoff, 2 * (m + q) + sub);
+          xv[q] = value(u + o, bits + o, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int kk = 2 * (m + q) + sub;
+          const double sk = SK ? __shfl_sync(FULL, mys, kk) : 1.0;
+          if (kk < cnt) a0[0] = SK ? fma(sk, xv[q], a0[0]) : a0[0] + xv[q];
+        }
+      }
+      for (; m < npairs; ++m) {
+        const int kk = 2 * m + sub;
+        const int64_t o = __shfl_sync(FULL, myoff, kk);
+        const double sk = SK ? __shfl_sync(FULL, mys, kk) : 1.0;
+        const double x = value(u + o, bits + o, 0);
+        if (kk < cnt) a0[0] = SK ? fma(sk, x, a0[0]) : a0[0] + x;
+      }
+      continue;
+    }
+    constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane (even: chain = q & 1)
+    int k = 0;
+    for (; k + UNR <= cnt; k += UNR) {
+      double xv[UNR][PPL];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int64_t o = __shfl_sync(FULL, myoff, k + q);
+        if (BITS) {
+          // u_0 = +-1 from the probe bitmask: one uniform 16-byte load covers 128 probes
+          const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
+          const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int j = 0; j < PPL; ++j) xv[q][j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
+        } else {
+          const VT* src = u + o;
+#pragma unroll
+          for (int j = 0; j < PPL; ++j) xv[q][j] = ldg_f64(src + pidx[j]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const double sk = SK ? __shfl_sync(FULL, mys, k + q) : 1.0;
+        const double wk = (EXACT && WEIGHTED) ? __shfl_sync(FULL, myw, k + q) : 1.0;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          if (EXACT) a0[j] = __dadd_rn(a0[j], gather_term<KIND, WEIGHTED>(xv[q][j], 1.0, sk, wk));
+          else if (q & 1) a1[j] = SK ? fma(sk, xv[q][j], a1[j]) : a1[j] + xv[q][j];
+          else a0[j] = SK ? fma(sk, xv[q][j], a0[j]) : a0[j] + xv[q][j];
+        }
+      }
+    }
+    for (; k < cnt; ++k) {
+      const int64_t o = __shfl_sync(FULL, myoff, k);
+      const double sk = SK ? __shfl_sync(FULL, mys, k) : 1.0;
+      const double wk = (EXACT && WEIGHTED) ? __shfl_sync(FULL, myw, k) : 1.0;
+      double xr[PPL];
+      if (BITS) {
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
+        const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) xr[j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
+      } else {
+        const VT* src = u + o;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) xr[j] = ldg_f64(src + pidx[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        if (EXACT) a0[j] = __dadd_rn(a0[j], gather_term<KIND, WEIGHTED>(xr[j], 1.0, sk, wk));
+        else if (k & 1) a1[j] = SK ? fma(sk, xr[j], a1[j]) : a1[j] + xr[j];
+        else a0[j] = SK ? fma(sk, xr[j], a0[j]) : a0[j] + xr[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    if (EXACT) acc[j] = a0[j];
+    else if (HALF) acc[j] = a0[j] + __shfl_xor_sync(FULL, a0[j], 16);   // s_even + s_odd in both halves
+    else acc[j] = a0[j] + a1[j];
+  }
+}
+
+// own-row value u[row][probe j] (from the bitmask on the first step); plane = probe lane
+template <typename VT, int PPL, bool BITS>
+__device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint32_t* bits, int64_t row, int j,
+                                            int plane) {
+  if (BITS) {
+    const uint32_t wd = __ldg(bits + row * kBitWords + j);
+    return ((wd >> plane) & 1u) ? 1.0 : -1.0;
+  }
+  return ldg_f64(u + row * ldi + 32 * j);
+}
+
+// Pass A.  Warp-level work items taken from an atomic counter: first the long-row segments (partial
+// sums to a.segpart), then the graph-fixed row tiles (one warp per tile: rows in order, alpha
+// partial per tile).  Which warp runs an item never changes its arithmetic, so results are
+// deterministic; dynamic scheduling removes the tail left by hub rows.  Long rows are finished by
+// spmm_long_finish_kernel or the step kernel's phase 0.
+#ifndef SLQ_SPMM_MINB4
+#define SLQ_SPMM_MINB4 3   // resident CTAs per SM for PPL = 4 (80 registers: no spills in the 4-probe lanes)
+#endif
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF>
+__global__ void __launch_bounds__(kSpmmWarps * 32, PPL == 4 ? SLQ_SPMM_MINB4 : 4)
+spmm_kernel(SpmmArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int plane = HALF ? (lane & 15) : lane;   // HALF: two half-warps share probes 0..15
+  const bool writer = !HALF || lane < 16;
+  const int pbase = blockIdx.y * kBlk + plane;
+  bool pv[PPL];
+  int pidx[PPL];   // column offsets within a gathered row, clamped to a valid probe
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    pv[j] = probe_ok(pbase + 32 * j, a.c);
+    pidx[j] = pv[j] ? 32 * j : (a.c - 1 - (blockIdx.y * kBlk + plane));
+  }
+  const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
+  VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
+  const int64_t* __restrict__ off = a.offsets;
+  const double* __restrict__ dinv = a.dinv;
+  const int64_t ldi = a.ldc_in;
+  const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
+  const int64_t nseg = a.long_counts ? a.long_counts[1] : 0;
+  unsigned long long* counter = a.work + blockIdx.y;   // [0..1] segments, [2..3] tiles (per probe block)
+
+  // phase 1: long-row segments, one warp each (dynamic)
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = static_cast<long long>(atomicAdd(counter, 1ull));
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= nseg) break;
+    const int64_t row = a.seg_row[item];
+    const int64_t beg = a.seg_begin[item];
+    const int64_t rend = off[row + 1];
+    const int64_t end = beg + kSeg < rend ? beg + kSeg : rend;
+    double acc[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, beg, end,
+                                                            acc);
+    double* dst = a.segpart + item * a.cpad + pbase;
+#pragma unroll
+    for (int j = 0; j < PPL; ++j)
+      if (pv[j] && writer) dst[32 * j] = acc[j];
+  }
+  // phase 2: row tiles, one warp each (dynamic); rows in order
+  unsigned long long* tcounter = counter + 2;
+  for (;;) {
+    long long item = 0;
+    if (lane == 0) item = static_cast<long long>(atomicAdd(tcounter, 1ull));
+    const int tile = static_cast<int>(__shfl_sync(0xffffffffu, item, 0));
+    if (tile >= a.ntiles) break;
+    const int64_t rb = a.tile_rows[tile], re = a.tile_rows[tile + 1];
+    for (int64_t row = rb; row < re; ++row) {
+      const int64_t beg = off[row], end = off[row + 1];
+      if (a.long_counts && end - beg > kLongRow) continue;   // finished from its segments
+      double acc[PPL];
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
+      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, beg, end,
+                                                              acc);
+      const double d = __ldg(a.degree + row);
+      const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        if (!pv[j] || !writer) continue;
+        const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + 32 * j);
+        const double x = __dmul_rn(own_value<VT, PPL, BITS>(u, ldi, a.bits, row, j, plane), rj);
+        const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * rj, d, dis, scale);
+        w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
+      }
+    }
+  }
+}
+
+// Long rows: sum the segment partials in segment order, then the operator epilogue.
+template <typename VT, int KIND, int PPL>
+__global__ void __launch_bounds__(kSpmmWarps * 32)
+spmm_long_finish_kernel(SpmmArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pbase = blockIdx.y * kBlk + lane;
+  const int64_t nlong = a.long_counts[0];
+  const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
+  VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
+  const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
+  for (int64_t lr = static_cast<int64_t>(blockIdx.x) * kSpmmWarps + warp; lr < a.max_long;
+       lr += static_cast<int64_t>(gridDim.x) * kSpmmWarps) {
+    if (lr < nlong) {
+      const int64_t row = a.long_rows[lr];
+      const int64_t s0 = a.long_seg_first[lr], s1 = a.long_seg_first[lr + 1];
+      const double d = __ldg(a.degree + row);
+      const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(a.dinv + row) : 0.0;
+#pragma unroll
+      for (int j = 0; j < PPL; ++j) {
+        const int p = pbase + 32 * j;
+        if (p >= a.c) continue;
+        double acc = 0.0;
+        for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, a.segpart[sg * a.cpad + p]);
+        if (a.r) acc *= a.r[p];   // Lanczos path: segments hold unscaled sums
+        const double rj = a.r ? a.r[p] : 1.0;
+        const double own = a.bits ? (((a.bits[row * kBitWords + j] >> lane) & 1u) ? 1.0 : -1.0)
+                                  : ldg_f64(u + row * a.ldc_in + 32 * j);
+        const double x = __dmul_rn(own, rj);
+        const double y = op_epilogue<KIND>(x, acc, d, dis, scale);
+        w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
+      }
+    }
+  }
+}
+
+static int ppl_for(int c) {
+  const int cb = c < kBlk ? c : kBlk;
+  return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
+}
+
+template <typename VT, int KIND, bool W, int PPL>
+static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
+  (void)coop;
+  (void)dev;
+  dim3 grid(148 * 4, gy);   // persistent: work is taken from the atomic counters
+  // EXACT (bit-identical operator apply) only for the apply entry (r == nullptr, double);
+  // HALF (two nonzeros per warp instruction) for Lanczos chunks of <= 16 probes.
+  const bool half = PPL == 1 && a.c <= 16 && a.ldc_in <= 16;
+  if (!a.r) {
+    if constexpr (std::is_same<VT, double>::value)
+      spmm_kernel<VT, KIND, W, PPL, false, true, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else if (half) {
+    if (a.bits) spmm_kernel<VT, KIND, W, 1, true, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    else spmm_kernel<VT, KIND, W, 1, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else if (a.bits) {
+    spmm_kernel<VT, KIND, W, PPL, true, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else {
+    spmm_kernel<VT, KIND, W, PPL, false, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  }
+}
+
+template <typename VT, int KIND>
+static void long_finish_dispatch(SpmmArgs& a, int gy, cudaStream_t st) {
+  dim3 g2(static_cast<unsigned>(std::min<int64_t>((a.max_long + kSpmmWarps - 1) / kSpmmWarps, 148 * 8)), gy);
+  switch (ppl_for(a.c)) {
+    case 1: spmm_long_finish_kernel<VT, KIND, 1><<<g2, kSpmmWarps * 32, 0, st>>>(a); break;
+    case 2: spmm_long_finish_kernel<VT, KIND, 2><<<g2, kSpmmWarps * 32, 0, st>>>(a); break;
+    default: spmm_long_finish_kernel<VT, KIND, 4><<<g2, kSpmmWarps * 32, 0, st>>>(a); break;
+  }
+}
+
+template <typename VT, int KIND, bool W>
+static void spmm_dispatch(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
+  switch (ppl_for(a.c)) {
+    case 1: spmm_launch_one<VT, KIND, W, 1>(a, gy, coop, dev, st); break;
+    case 2: spmm_launch_one<VT, KIND, W, 2>(a, gy, coop, dev, st); break;
+    default: spmm_launch_one<VT, KIND, W, 4>(a, gy, coop, dev, st); break;
+  }
+}
+
+template <typename VT>
+static void launch_spmm_main(int kind, SpmmArgs& a, bool coop, int dev, int gy, cudaStream_t st) {
+  LaunchScope ls(K_SPMM, st);
+  const bool wt = a.weights != nullptr;
+  if (kind == SLQ_NORMALIZED_LAPLACIAN) {
+    if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, gy, coop, dev, st);
+    else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, gy, coop, dev, st);
+  } else if (kind == SLQ_DENSITY) {
+    if (wt) spmm_dispatch<VT, SLQ_DENSITY, true>(a, gy, coop, dev, st);
+    else spmm_dispatch<VT, SLQ_DENSITY, false>(a, gy, coop, dev, st);
+  } else {
+    if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, gy, coop, dev, st);
+    else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, gy, coop, dev, st);
+  }
+}
+
+// The SpMM pass (short rows + long-row segments), then the long-row finish when the graph has any.
+template <typename VT>
+static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st, bool finish = true) {
+  const int gy = ceil_div(a.c, kBlk);
+  launch_spmm_main<VT>(kind, a, coop, dev, gy, st);
+  if (finish && a.long_counts && a.max_long > 0) {
+    LaunchScope ls(K_SPMM, st);
+    if (kind == SLQ_NORMALIZED_LAPLACIAN) long_finish_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN>(a, gy, st);
+    else if (kind == SLQ_DENSITY) long_finish_dispatch<VT, SLQ_DENSITY>(a, gy, st);
+    else long_finish_dispatch<VT, SLQ_LAPLACIAN>(a, gy, st);
+  }
+}
+
+// ----------------------------------------------------------------------------- pass B: CGS
+struct CgsArgs {
+  int64_t n, ldc, vec_stride;      // vec_stride = n*ldc elements between basis vectors
+  int64_t rows_per_tile;
+  int ntiles;
+  int c, cpad;
+  int i;                           // current Lanczos step
+  int k0, nk;                      // basis block [k0, k0+nk) handled by this launch (dot kernel)
+  int second;                      // 1: second CGS pass on u_{i+1}
+  int reorth;
+  const void* basis;               // u_0 .. u_S
+  const void* w;                   // Op(q_i)
+  ChunkState s;
+  double* partial;                 // [ntiles][nq][cpad]
+};
+
+// w' = (w - alpha q_i) - beta_{i-1} q_{i-1}    (lanczos.py:129, numpy left-to-right evaluation)
+__device__ __forceinline__ double three_term(double wv, double ui, double uim1, double al, double bp, double ri,
+                                             double rim1) {
+  const double qi = __dmul_rn(ui, ri);
+  const double qp = __dmul_rn(uim1, rim1);
+  return __dsub_rn(__dsub_rn(wv, __dmul_rn(al, qi)), __dmul_rn(bp, qp));
+}
+
+// Streaming CGS kernels use a flat layout: thread t of a CTA owns ONE probe column p = t % ldc and
+// one of kRowSlots row slots, for a group of tiles; a warp reads 256 contiguous bytes per load and
+// every per-probe scalar (alpha, beta, r, CGS coefficients) lives in registers.  The row slot of a
+// row is its index mod kRowSlots, so per-probe sums never depend on the chunk width.
+constexpr int kRowSlots = 2;
+constexpr int kStreamThreads = 256;
+
+struct FlatGeom {
+  int ldc, G;    // tiles per CTA
+};
+
+static FlatGeom flat_geom(int64_t ldc) {
+  FlatGeom f;
+  f.ldc = static_cast<int>(ldc);
+  f.G = std::max(1, static_cast<int>(kStreamThreads / (kRowSlots * ldc)));
+  return f;
+}
+
+// Partials of sum_rows u_k . w' (CGS coefficient before the r_k scale, lanczos.py:73) for k in
+// [k0, k0+nk) and of ||w'||^2 (lanczos.py:72).
+template <typename VT>
+__global__ void __launch_bounds__(512)
+cgs_dot_kernel(CgsArgs a, int ldc_i, int G) {
+  extern __shared__ double part[];   // [G][kRowSlots][nq][ldc]
+  if (a.second && *a.s.any_again == 0) return;
+  const int t = threadIdx.x;
+  const int p = t % ldc_i;
+  const int slot = (t / ldc_i) % kRowSlots;
+  const int gt = t / (ldc_i * kRowSlots);
+  const bool pv = p < a.c;
+  const int cp = a.cpad;
+  const int nq = a.nk + 1;
+  const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
+  const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
+  const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
+  const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
+  const VT* basis = static_cast<const VT*>(a.basis) + p;
+  const VT* w = static_cast<const VT*>(a.w) + p;
+  const int64_t vs = a.vec_stride;
+  const VT* ui = basis + static_cast<int64_t>(a.i) * vs;
+  const VT* uim1 = basis + static_cast<int64_t>(a.i > 0 ? a.i - 1 : 0) * vs;
+  const VT* unext = basis + static_cast<int64_t>(a.i + 1) * vs;
+  const VT* uk0 = basis + static_cast<int64_t>(a.k0) * vs;
+
+  for (int tb = blockIdx.x * G; tb < a.ntiles; tb += gridDim.x * G) {
+    const int tile = tb + gt;
+    double acc[kCgsBlock];
+#pragma unroll
+    for (int kk = 0; kk < kCgsBlock; ++kk) acc[kk] = 0.0;
+    double nb = 0.0;
+    if (pv && tile < a.ntiles) {
+      const int64_t rb = static_cast<int64_t>(tile) * a.rows_per_tile;
+      const int64_t re = min(a.n, rb + a.rows_per_tile);
+      for (int64_t row = rb + slot; row < re; row += kRowSlots) {
+        const int64_t idx = row * a.ldc;
+        const double wp = a.second ? ldg_f64(unext + idx)
+                                   : three_term(ldg_f64(w + idx), ldg_f64(ui + idx),
+                                                a.i > 0 ? ldg_f64(uim1 + idx) : 0.0, al, bp, ri, rim1);
+        nb = fma(wp, wp, nb);
+#pragma unroll
+        for (int kk = 0; kk < kCgsBlock; ++kk)
+          if (kk < a.nk) acc[kk] = fma(ldg_f64(uk0 + kk * vs + idx), wp, acc[kk]);
+      }
+    }
+    double* my = part + (static_cast<int64_t>(gt) * kRowSlots + slot) * nq * ldc_i + p;
+#pragma unroll
+    for (int kk = 0; kk < kCgsBlock; ++kk)
+      if (kk < a.nk) my[kk * ldc_i] = acc[kk];
+    my[a.nk * ldc_i] = nb;
+    __syncthreads();
+    // fixed-order combine of the row slots
+    const int per_tile = nq * ldc_i;
+    for (int e = t; e < G * per_tile; e += blockDim.x) {
+      const int g2 = e / per_tile, rem = e - g2 * per_tile;
+      const int q = rem / ldc_i, pp = rem - q * ldc_i;
+      const int tl = tb + g2;
+      if (tl >= a.ntiles || pp >= cp) continue;
+      const double* src = part + static_cast<int64_t>(g2) * kRowSlots * per_tile + rem;
+      double s = src[0];
+#pragma unroll
+      for (int rs = 1; rs < kRowSlots; ++rs) s += src[rs * per_tile];
+      a.partial[(static_cast<int64_t>(tl) * nq + q) * cp + pp] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// u_{i+1} = w' - sum_k coef_k u_k (coef_k = h_k r_k, i.e. basis.T @ h with q_k = u_k r_k, lanczos.py:73);
+// partials of ||u_{i+1}||^2.  Second pass: u_{i+1} -= sum_k coef2_k u_k for flagged probes only.
+template <typename VT>
+__global__ void __launch_bounds__(512)
+cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
+  extern __shared__ double part[];   // [G][kRowSlots][ldc]
+  if (a.second && *a.s.any_again == 0) return;
+  const int t = threadIdx.x;
+  const int p = t % ldc_i;
+  const int slot = (t / ldc_i) % kRowSlots;
+  const int gt = t / (ldc_i * kRowSlots);
+  const int cp = a.cpad;
+  const bool pv = p < a.c && (!a.second || a.s.again[p]);
+  const int nk = a.reorth ? a.i + 1 : 0;
+  double cf[kCgsBlock];
+#pragma unroll
+  for (int kk = 0; kk < kCgsBlock; ++kk) cf[kk] = (pv && kk < nk) ? a.s.h[kk * cp + p] * a.s.rsc[kk * cp + p] : 0.0;
+  const double al = pv ? a.s.alpha[a.i * cp + p] : 0.0;
+  const double bp = (pv && a.i > 0) ? a.s.beta[(a.i - 1) * cp + p] : 0.0;
+  const double ri = pv ? a.s.rsc[a.i * cp + p] : 0.0;
+  const double rim1 = (pv && a.i > 0) ? a.s.rsc[(a.i - 1) * cp + p] : 0.0;
+  VT* basis = const_cast<VT*>(static_cast<const VT*>(a.basis)) + p;
+  const VT* w = static_cast<const VT*>(a.w) + p;
+  const int64_t vs = a.vec_stride;
+  VT* out = basis + static_cast<int64_t>(a.i + 1) * vs;
+  const VT* ui = basis + static_cast<int64_t>(a.i) * vs;
+  const VT* uim1 = basis + static_cast<int64_t>(a.i > 0 ? a.i - 1 : 0) * vs;
+
+  for (int tb = blockIdx.x * G; tb < a.ntiles; tb += gridDim.x * G) {
+    const int tile = tb + gt;
+    double nrm = 0.0;
+    if (pv && tile < a.ntiles) {
+      const int64_t rb = static_cast<int64_t>(tile) * a.rows_per_tile;
+      const int64_t re = min(a.n, rb + a.rows_per_tile);
+      for (int64_t row = rb + slot; row < re; row += kRowSlots) {
+        const int64_t idx = row * a.ldc;
+        const double wp = a.second ? ldg_f64(out + idx)
+                                   : three_term(ldg_f64(w + idx), ldg_f64(ui + idx),
+                                                a.i > 0 ? ldg_f64(uim1 + idx) : 0.0, al, bp, ri, rim1);
+        double proj = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kCgsBlock; ++kk)
+          if (kk < nk) proj = fma(ldg_f64(basis + kk * vs + idx), cf[kk], proj);
+        for (int k = kCgsBlock; k < nk; ++k)   // s > 17 only
+          proj = fma(ldg_f64(basis + k * vs + idx), a.s.h[k * cp + p] * a.s.rsc[k * cp + p], proj);
+        const VT v = from_f64<VT>(nk ? __dsub_rn(wp, proj) : wp);
+        out[idx] = v;
+        const double vd = to_f64(v);
+        nrm = fma(vd, vd, nrm);
+      }
+    }
+    part[(gt * kRowSlots + slot) * ldc_i + p] = nrm;
+    __syncthreads();
+    for (int e = t; e < G * ldc_i; e += blockDim.x) {
+      const int g2 = e / ldc_i, pp = e - g2 * ldc_i;
+      const int tl = tb + g2;
+      if (tl >= a.ntiles || pp >= cp) continue;
+      double s = part[(g2 * kRowSlots) * ldc_i + pp];
+#pragma unroll
+      for (int rs = 1; rs < kRowSlots; ++rs) s += part[(g2 * kRowSlots + rs) * ldc_i + pp];
+      a.partial[static_cast<int64_t>(tl) * cp + pp] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- staged (TMA bulk) CGS step kernel
+// One persistent launch per Lanczos step does everything after the SpMM: kPersist CTAs, CTA b owns
+// the contiguous rows [n*b/G, n*(b+1)/G).  Warp 0 lane 0 is the producer: it streams row chunks of
+// every needed vector into a kStages-deep shared-memory ring with cp.async.bulk (completion on a
+// "full" mbarrier).  Consumer thread p owns probe column p, walks its CTA's rows in ascending
+// order from shared memory and releases each stage on an "empty" mbarrier (bytes in flight per SM
+// = the whole ring, no register cost).
+//
+// CGS in Gram form.  With q_k = r_k u_k and G(k,j) = q_k . q_j (kept per probe), the reference's
+// coefficient h_k = q_k . w' with w' = (w - alpha q_i) - beta q_{i-1} (lanczos.py:72-73,129) is
+//     h_k = r_k (u_k . w) - alpha G(k,i) - beta G(k,i-1),   alpha = r_i (u_i . w),
+// so one streaming phase (A) yields alpha and every h_k; the update phase (C) forms w' exactly as
+// the reference, subtracts sum_k h_k q_k, and accumulates ||w'||^2, ||u_{i+1}||^2 and the Gram row
+// u_k . u_{i+1} of the new vector.  The Gram row is also the second CGS pass's coefficients
+// (lanczos.py:75-76), so that pass is a single update phase (C').  Phases are separated by a
+// software grid barrier (all CTAs co-resident: one per SM).  Every per-probe sum runs in row order
+// inside a fixed row range, reduced in fixed stripes: independent of c and of chunking.
+constexpr int kPersist = 148;
+constexpr int kStageSlots = 3;          // consumer threads per probe column: rows (row - lo) % 3; 32+3*128 = 416 threads -> 128 regs
+constexpr int kStagedMaxLdc = 128;     // consumers = kStageSlots * round_up(ldc, 32) <= 512
+constexpr int kStages = 3;
+constexpr int kMaxStaged = kCgsBlock + 4;
+constexpr size_t kStagedSmem = 200 * 1024;   // + 20 KB static: within the 227 KB per CTA
+
+struct StagedArgs {
+  CgsArgs a;
+  int nvec;                       // VT vectors staged per chunk (source + u_1..u_{NK-1})
+  const void* vec[kMaxStaged];    // global base of each staged vector
+  const uint32_t* bits;           // u_0 as the probe bitmask [n][kBitWords], staged after the vectors
+  int slot_src, slot_ui, slot_uim1;
+  int slot_k[kCgsBlock];          // slot of basis vector k
+  int rt;                         // rows per chunk
+};
+
+struct StepArgs {
+  StagedArgs pass[2];             // [0]: src = w (phases A, C), [1]: src = u_{i+1} (phase C')
+  ReduceArgs red;
+  SpmmArgs spmm;                  // long rows of the preceding SpMM are finished in phase 0
+};
+
+template <typename VT>
+struct StageRing {
+  uint64_t* full;
+  uint64_t* empty;
+  VT* buf;
+  __device__ explicit StageRing(unsigned char* smem) {
+    full = reinterpret_cast<uint64_t*>(smem);
+    empty = full + kStages;
+    buf = reinterpret_cast<VT*>(smem + 128);
+  }
+};
+
+// One ring stage: nvec VT row blocks [rt][ldc], then the bitmask rows [rt][kBitWords] (in VT units).
+template <typename VT>
+__host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int64_t ldc) {
+  return static_cast<int64_t>(nvec) * rt * ldc + (static_cast<int64_t>(rt) * kBitWords * 4 + sizeof(VT) - 1) / sizeof(VT);
+}
+
+__device__ __forceinline__ double bit_value(const uint32_t* brow, int p) {
+  return ((brow[p >> 5] >> (p & 31)) & 1u) ? 1.0 : -1.0;
+}
+
+__device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
+  return hi > lo ? static_cast<int>((hi - lo + rt - 1) / rt) : 0;
+}
+
+// Producer (one lane): chunk j of [lo, hi) goes to ring slot (ch0 + j) % kStages.
+template <typename VT>
+__device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
+  const int64_t ldc = sa.a.ldc;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, ldc);
+  int ch = ch0;
+  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+    const int s = ch % kStages;
+    if (ch >= kStages) mbar_wait(&ring.empty[s], ((ch / kStages) - 1) & 1);
+    const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
+    const uint32_t bytes = static_cast<uint32_t>(rows * ldc * sizeof(VT));
+    const uint32_t bbytes = static_cast<uint32_t>(rows * kBitWords * sizeof(uint32_t));
+    mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec + bbytes);
+    VT* dst = ring.buf + s * stage_elems;
+    for (int v = 0; v < sa.nvec; ++v)
+      bulk_g2s(dst + static_cast<int64_t>(v) * sa.rt * ldc, static_cast<const VT*>(sa.vec[v]) + r0 * ldc, bytes,
+               &ring.full[s]);
+    bulk_g2s(dst + static_cast<int64_t>(sa.nvec) * sa.rt * ldc, sa.bits + r0 * kBitWords, bbytes, &ring.full[s]);
+  }
+}
+
+// Gram-matrix entry G(k, j) of probe p (G is symmetric; stored as [(S+1)*(S+1)][cpad]).
+__device__ __forceinline__ double gram_at(const ChunkState& s, int k, int j, int p) {
+  return s.G[(static_cast<int64_t>(k) * (s.S + 1) + j) * s.cpad + p];
+}
+
+// Shared-memory stage layout: [slot][row][ldc] with slot 0 = source (w or u_{i+1}) and slot k = u_k
+// for k >= 1, then the probe bitmask rows (u_0 = +-1).  NK = i + 1 basis vectors is a compile-time
+// constant, so every loop below is fully unrolled with no predicates.
+
+template <typename VT, int NK>
+struct StageView {
+  const VT* e;             // this thread's element of row r in slot 0
+  const uint32_t* brow;    // bitmask row r
+  int vstride, p;
+  __device__ __forceinline__ double src() const { return to_f64(e[0]); }
+  __device__ __forceinline__ double u(int k) const {   // k is a compile-time constant after unrolling
+    return k == 0 ? bit_value(brow, p) : to_f64(e[k * vstride]);
+  }
+};
+
+// Phase A (consumer side): partials [cta*slots+slot][nq][cpad] of u_k . w (k < NK); at i == 0 also
+// u_0 . u_0 (q = 1) for G(0,0).
+template <typename VT, int NK>
+__device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo,
+                                           int64_t hi, int nq, int cols_pad) {
+  const CgsArgs& a = sa.a;
+  const int t = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const int p = t % cols_pad, slot = t / cols_pad;
+  const bool pv = p < a.c;
+  const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
+  const int rt = sa.rt;
+  const int vstride = rt * ldc;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, ldc);
+  double acc[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) acc[kk] = 0.0;
+  double g00 = 0.0;
+  int ch = ch0;
+  for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
+    const int s = ch % kStages;
+    mbar_wait(&ring.full[s], (ch / kStages) & 1);
+    const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
+    if (pv) {
+      const VT* stage = ring.buf + s * stage_elems;
+      const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
+      // this thread's rows: (row - lo) % kStageSlots == slot, ascending
+      int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
+      for (; r < rows; r += kStageSlots) {
+        const StageView<VT, NK> v{stage + p + r * ldc, sbits + r * kBitWords, vstride, p};
+        const double wv = v.src();
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) acc[kk] = fma(v.u(kk), wv, acc[kk]);
+        if (NK == 1) g00 += 1.0;   // u_0 . u_0 = number of rows (+-1 entries)
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[s]);
+  }
+  if (p < cp) {
+    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * kStageSlots + slot) * nq * cp + p;
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) dst[kk * cp] = acc[kk];
+    if (NK == 1) dst[NK * cp] = g00;
+  }
+}
+
+// Phase C / C' (consumer side).  First pass: w' = three-term, u_{i+1} = w' - sum_k coef_k u_k.
+// Second pass (flagged probes): u_{i+1} -= sum_k coef_k u_k.  Partials [cta*slots+slot][nq][cpad]:
+// q=0 ||w'||^2, q=1 ||u_{i+1}||^2, q=2+k  u_k . u_{i+1}.
+template <typename VT, int NK, bool SECOND>
+__device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo,
+                                             int64_t hi, int cols_pad, double* cf_sm) {
+  const CgsArgs& a = sa.a;
+  const ChunkState& S = a.s;
+  const int t = threadIdx.x - 32, lane = threadIdx.x & 31;
+  const int p = t % cols_pad, slot = t / cols_pad;
+  const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
+  const bool pv = p < a.c && (!SECOND || S.again[p]);
+  constexpr int nq = NK + 2;
+  constexpr int i = NK - 1;
+  double al = 0.0, bp = 0.0, ri = 0.0, rim1 = 0.0;
+  if (pv) {
+    ri = S.rsc[i * cp + p];
+    rim1 = i > 0 ? S.rsc[(i - 1) * cp + p] : 0.0;
+    bp = i > 0 ? S.beta[(i - 1) * cp + p] : 0.0;
+    al = ri * S.cdot[i * cp + p];
+  }
+  // CGS coefficients coef_k = h_k r_k into shared memory [NK][cols_pad] (slot 0 computes)
+  if (slot == 0) {
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+      double c = 0.0;
+      if (pv) {
+        const double rk = S.rsc[kk * cp + p];
+        double h;
+        if (SECOND) {
+          h = rk * S.gram[kk * cp + p];                                           // q_k . w''
+        } else {
+          h = rk * S.cdot[kk * cp + p] - al * gram_at(S, kk, i, p);
+          if (i > 0) h -= bp * gram_at(S, kk, i - 1, p);
+        }
+        c = h * rk;
+      }
+      cf_sm[kk * cols_pad + p] = c;
+    }
+  }
+  named_barrier_sync(1, blockDim.x - 32);   // consumers only
+  double cf[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) cf[kk] = cf_sm[kk * cols_pad + p];
+  const int rt = sa.rt;
+  const int vstride = rt * ldc;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, ldc);
+  VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
+  double nb = 0.0, nrm = 0.0;
+  double gr[NK];
+#pragma unroll
+  for (int kk = 0; kk < NK; ++kk) gr[kk] = 0.0;
+  int ch = ch0;
+  for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
+    const int s = ch % kStages;
+    mbar_wait(&ring.full[s], (ch / kStages) & 1);
+    const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
+    if (pv) {
+      const VT* stage = ring.buf + s * stage_elems;
+      const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
+      int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
+      for (; r < rows; r += kStageSlots) {
+        const StageView<VT, NK> v{stage + p + r * ldc, sbits + r * kBitWords, vstride, p};
+        double wp;
+        if (SECOND) {
+          wp = v.src();
+        } else {
+          wp = three_term(v.src(), v.u(i), i > 0 ? v.u(i > 0 ? i - 1 : 0) : 0.0, al, bp, ri, rim1);
+          nb = fma(wp, wp, nb);
+        }
+        // basis.T @ h as two interleaved partial sums (shorter dependency chain), then one subtraction
+        double pe = 0.0, po = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) {
+          if (kk & 1) po = fma(v.u(kk), cf[kk], po);
+          else pe = fma(v.u(kk), cf[kk], pe);
+        }
+        const VT vv = from_f64<VT>(__dsub_rn(wp, pe + po));
+        out[(r0 + r) * a.ldc] = vv;
+        const double vd = to_f64(vv);
+        nrm = fma(vd, vd, nrm);
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) gr[kk] = fma(v.u(kk), vd, gr[kk]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[s]);
+  }
+  if (p < cp) {
+    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * kStageSlots + slot) * nq * cp + p;
+    dst[0] = nb;
+    dst[cp] = nrm;
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) dst[(2 + kk) * cp] = gr[kk];
+  }
+}
+
+// Fixed-order stripe reduction of quantity q for 32 probes; returns the total in warp 0's lanes.
+static __device__ double stripe_sum(const double* partial, int ntiles, int nq, int cpad, int q, int group, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int p = group * 32 + lane;
+  const int64_t stride = static_cast<int64_t>(nq) * cpad;
+  const double* src = partial + static_cast<int64_t>(q) * cpad + p;
+  for (int sidx = warp; sidx < kStripes; sidx += nw) {
+    double s = 0.0;
+    for (int t = sidx; t < ntiles; t += kStripes) s += src[t * stride];
+    red[sidx * 32 + lane] = s;
+  }
+  __syncthreads();
+  double tot = 0.0;
+  if (warp == 0) {
+    tot = red[lane];
+    for (int j = 1; j < kStripes; ++j) tot += red[j * 32 + lane];
+  }
+  __syncthreads();
+  return tot;
+}
+
+// Phases C (or C'), D, E of one CGS pass (SECOND: the conditional second pass, lanczos.py:75-76).
+template <typename VT, int NK, bool SECOND, typename Sync>
+__device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs& st, StageRing<VT>& ring, int& ch,
+                                            int64_t lo, int64_t hi, int cols_pad, int nrows_partial, double* cf_sm,
+                                            double* red, Sync& sync_grid) {
+  const CgsArgs& a = sa.pass[0].a;
+  const ChunkState& S = a.s;
+  const int ngroups = a.cpad / 32, cp = a.cpad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nk = a.i + 1, nq = nk + 2, nslot = S.S + 1;
+  // C / C': update
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
+  } else {
+    phase_update<VT, NK, SECOND>(st, ring, ch, lo, hi, cols_pad, cf_sm);
+  }
+  ch += chunk_count(lo, hi, st.rt);
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // u_{i+1} is bulk-read by a second pass
+  sync_grid();
+  // D: reduce ||w'||^2, ||u_{i+1}||^2 and the Gram row
+  for (int sl = blockIdx.x; sl < nq * ngroups; sl += gridDim.x) {
+    const int q = sl % nq, gidx = sl / nq, p = gidx * 32 + lane;
+    const double tot = stripe_sum(a.partial, nrows_partial, nq, cp, q, gidx, red);
+    if (warp == 0 && p < a.c) {
+      if (q == 0) { if (!SECOND) S.nb2[p] = tot; }
+      else if (q == 1) S.nrm2[p] = tot;
+      else S.gram[(q - 2) * cp + p] = tot;
+    }
+  }
+  sync_grid();
+  // E: beta, breakdown, second-pass flag, Gram column of q_{i+1} (lanczos.py:75,132-137)
+  for (int gidx = blockIdx.x; gidx < ngroups; gidx += gridDim.x) {
+    const int p = gidx * 32 + lane;
+    if (warp != 0 || p >= a.c || !S.alive[p]) continue;
+    if (SECOND && !S.again[p]) continue;
+    const double b = sqrt(S.nrm2[p]);
+    if (!SECOND && b < 0.5 * sqrt(S.nb2[p])) {
+      S.again[p] = 1;
+      *S.any_again = 1;
+      continue;
+    }
+    if (SECOND) S.again[p] = 0;
+    const double hi_int = sa.red.kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0
+                          : (sa.red.kind == SLQ_DENSITY ? 1.0 : sa.red.dscal[4]);   // interval_hi
+    if (b <= 1e-12 * hi_int) {
+      S.steps[p] = a.i + 1;
+      S.alive[p] = 0;
+      S.rsc[(a.i + 1) * cp + p] = 0.0;
+    } else {
+      const double rn = __ddiv_rn(1.0, b);
+      S.beta[a.i * cp + p] = b;
+      S.rsc[(a.i + 1) * cp + p] = rn;
+      const int j = a.i + 1;
+      for (int k = 0; k <= a.i; ++k) {
+        const double gkj = S.rsc[k * cp + p] * rn * S.gram[k * cp + p];
+        S.G[(static_cast<int64_t>(k) * nslot + j) * cp + p] = gkj;
+        S.G[(static_cast<int64_t>(j) * nslot + k) * cp + p] = gkj;
+      }
+      S.G[(static_cast<int64_t>(j) * nslot + j) * cp + p] = rn * rn * S.nrm2[p];
+    }
+  }
+  sync_grid();
+}
+
+template <typename VT, int NK>
+__global__ void __launch_bounds__(32 + kStageSlots * kStagedMaxLdc, 1)
+cgs_step_kernel(StepArgs sa) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double red[kStripes * 32];
+  __shared__ double cf_sm[kCgsBlock * kStagedMaxLdc];
+  StageRing<VT> ring(smem);
+  const CgsArgs& a = sa.pass[0].a;
+  const ChunkState& S = a.s;
+  unsigned int* bar = S.barrier + a.i;
+  unsigned int nbar = 0;
+  auto sync_grid = [&]() { grid_barrier(bar, ++nbar); };
+  const int nwc = (blockDim.x - 32) / 32;
+  const int cols_pad = (blockDim.x - 32) / kStageSlots;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t lo = a.n * blockIdx.x / gridDim.x, hi = a.n * (blockIdx.x + 1) / gridDim.x;
+  const int ngroups = a.cpad / 32, cp = a.cpad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nk = a.i + 1;
+  const int nslot = S.S + 1;
+  const int nrows_partial = gridDim.x * kStageSlots;
+  int ch = 0;
+  const StagedArgs& st0 = sa.pass[0];
+  const int nch0 = chunk_count(lo, hi, st0.rt);
+
+  // 0: finish the SpMM's long rows (segment partials in order + epilogue); skipped when none
+  const SpmmArgs& sp = sa.spmm;
+  const int64_t nlong = sp.long_counts ? sp.long_counts[0] : 0;
+  if (nlong > 0) {
+    const int nw = blockDim.x >> 5;
+    const VT* uu = static_cast<const VT*>(sp.u);
+    VT* ww = static_cast<VT*>(sp.w);
+    const double scale = sp.dscal[3];
+    for (int64_t lr = static_cast<int64_t>(blockIdx.x) * nw + warp; lr < nlong;
+         lr += static_cast<int64_t>(gridDim.x) * nw) {
+      const int64_t row = sp.long_rows[lr];
+      const int64_t s0 = sp.long_seg_first[lr], s1 = sp.long_seg_first[lr + 1];
+      const double d = sp.degree[row], dis = sp.dinv[row];
+      for (int p = lane; p < sp.c; p += 32) {
+        double acc = 0.0;
+        for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, sp.segpart[sg * sp.cpad + p]);
+        acc *= sp.r[p];   // segments hold unscaled sums
+        const double own = sp.bits ? (((sp.bits[row * kBitWords + (p >> 5)] >> (p & 31)) & 1u) ? 1.0 : -1.0)
+                                   : to_f64(uu[row * sp.ldc_in + p]);
+        const double x = __dmul_rn(own, sp.r[p]);
+        double y;
+        if (sa.red.kind == SLQ_NORMALIZED_LAPLACIAN) y = op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, acc, d, dis, scale);
+        else if (sa.red.kind == SLQ_DENSITY) y = op_epilogue<SLQ_DENSITY>(x, acc, d, dis, scale);
+        else y = op_epilogue<SLQ_LAPLACIAN>(x, acc, d, dis, scale);
+        ww[row * sp.ldc_out + p] = from_f64<VT>(y);
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // w is bulk-read in phase A
+    sync_grid();
+  }
+  // A: u_k . w for k <= i (and u_0 . u_0 at i == 0)
+  const int nqa = nk + (a.i == 0 ? 1 : 0);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) staged_produce<VT>(st0, ring, ch, lo, hi);
+  } else {
+    phase_dots<VT, NK>(st0, ring, ch, lo, hi, nqa, cols_pad);
+  }
+  ch += nch0;
+  sync_grid();
+  // B: reduce them (fixed stripes); G(0,0) at the first step
+  for (int sl = blockIdx.x; sl < nqa * ngroups; sl += gridDim.x) {
+    const int q = sl % nqa, gidx = sl / nqa, p = gidx * 32 + lane;
+    const double tot = stripe_sum(a.partial, nrows_partial, nqa, cp, q, gidx, red);
+    if (warp == 0 && p < a.c) {
+      if (q < nk) {
+        S.cdot[q * cp + p] = tot;
+        if (q == a.i && S.alive[p]) S.alpha[a.i * cp + p] = S.rsc[a.i * cp + p] * tot;   // alpha = q_i . w
+      } else {
+        const double r0 = S.rsc[p];
+        S.G[p] = r0 * r0 * tot;                                                       // G(0,0)
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *S.any_again = 0;
+  sync_grid();
+  update_pass<VT, NK, false>(sa, sa.pass[0], ring, ch, lo, hi, cols_pad, nrows_partial, cf_sm, red, sync_grid);
+  if (*S.any_again) {   // uniform: read after a grid barrier
+#ifdef SLQ_DEBUG_SECOND
+    if (blockIdx.x == 0 && threadIdx.x == 0) printf("second pass at step %d\n", a.i);
+#endif
+    update_pass<VT, NK, true>(sa, sa.pass[1], ring, ch, lo, hi, cols_pad, nrows_partial, cf_sm, red, sync_grid);
+  }
+}
+
+// Build the staged-vector list of one pass; false when the geometry does not fit.
+template <typename VT>
+static bool staged_setup(const CgsArgs& a, bool second, const uint32_t* bits, StagedArgs* out) {
+  StagedArgs s{};
+  s.a = a;
+  const VT* basis = static_cast<const VT*>(a.basis);
+  const int nk = a.i + 1;
+  if (!a.reorth || nk > kCgsBlock || !bits) return false;
+  int nv = 0;
+  s.slot_src = nv;
+  s.vec[nv++] = second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
+  for (int kk = 0; kk < kCgsBlock; ++kk) s.slot_k[kk] = 0;
+  for (int kk = 1; kk < nk; ++kk) {       // u_0 comes from the bitmask
+    s.slot_k[kk] = nv;
+    s.vec[nv++] = basis + static_cast<int64_t>(kk) * a.vec_stride;
+  }
+  s.bits = bits;
+  s.nvec = nv;
+  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t);
+  const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
+  int64_t rt = static_cast<int64_t>((kStagedSmem - 256) / (kStages * row_bytes));
+  rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
+  if (rt < 1 || a.ldc > kStagedMaxLdc) return false;
+  s.rt = static_cast<int>(rt);
+  *out = s;
+  return true;
+}
+
+static int coop_supported(int dev) {
+  static int v[64] = {0};
+  if (dev < 0 || dev >= 64) return 0;
+  if (v[dev] == 0) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    v[dev] = sms >= kPersist ? 1 : 2;
+  }
+  return v[dev] == 1;
+}
+
+// Launch everything after the SpMM of step i as one persistent kernel; false when the staged path
+// does not apply (the caller then runs the separate kernels).
+template <typename VT>
+static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
+                            int dev, cudaStream_t st, int* rc) {
+  *rc = SLQ_OK;
+  if (!coop_supported(dev)) return false;
+  StepArgs sa{};
+  if (!staged_setup<VT>(a, false, bits, &sa.pass[0]) || !staged_setup<VT>(a, true, bits, &sa.pass[1])) return false;
+  sa.red = red;
+  sa.spmm = spmm;
+  const size_t smem = 128 + kStages * sizeof(VT) *
+                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, a.ldc),
+                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, a.ldc));
+  const int threads = 32 + kStageSlots * (((static_cast<int>(a.ldc) + 31) / 32) * 32);
+  LaunchScope ls(K_CGS_UPDATE, st);
+  // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
+  // so the software grid barrier is safe (coop_supported() checked the SM count).
+  switch (a.i + 1) {
+#define SLQ_STEP_CASE(K)                                                                                  \
+    case K: {                                                                                              \
+      static bool attr = false;                                                                            \
+      if (!attr) {                                                                                         \
+        cudaFuncSetAttribute(cgs_step_kernel<VT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                             static_cast<int>(kStagedSmem));                                               \
+        attr = true;                                                                                       \
+      }                                                                                                    \
+      cgs_step_kernel<VT, K><<<kPersist, threads, smem, st>>>(sa);                                         \
+      break;                                                                                               \
+    }
+    SLQ_STEP_CASE(1) SLQ_STEP_CASE(2) SLQ_STEP_CASE(3) SLQ_STEP_CASE(4) SLQ_STEP_CASE(5) SLQ_STEP_CASE(6)
+    SLQ_STEP_CASE(7) SLQ_STEP_CASE(8) SLQ_STEP_CASE(9) SLQ_STEP_CASE(10) SLQ_STEP_CASE(11) SLQ_STEP_CASE(12)
+    SLQ_STEP_CASE(13) SLQ_STEP_CASE(14) SLQ_STEP_CASE(15) SLQ_STEP_CASE(16)
+#undef SLQ_STEP_CASE
+    default: return false;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *rc = cuda_fail(e, "cgs_step_kernel launch");
+    return true;
+  }
+  return true;
+}
+
+template <typename VT>
+static int launch_cgs_dot(CgsArgs a, int max_ctas, cudaStream_t st) {
+  const FlatGeom f = flat_geom(a.ldc);
+  const int threads = f.G * kRowSlots * f.ldc;
+  const int ctas = std::max(1, std::min(ceil_div(a.ntiles, f.G), max_ctas));
+  const size_t smem = sizeof(double) * threads * (a.nk + 1);
+  LaunchScope ls(K_CGS_DOT, st);
+  if (smem > 48 * 1024)
+    SLQ_CUDA(cudaFuncSetAttribute(cgs_dot_kernel<VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cgs_dot_kernel<VT><<<ctas, threads, smem, st>>>(a, f.ldc, f.G);
+  return SLQ_OK;
+}
+
+template <typename VT>
+static int launch_cgs_update(CgsArgs a, int max_ctas, cudaStream_t st) {
+  const FlatGeom f = flat_geom(a.ldc);
+  const int threads = f.G * kRowSlots * f.ldc;
+  const int ctas = std::max(1, std::min(ceil_div(a.ntiles, f.G), max_ctas));
+  const size_t smem = sizeof(double) * threads;
+  LaunchScope ls(K_CGS_UPDATE, st);
+  cgs_update_kernel<VT><<<ctas, threads, smem, st>>>(a, f.ldc, f.G);
+  return SLQ_OK;
+}
+
+static void launch_reduce(ReduceArgs a, cudaStream_t st) {
+  dim3 grid(a.nq, a.cpad / 32);
+  LaunchScope ls(K_REDUCE, st);
+  reduce_kernel<<<grid, kReduceWarps * 32, 0, st>>>(a);
+}
+
+// Per-vector-type entry points instantiated in spmm_{f32,f64}.cu and step_{f32,f64}.cu.
+void launch_spmm_f32(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish);
+void launch_spmm_f64(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish);
+bool launch_cgs_step_f32(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
+                         int dev, cudaStream_t st, int* rc);
+bool launch_cgs_step_f64(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
+                         int dev, cudaStream_t st, int* rc);
+
+template <typename VT>
+inline void spmm_entry(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish = true) {
+  if (sizeof(VT) == 4) launch_spmm_f32(kind, a, coop, dev, st, finish);
+  else launch_spmm_f64(kind, a, coop, dev, st, finish);
+}
+
+template <typename VT>
+inline bool cgs_step_entry(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
+                           int dev, cudaStream_t st, int* rc) {
+  return sizeof(VT) == 4 ? launch_cgs_step_f32(a, red, spmm, bits, dev, st, rc)
+                         : launch_cgs_step_f64(a, red, spmm, bits, dev, st, rc);
+}
+
+}  // namespace slq

@@ -1,0 +1,11 @@
+// Staged CGS step kernel instantiations for double vectors (engine.cuh: cgs_step_kernel).
+#include "engine.cuh"
+
+namespace slq {
+
+bool launch_cgs_step_f64(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits, int dev,
+                        cudaStream_t st, int* rc) {
+  return launch_cgs_step<double>(a, red, spmm, bits, dev, st, rc);
+}
+
+}  // namespace slq
