@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libslq_b200.so")
-SOURCES = ["capi.cu", "graph.cu", "lanczos.cu", "spmm_f32.cu", "spmm_f64.cu", "step_f32.cu", "step_f64.cu",
-           "rules.cu", "batched.cu", "rmat.cu"]
+SOURCES = ["capi.cu", "graph.cu", "lanczos.cu", "spmm_f32.cu", "spmm_f64.cu", "step_f32_wide.cu", "step_f32_narrow.cu",
+           "step_f64_wide.cu", "step_f64_narrow.cu", "rules.cu", "batched.cu", "rmat.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,7 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     flags = [nvcc(), "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
-             "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include")]
+             "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
+             *os.environ.get("SLQ_NVCC_FLAGS", "").split()]
     with tempfile.TemporaryDirectory() as tmp:
         objs = [os.path.join(tmp, s.replace(".cu", ".o")) for s in SOURCES]
 

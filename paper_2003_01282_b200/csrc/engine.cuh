@@ -810,21 +810,44 @@ cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
 // (lanczos.py:75-76), so that pass is a single update phase (C').  Phases are separated by a
 // software grid barrier (all CTAs co-resident: one per SM).  Every per-probe sum runs in row order
 // inside a fixed row range, reduced in fixed stripes: independent of c and of chunking.
+//
+// Consumer layout.  Three row slots (rows (row - lo) % 3) of T = round_up(M * ldc, 32) threads; in
+// a slot, M threads share one probe column and part t of them handles basis vectors k = t, t + M,
+// ... (step_parts picks M from ldc).  No per-(probe, k) sum depends on M.  The update's sum_k coef_k u_k runs as 8 chains (k mod 8) combined as
+// ((c0 + c4) + (c2 + c6)) + ((c1 + c5) + (c3 + c7)) for every M (a butterfly over the M parts), so
+// u_{i+1} is bitwise independent of M as well: narrow chunks keep the whole CTA busy without
+// changing any result.
 constexpr int kPersist = 148;
-constexpr int kStageSlots = 3;          // consumer threads per probe column: rows (row - lo) % 3; 32+3*128 = 416 threads -> 128 regs
-constexpr int kStagedMaxLdc = 128;     // consumers = kStageSlots * round_up(ldc, 32) <= 512
+constexpr int kStageSlots = 3;      // row slots of the wide class (ldc > 32)
+constexpr int kNarrowSlots = 12;    // row slots of the narrow class (ldc <= 32)
+constexpr int kSlotThreads = 128;                                 // max threads per row slot
+constexpr int kStepThreads = 32 + kStageSlots * kSlotThreads;   // producer warp + <= 384 consumers
+constexpr int kStagedMaxLdc = 128;
 constexpr int kStages = 3;
 constexpr int kMaxStaged = kCgsBlock + 4;
 constexpr size_t kStagedSmem = 200 * 1024;   // + 20 KB static: within the 227 KB per CTA
+
+// Row slots and parts per probe column of the step kernel for a chunk of leading dimension ldc.
+// Wide class (ldc > 32): 3 row slots, M = 1.  Narrow class (ldc <= 32): 12 row slots, M = 32 /
+// round_up(ldc) so a slot is one full warp.  Per-probe sums depend on the class (the slot count)
+// but not on M, so results are bitwise independent of the chunk width within a class.
+struct StepGeom { int slots, parts; };
+inline StepGeom step_geometry(int64_t ldc) {
+  StepGeom g = ldc <= 32 ? StepGeom{kNarrowSlots, ldc <= 8 ? 4 : (ldc <= 16 ? 2 : 1)} : StepGeom{kStageSlots, 1};
+  static const int forced = [] { const char* e = getenv("SLQ_STEP_M"); return e ? atoi(e) : 0; }();   // tuning
+  const int cap = g.slots == kNarrowSlots ? 32 : kSlotThreads;
+  if ((forced == 1 || forced == 2 || forced == 4 || forced == 8) && forced * ldc <= cap) g.parts = forced;
+  return g;
+}
+inline int step_parts(int64_t ldc) { return step_geometry(ldc).parts; }
 
 struct StagedArgs {
   CgsArgs a;
   int nvec;                       // VT vectors staged per chunk (source + u_1..u_{NK-1})
   const void* vec[kMaxStaged];    // global base of each staged vector
   const uint32_t* bits;           // u_0 as the probe bitmask [n][kBitWords], staged after the vectors
-  int slot_src, slot_ui, slot_uim1;
-  int slot_k[kCgsBlock];          // slot of basis vector k
   int rt;                         // rows per chunk
+  int vstride;                    // elements between vector slots in a stage (>= rt*ldc, bank-padded)
 };
 
 struct StepArgs {
@@ -845,10 +868,11 @@ struct StageRing {
   }
 };
 
-// One ring stage: nvec VT row blocks [rt][ldc], then the bitmask rows [rt][kBitWords] (in VT units).
+// One ring stage: nvec VT row blocks [rt][ldc] at vstride spacing, then the bitmask rows
+// [rt][kBitWords] (in VT units).
 template <typename VT>
-__host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int64_t ldc) {
-  return static_cast<int64_t>(nvec) * rt * ldc + (static_cast<int64_t>(rt) * kBitWords * 4 + sizeof(VT) - 1) / sizeof(VT);
+__host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int vstride) {
+  return static_cast<int64_t>(nvec) * vstride + (static_cast<int64_t>(rt) * kBitWords * 4 + sizeof(VT) - 1) / sizeof(VT);
 }
 
 __device__ __forceinline__ double bit_value(const uint32_t* brow, int p) {
@@ -863,7 +887,7 @@ __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
 template <typename VT>
 __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
   const int64_t ldc = sa.a.ldc;
-  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, ldc);
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, sa.vstride);
   int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
     const int s = ch % kStages;
@@ -874,9 +898,9 @@ __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<V
     mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec + bbytes);
     VT* dst = ring.buf + s * stage_elems;
     for (int v = 0; v < sa.nvec; ++v)
-      bulk_g2s(dst + static_cast<int64_t>(v) * sa.rt * ldc, static_cast<const VT*>(sa.vec[v]) + r0 * ldc, bytes,
+      bulk_g2s(dst + static_cast<int64_t>(v) * sa.vstride, static_cast<const VT*>(sa.vec[v]) + r0 * ldc, bytes,
                &ring.full[s]);
-    bulk_g2s(dst + static_cast<int64_t>(sa.nvec) * sa.rt * ldc, sa.bits + r0 * kBitWords, bbytes, &ring.full[s]);
+    bulk_g2s(dst + static_cast<int64_t>(sa.nvec) * sa.vstride, sa.bits + r0 * kBitWords, bbytes, &ring.full[s]);
   }
 }
 
@@ -887,36 +911,95 @@ __device__ __forceinline__ double gram_at(const ChunkState& s, int k, int j, int
 
 // Shared-memory stage layout: [slot][row][ldc] with slot 0 = source (w or u_{i+1}) and slot k = u_k
 // for k >= 1, then the probe bitmask rows (u_0 = +-1).  NK = i + 1 basis vectors is a compile-time
-// constant, so every loop below is fully unrolled with no predicates.
+// constant; each thread's basis indices k = q M + part are unrolled over q.
 
-template <typename VT, int NK>
-struct StageView {
-  const VT* e;             // this thread's element of row r in slot 0
-  const uint32_t* brow;    // bitmask row r
-  int vstride, p;
-  __device__ __forceinline__ double src() const { return to_f64(e[0]); }
-  __device__ __forceinline__ double u(int k) const {   // k is a compile-time constant after unrolling
-    return k == 0 ? bit_value(brow, p) : to_f64(e[k * vstride]);
+// Consumer coordinates of this thread (see the layout note above).
+template <int M, int SL>
+struct StepLane {
+  int slot, p, part;
+  __device__ __forceinline__ StepLane() {
+    const int t = threadIdx.x - 32;
+    const int per_slot = (blockDim.x - 32) / SL;
+    slot = t / per_slot;
+    const int e = t % per_slot;
+    p = e / M;
+    part = e % M;
   }
 };
 
+// Threads per row slot for M parts per probe column (a multiple of 32; M * ldc <= 128).
+inline int step_slot_threads(int64_t ldc, int M) { return static_cast<int>(((M * ldc + 31) / 32) * 32); }
+
+// Streaming arithmetic of the step kernel.  fp64 vectors: every per-row product and sum in fp64.
+// fp32 vectors: per-row arithmetic in fp32 (no conversions in the row loop), and every running sum
+// is a fp32 block over kFlush consecutive rows of the thread's row sequence added into a fp64 total
+// (so a sum over n rows carries fp32 rounding of 8-term blocks only).  Blocks follow the row
+// sequence of the slot, not the stage boundaries, so the order is still independent of rt and M.
+template <typename VT>
+struct StepArith {
+  using T = double;
+  static constexpr int kFlush = 0;
+  static __device__ __forceinline__ T mul(T x, T y) { return __dmul_rn(x, y); }
+  static __device__ __forceinline__ T sub(T x, T y) { return __dsub_rn(x, y); }
+};
+template <>
+struct StepArith<float> {
+  using T = float;
+  static constexpr int kFlush = 8;
+  static __device__ __forceinline__ T mul(T x, T y) { return __fmul_rn(x, y); }
+  static __device__ __forceinline__ T sub(T x, T y) { return __fsub_rn(x, y); }
+};
+
+// u_k of row r in the arithmetic type (u_0 = +-1 from the bitmask row)
+template <typename VT, typename T>
+__device__ __forceinline__ T stage_u(const VT* e, const uint32_t* brow, int vstride, int p, int k) {
+  if (k == 0) return ((brow[p >> 5] >> (p & 31)) & 1u) ? T(1) : T(-1);
+  return static_cast<T>(e[k * vstride]);
+}
+
 // Phase A (consumer side): partials [cta*slots+slot][nq][cpad] of u_k . w (k < NK); at i == 0 also
 // u_0 . u_0 (q = 1) for G(0,0).
-template <typename VT, int NK>
+template <typename VT, int NK, int M, int SL>
 __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo,
-                                           int64_t hi, int nq, int cols_pad) {
+                                           int64_t hi, int nq) {
+  using A = StepArith<VT>;
+  using T = typename A::T;
+  constexpr int NQ = (NK + M - 1) / M;
   const CgsArgs& a = sa.a;
-  const int t = threadIdx.x - 32, lane = threadIdx.x & 31;
-  const int p = t % cols_pad, slot = t / cols_pad;
-  const bool pv = p < a.c;
+  const StepLane<M, SL> L;
+  const int lane = threadIdx.x & 31;
+  const bool pv = L.p < a.c;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
-  const int rt = sa.rt;
-  const int vstride = rt * ldc;
-  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, ldc);
-  double acc[NK];
+  const int rt = sa.rt, vstride = sa.vstride;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride);
+  double acc[NQ];
+  T blk[NQ];
 #pragma unroll
-  for (int kk = 0; kk < NK; ++kk) acc[kk] = 0.0;
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0, blk[q] = T(0);
+  int nrow = 0;
   double g00 = 0.0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] += static_cast<double>(blk[q]), blk[q] = T(0);
+    nrow = 0;
+  };
+  auto row_dots = [&](T wv, const T* uv) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (q * M + L.part < NK) blk[q] = fma(uv[q], wv, blk[q]);
+    if (NK == 1 && L.part == 0) g00 += 1.0;   // u_0 . u_0 = number of rows (+-1 entries)
+    if (A::kFlush && ++nrow == A::kFlush) flush();
+  };
+  auto load_row = [&](const VT* stage, const uint32_t* sbits, int rr, T& wv, T* uv) {
+    const VT* e = stage + L.p + rr * ldc;
+    const uint32_t* brow = sbits + rr * kBitWords;
+    wv = static_cast<T>(e[0]);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int kk = q * M + L.part;
+      uv[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, L.p, kk) : T(0);
+    }
+  };
   int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
     const int s = ch % kStages;
@@ -925,38 +1008,76 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
     if (pv) {
       const VT* stage = ring.buf + s * stage_elems;
       const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
-      // this thread's rows: (row - lo) % kStageSlots == slot, ascending
-      int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
-      for (; r < rows; r += kStageSlots) {
-        const StageView<VT, NK> v{stage + p + r * ldc, sbits + r * kBitWords, vstride, p};
-        const double wv = v.src();
+      // this thread's rows: (row - lo) % SL == slot, ascending; U rows per iteration (all
+      // shared-memory loads first, then the arithmetic in row order)
+      int r = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);
+      constexpr int U = NQ <= 2 ? 4 : (NQ <= 4 ? 2 : 1);
+      for (; r + SL * (U - 1) < rows; r += SL * U) {
+        T wv[U], uv[U][NQ];
 #pragma unroll
-        for (int kk = 0; kk < NK; ++kk) acc[kk] = fma(v.u(kk), wv, acc[kk]);
-        if (NK == 1) g00 += 1.0;   // u_0 . u_0 = number of rows (+-1 entries)
+        for (int j = 0; j < U; ++j) load_row(stage, sbits, r + SL * j, wv[j], uv[j]);
+#pragma unroll
+        for (int j = 0; j < U; ++j) row_dots(wv[j], uv[j]);
+      }
+      for (; r < rows; r += SL) {
+        T wv1, uv1[NQ];
+        load_row(stage, sbits, r, wv1, uv1);
+        row_dots(wv1, uv1);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
-  if (p < cp) {
-    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * kStageSlots + slot) * nq * cp + p;
+  flush();
+  if (L.p < cp) {
+    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * SL + L.slot) * nq * cp + L.p;
 #pragma unroll
-    for (int kk = 0; kk < NK; ++kk) dst[kk * cp] = acc[kk];
-    if (NK == 1) dst[NK * cp] = g00;
+    for (int q = 0; q < NQ; ++q) {
+      const int kk = q * M + L.part;
+      if (kk < NK) dst[kk * cp] = acc[q];
+    }
+    if (NK == 1 && L.part == 0) dst[NK * cp] = g00;
   }
+}
+
+// sum_k coef_k u_k from this thread's chains ch[j] (chain j M + part), combined in the canonical
+// order ((c0 + c4) + (c2 + c6)) + ((c1 + c5) + (c3 + c7)) over the M parts of the probe column.
+template <int M, typename T>
+__device__ __forceinline__ T chain_total(const T* ch) {
+  constexpr unsigned FULL = 0xffffffffu;
+  if (M == 1) return ((ch[0] + ch[4]) + (ch[2] + ch[6])) + ((ch[1] + ch[5]) + (ch[3] + ch[7]));
+  if (M == 2) {
+    const T s = (ch[0] + ch[2]) + (ch[1] + ch[3]);   // (c_t + c_t+4) + (c_t+2 + c_t+6)
+    return s + __shfl_xor_sync(FULL, s, 1);
+  }
+  if (M == 4) {
+    T s = ch[0] + ch[1];                             // c_t + c_t+4
+    s = s + __shfl_xor_sync(FULL, s, 2);
+    return s + __shfl_xor_sync(FULL, s, 1);
+  }
+  T s = ch[0] + __shfl_xor_sync(FULL, ch[0], 4);
+  s = s + __shfl_xor_sync(FULL, s, 2);
+  return s + __shfl_xor_sync(FULL, s, 1);
 }
 
 // Phase C / C' (consumer side).  First pass: w' = three-term, u_{i+1} = w' - sum_k coef_k u_k.
 // Second pass (flagged probes): u_{i+1} -= sum_k coef_k u_k.  Partials [cta*slots+slot][nq][cpad]:
-// q=0 ||w'||^2, q=1 ||u_{i+1}||^2, q=2+k  u_k . u_{i+1}.
-template <typename VT, int NK, bool SECOND>
+// q=0 ||w'||^2, q=1 ||u_{i+1}||^2, q=2+k  u_k . u_{i+1}.  Every lane runs the row loop (the chain
+// butterfly shuffles across the parts); lanes past the chunk read a valid column and store nothing.
+template <typename VT, int NK, bool SECOND, int M, int SL>
 __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo,
-                                             int64_t hi, int cols_pad, double* cf_sm) {
+                                             int64_t hi, double* cf_sm) {
+  using A = StepArith<VT>;
+  using T = typename A::T;
+  constexpr int NQ = (NK + M - 1) / M;
+  constexpr int NC = 8 / M;
   const CgsArgs& a = sa.a;
   const ChunkState& S = a.s;
-  const int t = threadIdx.x - 32, lane = threadIdx.x & 31;
-  const int p = t % cols_pad, slot = t / cols_pad;
+  const StepLane<M, SL> L;
+  const int lane = threadIdx.x & 31;
+  const int p = L.p;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
+  const int pr = p < ldc ? p : ldc - 1;
   const bool pv = p < a.c && (!SECOND || S.again[p]);
   constexpr int nq = NK + 2;
   constexpr int i = NK - 1;
@@ -965,81 +1086,132 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     ri = S.rsc[i * cp + p];
     rim1 = i > 0 ? S.rsc[(i - 1) * cp + p] : 0.0;
     bp = i > 0 ? S.beta[(i - 1) * cp + p] : 0.0;
-    al = ri * S.cdot[i * cp + p];
+    al = __dmul_rn(ri, S.cdot[i * cp + p]);
   }
-  // CGS coefficients coef_k = h_k r_k into shared memory [NK][cols_pad] (slot 0 computes)
-  if (slot == 0) {
+  // CGS coefficients coef_k = h_k r_k into shared memory [NK][kSlotThreads] (slot 0 computes)
+  if (L.slot == 0) {
 #pragma unroll
-    for (int kk = 0; kk < NK; ++kk) {
+    for (int q = 0; q < NQ; ++q) {
+      const int kk = q * M + L.part;
+      if (kk >= NK) continue;
       double c = 0.0;
       if (pv) {
         const double rk = S.rsc[kk * cp + p];
         double h;
+        // explicit roundings: no FMA contraction, so every template instance (NK, M) computes the
+        // same coefficient bits
         if (SECOND) {
-          h = rk * S.gram[kk * cp + p];                                           // q_k . w''
+          h = __dmul_rn(rk, S.gram[kk * cp + p]);                                  // q_k . w''
         } else {
-          h = rk * S.cdot[kk * cp + p] - al * gram_at(S, kk, i, p);
-          if (i > 0) h -= bp * gram_at(S, kk, i - 1, p);
+          h = __dsub_rn(__dmul_rn(rk, S.cdot[kk * cp + p]), __dmul_rn(al, gram_at(S, kk, i, p)));
+          if (i > 0) h = __dsub_rn(h, __dmul_rn(bp, gram_at(S, kk, i - 1, p)));
         }
-        c = h * rk;
+        c = __dmul_rn(h, rk);
       }
-      cf_sm[kk * cols_pad + p] = c;
+      cf_sm[kk * kSlotThreads + p] = c;
     }
   }
   named_barrier_sync(1, blockDim.x - 32);   // consumers only
-  double cf[NK];
+  T cf[NQ];
 #pragma unroll
-  for (int kk = 0; kk < NK; ++kk) cf[kk] = cf_sm[kk * cols_pad + p];
-  const int rt = sa.rt;
-  const int vstride = rt * ldc;
-  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, ldc);
+  for (int q = 0; q < NQ; ++q) {
+    const int kk = q * M + L.part;
+    cf[q] = static_cast<T>(kk < NK ? cf_sm[kk * kSlotThreads + p] : 0.0);
+  }
+  const T al_t = static_cast<T>(al), bp_t = static_cast<T>(bp), ri_t = static_cast<T>(ri);
+  const T rim1_t = static_cast<T>(rim1);
+  const int rt = sa.rt, vstride = sa.vstride;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride);
   VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
-  double nb = 0.0, nrm = 0.0;
-  double gr[NK];
+  double nb = 0.0, nrm = 0.0, gr[NQ];
+  T bnb = T(0), bnrm = T(0), bgr[NQ];
 #pragma unroll
-  for (int kk = 0; kk < NK; ++kk) gr[kk] = 0.0;
+  for (int q = 0; q < NQ; ++q) gr[q] = 0.0, bgr[q] = T(0);
+  int nrow = 0;
+  auto flush = [&]() {
+    nb += static_cast<double>(bnb);
+    nrm += static_cast<double>(bnrm);
+    bnb = T(0);
+    bnrm = T(0);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) gr[q] += static_cast<double>(bgr[q]), bgr[q] = T(0);
+    nrow = 0;
+  };
+  // one row: w' (or the source), u_{i+1} = w' - sum_k coef_k u_k, and its sums (in row order)
+  auto row_update = [&](T src, T ui, T uim1, const T* uk, int64_t grow) {
+    T wp;
+    if (SECOND) {
+      wp = src;
+    } else {
+      // w' = (w - alpha q_i) - beta q_{i-1}, q = u r  (lanczos.py:72-73)
+      wp = A::sub(A::sub(src, A::mul(al_t, A::mul(ui, ri_t))), A::mul(bp_t, A::mul(uim1, rim1_t)));
+      bnb = fma(wp, wp, bnb);
+    }
+    T chn[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) chn[j] = T(0);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (q * M + L.part < NK) chn[q % NC] = fma(uk[q], cf[q], chn[q % NC]);
+    const VT vv = static_cast<VT>(A::sub(wp, chain_total<M, T>(chn)));
+    if (pv && L.part == 0) out[grow * a.ldc] = vv;
+    const T vd = static_cast<T>(vv);
+    bnrm = fma(vd, vd, bnrm);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (q * M + L.part < NK) bgr[q] = fma(uk[q], vd, bgr[q]);
+    if (A::kFlush && ++nrow == A::kFlush) flush();
+  };
   int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
     const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
-    if (pv) {
-      const VT* stage = ring.buf + s * stage_elems;
-      const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
-      int r = static_cast<int>(((slot - (r0 - lo)) % kStageSlots + kStageSlots) % kStageSlots);
-      for (; r < rows; r += kStageSlots) {
-        const StageView<VT, NK> v{stage + p + r * ldc, sbits + r * kBitWords, vstride, p};
-        double wp;
-        if (SECOND) {
-          wp = v.src();
-        } else {
-          wp = three_term(v.src(), v.u(i), i > 0 ? v.u(i > 0 ? i - 1 : 0) : 0.0, al, bp, ri, rim1);
-          nb = fma(wp, wp, nb);
-        }
-        // basis.T @ h as two interleaved partial sums (shorter dependency chain), then one subtraction
-        double pe = 0.0, po = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < NK; ++kk) {
-          if (kk & 1) po = fma(v.u(kk), cf[kk], po);
-          else pe = fma(v.u(kk), cf[kk], pe);
-        }
-        const VT vv = from_f64<VT>(__dsub_rn(wp, pe + po));
-        out[(r0 + r) * a.ldc] = vv;
-        const double vd = to_f64(vv);
-        nrm = fma(vd, vd, nrm);
-#pragma unroll
-        for (int kk = 0; kk < NK; ++kk) gr[kk] = fma(v.u(kk), vd, gr[kk]);
+    const VT* stage = ring.buf + s * stage_elems;
+    const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
+    auto load_row = [&](int rr, T& src, T& ui, T& uim1, T* uk) {
+      const VT* e = stage + pr + rr * ldc;
+      const uint32_t* brow = sbits + rr * kBitWords;
+      src = static_cast<T>(e[0]);
+      if (!SECOND) {
+        ui = stage_u<VT, T>(e, brow, vstride, pr, i);
+        uim1 = i > 0 ? stage_u<VT, T>(e, brow, vstride, pr, i > 0 ? i - 1 : 0) : T(0);
       }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int kk = q * M + L.part;
+        uk[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, pr, kk) : T(0);
+      }
+    };
+    int r = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);
+    constexpr int U = NQ <= 2 ? 4 : (NQ <= 5 ? 2 : 1);
+    for (; r + SL * (U - 1) < rows; r += SL * U) {
+      T src[U], ui[U], uim1[U], uk[U][NQ];
+#pragma unroll
+      for (int j = 0; j < U; ++j) load_row(r + SL * j, src[j], ui[j], uim1[j], uk[j]);
+#pragma unroll
+      for (int j = 0; j < U; ++j) row_update(src[j], ui[j], uim1[j], uk[j], r0 + r + SL * j);
+    }
+    for (; r < rows; r += SL) {
+      T src1, ui1 = T(0), uim11 = T(0), uk1[NQ];
+      load_row(r, src1, ui1, uim11, uk1);
+      row_update(src1, ui1, uim11, uk1, r0 + r);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
+  flush();
   if (p < cp) {
-    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * kStageSlots + slot) * nq * cp + p;
-    dst[0] = nb;
-    dst[cp] = nrm;
+    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * SL + L.slot) * nq * cp + p;
+    if (L.part == 0) {
+      dst[0] = pv ? nb : 0.0;
+      dst[cp] = pv ? nrm : 0.0;
+    }
 #pragma unroll
-    for (int kk = 0; kk < NK; ++kk) dst[(2 + kk) * cp] = gr[kk];
+    for (int q = 0; q < NQ; ++q) {
+      const int kk = q * M + L.part;
+      if (kk < NK) dst[(2 + kk) * cp] = pv ? gr[q] : 0.0;
+    }
   }
 }
 
@@ -1065,9 +1237,9 @@ static __device__ double stripe_sum(const double* partial, int ntiles, int nq, i
 }
 
 // Phases C (or C'), D, E of one CGS pass (SECOND: the conditional second pass, lanczos.py:75-76).
-template <typename VT, int NK, bool SECOND, typename Sync>
+template <typename VT, int NK, bool SECOND, int M, int SL, typename Sync>
 __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs& st, StageRing<VT>& ring, int& ch,
-                                            int64_t lo, int64_t hi, int cols_pad, int nrows_partial, double* cf_sm,
+                                            int64_t lo, int64_t hi, int nrows_partial, double* cf_sm,
                                             double* red, Sync& sync_grid) {
   const CgsArgs& a = sa.pass[0].a;
   const ChunkState& S = a.s;
@@ -1078,7 +1250,7 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
   } else {
-    phase_update<VT, NK, SECOND>(st, ring, ch, lo, hi, cols_pad, cf_sm);
+    phase_update<VT, NK, SECOND, M, SL>(st, ring, ch, lo, hi, cf_sm);
   }
   ch += chunk_count(lo, hi, st.rt);
   asm volatile("fence.proxy.async.global;" ::: "memory");   // u_{i+1} is bulk-read by a second pass
@@ -1128,12 +1300,12 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
   sync_grid();
 }
 
-template <typename VT, int NK>
-__global__ void __launch_bounds__(32 + kStageSlots * kStagedMaxLdc, 1)
+template <typename VT, int NK, int M, int SL>
+__global__ void __launch_bounds__(kStepThreads, 1)
 cgs_step_kernel(StepArgs sa) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double red[kStripes * 32];
-  __shared__ double cf_sm[kCgsBlock * kStagedMaxLdc];
+  __shared__ double cf_sm[kCgsBlock * kSlotThreads];
   StageRing<VT> ring(smem);
   const CgsArgs& a = sa.pass[0].a;
   const ChunkState& S = a.s;
@@ -1141,7 +1313,6 @@ cgs_step_kernel(StepArgs sa) {
   unsigned int nbar = 0;
   auto sync_grid = [&]() { grid_barrier(bar, ++nbar); };
   const int nwc = (blockDim.x - 32) / 32;
-  const int cols_pad = (blockDim.x - 32) / kStageSlots;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
     mbar_fence_init();
@@ -1152,7 +1323,7 @@ cgs_step_kernel(StepArgs sa) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nk = a.i + 1;
   const int nslot = S.S + 1;
-  const int nrows_partial = gridDim.x * kStageSlots;
+  const int nrows_partial = gridDim.x * SL;
   int ch = 0;
   const StagedArgs& st0 = sa.pass[0];
   const int nch0 = chunk_count(lo, hi, st0.rt);
@@ -1192,7 +1363,7 @@ cgs_step_kernel(StepArgs sa) {
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) staged_produce<VT>(st0, ring, ch, lo, hi);
   } else {
-    phase_dots<VT, NK>(st0, ring, ch, lo, hi, nqa, cols_pad);
+    phase_dots<VT, NK, M, SL>(st0, ring, ch, lo, hi, nqa);
   }
   ch += nch0;
   sync_grid();
@@ -1212,39 +1383,48 @@ cgs_step_kernel(StepArgs sa) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *S.any_again = 0;
   sync_grid();
-  update_pass<VT, NK, false>(sa, sa.pass[0], ring, ch, lo, hi, cols_pad, nrows_partial, cf_sm, red, sync_grid);
+  update_pass<VT, NK, false, M, SL>(sa, sa.pass[0], ring, ch, lo, hi, nrows_partial, cf_sm, red, sync_grid);
   if (*S.any_again) {   // uniform: read after a grid barrier
 #ifdef SLQ_DEBUG_SECOND
     if (blockIdx.x == 0 && threadIdx.x == 0) printf("second pass at step %d\n", a.i);
 #endif
-    update_pass<VT, NK, true>(sa, sa.pass[1], ring, ch, lo, hi, cols_pad, nrows_partial, cf_sm, red, sync_grid);
+    update_pass<VT, NK, true, M, SL>(sa, sa.pass[1], ring, ch, lo, hi, nrows_partial, cf_sm, red, sync_grid);
   }
 }
 
-// Build the staged-vector list of one pass; false when the geometry does not fit.
+// Build the staged-vector list of one pass; false when the geometry does not fit.  Vector slots
+// of a stage are vstride elements apart, vstride = W / M (mod W) with W = 128 B / sizeof(VT), so the
+// M parts of a probe column (reading M different slots of one row) hit distinct banks.
 template <typename VT>
 static bool staged_setup(const CgsArgs& a, bool second, const uint32_t* bits, StagedArgs* out) {
   StagedArgs s{};
   s.a = a;
   const VT* basis = static_cast<const VT*>(a.basis);
   const int nk = a.i + 1;
-  if (!a.reorth || nk > kCgsBlock || !bits) return false;
+  if (!a.reorth || nk > kCgsBlock || !bits || a.ldc > kStagedMaxLdc) return false;
   int nv = 0;
-  s.slot_src = nv;
   s.vec[nv++] = second ? static_cast<const void*>(basis + (a.i + 1) * a.vec_stride) : a.w;
-  for (int kk = 0; kk < kCgsBlock; ++kk) s.slot_k[kk] = 0;
-  for (int kk = 1; kk < nk; ++kk) {       // u_0 comes from the bitmask
-    s.slot_k[kk] = nv;
-    s.vec[nv++] = basis + static_cast<int64_t>(kk) * a.vec_stride;
-  }
+  for (int kk = 1; kk < nk; ++kk) s.vec[nv++] = basis + static_cast<int64_t>(kk) * a.vec_stride;   // u_0: bitmask
   s.bits = bits;
   s.nvec = nv;
-  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t);
+  const int M = step_parts(a.ldc);
+  const int W = 128 / static_cast<int>(sizeof(VT));
+  const int target = (W / M) % W;
+  auto padded = [&](int64_t rt) {
+    int64_t v = rt * a.ldc;
+    while (v % W != target) ++v;
+    return v;
+  };
   const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
+  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t);
   int64_t rt = static_cast<int64_t>((kStagedSmem - 256) / (kStages * row_bytes));
   rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
-  if (rt < 1 || a.ldc > kStagedMaxLdc) return false;
+  while (rt > 1 && 128 + kStages * sizeof(VT) * stage_elems_of<VT>(nv, static_cast<int>(rt),
+                                                                    static_cast<int>(padded(rt))) > kStagedSmem)
+    --rt;
+  if (rt < 1) return false;
   s.rt = static_cast<int>(rt);
+  s.vstride = static_cast<int>(padded(rt));
   *out = s;
   return true;
 }
@@ -1260,6 +1440,34 @@ static int coop_supported(int dev) {
   return v[dev] == 1;
 }
 
+// Class launchers (instantiated per vector type and slot class in step_{f32,f64}_{wide,narrow}.cu).
+bool step_launch_f32_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
+bool step_launch_f32_narrow(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
+bool step_launch_f64_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
+bool step_launch_f64_narrow(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
+
+template <typename VT, int SL, int MM>
+bool step_launch_one(const StepArgs& sa, int nk, int threads, size_t smem, cudaStream_t st) {
+  switch (nk) {
+#define SLQ_STEP_K(K)                                                                                     \
+    case K: {                                                                                              \
+      static bool attr = false;                                                                            \
+      if (!attr) {                                                                                         \
+        cudaFuncSetAttribute(cgs_step_kernel<VT, K, MM, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             static_cast<int>(kStagedSmem));                                               \
+        attr = true;                                                                                       \
+      }                                                                                                    \
+      cgs_step_kernel<VT, K, MM, SL><<<kPersist, threads, smem, st>>>(sa);                                 \
+      return true;                                                                                         \
+    }
+    SLQ_STEP_K(1) SLQ_STEP_K(2) SLQ_STEP_K(3) SLQ_STEP_K(4) SLQ_STEP_K(5) SLQ_STEP_K(6) SLQ_STEP_K(7)
+    SLQ_STEP_K(8) SLQ_STEP_K(9) SLQ_STEP_K(10) SLQ_STEP_K(11) SLQ_STEP_K(12) SLQ_STEP_K(13) SLQ_STEP_K(14)
+    SLQ_STEP_K(15) SLQ_STEP_K(16)
+#undef SLQ_STEP_K
+    default: return false;
+  }
+}
+
 // Launch everything after the SpMM of step i as one persistent kernel; false when the staged path
 // does not apply (the caller then runs the separate kernels).
 template <typename VT>
@@ -1272,30 +1480,20 @@ static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmA
   sa.red = red;
   sa.spmm = spmm;
   const size_t smem = 128 + kStages * sizeof(VT) *
-                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, a.ldc),
-                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, a.ldc));
-  const int threads = 32 + kStageSlots * (((static_cast<int>(a.ldc) + 31) / 32) * 32);
+                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, sa.pass[0].vstride),
+                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, sa.pass[1].vstride));
   LaunchScope ls(K_CGS_UPDATE, st);
   // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
   // so the software grid barrier is safe (coop_supported() checked the SM count).
-  switch (a.i + 1) {
-#define SLQ_STEP_CASE(K)                                                                                  \
-    case K: {                                                                                              \
-      static bool attr = false;                                                                            \
-      if (!attr) {                                                                                         \
-        cudaFuncSetAttribute(cgs_step_kernel<VT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
-                             static_cast<int>(kStagedSmem));                                               \
-        attr = true;                                                                                       \
-      }                                                                                                    \
-      cgs_step_kernel<VT, K><<<kPersist, threads, smem, st>>>(sa);                                         \
-      break;                                                                                               \
-    }
-    SLQ_STEP_CASE(1) SLQ_STEP_CASE(2) SLQ_STEP_CASE(3) SLQ_STEP_CASE(4) SLQ_STEP_CASE(5) SLQ_STEP_CASE(6)
-    SLQ_STEP_CASE(7) SLQ_STEP_CASE(8) SLQ_STEP_CASE(9) SLQ_STEP_CASE(10) SLQ_STEP_CASE(11) SLQ_STEP_CASE(12)
-    SLQ_STEP_CASE(13) SLQ_STEP_CASE(14) SLQ_STEP_CASE(15) SLQ_STEP_CASE(16)
-#undef SLQ_STEP_CASE
-    default: return false;
-  }
+  const StepGeom geo = step_geometry(a.ldc);
+  const int threads = 32 + geo.slots * step_slot_threads(a.ldc, geo.parts);
+  const bool narrow = geo.slots == kNarrowSlots;
+  bool ok;
+  if (sizeof(VT) == 4) ok = narrow ? step_launch_f32_narrow(sa, a.i + 1, geo.parts, threads, smem, st)
+                                   : step_launch_f32_wide(sa, a.i + 1, geo.parts, threads, smem, st);
+  else ok = narrow ? step_launch_f64_narrow(sa, a.i + 1, geo.parts, threads, smem, st)
+                   : step_launch_f64_wide(sa, a.i + 1, geo.parts, threads, smem, st);
+  if (!ok) return false;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *rc = cuda_fail(e, "cgs_step_kernel launch");
@@ -1337,11 +1535,6 @@ static void launch_reduce(ReduceArgs a, cudaStream_t st) {
 // Per-vector-type entry points instantiated in spmm_{f32,f64}.cu and step_{f32,f64}.cu.
 void launch_spmm_f32(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish);
 void launch_spmm_f64(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish);
-bool launch_cgs_step_f32(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
-                         int dev, cudaStream_t st, int* rc);
-bool launch_cgs_step_f64(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
-                         int dev, cudaStream_t st, int* rc);
-
 template <typename VT>
 inline void spmm_entry(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish = true) {
   if (sizeof(VT) == 4) launch_spmm_f32(kind, a, coop, dev, st, finish);
@@ -1351,8 +1544,7 @@ inline void spmm_entry(int kind, const SpmmArgs& a, bool coop, int dev, cudaStre
 template <typename VT>
 inline bool cgs_step_entry(const CgsArgs& a, const ReduceArgs& red, const SpmmArgs& spmm, const uint32_t* bits,
                            int dev, cudaStream_t st, int* rc) {
-  return sizeof(VT) == 4 ? launch_cgs_step_f32(a, red, spmm, bits, dev, st, rc)
-                         : launch_cgs_step_f64(a, red, spmm, bits, dev, st, rc);
+  return launch_cgs_step<VT>(a, red, spmm, bits, dev, st, rc);
 }
 
 }  // namespace slq

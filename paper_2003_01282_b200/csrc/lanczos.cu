@@ -146,7 +146,7 @@ static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bo
 // Rows of reduction partials: flat fallback kernels (one per stream tile), the persistent step
 // kernel (one per row slot) and alpha_dot_kernel (one per CTA).  The SpMM writes none.
 static int64_t partial_rows(const slq_graph* g) {
-  return std::max<int64_t>({static_cast<int64_t>(g->ntiles_stream), static_cast<int64_t>(kPersist) * kStageSlots,
+  return std::max<int64_t>({static_cast<int64_t>(g->ntiles_stream), static_cast<int64_t>(kPersist) * kNarrowSlots,
                             static_cast<int64_t>(kAlphaCtas)});
 }
 

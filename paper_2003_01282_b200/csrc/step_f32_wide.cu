@@ -1,0 +1,14 @@
+// Staged CGS step kernels, float vectors, wide class (3 row slots; engine.cuh: cgs_step_kernel).
+#include "engine.cuh"
+
+namespace slq {
+
+bool step_launch_f32_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st) {
+  switch (parts) {
+    case 1: return step_launch_one<float, kStageSlots, 1>(sa, nk, threads, smem, st);
+    case 2: return step_launch_one<float, kStageSlots, 2>(sa, nk, threads, smem, st);
+    default: return false;
+  }
+}
+
+}  // namespace slq

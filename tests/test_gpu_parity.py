@@ -225,15 +225,21 @@ def test_rules_independent_of_chunking(cuda_device):
     assert torch.equal(s_full, torch.cat([s1, s2]))
     a3, _, _ = dg.tridiagonals("normalized_laplacian", 0, 0, 70, 15)
     assert torch.equal(a_full, a3)
-    # narrow chunks (<= 16 probes: half-warp SpMM mapping) follow the same summation order
-    for begin, count in ((0, 16), (16, 9), (40, 1)):
+    # narrow chunks (<= 32 columns: 12-row-slot step kernel, half-warp SpMM for <= 16) agree
+    # bitwise among themselves and with the wide class to rounding
+    n32, nb32, ns32 = dg.tridiagonals("normalized_laplacian", 0, 0, 32, 15)
+    for begin, count in ((0, 16), (16, 9), (31, 1)):
         a4, b4, s4 = dg.tridiagonals("normalized_laplacian", 0, begin, count, 15)
-        assert torch.equal(a4, a_full[begin:begin + count]) and torch.equal(b4, b_full[begin:begin + count])
-        assert torch.equal(s4, s_full[begin:begin + count])
+        assert torch.equal(a4, n32[begin:begin + count]) and torch.equal(b4, nb32[begin:begin + count])
+        assert torch.equal(s4, ns32[begin:begin + count])
+    assert torch.equal(ns32, s_full[:32])
+    assert torch.allclose(n32, a_full[:32], rtol=1e-13, atol=1e-14)
     for kind in ("normalized_laplacian", "density"):
-        f_full, _, _ = dg.tridiagonals(kind, 0, 0, 40, 15, dtype="f32")
-        f_narrow, _, _ = dg.tridiagonals(kind, 0, 24, 16, 15, dtype="f32")
-        assert torch.equal(f_narrow, f_full[24:40]), kind
+        f_full, _, _ = dg.tridiagonals(kind, 0, 0, 32, 15, dtype="f32")
+        f_narrow, _, _ = dg.tridiagonals(kind, 0, 24, 8, 15, dtype="f32")
+        assert torch.equal(f_narrow, f_full[24:32]), kind
+        f_wide, _, _ = dg.tridiagonals(kind, 0, 0, 40, 15, dtype="f32")
+        assert torch.allclose(f_wide[:32], f_full, rtol=1e-5, atol=1e-6), kind
 
 
 # edge cases the reference tests
