@@ -3,8 +3,11 @@ probes are split into balanced contiguous ranges, each rank builds the Gauss
 rules of its own probes, and ONE all-gather of (nodes, weights, steps)
 assembles every rule on every rank in ascending probe order.  Per-probe
 arithmetic does not depend on the range a rank owns, so the result is
-bitwise identical for any world size.  The collective is a few tens of KB
-(latency-bound): NCCL over NVLink on GPUs, gloo in the CPU tests.
+bitwise identical for any world size as long as each rank's chunks fall in
+the same step-kernel slot class (<= 32 or > 32 vector columns) as the
+single-rank run's, and equal to rounding otherwise (tests/test_gpu_dist.py).
+The collective is a few tens of KB (latency-bound): NCCL over NVLink on
+GPUs, gloo in the CPU tests.
 """
 from __future__ import annotations
 

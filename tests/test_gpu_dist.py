@@ -1,0 +1,89 @@
+"""Probe sharding on the device path: two ranks (gloo, both on cuda:0 — their kernels never wait on
+each other; the only exchange is the host all-gather of the rules) assemble exactly the rules and
+descriptors of a single-rank run when every rank's chunk width falls in the same step-kernel slot
+class as the single run's (DESIGN §4 determinism), and agree to rounding otherwise."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_v, dtype, out):
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import golden
+    from paper_2003_01282_b200 import _lib
+    from paper_2003_01282_b200.descriptors import TimeGrid
+    from paper_2003_01282_b200.device import DeviceGraph
+    from paper_2003_01282_b200.dist import sharded_rules
+    from paper_2003_01282_b200.slq import SlqConfig
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dg = DeviceGraph(golden.graph(golden.load("sbm5k.npz")), torch.device("cuda", 0))
+    cfg = SlqConfig(n_v=n_v, s=15, seed=0)
+    rules = sharded_rules(dg, "normalized_laplacian", cfg, dtype=dtype)
+    vals, _ = rules.integrate(np.array(TimeGrid(1e-2, 1e2, 64).values), [_lib.FN_HEAT])
+    if rank == 0:
+        out.put((rules.nodes.cpu().numpy(), rules.weights.cpu().numpy(), rules.steps.cpu().numpy(),
+                 vals.cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _sharded(n_v, dtype):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_v, dtype, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def _single(n_v, dtype):
+    import golden
+    from paper_2003_01282_b200 import _lib
+    from paper_2003_01282_b200.descriptors import TimeGrid
+    from paper_2003_01282_b200.device import DeviceGraph
+
+    dg = DeviceGraph(golden.graph(golden.load("sbm5k.npz")), torch.device("cuda", 0))
+    r = dg.rules("normalized_laplacian", 0, 0, n_v, 15, dtype=dtype)
+    vals, _ = r.integrate(np.array(TimeGrid(1e-2, 1e2, 64).values), [_lib.FN_HEAT])
+    return r.nodes.cpu().numpy(), r.weights.cpu().numpy(), r.steps.cpu().numpy(), vals.cpu().numpy()
+
+
+@pytest.mark.parametrize("n_v,dtype", [(100, "f64"), (32, "f64"), (32, "f32")])
+def test_two_ranks_bitwise_equal_single_rank(cuda_device, n_v, dtype):
+    # 100 -> 50 + 50 (wide class both ways); 32 -> 16 + 16 (narrow class both ways)
+    got, ref = _sharded(n_v, dtype), _single(n_v, dtype)
+    for g, r in zip(got, ref):
+        assert np.array_equal(g, r)
+
+
+def test_two_ranks_across_slot_classes_agree_to_rounding(cuda_device):
+    # 40 probes on one rank (wide) vs 20 + 20 (narrow): same rules to rounding
+    got, ref = _sharded(40, "f64"), _single(40, "f64")
+    assert np.array_equal(got[2], ref[2])
+    assert np.max(np.abs(got[0] - ref[0])) <= 1e-13
+    assert np.max(np.abs(got[3] - ref[3]) / np.abs(ref[3])) <= 1e-13
