@@ -319,6 +319,14 @@ def run_ours(args):
             per_class[k]["achieved_GBs"] = (ab[k] * args.steps / (t_ms * 1e-3) / 1e9) if t_ms > 0 else None
     dom = max(ab, key=lambda k: per_class.get(k, {}).get("ms_per_step", 0.0))
     ach = per_class[dom]["achieved_GBs"]
+    traffic, traffic_src = args.traffic, "--traffic" if args.traffic else None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic_c2.json")
+    if traffic is None and os.path.exists(tpath):
+        with open(tpath) as f:
+            tk = json.load(f)["kernels"].get(dom)
+        if tk:
+            traffic = tk["dram_bytes_per_launch"]
+            traffic_src = "profiles/r1_traffic_c2.json (ncu --set full, dram read+write per launch, avg over a signature)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -326,7 +334,9 @@ def run_ours(args):
         "config": dict(WORKLOAD, parallelism=f"probe-sharded x{world}" if world > 1 else "single GPU",
                        total_probes=total_probes, nnz=g.nnz),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": (ach / peak) if ach else None, "traffic": args.traffic, "peak_source": peak_src},
+                     "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": ab[dom] / max(1.0, per_class[dom]["launches_per_step"]),
+                     "peak_source": peak_src},
         "kernels": per_class,
         "ms_per_step_profiled": float(np.mean(ptimes)),
         "ms_steps": [round(t, 3) for t in times],
