@@ -228,6 +228,9 @@ reduce_kernel(ReduceArgs a) {
 // set by the graph's tiles and the warp count, never by c.
 constexpr int kBlk = 128;
 constexpr int kSpmmWarps = 8;
+#ifndef SLQ_SPMM_UNRF
+#define SLQ_SPMM_UNRF 8    // gathered values in flight per lane in the full-warp mapping (UNR * PPL)
+#endif
 
 __device__ __forceinline__ bool probe_ok(int p, int c) { return p < c; }
 
@@ -353,7 +356,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       }
       continue;
     }
-    constexpr int UNR = 8 / PPL;     // 8 gathers in flight per lane (even: chain = q & 1)
+    constexpr int UNR = SLQ_SPMM_UNRF / PPL;   // gathers in flight per lane (even: chain = q & 1)
     int k = 0;
     for (; k + UNR <= cnt; k += UNR) {
       double xv[UNR][PPL];
