@@ -36,16 +36,19 @@ struct BatchArgs {
   int c;                   // probes per graph
   int S;                   // requested steps
   int64_t N;               // total vertices
-  void* vec;               // [S+1][N][c] workspace (slot S = w)
-  double* nodes;           // [G][c][S]
-  double* weights_out;     // [G][c][S]
-  int32_t* steps_out;      // [G][c]
+  void* vec;               // [gridDim.y][S+1][N][c] workspace (slot S = w)
+  double* nodes;           // [G][Y*c][S] (Y = gridDim.y probe blocks)
+  double* weights_out;     // [G][Y*c][S]
+  int32_t* steps_out;      // [G][Y*c]
   int* status;
+  uint64_t probe0;         // stream index of probe 0 of probe block 0
+  int64_t count;           // probes stored per graph (<= Y*c; the tail of the last block is dropped)
+  const int* dflags;       // graph flags (bad columns -> status bit 8), may be null
 };
 
 template <typename VT>
 __device__ __forceinline__ VT* vslot(const BatchArgs& a, int k) {
-  return static_cast<VT*>(a.vec) + static_cast<int64_t>(k) * a.N * a.c;
+  return static_cast<VT*>(a.vec) + (static_cast<int64_t>(blockIdx.y) * (a.S + 1) + k) * a.N * a.c;
 }
 
 // Sum the kRows slot partials of quantity q (smem part[kRows][nq][c]) in slot order.
@@ -95,7 +98,7 @@ batched_lanczos_kernel(BatchArgs a) {
     VT* u0 = vslot<VT>(a, 0);
     if (act) {
       u128 st, inc;
-      pcg64_seed_state(a.seed, static_cast<uint64_t>(p), &st, &inc);
+      pcg64_seed_state(a.seed, a.probe0 + static_cast<uint64_t>(blockIdx.y) * c + p, &st, &inc);
       const u128 mult = pcg_mult();
       // rows rs, rs+kRows, ...: output m holds entries 2m (bit 31) and 2m+1 (bit 63)
       int row = rs;
@@ -258,7 +261,9 @@ batched_lanczos_kernel(BatchArgs a) {
     }
     __syncthreads();
     // ---- Gauss rules per probe (lanczos.py:148-163 + slq.py:76-77)
-    if (t < c) {
+    const int64_t pg = static_cast<int64_t>(blockIdx.y) * c + t;   // probe index within the graph's output
+    const int64_t ow = static_cast<int64_t>(gridDim.y) * c;
+    if (t < c && pg < a.count) {
       double d[kMaxSteps], e[kMaxSteps], z[kMaxSteps];
       const int m = steps[t];
       bool finite = true;
@@ -269,8 +274,8 @@ batched_lanczos_kernel(BatchArgs a) {
         finite = finite && isfinite(d[k]) && isfinite(e[k]);
       }
       int rc = finite ? tridiag_ql_first_row(d, e, z, m) : -1;
-      double* nd = a.nodes + (gi * c + t) * a.S;
-      double* wt = a.weights_out + (gi * c + t) * a.S;
+      double* nd = a.nodes + (gi * ow + pg) * a.S;
+      double* wt = a.weights_out + (gi * ow + pg) * a.S;
       if (rc) {
         atomicOr(a.status, rc < 0 ? 2 : 1);
         for (int k = 0; k < a.S; ++k) { nd[k] = 0.0; wt[k] = 0.0; }
@@ -288,7 +293,8 @@ batched_lanczos_kernel(BatchArgs a) {
           wt[k] = k < m ? z[k] : 0.0;
         }
       }
-      a.steps_out[gi * c + t] = m;
+      a.steps_out[gi * ow + pg] = m;
+      if (a.dflags && a.dflags[0]) atomicOr(a.status, 8);
     }
   }
 }
@@ -364,7 +370,7 @@ extern "C" int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_off
   a.offsets = g->offsets; a.cols = g->cols; a.weights = g->weights; a.degree = g->degree; a.dinv = g->dinv;
   a.dscal = g->dscal; a.voff = vertex_offsets; a.G = num_graphs; a.kind = kind; a.seed = seed; a.c = n_v;
   a.S = steps; a.N = g->n; a.vec = vec; a.nodes = nodes; a.weights_out = weights; a.steps_out = steps_out;
-  a.status = status;
+  a.status = status; a.probe0 = 0; a.count = n_v; a.dflags = nullptr;
   const int threads = ((kRows * n_v + 31) / 32) * 32;
   const size_t smem = sizeof(double) * (kRows * (kCgsBlock + 1) * n_v + (4 * steps + 3) * n_v) +
                       sizeof(int) * (3 * n_v + 4);
@@ -391,6 +397,65 @@ extern "C" int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_off
   SLQ_CUDA(cudaFreeAsync(vec, st));
   return SLQ_OK;
 }
+
+// Single small graph (slq_rules for n <= small_graph_max_n()): the batched kernel with one graph
+// and one CTA per block of <= 64 probes (grid.y), so the whole Lanczos run stays on one SM per probe
+// block instead of ~2 grid-wide kernels per step.  Per-probe arithmetic does not depend on the
+// block, so a probe's rule is the same for every probe range and count.
+namespace slq {
+
+int64_t small_graph_max_n() {
+  static const int64_t v = [] {
+    const char* e = getenv("SLQ_SMALL_N");
+    return e ? static_cast<int64_t>(atoll(e)) : static_cast<int64_t>(128);   // measured crossover ~130 rows
+  }();
+  return v;
+}
+
+int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int S, int dtype,
+                double* nodes, double* weights, int32_t* steps_out, int32_t* status, cudaStream_t st) {
+  const int c = static_cast<int>(std::min<int64_t>(count, kBatchMaxProbes));
+  const int64_t blocks = (count + c - 1) / c;
+  const int vb = dtype == SLQ_F64 ? 8 : 4;
+  void* vec = nullptr;
+  int64_t* voff = nullptr;
+  SLQ_CUDA(cudaMallocAsync(&vec, static_cast<size_t>(blocks) * (S + 1) * std::max<int64_t>(g->n, 1) * c * vb, st));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&voff), 2 * sizeof(int64_t), st));
+  const int64_t hv[2] = {0, g->n};
+  SLQ_CUDA(cudaMemcpyAsync(voff, hv, sizeof(hv), cudaMemcpyHostToDevice, st));
+  BatchArgs a{};
+  a.offsets = g->offsets; a.cols = g->cols; a.weights = g->weights; a.degree = g->degree; a.dinv = g->dinv;
+  a.dscal = g->dscal; a.voff = voff; a.G = 1; a.kind = kind; a.seed = seed; a.c = c;
+  a.S = S; a.N = g->n; a.vec = vec; a.nodes = nodes; a.weights_out = weights; a.steps_out = steps_out;
+  a.status = status; a.probe0 = static_cast<uint64_t>(probe_begin); a.count = count; a.dflags = g->dflags;
+  const int threads = ((kRows * c + 31) / 32) * 32;
+  const size_t smem = sizeof(double) * (kRows * (kCgsBlock + 1) * c + (4 * S + 3) * c) + sizeof(int) * (3 * c + 4);
+  const dim3 grid(1, static_cast<unsigned>(blocks));
+  {
+    LaunchScope ls(K_BATCHED, st);
+#define SLQ_SMALL(VT, K)                                                                                       \
+  do {                                                                                                         \
+    if (smem > 48 * 1024)                                                                                      \
+      cudaFuncSetAttribute(batched_lanczos_kernel<VT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                           static_cast<int>(smem));                                                            \
+    batched_lanczos_kernel<VT, K><<<grid, threads, smem, st>>>(a);                                             \
+  } while (0)
+    if (dtype == SLQ_F64) {
+      if (kind == SLQ_NORMALIZED_LAPLACIAN) SLQ_SMALL(double, SLQ_NORMALIZED_LAPLACIAN);
+      else SLQ_SMALL(double, SLQ_DENSITY);
+    } else {
+      if (kind == SLQ_NORMALIZED_LAPLACIAN) SLQ_SMALL(float, SLQ_NORMALIZED_LAPLACIAN);
+      else SLQ_SMALL(float, SLQ_DENSITY);
+    }
+#undef SLQ_SMALL
+  }
+  SLQ_CUDA(cudaGetLastError());
+  SLQ_CUDA(cudaFreeAsync(vec, st));
+  SLQ_CUDA(cudaFreeAsync(voff, st));
+  return SLQ_OK;
+}
+
+}  // namespace slq
 
 extern "C" int slq_integrate_batched(const double* nodes, const double* weights, const int32_t* steps,
                                      int64_t num_graphs, int n_v, int ld, const int64_t* vertex_offsets,

@@ -257,6 +257,7 @@ struct SpmmArgs {
   const int32_t* seg_row;
   const int64_t* seg_begin;
   int64_t max_long;
+  int64_t max_seg;           // host upper bound of the segment count (grid sizing)
   double* segpart;
   unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
   const uint32_t* bits;      // first step: u_0 as a probe bitmask [n][kBitWords] (nullptr = use u)
@@ -554,7 +555,10 @@ template <typename VT, int KIND, bool W, int PPL>
 static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
   (void)coop;
   (void)dev;
-  dim3 grid(148 * 4, gy);   // persistent: work is taken from the atomic counters
+  // persistent: work is taken from the atomic counters; small graphs launch only the warps they can use
+  const int64_t items = static_cast<int64_t>(a.ntiles) + (a.long_counts ? a.max_seg : 0);
+  dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(148 * 4, (items + kSpmmWarps - 1) / kSpmmWarps))),
+            gy);
   // EXACT (bit-identical operator apply) only for the apply entry (r == nullptr, double);
   // HALF (two nonzeros per warp instruction) for Lanczos chunks of <= 16 probes.
   const bool half = PPL == 1 && a.c <= 16 && a.ldc_in <= 16;
@@ -821,6 +825,13 @@ cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
 // u_{i+1} is bitwise independent of M as well: narrow chunks keep the whole CTA busy without
 // changing any result.
 constexpr int kPersist = 148;
+constexpr int64_t kStepMinRows = 512;   // small graphs use fewer step CTAs (cheaper grid barriers)
+
+// CTAs of the step kernel for n rows: one per SM, or fewer for small graphs.  A function of n only,
+// so every probe of a graph sees the same row partition.
+inline int step_ctas(int64_t n) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kPersist, (n + kStepMinRows - 1) / kStepMinRows)));
+}
 constexpr int kStageSlots = 3;      // row slots of the wide class (ldc > 32)
 constexpr int kNarrowSlots = 12;    // row slots of the narrow class (ldc <= 32)
 constexpr int kSlotThreads = 128;                                 // max threads per row slot
@@ -1418,7 +1429,7 @@ static bool staged_setup(const CgsArgs& a, bool second, const uint32_t* bits, St
     while (v % W != target) ++v;
     return v;
   };
-  const int64_t rows_per_cta = (a.n + kPersist - 1) / kPersist;
+  const int64_t rows_per_cta = (a.n + step_ctas(a.n) - 1) / step_ctas(a.n);
   const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t);
   int64_t rt = static_cast<int64_t>((kStagedSmem - 256) / (kStages * row_bytes));
   rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
@@ -1460,7 +1471,7 @@ bool step_launch_one(const StepArgs& sa, int nk, int threads, size_t smem, cudaS
                              static_cast<int>(kStagedSmem));                                               \
         attr = true;                                                                                       \
       }                                                                                                    \
-      cgs_step_kernel<VT, K, MM, SL><<<kPersist, threads, smem, st>>>(sa);                                 \
+      cgs_step_kernel<VT, K, MM, SL><<<step_ctas(sa.pass[0].a.n), threads, smem, st>>>(sa);                \
       return true;                                                                                         \
     }
     SLQ_STEP_K(1) SLQ_STEP_K(2) SLQ_STEP_K(3) SLQ_STEP_K(4) SLQ_STEP_K(5) SLQ_STEP_K(6) SLQ_STEP_K(7)

@@ -75,6 +75,7 @@ static void set_long_rows(SpmmArgs& sa, const slq_graph* g, double* segpart) {
   sa.seg_row = g->seg_row;
   sa.seg_begin = g->seg_begin;
   sa.max_long = g->max_long;
+  sa.max_seg = g->max_seg;
   sa.segpart = segpart;
 }
 

@@ -285,6 +285,16 @@ extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   if (count == 0) return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int S = static_cast<int>(std::min<int64_t>(steps, std::max<int64_t>(g->n, 1)));
+  // small graphs: one CTA per probe block runs the whole recurrence (batched.cu)
+  const int ro = reorth < 0 ? (S <= 100 ? 1 : 0) : reorth;
+  if (g->n > 0 && g->n <= small_graph_max_n() && ro == 1 && steps >= 1 && S <= kMaxSteps && count > 0 &&
+      probe_begin >= 0 && (dtype == SLQ_F64 || dtype == SLQ_F32) &&
+      (kind == SLQ_NORMALIZED_LAPLACIAN || (kind == SLQ_DENSITY && g->nnz > 0))) {
+    const size_t ws = static_cast<size_t>((count + 63) / 64) * (S + 1) * g->n * std::min<int64_t>(count, 64) *
+                      (dtype == SLQ_F64 ? 8 : 4);
+    if (ws <= (size_t(1) << 30))
+      return small_rules(g, kind, seed, probe_begin, count, S, dtype, nodes, weights, steps_out, status, st);
+  }
   double* ab = nullptr;
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ab), sizeof(double) * 2 * count * S, st));
   int rc = slq_lanczos(g, kind, seed, probe_begin, count, steps, reorth, dtype, ab, ab + count * S, steps_out, stream);

@@ -47,6 +47,10 @@ void ensure_pool(int dev);   // keep the stream-ordered allocator's memory cache
 struct slq_graph;
 namespace slq {
 int fetch_host_scalars(slq_graph* g);
+// single small graph on the batched kernel (batched.cu); slq_rules routes n <= small_graph_max_n()
+int64_t small_graph_max_n();
+int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int S, int dtype,
+                double* nodes, double* weights, int32_t* steps_out, int32_t* status, cudaStream_t st);
 
 void launch_begin(KernelClass k, cudaStream_t s);
 void launch_end(KernelClass k, cudaStream_t s);
