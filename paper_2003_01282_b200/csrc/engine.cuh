@@ -291,12 +291,14 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
 // multiple of kSeg after it).
 //  EXACT (operator apply, r == 1): t = fl(dinv_c * u_c) [* w], acc = fl(acc + t) in stored order:
 //        the reference's csr_matvec order and rounding, bit for bit.
-//  !EXACT (Lanczos): two FMA chains, s_even over the even positions of the range and s_odd over
-//        the odd ones (s_c = dinv_c [* w]), acc = s_even + s_odd; the caller multiplies by the probe
-//        scale r (q = r u is never formed per gathered value).  This order is the same for the
-//        full-warp mapping (lane = probe, both chains in one lane) and the HALF mapping (c <= 16:
-//        each half-warp gathers every other nonzero, so one warp instruction fetches two rows'
-//        worth of probes), so results do not depend on the chunk width.
+//  !EXACT (Lanczos): FMA sums with s_c = dinv_c [* w]; the caller multiplies by the probe scale r
+//        (q = r u is never formed per gathered value).  Narrow chunks (c <= 32, PPL = 1) sum a row
+//        as two chains, s_even over its even positions and s_odd over the odd ones, acc = s_even +
+//        s_odd — the same order in the full-warp mapping (lane = probe, both chains in one lane)
+//        and the HALF mapping (c <= 16: each half-warp gathers every other nonzero, so one warp
+//        instruction fetches two rows' worth of probes).  Wide chunks (PPL >= 2) use one
+//        sequential chain (fewer registers, one more resident CTA per SM).  Results are bitwise
+//        independent of the chunk width within each class, like the step kernel's slot classes.
 // Columns are loaded 32 at a time; each lane turns its column into an element offset once and the
 // warp broadcasts offsets with one shuffle per nonzero.  Probe slots beyond c are clamped to a valid
 // column (loaded, never stored), so the loads need no predicates.
@@ -307,6 +309,9 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
                                              int64_t end, double* acc) {
   // EXACT runs only for the operator apply (probe scale r == 1: fl(x * 1) == x)
   constexpr unsigned FULL = 0xffffffffu;
+  // narrow chunks (PPL == 1, full-warp or HALF) sum a row as two chains (even / odd positions);
+  // wide chunks (PPL >= 2) as one sequential chain: each order is fixed within its class
+  constexpr bool TWO = PPL == 1;
   const int lane = threadIdx.x & 31;
   const int plane = HALF ? (lane & 15) : lane;   // probe lane
   const int sub = HALF ? (lane >> 4) : 0;        // HALF: chain (position parity) of this half
@@ -383,7 +388,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
           if (EXACT) a0[j] = __dadd_rn(a0[j], gather_term<KIND, WEIGHTED>(xv[q][j], 1.0, sk, wk));
-          else if (q & 1) a1[j] = SK ? fma(sk, xv[q][j], a1[j]) : a1[j] + xv[q][j];
+          else if (TWO && (q & 1)) a1[j] = SK ? fma(sk, xv[q][j], a1[j]) : a1[j] + xv[q][j];
           else a0[j] = SK ? fma(sk, xv[q][j], a0[j]) : a0[j] + xv[q][j];
         }
       }
@@ -406,7 +411,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         if (EXACT) a0[j] = __dadd_rn(a0[j], gather_term<KIND, WEIGHTED>(xr[j], 1.0, sk, wk));
-        else if (k & 1) a1[j] = SK ? fma(sk, xr[j], a1[j]) : a1[j] + xr[j];
+        else if (TWO && (k & 1)) a1[j] = SK ? fma(sk, xr[j], a1[j]) : a1[j] + xr[j];
         else a0[j] = SK ? fma(sk, xr[j], a0[j]) : a0[j] + xr[j];
       }
     }
@@ -415,7 +420,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
   for (int j = 0; j < PPL; ++j) {
     if (EXACT) acc[j] = a0[j];
     else if (HALF) acc[j] = a0[j] + __shfl_xor_sync(FULL, a0[j], 16);   // s_even + s_odd in both halves
-    else acc[j] = a0[j] + a1[j];
+    else acc[j] = TWO ? a0[j] + a1[j] : a0[j];
   }
 }
 
