@@ -97,6 +97,15 @@ void slq_graph_destroy(slq_graph* g);
  * draws slq_rmat_uniform_host(seed, j, l).  Synchronises `stream` (the unique-key count). */
 int slq_graph_create_rmat(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
                           void* stream, slq_graph** out);
+/* Canonical CSR built on the device from an edge list u[m], v[m] (int64) and optional weights w[m]
+ * (host or device pointers): self-loops dropped, both directions stored, duplicate edges collapsed
+ * to the maximum weight, rows and columns ascending — graphs.py:110-132 (`_build_csr`).  Endpoints
+ * outside [0, n) -> SLQ_ERR_VALUE.  Synchronises `stream` (the unique-edge count). */
+int slq_graph_create_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v, const double* w,
+                           void* stream, slq_graph** out);
+/* Stored edge weights [nnz] into `weights` (device or host; may be NULL); *has_weights_host = 0
+ * when the graph uses implicit unit weights (nothing is copied). */
+int slq_graph_weights(const slq_graph* g, double* weights, int32_t* has_weights_host, void* stream);
 /* Copy the prepared CSR (int64 offsets [n+1], int32 columns [nnz]) into caller buffers (device or
  * host; either may be NULL), stream-ordered. */
 int slq_graph_csr(const slq_graph* g, int64_t* offsets, int32_t* cols, void* stream);

@@ -164,7 +164,8 @@ static void* track(slq_graph* g, void* p) {
 // Either copies (offsets, int64 cols) or adopts device buffers the caller allocated with
 // cudaMallocAsync (adopt_off, adopt_cols: the graph frees them).
 static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols, const double* weights,
-                       cudaStream_t st, int64_t* adopt_off = nullptr, int32_t* adopt_cols = nullptr) {
+                       cudaStream_t st, int64_t* adopt_off = nullptr, int32_t* adopt_cols = nullptr,
+                       double* adopt_w = nullptr) {
   const int64_t n = g->n, nnz = g->nnz;
   void* p = nullptr;
   if (adopt_off) {
@@ -191,11 +192,15 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
     LaunchScope ls(K_PREPARE, st);
     narrow_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, const_cast<int32_t*>(g->cols), nnz, n, g->dflags);
   }
-  if (weights && nnz > 0) {
+  if ((weights || adopt_w) && nnz > 0) {
     // explicit weights are kept even if all are 1.0 (w * t == t exactly, so results are identical)
-    SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * nnz, st));
-    g->weights = static_cast<double*>(track(g, p));
-    SLQ_CUDA(cudaMemcpyAsync(const_cast<double*>(g->weights), weights, sizeof(double) * nnz, cudaMemcpyDefault, st));
+    if (adopt_w) {
+      g->weights = static_cast<double*>(track(g, adopt_w));
+    } else {
+      SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * nnz, st));
+      g->weights = static_cast<double*>(track(g, p));
+      SLQ_CUDA(cudaMemcpyAsync(const_cast<double*>(g->weights), weights, sizeof(double) * nnz, cudaMemcpyDefault, st));
+    }
     LaunchScope ls(K_PREPARE, st);
     unit_weight_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(g->weights, nnz, g->dflags + 1);
   }
@@ -270,8 +275,12 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   return SLQ_OK;
 }
 
-int graph_adopt(slq_graph* g, int64_t* offsets, int32_t* cols, cudaStream_t st) {
-  return graph_build(g, nullptr, nullptr, nullptr, st, offsets, cols);
+int graph_adopt(slq_graph* g, int64_t* offsets, int32_t* cols, cudaStream_t st, double* weights) {
+  if (weights && g->nnz == 0) {
+    cudaFreeAsync(weights, st);
+    weights = nullptr;
+  }
+  return graph_build(g, nullptr, nullptr, nullptr, st, offsets, cols, weights);
 }
 
 // Host mirror of the device scalars (synchronises the creation stream once).
@@ -388,6 +397,15 @@ extern "C" int slq_graph_csr(const slq_graph* g, int64_t* offsets, int32_t* cols
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (offsets) SLQ_CUDA(cudaMemcpyAsync(offsets, g->offsets, sizeof(int64_t) * (g->n + 1), cudaMemcpyDefault, st));
   if (cols && g->nnz > 0) SLQ_CUDA(cudaMemcpyAsync(cols, g->cols, sizeof(int32_t) * g->nnz, cudaMemcpyDefault, st));
+  return SLQ_OK;
+}
+
+extern "C" int slq_graph_weights(const slq_graph* g, double* weights, int32_t* has_weights_host, void* stream) {
+  if (!g || !has_weights_host) return fail(SLQ_ERR_VALUE, "NULL argument");
+  *has_weights_host = g->weights ? 1 : 0;
+  if (g->weights && weights && g->nnz > 0)
+    SLQ_CUDA(cudaMemcpyAsync(weights, g->weights, sizeof(double) * g->nnz, cudaMemcpyDefault,
+                             static_cast<cudaStream_t>(stream)));
   return SLQ_OK;
 }
 

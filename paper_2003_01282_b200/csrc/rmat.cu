@@ -9,13 +9,14 @@
 // int64 offsets and int32 columns only.  synth.rmat_device_reference() restates the same RNG on the
 // host so small scales can be checked edge for edge.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_select.cuh>
 
 #include "slq_common.cuh"
 
 namespace slq {
 
-int graph_adopt(slq_graph* g, int64_t* offsets, int32_t* cols, cudaStream_t st);   // graph.cu
+int graph_adopt(slq_graph* g, int64_t* offsets, int32_t* cols, cudaStream_t st, double* weights = nullptr);   // graph.cu
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -49,20 +50,18 @@ __global__ void rmat_keys_kernel(uint64_t seed, int scale, int64_t samples, doub
   }
 }
 
-__global__ void keys_to_cols_kernel(const uint64_t* __restrict__ keys, int64_t nnz, int scale,
+__global__ void keys_to_cols_kernel(const uint64_t* __restrict__ keys, int64_t nnz, int64_t n,
                                     int32_t* __restrict__ cols) {
-  const uint64_t mask = (1ull << scale) - 1;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    cols[i] = static_cast<int32_t>(keys[i] & mask);
+    cols[i] = static_cast<int32_t>(keys[i] % static_cast<uint64_t>(n));
 }
 
 // offsets[r] = first key >= r*n (lower bound), r in [0, n]
-__global__ void offsets_kernel(const uint64_t* __restrict__ keys, int64_t nnz, int scale, int64_t* __restrict__ off) {
-  const int64_t n = 1ll << scale;
+__global__ void offsets_kernel(const uint64_t* __restrict__ keys, int64_t nnz, int64_t n, int64_t* __restrict__ off) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r <= n;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t target = static_cast<uint64_t>(r) << scale;
+    const uint64_t target = static_cast<uint64_t>(r) * static_cast<uint64_t>(n);
     int64_t lo = 0, hi = nnz;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
@@ -126,11 +125,11 @@ extern "C" int slq_graph_create_rmat(int scale, int edge_factor, double a, doubl
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cols), sizeof(int32_t) * std::max<int64_t>(nnz, 1), st));
   {
     LaunchScope ls(K_PREPARE, st);
-    keys_to_cols_kernel<<<148 * 32, 256, 0, st>>>(k0, nnz, scale, cols);
+    keys_to_cols_kernel<<<148 * 32, 256, 0, st>>>(k0, nnz, n, cols);
   }
   {
     LaunchScope ls(K_PREPARE, st);
-    offsets_kernel<<<148 * 32, 256, 0, st>>>(k0, nnz, scale, off);
+    offsets_kernel<<<148 * 32, 256, 0, st>>>(k0, nnz, n, off);
   }
   SLQ_CUDA(cudaFreeAsync(k0, st));
   slq_graph* g = new slq_graph();
@@ -140,6 +139,156 @@ extern "C" int slq_graph_create_rmat(int scale, int edge_factor, double a, doubl
   cudaGetDevice(&g->device);
   ensure_pool(g->device);
   const int rc = graph_adopt(g, off, cols, st);
+  if (rc != SLQ_OK) {
+    slq_graph_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return SLQ_OK;
+}
+
+namespace slq {
+
+// directed keys of an edge list: both directions, self-loops and out-of-range endpoints become the
+// sentinel (out of range also sets *bad); weights duplicated to both directions
+__global__ void edge_keys_kernel(const int64_t* __restrict__ u, const int64_t* __restrict__ v,
+                                 const double* __restrict__ w, int64_t m, int64_t n, uint64_t* __restrict__ keys,
+                                 double* __restrict__ wout, int* __restrict__ bad) {
+  const uint64_t sentinel = ~0ull;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = u[e], b = v[e];
+    const bool range = a >= 0 && a < n && b >= 0 && b < n;
+    if (!range) atomicOr(bad, 1);
+    const bool keep = range && a != b;
+    keys[2 * e] = keep ? static_cast<uint64_t>(a) * static_cast<uint64_t>(n) + static_cast<uint64_t>(b) : sentinel;
+    keys[2 * e + 1] = keep ? static_cast<uint64_t>(b) * static_cast<uint64_t>(n) + static_cast<uint64_t>(a) : sentinel;
+    if (wout) {
+      const double x = w[e];
+      wout[2 * e] = x;
+      wout[2 * e + 1] = x;
+    }
+  }
+}
+
+struct MaxWeight {
+  __device__ __forceinline__ double operator()(double a, double b) const { return a > b ? a : b; }
+};
+
+}  // namespace slq
+
+// Edge list (u[m], v[m], optional w[m]; host or device pointers) -> canonical CSR on the device,
+// the semantics of graphs.csr_from_edges (graphs.py:110-132): self-loops dropped, both directions
+// stored, duplicates collapsed to the maximum weight, rows and columns ascending.
+extern "C" int slq_graph_create_edges(int64_t n, int64_t m, const int64_t* u, const int64_t* v, const double* w,
+                                      void* stream, slq_graph** out) {
+  if (!out) return fail(SLQ_ERR_VALUE, "out must not be NULL");
+  *out = nullptr;
+  if (n < 0 || m < 0) return fail(SLQ_ERR_VALUE, "negative n or m");
+  if (n >= (int64_t(1) << 31)) return fail(SLQ_ERR_VALUE, "n >= 2^31 is not supported (int32 columns)");
+  if (m > 0 && (!u || !v)) return fail(SLQ_ERR_VALUE, "NULL edge array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nkeys = 2 * m;
+  int64_t *du = nullptr, *dv = nullptr, *d_count = nullptr;
+  double* dw = nullptr;
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  double *w0 = nullptr, *w1 = nullptr;
+  int* bad = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), 16, st));   // [0] bad flag, [8] unique count
+  d_count = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(bad) + 8);
+  SLQ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  int64_t nuniq = 0;
+  if (m > 0) {
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&du), sizeof(int64_t) * m, st));
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dv), sizeof(int64_t) * m, st));
+    SLQ_CUDA(cudaMemcpyAsync(du, u, sizeof(int64_t) * m, cudaMemcpyDefault, st));
+    SLQ_CUDA(cudaMemcpyAsync(dv, v, sizeof(int64_t) * m, cudaMemcpyDefault, st));
+    if (w) {
+      SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dw), sizeof(double) * m, st));
+      SLQ_CUDA(cudaMemcpyAsync(dw, w, sizeof(double) * m, cudaMemcpyDefault, st));
+      SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w0), sizeof(double) * nkeys, st));
+      SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w1), sizeof(double) * nkeys, st));
+    }
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&k0), sizeof(uint64_t) * nkeys, st));
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&k1), sizeof(uint64_t) * nkeys, st));
+    {
+      LaunchScope ls(K_PREPARE, st);
+      edge_keys_kernel<<<148 * 32, 256, 0, st>>>(du, dv, dw, m, n, k0, w0, bad);
+    }
+    SLQ_CUDA(cudaFreeAsync(du, st));
+    SLQ_CUDA(cudaFreeAsync(dv, st));
+    if (dw) SLQ_CUDA(cudaFreeAsync(dw, st));
+    size_t tb_sort = 0, tb_red = 0;
+    void* tmp = nullptr;
+    if (!w) {
+      cub::DoubleBuffer<uint64_t> db(k0, k1);
+      SLQ_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb_sort, db, nkeys, 0, 64, st));
+      SLQ_CUDA(cub::DeviceSelect::Unique(nullptr, tb_red, k0, k1, d_count, nkeys, st));
+      SLQ_CUDA(cudaMallocAsync(&tmp, std::max(tb_sort, tb_red) + 256, st));
+      SLQ_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb_sort, db, nkeys, 0, 64, st));
+      uint64_t* sorted = db.Current();
+      uint64_t* uniq = db.Alternate();
+      SLQ_CUDA(cub::DeviceSelect::Unique(tmp, tb_red, sorted, uniq, d_count, nkeys, st));
+      k0 = uniq;
+      k1 = sorted;
+    } else {
+      // stable key sort carrying the weights, then max over equal keys
+      cub::DoubleBuffer<uint64_t> db(k0, k1);
+      cub::DoubleBuffer<double> dbw(w0, w1);
+      SLQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, db, dbw, nkeys, 0, 64, st));
+      SLQ_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, tb_red, k0, k1, w0, w1, d_count, MaxWeight(), nkeys, st));
+      SLQ_CUDA(cudaMallocAsync(&tmp, std::max(tb_sort, tb_red) + 256, st));
+      SLQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_sort, db, dbw, nkeys, 0, 64, st));
+      uint64_t* ks = db.Current();
+      double* ws = dbw.Current();
+      uint64_t* ku = db.Alternate();
+      double* wu = dbw.Alternate();
+      SLQ_CUDA(cub::DeviceReduce::ReduceByKey(tmp, tb_red, ks, ku, ws, wu, d_count, MaxWeight(), nkeys, st));
+      k0 = ku;
+      k1 = ks;
+      w0 = wu;
+      w1 = ws;
+    }
+    SLQ_CUDA(cudaFreeAsync(tmp, st));
+    SLQ_CUDA(cudaFreeAsync(k1, st));
+    if (w1) SLQ_CUDA(cudaFreeAsync(w1, st));
+  }
+  int hbad = 0;
+  SLQ_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (m > 0) SLQ_CUDA(cudaMemcpyAsync(&nuniq, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  SLQ_CUDA(cudaFreeAsync(bad, st));
+  if (hbad) {
+    if (k0) cudaFreeAsync(k0, st);
+    if (w0) cudaFreeAsync(w0, st);
+    return fail(SLQ_ERR_VALUE, "edge endpoint out of range");
+  }
+  uint64_t last = 0;
+  if (nuniq > 0) {
+    SLQ_CUDA(cudaMemcpyAsync(&last, k0 + nuniq - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SLQ_CUDA(cudaStreamSynchronize(st));
+  }
+  const int64_t nnz = (nuniq > 0 && last == ~0ull) ? nuniq - 1 : nuniq;
+  int64_t* off = nullptr;
+  int32_t* cols = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&off), sizeof(int64_t) * (n + 1), st));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cols), sizeof(int32_t) * std::max<int64_t>(nnz, 1), st));
+  if (nnz > 0) {
+    LaunchScope ls(K_PREPARE, st);
+    keys_to_cols_kernel<<<148 * 32, 256, 0, st>>>(k0, nnz, n, cols);
+  }
+  {
+    LaunchScope ls(K_PREPARE, st);
+    offsets_kernel<<<148 * 32, 256, 0, st>>>(k0, nnz, n, off);
+  }
+  if (k0) SLQ_CUDA(cudaFreeAsync(k0, st));
+  slq_graph* g = new slq_graph();
+  g->n = n;
+  g->nnz = nnz;
+  g->stream = stream;
+  cudaGetDevice(&g->device);
+  ensure_pool(g->device);
+  const int rc = graph_adopt(g, off, cols, st, w0);   // w0: max weights aligned with the unique keys
   if (rc != SLQ_OK) {
     slq_graph_destroy(g);
     return rc;

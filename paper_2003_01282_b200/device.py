@@ -65,6 +65,48 @@ class DeviceGraph:
         self.nnz = int(self.info.nnz)
         return self
 
+    @classmethod
+    def from_edges(cls, n: int, u, v, w=None, device=None) -> "DeviceGraph":
+        """Canonical CSR built on the device from an edge list (numpy arrays or torch tensors, host
+        or device): the semantics of ``graphs.csr_from_edges`` (self-loops dropped, both directions,
+        duplicates collapse to the maximum weight, sorted).  ``graph`` is None."""
+        torch = _lib.require_cuda()
+        self = cls.__new__(cls)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.graph = None
+        self.handle = ctypes.c_void_p()
+
+        def arr(x, dt):
+            if isinstance(x, torch.Tensor):
+                return x.to(dt).contiguous()
+            return torch.as_tensor(np.ascontiguousarray(x), dtype=dt)
+
+        ut, vt = arr(u, torch.int64), arr(v, torch.int64)
+        wt = None if w is None else arr(w, torch.float64)
+        if ut.numel() != vt.numel() or (wt is not None and wt.numel() != ut.numel()):
+            raise ValueError("u, v (and w) must have the same length")
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_create_edges(int(n), int(ut.numel()), _lib.ptr(ut), _lib.ptr(vt),
+                                                          _lib.ptr(wt), _lib.stream_handle(self.device),
+                                                          ctypes.byref(self.handle)))
+        self._info = None
+        self.n = int(self.info.n)
+        self.nnz = int(self.info.nnz)
+        return self
+
+    def weights(self):
+        """Stored edge weights [nnz] (float64) copied from the device, or None for implicit 1.0."""
+        import torch
+
+        if not self.nnz:
+            return None
+        w = torch.empty(self.nnz, dtype=torch.float64, device=self.device)
+        has = ctypes.c_int32()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_weights(self.handle, _lib.ptr(w), ctypes.byref(has),
+                                                      _lib.stream_handle(self.device)))
+        return w.cpu().numpy() if has.value else None
+
     def csr(self):
         """(row_offsets int64 [n+1], col_indices int32 [nnz]) copied from the device (small graphs)."""
         import torch

@@ -453,3 +453,37 @@ def test_device_rmat_descriptors_match_oracle(cuda_device):
     v, _ = p.integrate(None, [_lib.FN_XLOGX])
     ref_v, _ = O.vnge(g, 8, 15, 0)
     assert abs(-float(v.cpu().numpy()[0, 0]) - ref_v) <= FP64_TOL * abs(ref_v)
+
+
+# device edge list -> canonical CSR (graphs.py:110-132 semantics) vs the host builder
+@pytest.mark.parametrize("n,m,weighted,seed", [(50, 400, False, 0), (50, 400, True, 1), (1000, 20000, True, 2),
+                                               (7, 0, False, 3), (3000, 5, False, 4)])
+def test_device_edge_list_builder_matches_host(cuda_device, n, m, weighted, seed):
+    rng = np.random.default_rng(seed)
+    u = rng.integers(0, n, m)
+    v = rng.integers(0, n, m)
+    u[: m // 10] = v[: m // 10]                       # self-loops
+    if m > 20:
+        u[-5:], v[-5:] = v[:5], u[:5]                 # reversed duplicates
+    w = rng.choice([0.5, 1.0, 2.0, 3.5], size=m) if weighted else None
+    ref = csr_from_edges(n, u, v, w)
+    dg = DeviceGraph.from_edges(n, u, v, w, device=cuda_device)
+    off, cols = dg.csr()
+    assert dg.n == ref.n and dg.nnz == ref.nnz
+    assert np.array_equal(off, ref.row_offsets)
+    assert np.array_equal(cols.astype(np.int64), ref.col_indices)
+    got_w = dg.weights()
+    if weighted:
+        assert np.array_equal(got_w, ref.weights)
+    else:
+        assert got_w is None
+    if ref.nnz:
+        host = DeviceGraph(ref, cuda_device)
+        a1, _, s1 = dg.tridiagonals("normalized_laplacian", 0, 0, 8, 10)
+        a2, _, s2 = host.tridiagonals("normalized_laplacian", 0, 0, 8, 10)
+        assert torch.equal(a1, a2) and torch.equal(s1, s2)
+
+
+def test_device_edge_list_builder_rejects_out_of_range(cuda_device):
+    with pytest.raises(ValueError, match="out of range"):
+        DeviceGraph.from_edges(5, np.array([0, 1]), np.array([1, 5]), device=cuda_device)
