@@ -111,15 +111,50 @@ def slq_rules(op, cfg: SlqConfig, *, dtype: str = "f64", reorth: bool | None = N
 
     ``shard=True`` splits the probes over the ranks of the initialised
     torch.distributed group and all-gathers the rules (dist.py)."""
-    if cfg.distribution != "rademacher":
-        raise NotImplementedError("gaussian probes (numpy ziggurat, slq.py:66) are not on the device path")
     dg = _graph_of(op)
     code = -1 if reorth is None else int(bool(reorth))
+    if cfg.distribution == "gaussian":
+        if shard:
+            raise NotImplementedError("sharded Gaussian probes: shard Rademacher probes or run one rank")
+        return _gaussian_rules(dg, op, cfg, code, dtype)
     if shard:
         from .dist import sharded_rules
 
         return sharded_rules(dg, op.kind.value, cfg, dtype=dtype, reorth=code)
     return dg.rules(op.kind.value, cfg.seed, 0, cfg.n_v, cfg.s, reorth=code, dtype=dtype)
+
+
+_GAUSS_BLOCK = 64   # probes per uploaded start block
+
+
+def gaussian_start_block(n: int, seed: int, begin: int, count: int) -> np.ndarray:
+    """Unit Gaussian start vectors [n, count] of probes begin..begin+count-1, drawn exactly as the
+    reference (slq.py:63-73: ``default_rng(SeedSequence(seed, spawn_key=(i,))).standard_normal(n)``
+    normalised by ``np.linalg.norm``).  numpy's ziggurat runs on the host; the Lanczos recurrence,
+    rules and quadrature stay on the device (the start block is uploaded once per 64 probes)."""
+    out = np.empty((n, count))
+    for c in range(count):
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(begin + c,)))
+        v = rng.standard_normal(n)
+        out[:, c] = v / np.linalg.norm(v)
+    return out
+
+
+def _gaussian_rules(dg, op, cfg: SlqConfig, reorth: int, dtype: str) -> DeviceRules:
+    import torch
+
+    from .device import gauss_rules
+
+    s = min(cfg.s, dg.n)
+    alphas, betas, steps = [], [], []
+    for b in range(0, cfg.n_v, _GAUSS_BLOCK):
+        c = min(_GAUSS_BLOCK, cfg.n_v - b)
+        q0 = torch.as_tensor(gaussian_start_block(dg.n, cfg.seed, b, c), device=dg.device)
+        a, bt, st = dg.tridiagonals(op.kind.value, 0, 0, c, s, reorth=reorth, dtype=dtype, start=q0)
+        alphas.append(a)
+        betas.append(bt)
+        steps.append(st)
+    return gauss_rules(torch.cat(alphas), torch.cat(betas), torch.cat(steps), op.interval, dg.n)
 
 
 def _estimate_host(per_vector: np.ndarray, n: int) -> SlqEstimate:

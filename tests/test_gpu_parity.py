@@ -487,3 +487,25 @@ def test_device_edge_list_builder_matches_host(cuda_device, n, m, weighted, seed
 def test_device_edge_list_builder_rejects_out_of_range(cuda_device):
     with pytest.raises(ValueError, match="out of range"):
         DeviceGraph.from_edges(5, np.array([0, 1]), np.array([1, 5]), device=cuda_device)
+
+
+# Gaussian probes (slq.py:63-73): drawn on the host with numpy's ziggurat, Lanczos on the device
+@pytest.mark.parametrize("fname", ["c1_ba1000.npz", "rmat12.npz"])
+def test_gaussian_probes_match_oracle(cuda_device, fname):
+    g = golden.graph(golden.load(fname))
+    cfg = SlqConfig(n_v=70, s=10, seed=5, distribution="gaussian")   # 2 start blocks (64 + 6)
+    q0 = np.empty((g.n, cfg.n_v))
+    for i in range(cfg.n_v):   # restated from the reference's _draw_probe / _probe_rule
+        v = np.random.default_rng(np.random.SeedSequence(entropy=cfg.seed, spawn_key=(i,))).standard_normal(g.n)
+        q0[:, i] = v / np.linalg.norm(v)
+    for kind, okind in (("heat", O.NORMALIZED_LAPLACIAN), ("vnge", O.DENSITY)):
+        op = O.make_block_operator(g, okind)
+        ref_rules = O.gauss_rules(O.lanczos_block(op, q0, cfg.s), op.interval)
+        if kind == "heat":
+            ref, _ = O.heat_from_rules(ref_rules, g.n, np.array(GRID.values))
+            got = netlsd_slq(g, GRID, cfg).values
+            assert golden.rel_l2(got, ref) <= FP64_TOL
+        else:
+            ref, _ = O.vnge_from_rules(ref_rules, g.n)
+            got = vnge_slq(g, cfg).value
+            assert abs(got - ref) <= FP64_TOL * abs(ref)
