@@ -387,6 +387,13 @@ def test_long_rows_split_into_segments(cuda_device):
     v = vnge_slq(g, cfg)
     rv, _ = O.vnge(g, 24, 15, 2)
     assert abs(v.value - rv) <= FP64_TOL * abs(rv)
+    # long rows under every SpMM mapping: half-warp (<= 16 probes), full warp, 2/4 probes per lane
+    for n_v, dtype, tol in ((12, "f64", FP64_TOL), (12, "f32", FP32_TOL), (70, "f64", FP64_TOL),
+                            (100, "f32", FP32_TOL)):
+        c = SlqConfig(n_v=n_v, s=15, seed=2)
+        h = netlsd_slq(g, GRID, c, dtype=dtype)
+        ref, _ = O.heat_trace(g, GRID.values, n_v, 15, 2)
+        assert golden.rel_l2(h.values, ref) <= tol, (n_v, dtype)
 
 
 # batched block-diagonal path (C3)
