@@ -116,6 +116,10 @@ int slq_rmat_uniform_host(uint64_t seed, uint64_t sample, int level, double* out
  * device buffers (either may be NULL).  operators.py:58-62, 84-86. */
 int slq_graph_degrees(const slq_graph* g, double* degree, double* dinv, void* stream);
 
+/* Exact trace of the squared operator from one edge pass (operators.py:119-141; the control-variate
+ * companion of the degree identity tr M = slq_graph_info): writes the host double *out_host. */
+int slq_trace_squared(const slq_graph* g, int kind, double* out_host);
+
 /* Spectrum bounds used for node clamping (operators.py:79,90,101). */
 int slq_operator_interval(const slq_graph* g, int kind, double* lo, double* hi);
 

@@ -14,7 +14,7 @@ __version__ = "0.1.0"
 _LAZY = {
     # operators.py mirror
     "OperatorKind": "operators", "LinearOperator": "operators", "make_operator": "operators",
-    "degrees": "operators",
+    "degrees": "operators", "trace": "operators", "trace_squared": "operators",
     # lanczos.py mirror
     "Tridiagonal": "lanczos", "QuadratureRule": "lanczos", "quadrature_rule": "lanczos",
     "lanczos_tridiagonalize": "lanczos",
@@ -29,7 +29,7 @@ _LAZY = {
     "relative_error": "descriptors", "descriptor_distance": "descriptors",
     "descriptor_to_json": "descriptors", "descriptor_from_json": "descriptors",
     # batched small graphs
-    "netlsd_slq_batch": "batched",
+    "netlsd_slq_batch": "batched", "vnge_slq_batch": "batched", "BatchedGraphs": "batched",
 }
 
 

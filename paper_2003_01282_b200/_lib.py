@@ -45,6 +45,7 @@ _SIGS = {
     "slq_graph_csr": (_int, [_vp, _vp, _vp, _vp]),
     "slq_graph_create_edges": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "slq_graph_weights": (_int, [_vp, _vp, ctypes.POINTER(_i32), _vp]),
+    "slq_trace_squared": (_int, [_vp, _int, ctypes.POINTER(_dbl)]),
     "slq_graph_info": (_int, [_vp, ctypes.POINTER(GraphInfo)]),
     "slq_graph_destroy": (None, [_vp]),
     "slq_graph_degrees": (_int, [_vp, _vp, _vp]),

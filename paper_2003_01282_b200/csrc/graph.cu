@@ -400,6 +400,86 @@ extern "C" int slq_graph_csr(const slq_graph* g, int64_t* offsets, int32_t* cols
   return SLQ_OK;
 }
 
+namespace slq {
+
+// Partial sums of the squared-operator trace identities (operators.py:119-141) in a fixed order:
+// thread t of block b owns rows [lo, hi) of a fixed partition; per row the stored entries in order.
+//   s[0] = sum_r d_r^2, s[1] = sum_e w_e^2, s[2] = sum_e w_e^2 / (d_r d_c)
+constexpr int kTrBlocks = 148 * 4, kTrThreads = 256;
+__global__ void __launch_bounds__(kTrThreads) trace_sq_kernel(const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ cols,
+                                                              const double* __restrict__ w,
+                                                              const double* __restrict__ deg, int64_t n,
+                                                              double* __restrict__ part) {
+  __shared__ double red[3][kTrThreads];
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * kTrThreads + threadIdx.x;
+  const int64_t T = static_cast<int64_t>(kTrBlocks) * kTrThreads;
+  const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t r = lo; r < hi; ++r) {
+    const double dr = deg[r];
+    s0 = fma(dr, dr, s0);
+    for (int64_t e = off[r]; e < off[r + 1]; ++e) {
+      const double we = w ? w[e] : 1.0;
+      const double w2 = we * we;
+      s1 += w2;
+      s2 += w2 / (dr * deg[cols[e]]);
+    }
+  }
+  red[0][threadIdx.x] = s0;
+  red[1][threadIdx.x] = s1;
+  red[2][threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double acc = 0.0;
+    for (int i = 0; i < kTrThreads; ++i) acc += red[threadIdx.x][i];
+    part[blockIdx.x * 3 + threadIdx.x] = acc;
+  }
+}
+
+__global__ void trace_sq_final(const double* __restrict__ part, double* __restrict__ out) {
+  if (threadIdx.x < 3) {
+    double acc = 0.0;
+    for (int b = 0; b < kTrBlocks; ++b) acc += part[b * 3 + threadIdx.x];
+    out[threadIdx.x] = acc;
+  }
+}
+
+}  // namespace slq
+
+// Exact trace of the squared operator (operators.py:119-141): L: sum d^2 + sum w^2; normalized
+// Laplacian: #non-isolated + sum_e w^2 / (d_r d_c); density: tr(L^2) / tr(L)^2.  Synchronises.
+extern "C" int slq_trace_squared(const slq_graph* g, int kind, double* out_host) {
+  if (!g || !out_host) return fail(SLQ_ERR_VALUE, "NULL argument");
+  int rc = fetch_host_scalars(const_cast<slq_graph*>(g));
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(g->stream);
+  double* part = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * (3 * kTrBlocks + 3), st));
+  {
+    LaunchScope ls(K_PREPARE, st);
+    trace_sq_kernel<<<kTrBlocks, kTrThreads, 0, st>>>(g->offsets, g->cols, g->weights, g->degree, g->n, part);
+    trace_sq_final<<<1, 32, 0, st>>>(part, part + 3 * kTrBlocks);
+  }
+  double s[3];
+  SLQ_CUDA(cudaMemcpyAsync(s, part + 3 * kTrBlocks, sizeof(s), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  SLQ_CUDA(cudaFreeAsync(part, st));
+  const double trl = g->trace_l;
+  switch (kind) {
+    case SLQ_LAPLACIAN: *out_host = s[0] + s[1]; break;
+    case SLQ_NORMALIZED_LAPLACIAN:
+      *out_host = static_cast<double>(g->n - g->isolated) + (g->nnz > 0 ? s[2] : 0.0);
+      break;
+    case SLQ_DENSITY:
+      if (g->nnz == 0 || trl <= 0.0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
+      *out_host = (s[0] + s[1]) / (trl * trl);
+      break;
+    default: return fail(SLQ_ERR_VALUE, "unknown operator kind");
+  }
+  return SLQ_OK;
+}
+
 extern "C" int slq_graph_weights(const slq_graph* g, double* weights, int32_t* has_weights_host, void* stream) {
   if (!g || !has_weights_host) return fail(SLQ_ERR_VALUE, "NULL argument");
   *has_weights_host = g->weights ? 1 : 0;

@@ -16,10 +16,13 @@ from typing import Callable
 
 import numpy as np
 
+from . import _lib
 from .device import DeviceGraph, device_graph
 from .graphs import Graph
 
-__all__ = ["OperatorKind", "LinearOperator", "degrees", "make_operator", "trace"]
+__all__ = ["OperatorKind", "LinearOperator", "degrees", "make_operator", "trace", "trace_squared"]
+
+_KIND_CODE = {"laplacian": _lib.LAPLACIAN, "normalized_laplacian": _lib.NORMALIZED_LAPLACIAN, "density": _lib.DENSITY}
 
 
 class OperatorKind(Enum):
@@ -73,3 +76,17 @@ def trace(g: Graph, kind: OperatorKind) -> float:
     if g.m == 0:
         raise ValueError("density matrix undefined for a graph without edges")
     return 1.0
+
+
+def trace_squared(g: Graph, kind: OperatorKind) -> float:
+    """Exact tr(M^2) in one edge pass on the device (operators.py:119-141): L: sum d^2 + sum w^2;
+    normalized Laplacian: #non-isolated + sum_e w^2 / (d_r d_c); density: tr(L^2) / tr(L)^2.
+    Fixed-order device sums (the reference uses numpy's pairwise sum): equal to rounding."""
+    import ctypes
+
+    kind = OperatorKind(kind)
+    if kind is OperatorKind.DENSITY and g.m == 0:
+        raise ValueError("density matrix undefined for a graph without edges")
+    out = ctypes.c_double()
+    _lib.check(_lib.load().slq_trace_squared(device_graph(g).handle, _KIND_CODE[kind.value], ctypes.byref(out)))
+    return float(out.value)

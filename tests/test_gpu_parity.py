@@ -516,3 +516,27 @@ def test_gaussian_probes_match_oracle(cuda_device, fname):
             ref, _ = O.vnge_from_rules(ref_rules, g.n)
             got = vnge_slq(g, cfg).value
             assert abs(got - ref) <= FP64_TOL * abs(ref)
+
+
+# trace identities (operators.py:105-141): tr M from degrees, tr M^2 from one edge pass
+@pytest.mark.parametrize("fname", ["c1_ba1000.npz", "rmat12.npz"])
+def test_trace_identities_match_reference_definitions(cuda_device, fname):
+    from paper_2003_01282_b200.operators import OperatorKind, trace, trace_squared
+
+    g = golden.graph(golden.load(fname))
+    deg = O.degrees(g)
+    w = np.asarray(g.weights, dtype=np.float64)
+    src = np.repeat(np.arange(g.n), np.diff(g.row_offsets))
+    ref_l2 = float(np.sum(deg * deg) + np.sum(w * w))
+    ref_nl2 = float(np.count_nonzero(deg > 0)) + float(np.sum(w * w / (deg[src] * deg[g.col_indices])))
+    trl = float(deg.sum())
+    assert trace(g, OperatorKind.LAPLACIAN) == trl
+    assert trace(g, OperatorKind.NORMALIZED_LAPLACIAN) == float(np.count_nonzero(deg > 0))
+    assert abs(trace_squared(g, OperatorKind.LAPLACIAN) - ref_l2) <= 1e-13 * ref_l2
+    assert abs(trace_squared(g, OperatorKind.NORMALIZED_LAPLACIAN) - ref_nl2) <= 1e-13 * ref_nl2
+    assert abs(trace_squared(g, OperatorKind.DENSITY) - ref_l2 / trl ** 2) <= 1e-13 * ref_l2 / trl ** 2
+    # dense check of the identity on the oracle operator
+    n = g.n
+    if n <= 1500:
+        L = O.make_block_operator(g, O.NORMALIZED_LAPLACIAN).apply(np.eye(n))
+        assert abs(np.sum(L * L) - ref_nl2) <= 1e-10 * ref_nl2
