@@ -9,6 +9,11 @@ so correctness is checked through size-independent properties:
   * a probe prefix of the full run is bitwise the rules of the prefix run (chunk independence).
 
     python tools/run_c5.py [--scale 27] [--probes 128] [--reps 1] [--check]
+    torchrun --nproc-per-node 8 --master-addr 127.0.0.1 tools/run_c5.py   # probes sharded over GPUs
+
+Under torchrun every rank builds the same graph on its GPU, runs its contiguous probe range and
+the rules are all-gathered (dist.sharded_rules); times are the max over ranks.  C5_DIST_BACKEND=gloo
+lets several ranks share one GPU for testing at small scales.
 """
 import argparse
 import json
@@ -24,6 +29,8 @@ import torch
 from paper_2003_01282_b200 import _lib
 from paper_2003_01282_b200.descriptors import TimeGrid
 from paper_2003_01282_b200.device import DeviceGraph, device_probes
+from paper_2003_01282_b200.dist import sharded_rules
+from paper_2003_01282_b200.slq import SlqConfig
 
 
 def timed(fn):
@@ -46,11 +53,30 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--profile", action="store_true", help="per-kernel-class device time of one more NL run")
     args = ap.parse_args()
-    dev = torch.device("cuda", 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group(os.environ.get("C5_DIST_BACKEND", "nccl"))
+    cfg_all = SlqConfig(n_v=args.probes, s=args.steps, seed=0)
+
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     t0 = time.perf_counter()
     dg, gen_ms = timed(lambda: DeviceGraph.rmat(args.scale, 16, 0.57, 0.19, 0.19, seed=0, device=dev))
     out = {"config": "c5", "scale": args.scale, "n": dg.n, "nnz": dg.nnz, "gen_wall_s": time.perf_counter() - t0,
-           "gen_ms": gen_ms, "probes": args.probes, "steps": args.steps, "dtype": args.dtype}
+           "gen_ms": gen_ms, "probes": args.probes, "steps": args.steps, "dtype": args.dtype, "n_gpus": world}
     tgrid = torch.tensor(np.array(TimeGrid(1e-2, 1e2, 250).values), device=dev)
     units = dg.nnz * args.probes * args.steps
     total_ms = 0.0
@@ -60,12 +86,19 @@ def main():
         times = []
         for _ in range(args.reps):
             def run():
-                r = dg.rules(kind, 0, 0, args.probes, args.steps, dtype=args.dtype)
+                if world > 1:
+                    r = sharded_rules(dg, kind, cfg_all, dtype=args.dtype)
+                else:
+                    r = dg.rules(kind, 0, 0, args.probes, args.steps, dtype=args.dtype)
                 v, s = r.integrate(tgrid if kind == "normalized_laplacian" else None, fns)
                 return r, v, s
+            if world > 1:
+                import torch.distributed as dist
+
+                dist.barrier()
             (rules, vals, stds), ms = timed(run)
             rules.check()
-            times.append(ms)
+            times.append(max_over_ranks(ms))
         keep[kind] = (rules, vals)
         ms = float(min(times))
         total_ms += ms
@@ -74,6 +107,14 @@ def main():
     out["signature_s"] = total_ms * 1e-3
     out["units_per_s_all"] = 2 * units / (total_ms * 1e-3)
     out["vnge"] = -float(keep["density"][1][0, 0])
+    if world > 1:
+        import torch.distributed as dist
+
+        if rank == 0:
+            print(json.dumps(out))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if args.profile:
         _lib.profile_begin()
         r = dg.rules("normalized_laplacian", 0, 0, args.probes, args.steps, dtype=args.dtype)
