@@ -9,7 +9,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-#include <cooperative_groups.h>
 #include <type_traits>
 #include "bulk_pipe.cuh"
 #include "pcg64.cuh"
@@ -18,7 +17,6 @@
 namespace slq {
 
 
-namespace cg = cooperative_groups;
 
 constexpr int kProbeRun = 32;        // 64-bit PCG outputs per thread in probe_init (64 rows)
 constexpr int kSecondPassGrid = 148 * 4;
@@ -249,7 +247,7 @@ struct SpmmArgs {
   void* w;                 // [n][ldc] output
   int64_t ldc_in, ldc_out;
   int c, cpad;
-  ReduceArgs red;          // cooperative launches: alpha reduced in-kernel after a grid barrier
+  ReduceArgs red;          // operator kind / scalars for the step kernel's long-row finish
   // long rows (graph.cu): device counts, segment table, per-segment partial sums [max_seg][cpad]
   const int64_t* long_counts;
   const int32_t* long_rows;
@@ -557,9 +555,7 @@ static int ppl_for(int c) {
 }
 
 template <typename VT, int KIND, bool W, int PPL>
-static void spmm_launch_one(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
-  (void)coop;
-  (void)dev;
+static void spmm_launch_one(SpmmArgs& a, int gy, cudaStream_t st) {
   // persistent: work is taken from the atomic counters; small graphs launch only the warps they can use
   const int64_t items = static_cast<int64_t>(a.ntiles) + (a.long_counts ? a.max_seg : 0);
   dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(148 * 4, (items + kSpmmWarps - 1) / kSpmmWarps))),
@@ -591,35 +587,35 @@ static void long_finish_dispatch(SpmmArgs& a, int gy, cudaStream_t st) {
 }
 
 template <typename VT, int KIND, bool W>
-static void spmm_dispatch(SpmmArgs& a, int gy, bool coop, int dev, cudaStream_t st) {
+static void spmm_dispatch(SpmmArgs& a, int gy, cudaStream_t st) {
   switch (ppl_for(a.c)) {
-    case 1: spmm_launch_one<VT, KIND, W, 1>(a, gy, coop, dev, st); break;
-    case 2: spmm_launch_one<VT, KIND, W, 2>(a, gy, coop, dev, st); break;
-    default: spmm_launch_one<VT, KIND, W, 4>(a, gy, coop, dev, st); break;
+    case 1: spmm_launch_one<VT, KIND, W, 1>(a, gy, st); break;
+    case 2: spmm_launch_one<VT, KIND, W, 2>(a, gy, st); break;
+    default: spmm_launch_one<VT, KIND, W, 4>(a, gy, st); break;
   }
 }
 
 template <typename VT>
-static void launch_spmm_main(int kind, SpmmArgs& a, bool coop, int dev, int gy, cudaStream_t st) {
+static void launch_spmm_main(int kind, SpmmArgs& a, int gy, cudaStream_t st) {
   LaunchScope ls(K_SPMM, st);
   const bool wt = a.weights != nullptr;
   if (kind == SLQ_NORMALIZED_LAPLACIAN) {
-    if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, gy, coop, dev, st);
-    else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, gy, coop, dev, st);
+    if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, gy, st);
+    else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, gy, st);
   } else if (kind == SLQ_DENSITY) {
-    if (wt) spmm_dispatch<VT, SLQ_DENSITY, true>(a, gy, coop, dev, st);
-    else spmm_dispatch<VT, SLQ_DENSITY, false>(a, gy, coop, dev, st);
+    if (wt) spmm_dispatch<VT, SLQ_DENSITY, true>(a, gy, st);
+    else spmm_dispatch<VT, SLQ_DENSITY, false>(a, gy, st);
   } else {
-    if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, gy, coop, dev, st);
-    else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, gy, coop, dev, st);
+    if (wt) spmm_dispatch<VT, SLQ_LAPLACIAN, true>(a, gy, st);
+    else spmm_dispatch<VT, SLQ_LAPLACIAN, false>(a, gy, st);
   }
 }
 
 // The SpMM pass (short rows + long-row segments), then the long-row finish when the graph has any.
 template <typename VT>
-static void launch_spmm(int kind, SpmmArgs a, bool coop, int dev, cudaStream_t st, bool finish = true) {
+static void launch_spmm(int kind, SpmmArgs a, cudaStream_t st, bool finish = true) {
   const int gy = ceil_div(a.c, kBlk);
-  launch_spmm_main<VT>(kind, a, coop, dev, gy, st);
+  launch_spmm_main<VT>(kind, a, gy, st);
   if (finish && a.long_counts && a.max_long > 0) {
     LaunchScope ls(K_SPMM, st);
     if (kind == SLQ_NORMALIZED_LAPLACIAN) long_finish_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN>(a, gy, st);
@@ -892,10 +888,6 @@ struct StageRing {
 template <typename VT>
 __host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int vstride) {
   return static_cast<int64_t>(nvec) * vstride + (static_cast<int64_t>(rt) * kBitWords * 4 + sizeof(VT) - 1) / sizeof(VT);
-}
-
-__device__ __forceinline__ double bit_value(const uint32_t* brow, int p) {
-  return ((brow[p >> 5] >> (p & 31)) & 1u) ? 1.0 : -1.0;
 }
 
 __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
@@ -1552,12 +1544,12 @@ static void launch_reduce(ReduceArgs a, cudaStream_t st) {
 }
 
 // Per-vector-type entry points instantiated in spmm_{f32,f64}.cu and step_{f32,f64}.cu.
-void launch_spmm_f32(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish);
-void launch_spmm_f64(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish);
+void launch_spmm_f32(int kind, const SpmmArgs& a, cudaStream_t st, bool finish);
+void launch_spmm_f64(int kind, const SpmmArgs& a, cudaStream_t st, bool finish);
 template <typename VT>
-inline void spmm_entry(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish = true) {
-  if (sizeof(VT) == 4) launch_spmm_f32(kind, a, coop, dev, st, finish);
-  else launch_spmm_f64(kind, a, coop, dev, st, finish);
+inline void spmm_entry(int kind, const SpmmArgs& a, cudaStream_t st, bool finish = true) {
+  if (sizeof(VT) == 4) launch_spmm_f32(kind, a, st, finish);
+  else launch_spmm_f64(kind, a, st, finish);
 }
 
 template <typename VT>

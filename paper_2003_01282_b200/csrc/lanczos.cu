@@ -270,7 +270,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     const bool staged = coop && reorth && i < S - 1 && i + 1 <= kCgsBlock && ldc <= kStagedMaxLdc;
     // alpha: step kernel (staged) or alpha_dot_kernel
     SLQ_TRACE("spmm launch");
-    spmm_entry<VT>(kind, sa, false, g->device, st, /*finish=*/!staged);   // staged: phase 0 finishes
+    spmm_entry<VT>(kind, sa, st, /*finish=*/!staged);   // staged: phase 0 finishes
     SLQ_TRACE("spmm launched");
     if (!staged) {
       // the long rows of w must be complete before alpha: finish kernel ran inside launch_spmm
@@ -398,7 +398,7 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
     sa.cpad = ceil_div(sa.c, 32) * 32;
     sa.work = work + 4 * pi;
     set_long_rows(sa, g, segpart);
-    spmm_entry<double>(kind, sa, false, g->device, st);
+    spmm_entry<double>(kind, sa, st);
   }
   SLQ_CUDA(cudaFreeAsync(segpart, st));
   SLQ_CUDA(cudaFreeAsync(work, st));

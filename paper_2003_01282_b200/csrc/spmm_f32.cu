@@ -3,8 +3,8 @@
 
 namespace slq {
 
-void launch_spmm_f32(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish) {
-  launch_spmm<float>(kind, a, coop, dev, st, finish);
+void launch_spmm_f32(int kind, const SpmmArgs& a, cudaStream_t st, bool finish) {
+  launch_spmm<float>(kind, a, st, finish);
 }
 
 }  // namespace slq

@@ -3,8 +3,8 @@
 
 namespace slq {
 
-void launch_spmm_f64(int kind, const SpmmArgs& a, bool coop, int dev, cudaStream_t st, bool finish) {
-  launch_spmm<double>(kind, a, coop, dev, st, finish);
+void launch_spmm_f64(int kind, const SpmmArgs& a, cudaStream_t st, bool finish) {
+  launch_spmm<double>(kind, a, st, finish);
 }
 
 }  // namespace slq
