@@ -112,6 +112,18 @@ int slq_graph_csr(const slq_graph* g, int64_t* offsets, int32_t* cols, void* str
 /* The generator's uniform for (seed, sample, level), for host restatements of the generator. */
 int slq_rmat_uniform_host(uint64_t seed, uint64_t sample, int level, double* out);
 
+/* Isolated-vertex fold.  Vertices with an empty row that no row references (degree 0: every
+ * operator gives 0 there, operators.py:76-99) evolve in the Lanczos recurrence as the probe sign times
+ * one per-probe scalar, so the recurrence can run on the graph without them plus ONE trailing empty
+ * row standing for all m of them (value sqrt(m) times that scalar): dot products agree with the
+ * unfolded ones to rounding, the Lanczos vectors lose m rows.  Builds the fold when m >= 1 and
+ * m >= min_fraction * n (min_fraction < 0 drops an existing fold); *folded_host = m (0: not folded).
+ * Afterwards slq_lanczos / slq_rules / slq_signature on g use the fold whenever the all-staged
+ * schedule runs (generated probes, reorth on, 2 <= s' <= 17, <= 128 probes per chunk); the operator
+ * apply, degrees, CSR export and the batched path keep using g itself.  Synchronises the creation
+ * stream; the fold holds a second copy of the CSR. */
+int slq_graph_fold_isolated(slq_graph* g, double min_fraction, int64_t* folded_host);
+
 /* Copy the prepared degree vector d = A.1 and dinv = 1/sqrt(d) (0 if isolated) into [n]
  * device buffers (either may be NULL).  operators.py:58-62, 84-86. */
 int slq_graph_degrees(const slq_graph* g, double* degree, double* dinv, void* stream);

@@ -47,6 +47,7 @@ _SIGS = {
     "slq_graph_weights": (_int, [_vp, _vp, ctypes.POINTER(_i32), _vp]),
     "slq_trace_squared": (_int, [_vp, _int, ctypes.POINTER(_dbl)]),
     "slq_graph_info": (_int, [_vp, ctypes.POINTER(GraphInfo)]),
+    "slq_graph_fold_isolated": (_int, [_vp, _dbl, ctypes.POINTER(_i64)]),
     "slq_graph_destroy": (None, [_vp]),
     "slq_graph_degrees": (_int, [_vp, _vp, _vp]),
     "slq_operator_interval": (_int, [_vp, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),

@@ -37,7 +37,7 @@ class BatchedGraphs:
         self.stacked = stacked
         self.voff = np.asarray(vertex_offsets, dtype=np.int64)
         self.count = int(self.voff.size - 1)
-        self.dg = DeviceGraph(stacked, device)
+        self.dg = DeviceGraph(stacked, device, fold=None)   # the batched kernels use the stacked CSR itself
         self.voff_d = torch.tensor(self.voff, device=self.dg.device)
 
     @property

@@ -30,7 +30,8 @@ constexpr int kBitWords = 4;   // bitmask row stride in 32-bit words (16 B: bulk
 
 template <typename VT>
 __global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* __restrict__ u,
-                                  int64_t ldc, uint32_t* __restrict__ bits) {
+                                  int64_t ldc, uint32_t* __restrict__ bits,
+                                  const int32_t* __restrict__ remap) {
   const int lane = threadIdx.x & 31;
   const int64_t run = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int p = blockIdx.y * 32 + lane;
@@ -59,8 +60,11 @@ __global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int
       const uint32_t w0 = __ballot_sync(0xffffffffu, pv && b0);
       const uint32_t w1 = __ballot_sync(0xffffffffu, pv && b1);
       if (lane == 0) {
-        if (r < n) bits[r * kBitWords + blockIdx.y] = w0;
-        if (r + 1 < n) bits[(r + 1) * kBitWords + blockIdx.y] = w1;
+        // remap (isolated-vertex fold): stream position r -> folded row, -1 = folded away
+        const int64_t d0 = r < n ? (remap ? remap[r] : r) : -1;
+        const int64_t d1 = r + 1 < n ? (remap ? remap[r + 1] : r + 1) : -1;
+        if (d0 >= 0) bits[d0 * kBitWords + blockIdx.y] = w0;
+        if (d1 >= 0) bits[d1 * kBitWords + blockIdx.y] = w1;
       }
     }
   }
@@ -68,11 +72,11 @@ __global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int
 
 template <typename VT>
 static void launch_probes(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* u, int64_t ldc,
-                          cudaStream_t st, uint32_t* bits = nullptr) {
+                          cudaStream_t st, uint32_t* bits = nullptr, const int32_t* remap = nullptr) {
   const int64_t runs = (n + 2 * kProbeRun - 1) / (2 * kProbeRun);
   dim3 grid(ceil_div(runs, 4), ceil_div(c, 32));
   LaunchScope ls(K_PROBE, st);
-  probe_init_kernel<VT><<<grid, 128, 0, st>>>(seed, probe_begin, c, n, u, ldc, bits);
+  probe_init_kernel<VT><<<grid, 128, 0, st>>>(seed, probe_begin, c, n, u, ldc, bits, remap);
 }
 
 template <typename VT>
@@ -638,6 +642,10 @@ struct CgsArgs {
   const void* w;                   // Op(q_i)
   ChunkState s;
   double* partial;                 // [ntiles][nq][cpad]
+  // isolated-vertex fold: row virt_row stands for m isolated vertices; its u_0 is sqrt(m) (virt_root)
+  // instead of a +-1 probe bit (-1: no such row)
+  int64_t virt_row = -1;
+  double virt_root = 0.0;
 };
 
 // w' = (w - alpha q_i) - beta_{i-1} q_{i-1}    (lanczos.py:129, numpy left-to-right evaluation)
@@ -961,10 +969,12 @@ struct StepArith<float> {
   static __device__ __forceinline__ T sub(T x, T y) { return __fsub_rn(x, y); }
 };
 
-// u_k of row r in the arithmetic type (u_0 = +-1 from the bitmask row)
+// u_k of row r in the arithmetic type (u_0 = +-1 from the bitmask row; sqrt(m) on the fold's
+// trailing row, virt)
 template <typename VT, typename T>
-__device__ __forceinline__ T stage_u(const VT* e, const uint32_t* brow, int vstride, int p, int k) {
-  if (k == 0) return ((brow[p >> 5] >> (p & 31)) & 1u) ? T(1) : T(-1);
+__device__ __forceinline__ T stage_u(const VT* e, const uint32_t* brow, int vstride, int p, int k, bool virt,
+                                     T vroot) {
+  if (k == 0) return virt ? vroot : (((brow[p >> 5] >> (p & 31)) & 1u) ? T(1) : T(-1));
   return static_cast<T>(e[k * vstride]);
 }
 
@@ -994,21 +1004,24 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
     for (int q = 0; q < NQ; ++q) acc[q] += static_cast<double>(blk[q]), blk[q] = T(0);
     nrow = 0;
   };
+  const T vroot = static_cast<T>(a.virt_root);
   auto row_dots = [&](T wv, const T* uv) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
       if (q * M + L.part < NK) blk[q] = fma(uv[q], wv, blk[q]);
-    if (NK == 1 && L.part == 0) g00 += 1.0;   // u_0 . u_0 = number of rows (+-1 entries)
+    // u_0 . u_0: 1 per +-1 row (exact), m for the fold's trailing row
+    if (NK == 1 && L.part == 0) g00 += static_cast<double>(uv[0]) * static_cast<double>(uv[0]);
     if (A::kFlush && ++nrow == A::kFlush) flush();
   };
-  auto load_row = [&](const VT* stage, const uint32_t* sbits, int rr, T& wv, T* uv) {
+  auto load_row = [&](const VT* stage, const uint32_t* sbits, int rr, int64_t grow, T& wv, T* uv) {
     const VT* e = stage + L.p + rr * ldc;
     const uint32_t* brow = sbits + rr * kBitWords;
+    const bool virt = grow == a.virt_row;
     wv = static_cast<T>(e[0]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int kk = q * M + L.part;
-      uv[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, L.p, kk) : T(0);
+      uv[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, L.p, kk, virt, vroot) : T(0);
     }
   };
   int ch = ch0;
@@ -1026,13 +1039,13 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
       for (; r + SL * (U - 1) < rows; r += SL * U) {
         T wv[U], uv[U][NQ];
 #pragma unroll
-        for (int j = 0; j < U; ++j) load_row(stage, sbits, r + SL * j, wv[j], uv[j]);
+        for (int j = 0; j < U; ++j) load_row(stage, sbits, r + SL * j, r0 + r + SL * j, wv[j], uv[j]);
 #pragma unroll
         for (int j = 0; j < U; ++j) row_dots(wv[j], uv[j]);
       }
       for (; r < rows; r += SL) {
         T wv1, uv1[NQ];
-        load_row(stage, sbits, r, wv1, uv1);
+        load_row(stage, sbits, r, r0 + r, wv1, uv1);
         row_dots(wv1, uv1);
       }
     }
@@ -1131,6 +1144,7 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
   }
   const T al_t = static_cast<T>(al), bp_t = static_cast<T>(bp), ri_t = static_cast<T>(ri);
   const T rim1_t = static_cast<T>(rim1);
+  const T vroot = static_cast<T>(a.virt_root);
   const int rt = sa.rt, vstride = sa.vstride;
   const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride);
   VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
@@ -1183,15 +1197,16 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     auto load_row = [&](int rr, T& src, T& ui, T& uim1, T* uk) {
       const VT* e = stage + pr + rr * ldc;
       const uint32_t* brow = sbits + rr * kBitWords;
+      const bool virt = r0 + rr == a.virt_row;
       src = static_cast<T>(e[0]);
       if (!SECOND) {
-        ui = stage_u<VT, T>(e, brow, vstride, pr, i);
-        uim1 = i > 0 ? stage_u<VT, T>(e, brow, vstride, pr, i > 0 ? i - 1 : 0) : T(0);
+        ui = stage_u<VT, T>(e, brow, vstride, pr, i, virt, vroot);
+        uim1 = i > 0 ? stage_u<VT, T>(e, brow, vstride, pr, i > 0 ? i - 1 : 0, virt, vroot) : T(0);
       }
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int kk = q * M + L.part;
-        uk[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, pr, kk) : T(0);
+        uk[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, pr, kk, virt, vroot) : T(0);
       }
     };
     int r = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);

@@ -301,6 +301,139 @@ int fetch_host_scalars(slq_graph* g) {
   return SLQ_OK;
 }
 
+// ----------------------------------------------------------------------------- isolated-vertex fold
+// A vertex whose row is empty and which no row references is isolated in the operator sense: every
+// operator kind gives y_v = 0 (operators.py:76-99: d_v = 0, dinv_v = 0, no neighbours).  In the
+// Lanczos recurrence such a row only ever sees row-local linear updates (three-term, CGS
+// subtraction, 1/beta), whose arithmetic is sign-symmetric, so u_k[v] = z_v * e_k with the probe sign
+// z_v = +-1 and ONE per-probe scalar sequence e_k shared by all isolated rows (bit for bit).  The fold
+// drops those rows and appends a single empty row that carries sqrt(m) * e_k for the m of them: every
+// dot product over the original rows equals the folded one up to rounding (m e_k e_l), while the
+// vectors shrink by m rows.  The relabelling is monotone, so rows keep their stored column order and
+// the SpMM's in-row sums are bitwise those of the unfolded graph.
+__global__ void fold_mark_rows_kernel(const int64_t* __restrict__ off, int64_t n, int32_t* __restrict__ keep) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x)
+    keep[v] = v < n && off[v + 1] > off[v] ? 1 : 0;
+}
+
+__global__ void fold_mark_cols_kernel(const int32_t* __restrict__ cols, int64_t nnz, int32_t* __restrict__ keep) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = cols[e];
+    if (!keep[c]) keep[c] = 1;   // benign race: every writer stores 1
+  }
+}
+
+// keep[] becomes the remap (folded row or -1) in place; off_f[newid[v]] = off[v] for kept rows and
+// the trailing row n' is empty.
+__global__ void fold_offsets_kernel(const int64_t* __restrict__ off, int32_t* __restrict__ keep_remap,
+                                    const int32_t* __restrict__ newid, int64_t n, int64_t nprime, int64_t nnz,
+                                    int64_t* __restrict__ off_f) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (v == n) {
+      off_f[nprime] = nnz;
+      off_f[nprime + 1] = nnz;
+      continue;
+    }
+    const bool k = keep_remap[v] != 0;
+    if (k) off_f[newid[v]] = off[v];
+    keep_remap[v] = k ? newid[v] : -1;
+  }
+}
+
+__global__ void fold_cols_kernel(const int32_t* __restrict__ cols, const int32_t* __restrict__ newid, int64_t nnz,
+                                 int32_t* __restrict__ cols_f) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    cols_f[e] = newid[cols[e]];
+}
+
+static void drop_fold(slq_graph* g) {
+  if (g->folded) slq_graph_destroy(g->folded);
+  if (g->fold_remap) cudaFreeAsync(g->fold_remap, static_cast<cudaStream_t>(g->stream));
+  g->folded = nullptr;
+  g->fold_remap = nullptr;
+  g->fold_m = 0;
+}
+
+static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
+  *folded_out = 0;
+  if (min_fraction < 0.0) {
+    drop_fold(g);
+    return SLQ_OK;
+  }
+  if (g->folded) {
+    *folded_out = g->fold_m;
+    return SLQ_OK;
+  }
+  int rc = fetch_host_scalars(g);
+  if (rc) return rc;
+  const int64_t n = g->n, nnz = g->nnz;
+  // degree-0 vertices bound the foldable ones from above; nothing to do below the threshold
+  if (g->bad_columns || nnz == 0 || g->isolated < 1 ||
+      static_cast<double>(g->isolated) < min_fraction * static_cast<double>(n))
+    return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(g->stream);
+  int32_t* keep = nullptr;    // [n+1] keep flags, then the remap
+  int32_t* newid = nullptr;   // [n+1] exclusive scan of keep
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keep), sizeof(int32_t) * (n + 1), st));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&newid), sizeof(int32_t) * (n + 1), st));
+  {
+    LaunchScope ls(K_PREPARE, st);
+    fold_mark_rows_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(g->offsets, n, keep);
+    fold_mark_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(g->cols, nnz, keep);
+  }
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, keep, newid, static_cast<int>(n + 1), st);
+  void* cubtmp = nullptr;
+  SLQ_CUDA(cudaMallocAsync(&cubtmp, tb + 16, st));
+  SLQ_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, newid, static_cast<int>(n + 1), st));
+  SLQ_CUDA(cudaFreeAsync(cubtmp, st));
+  int32_t nprime32 = 0;
+  SLQ_CUDA(cudaMemcpyAsync(&nprime32, newid + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  const int64_t nprime = nprime32, m = n - nprime;
+  if (m < 1 || static_cast<double>(m) < min_fraction * static_cast<double>(n)) {
+    cudaFreeAsync(keep, st);
+    cudaFreeAsync(newid, st);
+    return SLQ_OK;
+  }
+  int64_t* off_f = nullptr;
+  int32_t* cols_f = nullptr;
+  double* w_f = nullptr;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&off_f), sizeof(int64_t) * (nprime + 2), st));
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cols_f), sizeof(int32_t) * nnz, st));
+  {
+    LaunchScope ls(K_PREPARE, st);
+    fold_offsets_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(g->offsets, keep, newid, n, nprime, nnz, off_f);
+    fold_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(g->cols, newid, nnz, cols_f);
+  }
+  SLQ_CUDA(cudaFreeAsync(newid, st));
+  if (g->weights) {
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w_f), sizeof(double) * nnz, st));
+    SLQ_CUDA(cudaMemcpyAsync(w_f, g->weights, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
+  }
+  slq_graph* f = new slq_graph();
+  f->n = nprime + 1;
+  f->nnz = nnz;
+  f->stream = g->stream;
+  f->device = g->device;
+  rc = graph_adopt(f, off_f, cols_f, st, w_f);
+  if (rc) {
+    slq_graph_destroy(f);
+    cudaFreeAsync(keep, st);
+    return rc;
+  }
+  // the operator scalars are the original graph's (tr L, max degree, 1/tr L, interval): the same
+  // values, and for weighted graphs the same summation order
+  SLQ_CUDA(cudaMemcpyAsync(f->dscal, g->dscal, sizeof(double) * 8, cudaMemcpyDeviceToDevice, st));
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  SLQ_CUDA(cudaGetLastError());
+  g->folded = f;
+  g->fold_remap = keep;
+  g->fold_m = m;
+  *folded_out = m;
+  return SLQ_OK;
+}
+
 }  // namespace slq
 
 using namespace slq;
@@ -367,9 +500,15 @@ extern "C" int slq_graph_info(const slq_graph* g, slq_graph_info_t* out) {
 
 extern "C" void slq_graph_destroy(slq_graph* g) {
   if (!g) return;
+  drop_fold(g);
   // stream-ordered frees on the creation stream (it must outlive the graph)
   for (int i = 0; i < g->n_owned; ++i) cudaFreeAsync(g->owned[i], static_cast<cudaStream_t>(g->stream));
   delete g;
+}
+
+extern "C" int slq_graph_fold_isolated(slq_graph* g, double min_fraction, int64_t* folded_host) {
+  if (!g || !folded_host) return fail(SLQ_ERR_VALUE, "NULL argument");
+  return graph_fold(g, min_fraction, folded_host);
 }
 
 extern "C" int slq_operator_interval(const slq_graph* g, int kind, double* lo, double* hi) {

@@ -151,12 +151,20 @@ static int64_t partial_rows(const slq_graph* g) {
                             static_cast<int64_t>(kAlphaCtas)});
 }
 
+// The recurrence runs on `g`; with an isolated-vertex fold, g is the folded graph and `orig` the
+// graph the probes and the start-vector norm belong to (probe stream positions are original vertex
+// ids, remapped to folded rows; the trailing row carries sqrt(m)).
+struct FoldRun {
+  const slq_graph* orig = nullptr;   // nullptr: no fold
+};
+
 template <typename VT>
 static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0, const double* q0, int64_t ldq,
                      int c, int S, int reorth, double* alpha_out, double* beta_out, int32_t* steps_out, int64_t col0,
-                     cudaStream_t st) {
+                     cudaStream_t st, FoldRun fold = FoldRun{}) {
   const double t_host0 = host_ms();
   const int64_t n = g->n;
+  const int64_t n_probe = fold.orig ? fold.orig->n : n;   // probe length: ||v||^2 = n (slq.py:73)
   const int vb = sizeof(VT);
   // ldc: probes padded to a 32-byte sector multiple
   const int64_t ldc = ((c * vb + 31) / 32) * 32 / vb;
@@ -213,12 +221,16 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
 
   {
     LaunchScope ls(K_PROBE, st);
-    state_init_kernel<<<ceil_div(std::max(cpad, 4 * S), 128), 128, 0, st>>>(s, n, q0 != nullptr);
+    state_init_kernel<<<ceil_div(std::max(cpad, 4 * S), 128), 128, 0, st>>>(s, n_probe, q0 != nullptr);
   }
   uint32_t* bits = use_bits ? reinterpret_cast<uint32_t*>(ws + off_bits) : nullptr;
   if (q0) {
     LaunchScope ls(K_PROBE, st);
     copy_start_kernel<VT><<<std::max(1, std::min(ceil_div(n * c, 256), 148 * 16)), 256, 0, st>>>(q0, ldq, c, n, basis, ldc);
+  } else if (fold.orig) {
+    if (!all_staged) return fail(SLQ_ERR_VALUE, "isolated-vertex fold needs the all-staged schedule");
+    launch_probes<VT>(seed, probe0, c, n_probe, nullptr, ldc, st, bits, fold.orig->fold_remap);
+    SLQ_CUDA(cudaMemsetAsync(bits + (n - 1) * kBitWords, 0xff, sizeof(uint32_t) * kBitWords, st));
   } else {
     launch_probes<VT>(seed, probe0, c, n, all_staged ? nullptr : basis, ldc, st, bits);
   }
@@ -234,6 +246,10 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   ca.n = n; ca.ldc = ldc; ca.vec_stride = vs; ca.rows_per_tile = g->rows_per_stream_tile;
   ca.ntiles = g->ntiles_stream; ca.c = c; ca.cpad = cpad; ca.basis = basis; ca.w = wv; ca.s = s;
   ca.partial = partial; ca.reorth = reorth;
+  if (fold.orig) {
+    ca.virt_row = n - 1;
+    ca.virt_root = std::sqrt(static_cast<double>(fold.orig->fold_m));
+  }
 
   ReduceArgs ra{};
   ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.kind = kind; ra.dscal = g->dscal; ra.reorth = reorth;
@@ -344,14 +360,24 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   ensure_pool(g->device);
   const int vb = dtype == SLQ_F64 ? 8 : 4;
   const double t_host0 = host_ms();
-  const int cmax = choose_chunk(g, count, S, vb, lean_schedule(g, q0 != nullptr, S, reorth));
+  // isolated-vertex fold (slq_graph_fold_isolated): only under the all-staged schedule (u_0 as the
+  // probe bitmask, which is where the trailing row's sqrt(m) is substituted)
+  const bool lean = lean_schedule(g, q0 != nullptr, S, reorth);
+  FoldRun fold;
+  const slq_graph* gr = g;
+  if (g->folded && lean) {
+    fold.orig = g;
+    gr = g->folded;
+  }
+  int cmax = choose_chunk(gr, count, S, vb, lean);
+  if (fold.orig) cmax = std::min(cmax, kBlk);   // bitmask probes: <= 128 per chunk
   SLQ_TRACE("choose_chunk");
   for (int64_t done = 0; done < count;) {
     const int c = static_cast<int>(std::min<int64_t>(cmax, count - done));
     const double* qc = q0 ? q0 + done : nullptr;
     rc = dtype == SLQ_F64
-             ? run_chunk<double>(g, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st)
-             : run_chunk<float>(g, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st);
+             ? run_chunk<double>(gr, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st, fold)
+             : run_chunk<float>(gr, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st, fold);
     if (rc) return rc;
     done += c;
   }

@@ -111,6 +111,11 @@ struct slq_graph {
   int64_t* long_seg_first = nullptr;   // [max_long+1] first segment of each long row
   int32_t* seg_row = nullptr;          // [max_seg]
   int64_t* seg_begin = nullptr;        // [max_seg] first nonzero of each segment
+  // isolated-vertex fold (slq_graph_fold_isolated): the graph without its unreferenced empty rows
+  // plus ONE trailing empty row that stands for all of them (see graph.cu)
+  slq_graph* folded = nullptr;
+  int32_t* fold_remap = nullptr;       // [n] original vertex -> folded row, -1 for folded-away rows
+  int64_t fold_m = 0;                  // vertices folded into the trailing row
   // owned device allocations
   void* owned[12] = {nullptr};
   int n_owned = 0;

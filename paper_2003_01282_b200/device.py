@@ -17,10 +17,19 @@ KIND_CODES = {"laplacian": _lib.LAPLACIAN, "normalized_laplacian": _lib.NORMALIZ
               "density": _lib.DENSITY}
 
 
+# Isolated-vertex fold (slq_graph_fold_isolated): graphs with at least this fraction of unreferenced
+# empty rows (and at least FOLD_MIN_N vertices) run the Lanczos recurrence on the folded graph.
+FOLD_MIN_FRACTION = 1.0 / 64
+FOLD_MIN_N = 256
+
+
 class DeviceGraph:
     """Prepared CSR on one GPU: int32 columns, implicit unit weights, degrees, dinv, tiles."""
 
-    def __init__(self, g: Graph, device=None, *, from_device: bool = False):
+    folded = 0   # vertices folded into the trailing row of the isolated-vertex fold (0: none)
+
+    def __init__(self, g: Graph, device=None, *, from_device: bool = False,
+                 fold: float | None = FOLD_MIN_FRACTION):
         torch = _lib.require_cuda()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.graph = g
@@ -45,10 +54,24 @@ class DeviceGraph:
                                                ctypes.byref(self.handle))
         _lib.check(rc)
         self._info = None
+        # empty rows counted on the host first: graphs below the threshold never synchronise here
+        if fold is not None and self.n >= FOLD_MIN_N and g.nnz > 0:
+            empty = int(np.count_nonzero(np.diff(np.asarray(g.row_offsets)) == 0))
+            if empty >= 1 and empty >= fold * self.n:
+                self.fold_isolated(fold)
+
+    def fold_isolated(self, min_fraction: float = FOLD_MIN_FRACTION) -> int:
+        """Build (or with ``min_fraction < 0`` drop) the isolated-vertex fold; returns the number of
+        folded vertices (0: not folded).  Synchronises the graph's stream."""
+        m = ctypes.c_int64()
+        with _lib.require_cuda().cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_fold_isolated(self.handle, float(min_fraction), ctypes.byref(m)))
+        self.folded = int(m.value)
+        return self.folded
 
     @classmethod
     def rmat(cls, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
-             seed: int = 0, device=None) -> "DeviceGraph":
+             seed: int = 0, device=None, fold: float | None = FOLD_MIN_FRACTION) -> "DeviceGraph":
         """An R-MAT graph generated and converted to canonical CSR on the device (no host copy of the
         edges: the C5 workload's 4e9 directed edges never leave HBM).  ``graph`` is None."""
         torch = _lib.require_cuda()
@@ -63,10 +86,12 @@ class DeviceGraph:
         self._info = None
         self.n = int(self.info.n)
         self.nnz = int(self.info.nnz)
+        if fold is not None and self.n >= FOLD_MIN_N:
+            self.fold_isolated(fold)
         return self
 
     @classmethod
-    def from_edges(cls, n: int, u, v, w=None, device=None) -> "DeviceGraph":
+    def from_edges(cls, n: int, u, v, w=None, device=None, fold: float | None = FOLD_MIN_FRACTION) -> "DeviceGraph":
         """Canonical CSR built on the device from an edge list (numpy arrays or torch tensors, host
         or device): the semantics of ``graphs.csr_from_edges`` (self-loops dropped, both directions,
         duplicates collapse to the maximum weight, sorted).  ``graph`` is None."""
@@ -92,6 +117,8 @@ class DeviceGraph:
         self._info = None
         self.n = int(self.info.n)
         self.nnz = int(self.info.nnz)
+        if fold is not None and self.n >= FOLD_MIN_N:
+            self.fold_isolated(fold)
         return self
 
     def weights(self):

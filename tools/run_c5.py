@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--profile", action="store_true", help="per-kernel-class device time of one more NL run")
+    ap.add_argument("--no-fold", action="store_true", help="keep the isolated vertices in the Lanczos vectors")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -74,9 +75,11 @@ def main():
         return float(t.item())
 
     t0 = time.perf_counter()
-    dg, gen_ms = timed(lambda: DeviceGraph.rmat(args.scale, 16, 0.57, 0.19, 0.19, seed=0, device=dev))
+    dg, gen_ms = timed(lambda: DeviceGraph.rmat(args.scale, 16, 0.57, 0.19, 0.19, seed=0, device=dev, fold=None))
+    folded, fold_ms = (0, 0.0) if args.no_fold else timed(lambda: dg.fold_isolated())
     out = {"config": "c5", "scale": args.scale, "n": dg.n, "nnz": dg.nnz, "gen_wall_s": time.perf_counter() - t0,
-           "gen_ms": gen_ms, "probes": args.probes, "steps": args.steps, "dtype": args.dtype, "n_gpus": world}
+           "gen_ms": gen_ms, "folded_isolated": folded, "fold_ms": fold_ms, "probes": args.probes,
+           "steps": args.steps, "dtype": args.dtype, "n_gpus": world}
     tgrid = torch.tensor(np.array(TimeGrid(1e-2, 1e2, 250).values), device=dev)
     units = dg.nnz * args.probes * args.steps
     total_ms = 0.0
@@ -148,6 +151,12 @@ def main():
         v64, _ = r64.integrate(tgrid, [_lib.FN_HEAT])
         v32, _ = r32.integrate(tgrid, [_lib.FN_HEAT])
         chk["heat_f32_vs_f64_rel_l2"] = float(torch.linalg.norm(v32 - v64) / torch.linalg.norm(v64))
+        if folded:
+            # the fold against the unfolded recurrence on the same 4-probe prefix (fp32 storage)
+            dg.fold_isolated(-1.0)
+            r_un = dg.rules("normalized_laplacian", 0, 0, 4, args.steps, dtype="f32")
+            v_un, _ = r_un.integrate(tgrid, [_lib.FN_HEAT])
+            chk["heat_fold_vs_unfolded_rel_l2"] = float(torch.linalg.norm(v32 - v_un) / torch.linalg.norm(v_un))
         out["checks"] = chk
     print(json.dumps(out))
 
