@@ -336,6 +336,58 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       if (WEIGHTED) myw = __ldg(wts + base + lane);
       if (!EXACT && WEIGHTED) mys *= myw;   // s_c = dinv_c * w (or w)
     }
+    if (HALF && PPL == 2) {
+      // HALF2 (16 < c <= 32): lane (plane) holds probes 2 plane, 2 plane + 1 and reads them with one
+      // 2-element vector load, so a half-warp gathers a whole row and a warp instruction two rows;
+      // this half takes positions 2m + sub (its chain), U pairs in flight
+      using V2 = typename std::conditional<std::is_same<VT, double>::value, double2, float2>::type;
+      constexpr int U = 8;
+      const int npairs = (cnt + 1) >> 1;
+      int m = 0;
+      for (; m + U <= npairs; m += U) {
+        V2 xv[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int64_t o = __shfl_sync(FULL, myoff, 2 * (m + q) + sub);
+          if (BITS) {
+            const uint32_t wd = __ldg(bits + o);
+            xv[q].x = ((wd >> (2 * plane)) & 1u) ? VT(1) : VT(-1);
+            xv[q].y = ((wd >> (2 * plane + 1)) & 1u) ? VT(1) : VT(-1);
+          } else {
+            xv[q] = __ldg(reinterpret_cast<const V2*>(u + o + pidx[0]));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int kk = 2 * (m + q) + sub;
+          const double sk = SK ? __shfl_sync(FULL, mys, kk) : 1.0;
+          if (kk < cnt) {
+            const double x0 = static_cast<double>(xv[q].x), x1 = static_cast<double>(xv[q].y);
+            a0[0] = SK ? fma(sk, x0, a0[0]) : a0[0] + x0;
+            a0[1] = SK ? fma(sk, x1, a0[1]) : a0[1] + x1;
+          }
+        }
+      }
+      for (; m < npairs; ++m) {
+        const int kk = 2 * m + sub;
+        const int64_t o = __shfl_sync(FULL, myoff, kk);
+        const double sk = SK ? __shfl_sync(FULL, mys, kk) : 1.0;
+        V2 xv;
+        if (BITS) {
+          const uint32_t wd = __ldg(bits + o);
+          xv.x = ((wd >> (2 * plane)) & 1u) ? VT(1) : VT(-1);
+          xv.y = ((wd >> (2 * plane + 1)) & 1u) ? VT(1) : VT(-1);
+        } else {
+          xv = __ldg(reinterpret_cast<const V2*>(u + o + pidx[0]));
+        }
+        if (kk < cnt) {
+          const double x0 = static_cast<double>(xv.x), x1 = static_cast<double>(xv.y);
+          a0[0] = SK ? fma(sk, x0, a0[0]) : a0[0] + x0;
+          a0[1] = SK ? fma(sk, x1, a0[1]) : a0[1] + x1;
+        }
+      }
+      continue;
+    }
     if (HALF) {
       // pair m: this half takes position 2m + sub; U pairs in flight
       constexpr int U = 8;
@@ -426,15 +478,17 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
   }
 }
 
-// own-row value u[row][probe j] (from the bitmask on the first step); plane = probe lane
-template <typename VT, int PPL, bool BITS>
+// own-row value u[row][probe j of this lane] (from the bitmask on the first step).  u points at the
+// lane's first probe; probe j of the lane is PS j further, and `probe` is its index within the
+// 128-probe block (the bitmask word probe / 32, bit probe % 32).
+template <typename VT, int PPL, bool BITS, int PS = 32>
 __device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint32_t* bits, int64_t row, int j,
-                                            int plane) {
+                                            int probe) {
   if (BITS) {
-    const uint32_t wd = __ldg(bits + row * kBitWords + j);
-    return ((wd >> plane) & 1u) ? 1.0 : -1.0;
+    const uint32_t wd = __ldg(bits + row * kBitWords + (probe >> 5));
+    return ((wd >> (probe & 31)) & 1u) ? 1.0 : -1.0;
   }
-  return ldg_f64(u + row * ldi + 32 * j);
+  return ldg_f64(u + row * ldi + PS * j);
 }
 
 // Pass A.  Warp-level work items taken from an atomic counter: first the long-row segments (partial
@@ -449,15 +503,23 @@ template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, 
 __global__ void __launch_bounds__(kSpmmWarps * 32, PPL == 4 ? SLQ_SPMM_MINB4 : 4)
 spmm_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
-  const int plane = HALF ? (lane & 15) : lane;   // HALF: two half-warps share probes 0..15
+  const int plane = HALF ? (lane & 15) : lane;   // HALF: two half-warps share probes 0..15 (0..31)
   const bool writer = !HALF || lane < 16;
-  const int pbase = blockIdx.y * kBlk + plane;
+  // probe j of this lane: pbase + PS j.  HALF2 (HALF, PPL = 2): probes 2 plane, 2 plane + 1.
+  constexpr int PS = HALF ? 1 : 32;
+  const int pbase = blockIdx.y * kBlk + (HALF ? PPL : 1) * plane;
   bool pv[PPL];
   int pidx[PPL];   // column offsets within a gathered row, clamped to a valid probe
 #pragma unroll
   for (int j = 0; j < PPL; ++j) {
-    pv[j] = probe_ok(pbase + 32 * j, a.c);
-    pidx[j] = pv[j] ? 32 * j : (a.c - 1 - (blockIdx.y * kBlk + plane));
+    pv[j] = probe_ok(pbase + PS * j, a.c);
+    pidx[j] = pv[j] ? PS * j : (a.c - 1 - (pbase - blockIdx.y * kBlk));
+  }
+  if (HALF && PPL == 2) {
+    // one vector load per pair: a pair past the row's end (2 plane + 1 >= ldc) reads the row's first
+    // pair instead (a valid address; those probes are never stored)
+    pidx[0] = 2 * plane + 1 < a.ldc_in ? 0 : -2 * plane;
+    pidx[1] = pidx[0] + 1;
   }
   const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
   VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
@@ -486,7 +548,7 @@ spmm_kernel(SpmmArgs a) {
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
     for (int j = 0; j < PPL; ++j)
-      if (pv[j] && writer) dst[32 * j] = acc[j];
+      if (pv[j] && writer) dst[PS * j] = acc[j];
   }
   // phase 2: row tiles, one warp each (dynamic); rows in order
   unsigned long long* tcounter = counter + 2;
@@ -509,10 +571,11 @@ spmm_kernel(SpmmArgs a) {
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         if (!pv[j] || !writer) continue;
-        const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + 32 * j);
-        const double x = __dmul_rn(own_value<VT, PPL, BITS>(u, ldi, a.bits, row, j, plane), rj);
+        const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + PS * j);
+        const double x = __dmul_rn(
+            own_value<VT, PPL, BITS, PS>(u, ldi, a.bits, row, j, pbase - blockIdx.y * kBlk + PS * j), rj);
         const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * rj, d, dis, scale);
-        w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
+        w[row * a.ldc_out + PS * j] = from_f64<VT>(y);
       }
     }
   }
@@ -567,9 +630,18 @@ static void spmm_launch_one(SpmmArgs& a, int gy, cudaStream_t st) {
   // EXACT (bit-identical operator apply) only for the apply entry (r == nullptr, double);
   // HALF (two nonzeros per warp instruction) for Lanczos chunks of <= 16 probes.
   const bool half = PPL == 1 && a.c <= 16 && a.ldc_in <= 16;
+  // HALF2 for 16 < c <= 32 (SLQ_SPMM_HALF2=0 keeps the full-warp mapping; same arithmetic)
+  static const bool half2_on = [] { const char* e = getenv("SLQ_SPMM_HALF2"); return !(e && e[0] == '0'); }();
+  const bool half2 = half2_on && std::is_same<VT, float>::value && PPL == 1 && !half && a.c <= 32 && a.ldc_in <= 32;
   if (!a.r) {
     if constexpr (std::is_same<VT, double>::value)
       spmm_kernel<VT, KIND, W, PPL, false, true, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else if (half2) {
+    // fp32 rows only: fp64 pairs (16-byte loads) do not fit the register budget without spills
+    if constexpr (std::is_same<VT, float>::value) {
+      if (a.bits) spmm_kernel<VT, KIND, W, 2, true, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+      else spmm_kernel<VT, KIND, W, 2, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    }
   } else if (half) {
     if (a.bits) spmm_kernel<VT, KIND, W, 1, true, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
     else spmm_kernel<VT, KIND, W, 1, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);

@@ -540,3 +540,26 @@ def test_trace_identities_match_reference_definitions(cuda_device, fname):
     if n <= 1500:
         L = O.make_block_operator(g, O.NORMALIZED_LAPLACIAN).apply(np.eye(n))
         assert abs(np.sum(L * L) - ref_nl2) <= 1e-10 * ref_nl2
+
+
+@pytest.mark.parametrize("count", [24, 32])
+def test_spmm_half2_mapping_bitwise_equals_full_warp(cuda_device, tmp_path, count):
+    # fp32 chunks of 17..32 probes: the HALF2 mapping (two probes per lane, a half-warp per gathered
+    # row) sums every row in the same two chains as the full-warp mapping (SLQ_SPMM_HALF2=0), so the
+    # rules are bitwise equal; the hub graph adds long-row segments
+    import os
+    import subprocess
+    import sys
+
+    out = tmp_path / "nodes.npy"
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests'); import numpy as np, golden; "
+            "from test_gpu_parity import _hub_graph; "
+            "from paper_2003_01282_b200.device import DeviceGraph; "
+            f"r = DeviceGraph(_hub_graph()).rules('normalized_laplacian', 3, 0, {count}, 12, dtype='f32'); "
+            f"np.save('{out}', np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]))")
+    env = dict(os.environ, SLQ_SPMM_HALF2="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env,
+                   cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    full = np.load(out)
+    r = DeviceGraph(_hub_graph(), cuda_device).rules("normalized_laplacian", 3, 0, count, 12, dtype="f32")
+    assert np.array_equal(np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]), full)
