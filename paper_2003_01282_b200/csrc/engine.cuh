@@ -263,11 +263,18 @@ struct SpmmArgs {
   double* segpart;
   unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
   const uint32_t* bits;      // first step: u_0 as a probe bitmask [n][kBitWords] (nullptr = use u)
+  const void* upre;          // normalized Laplacian: dinv (.) u to gather (nullptr = gather u, times dinv[col])
 };
+
+// SpMM-internal kind: the normalized Laplacian gathering the PRESCALED vector dinv (.) u (written by
+// the previous step kernel), so no dinv[col] gather per nonzero; the epilogue is the normalized one.
+constexpr int kNLPre = 3;
+template <int KIND>
+__host__ __device__ constexpr bool nl_kind() { return KIND == SLQ_NORMALIZED_LAPLACIAN || KIND == kNLPre; }
 
 template <int KIND>
 __device__ __forceinline__ double op_epilogue(double x, double acc, double d, double dis, double scale) {
-  if (KIND == SLQ_NORMALIZED_LAPLACIAN) {
+  if (nl_kind<KIND>()) {
     // nonisolated * x - dinv_sqrt * (A @ (dinv_sqrt * x))       operators.py:88-89
     const double keep = d > 0.0 ? 1.0 : 0.0;
     return __dsub_rn(__dmul_rn(keep, x), __dmul_rn(dis, acc));
@@ -317,7 +324,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
   const int lane = threadIdx.x & 31;
   const int plane = HALF ? (lane & 15) : lane;   // probe lane
   const int sub = HALF ? (lane >> 4) : 0;        // HALF: chain (position parity) of this half
-  constexpr bool SK = KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED);
+  constexpr bool SK = KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED);   // kNLPre: weights only
   double a0[PPL], a1[PPL];
 #pragma unroll
   for (int j = 0; j < PPL; ++j) a0[j] = a1[j] = 0.0;
@@ -522,6 +529,8 @@ spmm_kernel(SpmmArgs a) {
     pidx[1] = pidx[0] + 1;
   }
   const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
+  // gathered rows: u, or the prescaled dinv (.) u (kNLPre); own-row values always from u
+  const VT* __restrict__ ug = KIND == kNLPre ? static_cast<const VT*>(a.upre) + pbase : u;
   VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
   const int64_t* __restrict__ off = a.offsets;
   const double* __restrict__ dinv = a.dinv;
@@ -543,7 +552,7 @@ spmm_kernel(SpmmArgs a) {
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, beg, end,
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg, end,
                                                             acc);
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
@@ -564,10 +573,10 @@ spmm_kernel(SpmmArgs a) {
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, u, ldi, a.bits, pidx, beg, end,
+      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg, end,
                                                               acc);
       const double d = __ldg(a.degree + row);
-      const double dis = KIND == SLQ_NORMALIZED_LAPLACIAN ? __ldg(dinv + row) : 0.0;
+      const double dis = nl_kind<KIND>() ? __ldg(dinv + row) : 0.0;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         if (!pv[j] || !writer) continue;
@@ -675,7 +684,10 @@ template <typename VT>
 static void launch_spmm_main(int kind, SpmmArgs& a, int gy, cudaStream_t st) {
   LaunchScope ls(K_SPMM, st);
   const bool wt = a.weights != nullptr;
-  if (kind == SLQ_NORMALIZED_LAPLACIAN) {
+  if (kind == SLQ_NORMALIZED_LAPLACIAN && a.upre && !a.bits && a.r) {
+    if (wt) spmm_dispatch<VT, kNLPre, true>(a, gy, st);
+    else spmm_dispatch<VT, kNLPre, false>(a, gy, st);
+  } else if (kind == SLQ_NORMALIZED_LAPLACIAN) {
     if (wt) spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, gy, st);
     else spmm_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN, false>(a, gy, st);
   } else if (kind == SLQ_DENSITY) {
@@ -718,6 +730,9 @@ struct CgsArgs {
   // instead of a +-1 probe bit (-1: no such row)
   int64_t virt_row = -1;
   double virt_root = 0.0;
+  // normalized Laplacian, prescaled gathers: the update also writes dinv (.) u_{i+1} into the (still
+  // unused) slot i+2 for the next SpMM (nullptr: not this step)
+  const double* pre_dinv = nullptr;
 };
 
 // w' = (w - alpha q_i) - beta_{i-1} q_{i-1}    (lanczos.py:129, numpy left-to-right evaluation)
@@ -964,10 +979,18 @@ struct StageRing {
 };
 
 // One ring stage: nvec VT row blocks [rt][ldc] at vstride spacing, then the bitmask rows
-// [rt][kBitWords] (in VT units).
+// [rt][kBitWords], then (prescaled gathers) a window of rt + 2 (even) dinv values starting at the even row
+// at or below the chunk's first row (in VT units).
 template <typename VT>
-__host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int vstride) {
-  return static_cast<int64_t>(nvec) * vstride + (static_cast<int64_t>(rt) * kBitWords * 4 + sizeof(VT) - 1) / sizeof(VT);
+__host__ __device__ __forceinline__ int64_t stage_elems_of(int nvec, int rt, int vstride, bool dwin = false) {
+  return static_cast<int64_t>(nvec) * vstride +
+         (static_cast<int64_t>(rt) * kBitWords * 4 + (dwin ? 8 * ((static_cast<int64_t>(rt) + 3) & ~int64_t(1)) : 0) + sizeof(VT) - 1) /
+             sizeof(VT);
+}
+template <typename VT>
+__device__ __forceinline__ const double* stage_dinv(const VT* stage, int nvec, int rt, int vstride) {
+  return reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(stage + static_cast<int64_t>(nvec) * vstride) +
+                                         static_cast<int64_t>(rt) * kBitWords * 4);
 }
 
 __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
@@ -978,7 +1001,8 @@ __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
 template <typename VT>
 __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
   const int64_t ldc = sa.a.ldc;
-  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, sa.vstride);
+  const bool dw = sa.a.pre_dinv != nullptr;
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, sa.vstride, dw);
   int ch = ch0;
   for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
     const int s = ch % kStages;
@@ -986,12 +1010,18 @@ __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<V
     const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
     const uint32_t bytes = static_cast<uint32_t>(rows * ldc * sizeof(VT));
     const uint32_t bbytes = static_cast<uint32_t>(rows * kBitWords * sizeof(uint32_t));
-    mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec + bbytes);
+    // dinv window: even start (16-byte aligned source), even length (16-byte multiple)
+    const int64_t d0 = r0 & ~int64_t(1);
+    const uint32_t dbytes = dw ? static_cast<uint32_t>(((r0 - d0 + rows + 1) & ~int64_t(1)) * sizeof(double)) : 0u;
+    mbar_arrive_expect_tx(&ring.full[s], bytes * sa.nvec + bbytes + dbytes);
     VT* dst = ring.buf + s * stage_elems;
     for (int v = 0; v < sa.nvec; ++v)
       bulk_g2s(dst + static_cast<int64_t>(v) * sa.vstride, static_cast<const VT*>(sa.vec[v]) + r0 * ldc, bytes,
                &ring.full[s]);
     bulk_g2s(dst + static_cast<int64_t>(sa.nvec) * sa.vstride, sa.bits + r0 * kBitWords, bbytes, &ring.full[s]);
+    if (dw)
+      bulk_g2s(const_cast<double*>(stage_dinv<VT>(dst, sa.nvec, sa.rt, sa.vstride)), sa.a.pre_dinv + d0, dbytes,
+               &ring.full[s]);
   }
 }
 
@@ -1064,7 +1094,7 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
   const bool pv = L.p < a.c;
   const int cp = a.cpad, ldc = static_cast<int>(a.ldc);
   const int rt = sa.rt, vstride = sa.vstride;
-  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride);
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride, a.pre_dinv != nullptr);
   double acc[NQ];
   T blk[NQ];
 #pragma unroll
@@ -1218,8 +1248,9 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
   const T rim1_t = static_cast<T>(rim1);
   const T vroot = static_cast<T>(a.virt_root);
   const int rt = sa.rt, vstride = sa.vstride;
-  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride);
+  const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride, a.pre_dinv != nullptr);
   VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
+  VT* out_pre = a.pre_dinv ? out + a.vec_stride : nullptr;   // slot i+2: dinv (.) u_{i+1}
   double nb = 0.0, nrm = 0.0, gr[NQ];
   T bnb = T(0), bnrm = T(0), bgr[NQ];
 #pragma unroll
@@ -1235,7 +1266,7 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     nrow = 0;
   };
   // one row: w' (or the source), u_{i+1} = w' - sum_k coef_k u_k, and its sums (in row order)
-  auto row_update = [&](T src, T ui, T uim1, const T* uk, int64_t grow) {
+  auto row_update = [&](T src, T ui, T uim1, const T* uk, int64_t grow, double dv) {
     T wp;
     if (SECOND) {
       wp = src;
@@ -1251,7 +1282,10 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     for (int q = 0; q < NQ; ++q)
       if (q * M + L.part < NK) chn[q % NC] = fma(uk[q], cf[q], chn[q % NC]);
     const VT vv = static_cast<VT>(A::sub(wp, chain_total<M, T>(chn)));
-    if (pv && L.part == 0) out[grow * a.ldc] = vv;
+    if (pv && L.part == 0) {
+      out[grow * a.ldc] = vv;
+      if (out_pre) out_pre[grow * a.ldc] = static_cast<VT>(__dmul_rn(dv, static_cast<double>(vv)));
+    }
     const T vd = static_cast<T>(vv);
     bnrm = fma(vd, vd, bnrm);
 #pragma unroll
@@ -1266,8 +1300,10 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
     const VT* stage = ring.buf + s * stage_elems;
     const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
-    auto load_row = [&](int rr, T& src, T& ui, T& uim1, T* uk) {
+    const double* sdinv = stage_dinv<VT>(stage, sa.nvec, rt, vstride);
+    auto load_row = [&](int rr, T& src, T& ui, T& uim1, T* uk, double& dv) {
       const VT* e = stage + pr + rr * ldc;
+      dv = out_pre ? sdinv[(r0 & 1) + rr] : 0.0;   // staged dinv window
       const uint32_t* brow = sbits + rr * kBitWords;
       const bool virt = r0 + rr == a.virt_row;
       src = static_cast<T>(e[0]);
@@ -1285,15 +1321,17 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     constexpr int U = NQ <= 2 ? 4 : (NQ <= 5 ? 2 : 1);
     for (; r + SL * (U - 1) < rows; r += SL * U) {
       T src[U], ui[U], uim1[U], uk[U][NQ];
+      double dv[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) load_row(r + SL * j, src[j], ui[j], uim1[j], uk[j]);
+      for (int j = 0; j < U; ++j) load_row(r + SL * j, src[j], ui[j], uim1[j], uk[j], dv[j]);
 #pragma unroll
-      for (int j = 0; j < U; ++j) row_update(src[j], ui[j], uim1[j], uk[j], r0 + r + SL * j);
+      for (int j = 0; j < U; ++j) row_update(src[j], ui[j], uim1[j], uk[j], r0 + r + SL * j, dv[j]);
     }
     for (; r < rows; r += SL) {
       T src1, ui1 = T(0), uim11 = T(0), uk1[NQ];
-      load_row(r, src1, ui1, uim11, uk1);
-      row_update(src1, ui1, uim11, uk1, r0 + r);
+      double dv1;
+      load_row(r, src1, ui1, uim11, uk1, dv1);
+      row_update(src1, ui1, uim11, uk1, r0 + r, dv1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[s]);
@@ -1514,11 +1552,12 @@ static bool staged_setup(const CgsArgs& a, bool second, const uint32_t* bits, St
     return v;
   };
   const int64_t rows_per_cta = (a.n + step_ctas(a.n) - 1) / step_ctas(a.n);
-  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t);
+  const bool dw = a.pre_dinv != nullptr;
+  const size_t row_bytes = static_cast<size_t>(nv) * a.ldc * sizeof(VT) + kBitWords * sizeof(uint32_t) + (dw ? 8 : 0);
   int64_t rt = static_cast<int64_t>((kStagedSmem - 256) / (kStages * row_bytes));
   rt = std::min<int64_t>(rt, std::max<int64_t>(1, rows_per_cta));
   while (rt > 1 && 128 + kStages * sizeof(VT) * stage_elems_of<VT>(nv, static_cast<int>(rt),
-                                                                    static_cast<int>(padded(rt))) > kStagedSmem)
+                                                                    static_cast<int>(padded(rt)), dw) > kStagedSmem)
     --rt;
   if (rt < 1) return false;
   s.rt = static_cast<int>(rt);
@@ -1578,8 +1617,10 @@ static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmA
   sa.red = red;
   sa.spmm = spmm;
   const size_t smem = 128 + kStages * sizeof(VT) *
-                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, sa.pass[0].vstride),
-                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, sa.pass[1].vstride));
+                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, sa.pass[0].vstride,
+                                                            a.pre_dinv != nullptr),
+                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, sa.pass[1].vstride,
+                                                            a.pre_dinv != nullptr));
   LaunchScope ls(K_CGS_UPDATE, st);
   // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
   // so the software grid barrier is safe (coop_supported() checked the SM count).

@@ -179,10 +179,14 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
     SLQ_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), st));
     g->cols = static_cast<int32_t*>(track(g, p));
   }
-  SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * std::max<int64_t>(n, 1) * 2, st));
+  // degree and dinv, each padded to an even length + 2 (16-byte aligned; bulk copies of dinv windows
+  // may read one element past n)
+  const int64_t dstride = ((std::max<int64_t>(n, 1) + 1) / 2) * 2 + 2;
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * dstride * 2, st));
+  SLQ_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * dstride * 2, st));
   track(g, p);
   g->degree = static_cast<double*>(p);
-  g->dinv = g->degree + std::max<int64_t>(n, 1);
+  g->dinv = g->degree + dstride;
   SLQ_CUDA(cudaMallocAsync(&p, sizeof(double) * 8 + sizeof(int) * 4, st));
   track(g, p);
   g->dscal = static_cast<double*>(p);

@@ -254,6 +254,17 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   ReduceArgs ra{};
   ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.kind = kind; ra.dscal = g->dscal; ra.reorth = reorth;
 
+  // Prescaled gathers (normalized Laplacian, narrow class, graphs whose dinv does not stay in L2):
+  // step kernel i also writes dinv (.) u_{i+1} into the slot of u_{i+2} (unused until step kernel i+1),
+  // and SpMM i+1 gathers it instead of u_{i+1} times a dinv[col] gather per nonzero.  Steps 1..S-2
+  // (step 0 gathers the probe bitmask, the last SpMM has no free slot).  A function of the graph and
+  // the step kernel's slot class only, so results stay bitwise independent of the chunk width.
+  static const bool pre_env = [] { const char* e = getenv("SLQ_PRESCALE"); return !(e && e[0] == '0'); }();
+  static const int64_t pre_min_n = [] {   // SLQ_PRESCALE_MIN_N: testing knob
+    const char* e = getenv("SLQ_PRESCALE_MIN_N");
+    return e ? static_cast<int64_t>(atoll(e)) : (int64_t(1) << 22);
+  }();
+  const bool prescale = pre_env && kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && ldc <= 32 && n >= pre_min_n;
   const int gx = 1 << 30;                 // one CTA per tile group
   const bool coop = coop_ok && bits != nullptr;
   const int gx2 = kSecondPassGrid;        // second pass: small grid-stride launch
@@ -279,6 +290,8 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     sa.red = ra;
     sa.work = s.work + 4 * i;
     sa.bits = (i == 0) ? bits : nullptr;
+    sa.upre = (prescale && i >= 1 && i <= S - 2) ? static_cast<const void*>(basis + (i + 1) * vs) : nullptr;
+    ca.pre_dinv = (prescale && i + 1 <= S - 2) ? g->dinv : nullptr;
     ca.i = i;
     ca.second = 0;
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only

@@ -563,3 +563,32 @@ def test_spmm_half2_mapping_bitwise_equals_full_warp(cuda_device, tmp_path, coun
     full = np.load(out)
     r = DeviceGraph(_hub_graph(), cuda_device).rules("normalized_laplacian", 3, 0, count, 12, dtype="f32")
     assert np.array_equal(np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]), full)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", FP64_TOL), ("f32", FP32_TOL)])
+def test_prescaled_gathers_match_oracle(cuda_device, tmp_path, dtype, tol):
+    # narrow-class normalized-Laplacian runs on large graphs gather dinv (.) u written by the step
+    # kernel instead of u times a dinv[col] gather; forced on a small graph here (SLQ_PRESCALE_MIN_N=0):
+    # heat within the north-star tolerance of the oracle, and within rounding of the unscaled gathers
+    import os
+    import subprocess
+    import sys
+
+    out = tmp_path / "heat.npy"
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests'); import numpy as np, golden; "
+            "from test_gpu_parity import _hub_graph, GRID; from paper_2003_01282_b200 import _lib; "
+            "from paper_2003_01282_b200.device import DeviceGraph; "
+            f"r = DeviceGraph(_hub_graph()).rules('normalized_laplacian', 0, 0, 24, 15, dtype='{dtype}'); "
+            "v, _ = r.integrate(np.array(GRID.values), [_lib.FN_HEAT]); "
+            f"np.save('{out}', v.cpu().numpy()[0])")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, SLQ_PRESCALE_MIN_N="0"), cwd=root)
+    pre = np.load(out)
+    g = _hub_graph()
+    r = DeviceGraph(g, cuda_device).rules("normalized_laplacian", 0, 0, 24, 15, dtype=dtype)
+    plain, _ = r.integrate(np.array(GRID.values), [_lib.FN_HEAT])
+    plain = plain.cpu().numpy()[0]
+    ref, _ = O.heat_trace(g, GRID.values, 24, 15, 0)
+    assert golden.rel_l2(pre, ref) <= tol
+    assert golden.rel_l2(pre, plain) <= (1e-12 if dtype == "f64" else 1e-5)
+    assert not np.array_equal(pre, plain) or dtype == "f64"   # the prescaled path actually ran (fp32 rounding differs)
