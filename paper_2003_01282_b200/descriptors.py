@@ -86,16 +86,19 @@ def _params(cfg: SlqConfig) -> dict:
     return {"n_v": cfg.n_v, "s": cfg.s, "distribution": cfg.distribution, "seed": cfg.seed}
 
 
-def _integrate_host(rules, t, codes):
-    """Device quadrature + aggregate for every integrand, ONE device->host copy, then the status check."""
+def _integrate_host(rules, t, codes, host_work=None):
+    """Device quadrature + aggregate for every integrand, ONE device->host copy, then the status check.
+    ``host_work()`` (the descriptor's graph hash) runs on the host while the device computes."""
     import torch
 
     vals, stds = rules.integrate(t, codes)
-    packed = torch.cat([vals.reshape(-1), stds.reshape(-1), rules.status.to(torch.float64)]).cpu().numpy()
+    packed = torch.cat([vals.reshape(-1), stds.reshape(-1), rules.status.to(torch.float64)])
+    extra = host_work() if host_work is not None else None   # overlaps the queued device work
+    packed = packed.cpu().numpy()
     _lib.check_status(int(packed[-1]))
     k = vals.numel()
     shape = tuple(vals.shape)
-    return packed[:k].reshape(shape), packed[k:2 * k].reshape(shape)
+    return packed[:k].reshape(shape), packed[k:2 * k].reshape(shape), extra
 
 
 def _hash(g: Graph, with_hash: bool) -> str:
@@ -113,8 +116,7 @@ def netlsd_heat_wave_slq(g: Graph, grid: TimeGrid | None = None, cfg: SlqConfig 
     rules = slq_rules(op, cfg, dtype=dtype, shard=shard)
     t = np.asarray(grid.values, dtype=np.float64)
     codes = [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM] if wave else [_lib.FN_HEAT]
-    vals, stds = _integrate_host(rules, t, codes)
-    gh = _hash(g, with_hash)
+    vals, stds, gh = _integrate_host(rules, t, codes, lambda: _hash(g, with_hash))
     heat = HeatTraceDescriptor(grid=grid, values=vals[0], method="slq", params=_params(cfg), graph_hash=gh,
                                std_errors=stds[0])
     if not wave:
@@ -143,8 +145,8 @@ def vnge_slq(g: Graph, cfg: SlqConfig | None = None, *, threads: int = 1, dtype:
     cfg = cfg or SlqConfig()
     op = make_operator(g, OperatorKind.DENSITY)
     rules = slq_rules(op, cfg, dtype=dtype, shard=shard)
-    val, std = _integrate_host(rules, None, [_lib.FN_XLOGX])
-    return EntropyValue(value=-float(val[0, 0]), method="slq", params=_params(cfg), graph_hash=_hash(g, with_hash),
+    val, std, gh = _integrate_host(rules, None, [_lib.FN_XLOGX], lambda: _hash(g, with_hash))
+    return EntropyValue(value=-float(val[0, 0]), method="slq", params=_params(cfg), graph_hash=gh,
                         std_error=float(std[0, 0]))
 
 

@@ -56,7 +56,8 @@ class DeviceGraph:
         self._info = None
         # empty rows counted on the host first: graphs below the threshold never synchronise here
         if fold is not None and self.n >= FOLD_MIN_N and g.nnz > 0:
-            empty = int(np.count_nonzero(np.diff(np.asarray(g.row_offsets)) == 0))
+            off = np.asarray(g.row_offsets)
+            empty = int(off.size - 1 - np.count_nonzero(off[1:] != off[:-1]))
             if empty >= 1 and empty >= fold * self.n:
                 self.fold_isolated(fold)
 

@@ -72,9 +72,10 @@ class Graph:
         if not self._hash:
             h = hashlib.sha256()
             h.update(np.int64(self.n).tobytes())
-            h.update(np.ascontiguousarray(self.row_offsets, dtype=np.int64).tobytes())
-            h.update(np.ascontiguousarray(self.col_indices, dtype=np.int64).tobytes())
-            h.update(np.ascontiguousarray(self.weights, dtype=np.float64).tobytes())
+            # buffer views, no byte copies (hashlib reads contiguous arrays in place)
+            h.update(memoryview(np.ascontiguousarray(self.row_offsets, dtype=np.int64)).cast("B"))
+            h.update(memoryview(np.ascontiguousarray(self.col_indices, dtype=np.int64)).cast("B"))
+            h.update(memoryview(np.ascontiguousarray(self.weights, dtype=np.float64)).cast("B"))
             self._hash.append(h.hexdigest())
         return self._hash[0]
 
