@@ -35,7 +35,18 @@ __device__ __forceinline__ int tridiag_ql_first_row(double* d, double* e, double
       for (int i = mm - 1; i >= l; --i) {
         double f = s * e[i];
         const double b = c * e[i];
-        r = fast_hypot(f, g);
+        // r = hypot(f, g) and 1/r from one reciprocal square root (one long-latency sequence on the
+        // rotation's dependent chain instead of a square root and a division)
+        double rinv;
+        const double mfg = fmax(fabs(f), fabs(g));
+        if (mfg > 1e-150 && mfg < 1e150) {
+          const double h2 = fma(f, f, g * g);
+          rinv = rsqrt(h2);
+          r = h2 * rinv;
+        } else {
+          r = hypot(f, g);
+          rinv = r != 0.0 ? 1.0 / r : 0.0;
+        }
         e[i + 1] = r;
         if (r == 0.0) {          // underflow: split the matrix here and restart
           d[i + 1] -= p;
@@ -43,7 +54,6 @@ __device__ __forceinline__ int tridiag_ql_first_row(double* d, double* e, double
           deflated = true;
           break;
         }
-        const double rinv = 1.0 / r;
         s = f * rinv;
         c = g * rinv;
         g = d[i + 1] - p;

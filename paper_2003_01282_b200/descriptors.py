@@ -110,11 +110,15 @@ def netlsd_heat_wave_slq(g: Graph, grid: TimeGrid | None = None, cfg: SlqConfig 
                          with_hash: bool = True):
     """Heat (and wave) traces from one device Lanczos run on the normalized Laplacian."""
     del threads
+    import torch
+
     grid = grid or TimeGrid()
     cfg = cfg or SlqConfig()
+    # the timescales go up first, while the stream is idle: a pageable upload queued behind the
+    # Lanczos run would block the host until the device finishes (no overlap with the graph hash)
+    t = torch.tensor(np.array(grid.values, dtype=np.float64), device=_lib.require_cuda().cuda.current_device())
     op = make_operator(g, OperatorKind.NORMALIZED_LAPLACIAN)
     rules = slq_rules(op, cfg, dtype=dtype, shard=shard)
-    t = np.asarray(grid.values, dtype=np.float64)
     codes = [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM] if wave else [_lib.FN_HEAT]
     vals, stds, gh = _integrate_host(rules, t, codes, lambda: _hash(g, with_hash))
     heat = HeatTraceDescriptor(grid=grid, values=vals[0], method="slq", params=_params(cfg), graph_hash=gh,
