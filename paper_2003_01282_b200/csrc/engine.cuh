@@ -933,6 +933,10 @@ constexpr int kNarrowSlots = 12;    // row slots of the narrow class (ldc <= 32)
 constexpr int kSlotThreads = 128;                                 // max threads per row slot
 constexpr int kStepThreads = 32 + kStageSlots * kSlotThreads;   // producer warp + <= 384 consumers
 constexpr int kStagedMaxLdc = 128;
+#ifndef SLQ_STEP_REVERSE
+#define SLQ_STEP_REVERSE 1
+#endif
+constexpr bool kReverseUpdate = SLQ_STEP_REVERSE != 0;   // update phases stream their chunks backwards
 constexpr int kStages = 3;
 constexpr int kMaxStaged = kCgsBlock + 4;
 constexpr size_t kStagedSmem = 200 * 1024;   // + 20 KB static: within the 227 KB per CTA
@@ -999,12 +1003,15 @@ __device__ __forceinline__ int chunk_count(int64_t lo, int64_t hi, int rt) {
 
 // Producer (one lane): chunk j of [lo, hi) goes to ring slot (ch0 + j) % kStages.
 template <typename VT>
-__device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi) {
+__device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<VT>& ring, int ch0, int64_t lo, int64_t hi,
+                                               bool rev = false) {
   const int64_t ldc = sa.a.ldc;
   const bool dw = sa.a.pre_dinv != nullptr;
   const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, sa.rt, sa.vstride, dw);
   int ch = ch0;
-  for (int64_t r0 = lo; r0 < hi; r0 += sa.rt, ++ch) {
+  const int nch = chunk_count(lo, hi, sa.rt);
+  for (int jc = 0; jc < nch; ++jc, ++ch) {
+    const int64_t r0 = lo + static_cast<int64_t>(rev ? nch - 1 - jc : jc) * sa.rt;
     const int s = ch % kStages;
     if (ch >= kStages) mbar_wait(&ring.empty[s], ((ch / kStages) - 1) & 1);
     const int rows = static_cast<int>(hi - r0 < sa.rt ? hi - r0 : sa.rt);
@@ -1294,7 +1301,11 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     if (A::kFlush && ++nrow == A::kFlush) flush();
   };
   int ch = ch0;
-  for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
+  // chunks in REVERSE order: the first chunks of the update are the last ones phase A streamed, still
+  // in L2 (rows keep their slots, so only the order of the per-slot partial sums changes)
+  const int nch = chunk_count(lo, hi, rt);
+  for (int jc = 0; jc < nch; ++jc, ++ch) {
+    const int64_t r0 = lo + static_cast<int64_t>(kReverseUpdate ? nch - 1 - jc : jc) * rt;
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
     const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
@@ -1317,17 +1328,25 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
         uk[q] = kk < NK ? stage_u<VT, T>(e, brow, vstride, pr, kk, virt, vroot) : T(0);
       }
     };
-    int r = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);
+    // this slot's rows of the chunk; with kReverseUpdate they run in DESCENDING order (chunks
+    // backwards and rows backwards within them), so every slot's row sequence is the reverse of its
+    // ascending one whatever the chunk size rt (results stay independent of the chunk width)
     constexpr int U = NQ <= 2 ? 4 : (NQ <= 5 ? 2 : 1);
-    for (; r + SL * (U - 1) < rows; r += SL * U) {
+    constexpr int D = kReverseUpdate ? -SL : SL;   // row step
+    const int first = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);
+    const int last = first < rows ? first + SL * ((rows - 1 - first) / SL) : first - SL;
+    const int cnt = first < rows ? (last - first) / SL + 1 : 0;
+    int r = kReverseUpdate ? last : first;
+    int k = 0;
+    for (; k + U <= cnt; k += U, r += D * U) {
       T src[U], ui[U], uim1[U], uk[U][NQ];
       double dv[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) load_row(r + SL * j, src[j], ui[j], uim1[j], uk[j], dv[j]);
+      for (int j = 0; j < U; ++j) load_row(r + D * j, src[j], ui[j], uim1[j], uk[j], dv[j]);
 #pragma unroll
-      for (int j = 0; j < U; ++j) row_update(src[j], ui[j], uim1[j], uk[j], r0 + r + SL * j, dv[j]);
+      for (int j = 0; j < U; ++j) row_update(src[j], ui[j], uim1[j], uk[j], r0 + r + D * j, dv[j]);
     }
-    for (; r < rows; r += SL) {
+    for (; k < cnt; ++k, r += D) {
       T src1, ui1 = T(0), uim11 = T(0), uk1[NQ];
       double dv1;
       load_row(r, src1, ui1, uim11, uk1, dv1);
@@ -1384,7 +1403,7 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
   const int nk = a.i + 1, nq = nk + 2, nslot = S.S + 1;
   // C / C': update
   if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi);
+    if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi, kReverseUpdate);
   } else {
     phase_update<VT, NK, SECOND, M, SL>(st, ring, ch, lo, hi, cf_sm);
   }
