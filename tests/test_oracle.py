@@ -140,3 +140,44 @@ def test_er_batch_sample_matches_reference():
         g = golden.graph(z, f"{k}/")
         heat, _ = O.heat_trace(g, t, 20, 10, 0)
         assert golden.rel_l2(heat, z[f"{k}/heat"]) <= 1e-12, k
+
+
+def _fold(g):
+    """CPU restatement of the isolated-vertex fold (csrc/graph.cu graph_fold): unreferenced empty
+    rows leave the graph, one trailing empty row is appended, columns relabelled monotonically."""
+    from paper_2003_01282_b200.graphs import Graph
+
+    off = np.asarray(g.row_offsets)
+    cols = np.asarray(g.col_indices)
+    keep = np.diff(off) > 0
+    keep[cols] = True
+    newid = np.cumsum(keep) - keep
+    nprime = int(keep.sum())
+    off_f = np.append(off[:-1][keep], [g.nnz, g.nnz]).astype(np.int64)
+    folded = Graph(n=nprime + 1, row_offsets=off_f, col_indices=newid[cols].astype(np.int64),
+                   weights=np.array(g.weights, dtype=np.float64), m=g.m)
+    return folded, keep, g.n - nprime
+
+
+@pytest.mark.parametrize("kind", ["L", "NL", "P"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_isolated_vertex_fold_identity(kind, weighted):
+    # The fold's claim (DESIGN §3): Lanczos on the folded graph from the folded start vector
+    # [z_kept, sqrt(m)] / sqrt(n) gives the tridiagonals of the unfolded run up to rounding.
+    from paper_2003_01282_b200.graphs import csr_from_edges
+
+    rng = np.random.default_rng(7)
+    n = 400
+    live = np.flatnonzero(rng.random(n) < 0.55)
+    u, v = live[rng.integers(0, live.size, 900)], live[rng.integers(0, live.size, 900)]
+    g = csr_from_edges(n, u, v, rng.uniform(0.5, 2.0, 900) if weighted else None)
+    gf, keep, m = _fold(g)
+    assert m > 100 and gf.n == n - m + 1
+    q0 = O.draw_probes(n, 3, range(6))
+    q0f = np.vstack([q0[keep], np.sqrt(m) * np.abs(q0[~keep][:1])])   # |z| = 1/sqrt(n) on every row
+    t1 = O.lanczos_block(O.make_block_operator(g, KIND[kind]), q0, 12)
+    t2 = O.lanczos_block(O.make_block_operator(gf, KIND[kind]), q0f, 12)
+    assert np.array_equal(t1.steps, t2.steps)
+    scale = np.abs(t1.alpha).max()
+    assert np.max(np.abs(t1.alpha - t2.alpha)) <= 1e-12 * scale
+    assert np.max(np.abs(t1.beta - t2.beta)) <= 1e-12 * scale
