@@ -229,6 +229,12 @@ reduce_kernel(ReduceArgs a) {
 // Which thread owns a probe never changes its arithmetic: every per-probe sum runs in a fixed order
 // set by the graph's tiles and the warp count, never by c.
 constexpr int kBlk = 128;
+// probes per SpMM CTA block (grid.y = ceil(c / kSpmmBlk)): 64 gives each lane <= 2 probes, so a warp
+// keeps twice the gathered rows in flight in the same registers
+#ifndef SLQ_SPMM_BLK
+#define SLQ_SPMM_BLK 128
+#endif
+constexpr int kSpmmBlk = SLQ_SPMM_BLK;
 constexpr int kSpmmWarps = 8;
 #ifndef SLQ_SPMM_UNRF
 #define SLQ_SPMM_UNRF 8    // gathered values in flight per lane in the full-warp mapping (UNR * PPL)
@@ -324,12 +330,13 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
   const int lane = threadIdx.x & 31;
   const int plane = HALF ? (lane & 15) : lane;   // probe lane
   const int sub = HALF ? (lane >> 4) : 0;        // HALF: chain (position parity) of this half
+  const int boff = blockIdx.y * (kSpmmBlk / 32);  // bitmask word of this CTA's first probe
   constexpr bool SK = KIND == SLQ_NORMALIZED_LAPLACIAN || (!EXACT && WEIGHTED);   // kNLPre: weights only
   double a0[PPL], a1[PPL];
 #pragma unroll
   for (int j = 0; j < PPL; ++j) a0[j] = a1[j] = 0.0;
   auto value = [&](const VT* src, const uint32_t* brow, int j) -> double {
-    if (BITS) return ((__ldg(brow + j) >> plane) & 1u) ? 1.0 : -1.0;
+    if (BITS) return ((__ldg(brow + boff + j) >> plane) & 1u) ? 1.0 : -1.0;
     return ldg_f64(src + pidx[j]);
   };
   for (int64_t base = beg; base < end; base += 32) {
@@ -435,7 +442,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
           const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
           const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-          for (int j = 0; j < PPL; ++j) xv[q][j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
+          for (int j = 0; j < PPL; ++j) xv[q][j] = ((wd[boff + j] >> lane) & 1u) ? 1.0 : -1.0;
         } else {
           const VT* src = u + o;
 #pragma unroll
@@ -463,7 +470,7 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
         const uint4 wv = __ldg(reinterpret_cast<const uint4*>(bits + o));
         const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) xr[j] = ((wd[j] >> lane) & 1u) ? 1.0 : -1.0;
+        for (int j = 0; j < PPL; ++j) xr[j] = ((wd[boff + j] >> lane) & 1u) ? 1.0 : -1.0;
       } else {
         const VT* src = u + o;
 #pragma unroll
@@ -514,13 +521,13 @@ spmm_kernel(SpmmArgs a) {
   const bool writer = !HALF || lane < 16;
   // probe j of this lane: pbase + PS j.  HALF2 (HALF, PPL = 2): probes 2 plane, 2 plane + 1.
   constexpr int PS = HALF ? 1 : 32;
-  const int pbase = blockIdx.y * kBlk + (HALF ? PPL : 1) * plane;
+  const int pbase = blockIdx.y * kSpmmBlk + (HALF ? PPL : 1) * plane;
   bool pv[PPL];
   int pidx[PPL];   // column offsets within a gathered row, clamped to a valid probe
 #pragma unroll
   for (int j = 0; j < PPL; ++j) {
     pv[j] = probe_ok(pbase + PS * j, a.c);
-    pidx[j] = pv[j] ? PS * j : (a.c - 1 - (pbase - blockIdx.y * kBlk));
+    pidx[j] = pv[j] ? PS * j : (a.c - 1 - (pbase - blockIdx.y * kSpmmBlk));
   }
   if (HALF && PPL == 2) {
     // one vector load per pair: a pair past the row's end (2 plane + 1 >= ldc) reads the row's first
@@ -582,7 +589,7 @@ spmm_kernel(SpmmArgs a) {
         if (!pv[j] || !writer) continue;
         const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + PS * j);
         const double x = __dmul_rn(
-            own_value<VT, PPL, BITS, PS>(u, ldi, a.bits, row, j, pbase - blockIdx.y * kBlk + PS * j), rj);
+            own_value<VT, PPL, BITS, PS>(u, ldi, a.bits, row, j, pbase + PS * j), rj);
         const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * rj, d, dis, scale);
         w[row * a.ldc_out + PS * j] = from_f64<VT>(y);
       }
@@ -595,7 +602,7 @@ template <typename VT, int KIND, int PPL>
 __global__ void __launch_bounds__(kSpmmWarps * 32)
 spmm_long_finish_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pbase = blockIdx.y * kBlk + lane;
+  const int pbase = blockIdx.y * kSpmmBlk + lane;
   const int64_t nlong = a.long_counts[0];
   const VT* __restrict__ u = static_cast<const VT*>(a.u) + pbase;
   VT* __restrict__ w = static_cast<VT*>(a.w) + pbase;
@@ -615,7 +622,7 @@ spmm_long_finish_kernel(SpmmArgs a) {
         for (int64_t sg = s0; sg < s1; ++sg) acc = __dadd_rn(acc, a.segpart[sg * a.cpad + p]);
         if (a.r) acc *= a.r[p];   // Lanczos path: segments hold unscaled sums
         const double rj = a.r ? a.r[p] : 1.0;
-        const double own = a.bits ? (((a.bits[row * kBitWords + j] >> lane) & 1u) ? 1.0 : -1.0)
+        const double own = a.bits ? (((a.bits[row * kBitWords + (p >> 5)] >> (p & 31)) & 1u) ? 1.0 : -1.0)
                                   : ldg_f64(u + row * a.ldc_in + 32 * j);
         const double x = __dmul_rn(own, rj);
         const double y = op_epilogue<KIND>(x, acc, d, dis, scale);
@@ -626,7 +633,7 @@ spmm_long_finish_kernel(SpmmArgs a) {
 }
 
 static int ppl_for(int c) {
-  const int cb = c < kBlk ? c : kBlk;
+  const int cb = c < kSpmmBlk ? c : kSpmmBlk;
   return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
 }
 
@@ -702,7 +709,7 @@ static void launch_spmm_main(int kind, SpmmArgs& a, int gy, cudaStream_t st) {
 // The SpMM pass (short rows + long-row segments), then the long-row finish when the graph has any.
 template <typename VT>
 static void launch_spmm(int kind, SpmmArgs a, cudaStream_t st, bool finish = true) {
-  const int gy = ceil_div(a.c, kBlk);
+  const int gy = ceil_div(a.c, kSpmmBlk);
   launch_spmm_main<VT>(kind, a, gy, st);
   if (finish && a.long_counts && a.max_long > 0) {
     LaunchScope ls(K_SPMM, st);
