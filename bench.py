@@ -354,6 +354,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": UNIT, "seconds_per_signature": e2e_s,
+                "ms_signatures": [round(1e3 * x, 3) for x in e2e_times],
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "netlsd_heat_wave_slq(Graph on pinned host arrays) incl. H2D, device prepare, D2H",
                 "seconds_per_signature_with_graph_hash": float(np.min(hash_times))},
