@@ -376,6 +376,22 @@ static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
       static_cast<double>(g->isolated) < min_fraction * static_cast<double>(n))
     return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(g->stream);
+  {
+    // the fold holds a second CSR: skip it (not an error) when the device cannot hold it comfortably
+    size_t freeb = 0, total = 0;
+    cudaMemGetInfo(&freeb, &total);
+    double avail = static_cast<double>(freeb);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+      uint64_t reserved = 0, used = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      if (reserved > used) avail += static_cast<double>(reserved - used);
+    }
+    const double need = 40.0 * static_cast<double>(n) + (g->weights ? 12.0 : 4.0) * static_cast<double>(nnz) +
+                        static_cast<double>(1ull << 28);
+    if (need > 0.9 * avail) return SLQ_OK;
+  }
   int32_t* keep = nullptr;    // [n+1] keep flags, then the remap
   int32_t* newid = nullptr;   // [n+1] exclusive scan of keep
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keep), sizeof(int32_t) * (n + 1), st));

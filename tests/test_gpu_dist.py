@@ -87,3 +87,56 @@ def test_two_ranks_across_slot_classes_agree_to_rounding(cuda_device):
     assert np.array_equal(got[2], ref[2])
     assert np.max(np.abs(got[0] - ref[0])) <= 1e-13
     assert np.max(np.abs(got[3] - ref[3]) / np.abs(ref[3])) <= 1e-13
+
+
+def _worker_rmat(rank, world, port, out, env):
+    import torch.distributed as dist
+
+    os.environ.update(env)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2003_01282_b200 import _lib
+    from paper_2003_01282_b200.descriptors import TimeGrid
+    from paper_2003_01282_b200.device import DeviceGraph
+    from paper_2003_01282_b200.dist import sharded_rules
+    from paper_2003_01282_b200.slq import SlqConfig
+
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    dg = DeviceGraph.rmat(14, 16, seed=5, device=torch.device("cuda", 0))
+    cfg = SlqConfig(n_v=32, s=15, seed=0)
+    if world > 1:
+        rules = sharded_rules(dg, "normalized_laplacian", cfg, dtype="f32")
+    else:
+        rules = dg.rules("normalized_laplacian", 0, 0, 32, 15, dtype="f32")
+    vals, _ = rules.integrate(np.array(TimeGrid(1e-2, 1e2, 64).values), [_lib.FN_HEAT])
+    if rank == 0:
+        out.put((dg.folded, rules.nodes.cpu().numpy(), rules.weights.cpu().numpy(), vals.cpu().numpy()))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _run_rmat(world, env):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_rmat, args=(r, world, port, q, env)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_two_ranks_folded_prescaled_bitwise_equal_single_rank(cuda_device):
+    # the C5 configuration in miniature: a device-built R-MAT graph with its isolated vertices folded,
+    # fp32, prescaled gathers forced on (SLQ_PRESCALE_MIN_N=0); one rank runs a 32-probe chunk (HALF2
+    # SpMM), two ranks run 16 each (HALF SpMM) — same narrow class, so the rules are bitwise equal
+    env = {"SLQ_PRESCALE_MIN_N": "0"}
+    one, two = _run_rmat(1, env), _run_rmat(2, env)
+    assert one[0] > 0 and one[0] == two[0]
+    for a, b in zip(one[1:], two[1:]):
+        assert np.array_equal(a, b)
