@@ -317,7 +317,7 @@ __device__ __forceinline__ double gather_term(double xraw, double r, double sk, 
 // Columns are loaded 32 at a time; each lane turns its column into an element offset once and the
 // warp broadcasts offsets with one shuffle per nonzero.  Probe slots beyond c are clamped to a valid
 // column (loaded, never stored), so the loads need no predicates.
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF>
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF, bool V2 = false>
 __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
                                              const double* __restrict__ wts, const VT* __restrict__ u, int64_t ldi,
                                              const uint32_t* __restrict__ bits, const int* pidx, int64_t beg,
@@ -430,6 +430,46 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
       }
       continue;
     }
+    if constexpr (V2 && !HALF && !BITS && !EXACT && PPL >= 2) {
+      // VEC2 (wide chunks): lane l holds probe pairs (64 j + 2 l, 64 j + 2 l + 1) and reads each pair
+      // with one 2-element vector load (half the load instructions of the scalar mapping); every
+      // probe is still one sequential chain, so results equal the scalar mapping bit for bit
+      using P2 = typename std::conditional<std::is_same<VT, double>::value, double2, float2>::type;
+      constexpr int NP = PPL / 2;
+      constexpr int U2 = SLQ_SPMM_UNRF / PPL;
+      int k = 0;
+      for (; k + U2 <= cnt; k += U2) {
+        P2 xv[U2][NP];
+#pragma unroll
+        for (int q = 0; q < U2; ++q) {
+          const int64_t o = __shfl_sync(FULL, myoff, k + q);
+#pragma unroll
+          for (int jj = 0; jj < NP; ++jj) xv[q][jj] = __ldg(reinterpret_cast<const P2*>(u + o + pidx[jj]));
+        }
+#pragma unroll
+        for (int q = 0; q < U2; ++q) {
+          const double sk = SK ? __shfl_sync(FULL, mys, k + q) : 1.0;
+#pragma unroll
+          for (int jj = 0; jj < NP; ++jj) {
+            const double x0 = static_cast<double>(xv[q][jj].x), x1 = static_cast<double>(xv[q][jj].y);
+            a0[2 * jj] = SK ? fma(sk, x0, a0[2 * jj]) : a0[2 * jj] + x0;
+            a0[2 * jj + 1] = SK ? fma(sk, x1, a0[2 * jj + 1]) : a0[2 * jj + 1] + x1;
+          }
+        }
+      }
+      for (; k < cnt; ++k) {
+        const int64_t o = __shfl_sync(FULL, myoff, k);
+        const double sk = SK ? __shfl_sync(FULL, mys, k) : 1.0;
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) {
+          const P2 xv = __ldg(reinterpret_cast<const P2*>(u + o + pidx[jj]));
+          const double x0 = static_cast<double>(xv.x), x1 = static_cast<double>(xv.y);
+          a0[2 * jj] = SK ? fma(sk, x0, a0[2 * jj]) : a0[2 * jj] + x0;
+          a0[2 * jj + 1] = SK ? fma(sk, x1, a0[2 * jj + 1]) : a0[2 * jj + 1] + x1;
+        }
+      }
+      continue;
+    }
     constexpr int UNR = SLQ_SPMM_UNRF / PPL;   // gathers in flight per lane (even: chain = q & 1)
     int k = 0;
     for (; k + UNR <= cnt; k += UNR) {
@@ -513,21 +553,32 @@ __device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint
 #ifndef SLQ_SPMM_MINB4
 #define SLQ_SPMM_MINB4 3   // resident CTAs per SM for PPL = 4 (80 registers: no spills in the 4-probe lanes)
 #endif
-template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF>
-__global__ void __launch_bounds__(kSpmmWarps * 32, PPL == 4 ? SLQ_SPMM_MINB4 : 4)
+#ifndef SLQ_SPMM_MINB1
+#define SLQ_SPMM_MINB1 4   // resident CTAs per SM for PPL = 1 and 2
+#endif
+template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF, bool V2 = false>
+__global__ void __launch_bounds__(kSpmmWarps * 32, PPL == 4 ? SLQ_SPMM_MINB4 : SLQ_SPMM_MINB1)
 spmm_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   const int plane = HALF ? (lane & 15) : lane;   // HALF: two half-warps share probes 0..15 (0..31)
   const bool writer = !HALF || lane < 16;
-  // probe j of this lane: pbase + PS j.  HALF2 (HALF, PPL = 2): probes 2 plane, 2 plane + 1.
+  // probe j of this lane: pbase + poff(j).  HALF2 (HALF, PPL = 2): probes 2 plane, 2 plane + 1;
+  // VEC2: probes 64 (j / 2) + 2 lane + (j % 2); otherwise plane + 32 j.
   constexpr int PS = HALF ? 1 : 32;
-  const int pbase = blockIdx.y * kSpmmBlk + (HALF ? PPL : 1) * plane;
+  auto poff = [](int j) { return V2 ? 64 * (j >> 1) + (j & 1) : PS * j; };
+  const int pbase = blockIdx.y * kSpmmBlk + ((HALF || V2) ? (HALF ? PPL : 2) : 1) * plane;
   bool pv[PPL];
   int pidx[PPL];   // column offsets within a gathered row, clamped to a valid probe
 #pragma unroll
   for (int j = 0; j < PPL; ++j) {
-    pv[j] = probe_ok(pbase + PS * j, a.c);
-    pidx[j] = pv[j] ? PS * j : (a.c - 1 - (pbase - blockIdx.y * kSpmmBlk));
+    pv[j] = probe_ok(pbase + poff(j), a.c);
+    pidx[j] = pv[j] ? poff(j) : (a.c - 1 - (pbase - blockIdx.y * kSpmmBlk));
+  }
+  if (V2) {
+    // pair jj: one vector load at offset 64 jj; a pair past the row's end reads the row's first pair
+#pragma unroll
+    for (int jj = 0; jj < PPL / 2; ++jj)
+      pidx[jj] = blockIdx.y * kSpmmBlk + 64 * jj + 2 * plane + 1 < a.ldc_in ? 64 * jj : -2 * plane;
   }
   if (HALF && PPL == 2) {
     // one vector load per pair: a pair past the row's end (2 plane + 1 >= ldc) reads the row's first
@@ -559,12 +610,12 @@ spmm_kernel(SpmmArgs a) {
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg, end,
-                                                            acc);
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg,
+                                                                end, acc);
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
     for (int j = 0; j < PPL; ++j)
-      if (pv[j] && writer) dst[PS * j] = acc[j];
+      if (pv[j] && writer) dst[poff(j)] = acc[j];
   }
   // phase 2: row tiles, one warp each (dynamic); rows in order
   unsigned long long* tcounter = counter + 2;
@@ -580,18 +631,19 @@ spmm_kernel(SpmmArgs a) {
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg, end,
-                                                              acc);
+      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg,
+                                                                  end, acc);
       const double d = __ldg(a.degree + row);
       const double dis = nl_kind<KIND>() ? __ldg(dinv + row) : 0.0;
 #pragma unroll
       for (int j = 0; j < PPL; ++j) {
         if (!pv[j] || !writer) continue;
-        const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + PS * j);
-        const double x = __dmul_rn(
-            own_value<VT, PPL, BITS, PS>(u, ldi, a.bits, row, j, pbase + PS * j), rj);
+        const double rj = EXACT ? 1.0 : __ldg(a.r + pbase + poff(j));
+        const double own = BITS ? own_value<VT, PPL, BITS, PS>(u, ldi, a.bits, row, j, pbase + poff(j))
+                                : ldg_f64(u + row * ldi + poff(j));
+        const double x = __dmul_rn(own, rj);
         const double y = op_epilogue<KIND>(x, EXACT ? acc[j] : acc[j] * rj, d, dis, scale);
-        w[row * a.ldc_out + PS * j] = from_f64<VT>(y);
+        w[row * a.ldc_out + poff(j)] = from_f64<VT>(y);
       }
     }
   }
@@ -632,6 +684,12 @@ spmm_long_finish_kernel(SpmmArgs a) {
   }
 }
 
+// VEC2 mapping for wide chunks (SLQ_SPMM_VEC2=0 keeps the scalar mapping; same arithmetic)
+static bool vec2_on() {
+  static const bool v = [] { const char* e = getenv("SLQ_SPMM_VEC2"); return !(e && e[0] == '0'); }();
+  return v;
+}
+
 static int ppl_for(int c) {
   const int cb = c < kSpmmBlk ? c : kSpmmBlk;
   return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
@@ -663,6 +721,8 @@ static void spmm_launch_one(SpmmArgs& a, int gy, cudaStream_t st) {
     else spmm_kernel<VT, KIND, W, 1, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   } else if (a.bits) {
     spmm_kernel<VT, KIND, W, PPL, true, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+  } else if (PPL >= 2 && vec2_on()) {
+    spmm_kernel<VT, KIND, W, PPL, false, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   } else {
     spmm_kernel<VT, KIND, W, PPL, false, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
   }

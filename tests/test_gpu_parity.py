@@ -592,3 +592,25 @@ def test_prescaled_gathers_match_oracle(cuda_device, tmp_path, dtype, tol):
     assert golden.rel_l2(pre, ref) <= tol
     assert golden.rel_l2(pre, plain) <= (1e-12 if dtype == "f64" else 1e-5)
     assert not np.array_equal(pre, plain) or dtype == "f64"   # the prescaled path actually ran (fp32 rounding differs)
+
+
+@pytest.mark.parametrize("count,dtype", [(100, "f64"), (50, "f64"), (70, "f32"), (128, "f32")])
+def test_spmm_vec2_mapping_bitwise_equals_scalar(cuda_device, tmp_path, count, dtype):
+    # wide chunks: the VEC2 mapping (probe pairs per lane, one vector load per pair) sums every probe
+    # in the same sequential chain as the scalar mapping (SLQ_SPMM_VEC2=0): rules bitwise equal
+    import os
+    import subprocess
+    import sys
+
+    out = tmp_path / "nodes.npy"
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests'); import numpy as np, golden; "
+            "from test_gpu_parity import _hub_graph; "
+            "from paper_2003_01282_b200.device import DeviceGraph; "
+            f"r = DeviceGraph(_hub_graph()).rules('normalized_laplacian', 1, 0, {count}, 12, dtype='{dtype}'); "
+            f"np.save('{out}', np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]))")
+    env = dict(os.environ, SLQ_SPMM_VEC2="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env,
+                   cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    scalar = np.load(out)
+    r = DeviceGraph(_hub_graph(), cuda_device).rules("normalized_laplacian", 1, 0, count, 12, dtype=dtype)
+    assert np.array_equal(np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]), scalar)
