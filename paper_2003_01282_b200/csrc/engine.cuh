@@ -1444,8 +1444,17 @@ static __device__ double stripe_sum(const double* partial, int ntiles, int nq, i
   const int64_t stride = static_cast<int64_t>(nq) * cpad;
   const double* src = partial + static_cast<int64_t>(q) * cpad + p;
   for (int sidx = warp; sidx < kStripes; sidx += nw) {
+    // 8 loads in flight, then the adds in the same sequential order (bitwise the plain loop)
     double s = 0.0;
-    for (int t = sidx; t < ntiles; t += kStripes) s += src[t * stride];
+    int t = sidx;
+    for (; t + 7 * kStripes < ntiles; t += 8 * kStripes) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = src[static_cast<int64_t>(t + j * kStripes) * stride];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; t < ntiles; t += kStripes) s += src[static_cast<int64_t>(t) * stride];
     red[sidx * 32 + lane] = s;
   }
   __syncthreads();
