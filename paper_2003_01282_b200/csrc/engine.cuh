@@ -800,6 +800,7 @@ struct CgsArgs {
   // normalized Laplacian, prescaled gathers: the update also writes dinv (.) u_{i+1} into the (still
   // unused) slot i+2 for the next SpMM (nullptr: not this step)
   const double* pre_dinv = nullptr;
+  unsigned long long* dbg = nullptr;   // SLQ_STEP_TIMING: %globaltimer of CTA 0 around each grid barrier
 };
 
 // w' = (w - alpha q_i) - beta_{i-1} q_{i-1}    (lanczos.py:129, numpy left-to-right evaluation)
@@ -1519,9 +1520,14 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
       const double rn = __ddiv_rn(1.0, b);
       S.beta[a.i * cp + p] = b;
       S.rsc[(a.i + 1) * cp + p] = rn;
-      const int j = a.i + 1;
-      for (int k = 0; k <= a.i; ++k) {
-        const double gkj = S.rsc[k * cp + p] * rn * S.gram[k * cp + p];
+      const int j = a.i + 1;   // == NK
+      // all loads first (the stores below could alias them for the compiler), then the stores
+      double rk[NK], gk[NK];
+#pragma unroll
+      for (int k = 0; k < NK; ++k) { rk[k] = S.rsc[k * cp + p]; gk[k] = S.gram[k * cp + p]; }
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const double gkj = rk[k] * rn * gk[k];
         S.G[(static_cast<int64_t>(k) * nslot + j) * cp + p] = gkj;
         S.G[(static_cast<int64_t>(j) * nslot + k) * cp + p] = gkj;
       }
@@ -1542,7 +1548,19 @@ cgs_step_kernel(StepArgs sa) {
   const ChunkState& S = a.s;
   unsigned int* bar = S.barrier + a.i;
   unsigned int nbar = 0;
-  auto sync_grid = [&]() { grid_barrier(bar, ++nbar); };
+  auto stamp = [&](int k) {
+    if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && k < 32) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.dbg[k] = t;
+    }
+  };
+  stamp(0);
+  auto sync_grid = [&]() {
+    stamp(2 * nbar + 1);   // entry of barrier nbar+1
+    grid_barrier(bar, ++nbar);
+    stamp(2 * nbar);       // exit
+  };
   const int nwc = (blockDim.x - 32) / 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&ring.full[s], 1); mbar_init(&ring.empty[s], nwc); }
