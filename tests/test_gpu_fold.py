@@ -144,3 +144,22 @@ def test_fold_device_rmat_matches_host_graph(cuda_device):
     vals, _ = dg.rules("normalized_laplacian", 0, 0, 16, 15, dtype="f32").integrate(np.array(GRID.values),
                                                                                    [_lib.FN_HEAT])
     assert golden.rel_l2(vals.cpu().numpy()[0], ref_h) <= FP32_TOL
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_fold_nearly_all_isolated(cuda_device, kind):
+    # one edge among 1000 vertices: the folded recurrence runs on 3 rows (the edge's endpoints and
+    # the trailing row) and must break down at the same step as the unfolded one
+    g = csr_from_edges(1000, [3], [998])
+    folded = DeviceGraph(g, cuda_device)
+    plain = DeviceGraph(g, cuda_device, fold=None)
+    assert folded.folded == 998
+    a1, b1, s1 = folded.tridiagonals(kind, 0, 0, 20, 15)
+    a2, b2, s2 = plain.tridiagonals(kind, 0, 0, 20, 15)
+    assert torch.equal(s1, s2)
+    assert np.allclose(a1.cpu().numpy(), a2.cpu().numpy(), rtol=0, atol=1e-13)
+    assert np.allclose(b1.cpu().numpy(), b2.cpu().numpy(), rtol=0, atol=1e-13)
+    r1 = folded.rules(kind, 0, 0, 20, 15)
+    r2 = plain.rules(kind, 0, 0, 20, 15)
+    assert np.allclose(r1.nodes.cpu().numpy(), r2.nodes.cpu().numpy(), rtol=0, atol=1e-12)
+    assert np.allclose(r1.weights.cpu().numpy(), r2.weights.cpu().numpy(), rtol=0, atol=1e-12)
