@@ -594,7 +594,7 @@ def test_prescaled_gathers_match_oracle(cuda_device, tmp_path, dtype, tol):
     assert not np.array_equal(pre, plain) or dtype == "f64"   # the prescaled path actually ran (fp32 rounding differs)
 
 
-@pytest.mark.parametrize("count,dtype", [(100, "f64"), (50, "f64"), (70, "f32"), (128, "f32")])
+@pytest.mark.parametrize("count,dtype", [(100, "f64"), (50, "f64"), (128, "f64")])
 def test_spmm_vec2_mapping_bitwise_equals_scalar(cuda_device, tmp_path, count, dtype):
     # wide chunks: the VEC2 mapping (probe pairs per lane, one vector load per pair) sums every probe
     # in the same sequential chain as the scalar mapping (SLQ_SPMM_VEC2=0): rules bitwise equal
