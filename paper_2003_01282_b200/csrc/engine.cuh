@@ -1551,14 +1551,17 @@ cgs_step_kernel(StepArgs sa) {
   unsigned int* bar = S.barrier + a.i;
   unsigned int nbar = 0;
   auto stamp = [&](int k) {
-    if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && k < 32) {
+    if (a.dbg && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.dbg[k] = t;
+      if (blockIdx.x == 0 && k < 32) a.dbg[k] = t;
+      // every CTA: start and the entries of barriers 1 and 3 (ends of the two streaming phases)
+      if (k == 0 || k == 1 || k == 5) a.dbg[32 + 4 * blockIdx.x + (k == 0 ? 0 : (k == 1 ? 1 : 2))] = t;
     }
   };
   stamp(0);
   auto sync_grid = [&]() {
+    if (a.dbg) __syncthreads();   // diagnostics: stamp when the whole CTA has arrived
     stamp(2 * nbar + 1);   // entry of barrier nbar+1
     grid_barrier(bar, ++nbar);
     stamp(2 * nbar);       // exit

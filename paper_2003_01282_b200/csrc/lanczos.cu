@@ -69,6 +69,7 @@ alpha_dot_kernel(const VT* __restrict__ u, const double* __restrict__ r, const V
 
 // ----------------------------------------------------------------------------- engine
 static unsigned long long* g_step_dbg = nullptr;   // SLQ_STEP_TIMING buffer (diagnostics)
+constexpr int kDbgStride = 32 + 4 * 160;           // per step: CTA 0's barrier stamps, then 4 per CTA
 static void set_long_rows(SpmmArgs& sa, const slq_graph* g, double* segpart) {
   sa.long_counts = g->long_counts;
   sa.long_rows = g->long_rows;
@@ -270,7 +271,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   static unsigned long long* dbgbuf = [] {
     unsigned long long* p = nullptr;
     const char* e = getenv("SLQ_STEP_TIMING");
-    if (e && e[0] == '1' && cudaMalloc(&p, sizeof(unsigned long long) * 32 * kMaxSteps) != cudaSuccess) p = nullptr;
+    if (e && e[0] == '1' && cudaMalloc(&p, sizeof(unsigned long long) * kDbgStride * kMaxSteps) != cudaSuccess) p = nullptr;
     return p;
   }();
   g_step_dbg = dbgbuf;
@@ -301,7 +302,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     sa.bits = (i == 0) ? bits : nullptr;
     sa.upre = (prescale && i >= 1 && i <= S - 2) ? static_cast<const void*>(basis + (i + 1) * vs) : nullptr;
     ca.pre_dinv = (prescale && i + 1 <= S - 2) ? g->dinv : nullptr;
-    ca.dbg = dbgbuf ? dbgbuf + 32 * i : nullptr;
+    ca.dbg = dbgbuf ? dbgbuf + kDbgStride * i : nullptr;
     ca.i = i;
     ca.second = 0;
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
@@ -480,10 +481,10 @@ extern "C" int slq_probe_state(uint64_t seed, uint64_t index, uint64_t out_host[
 }
 
 // Diagnostics (not part of the C ABI header): the SLQ_STEP_TIMING stamps of the last chunk,
-// [step][32] %globaltimer values (ns); returns the number of values copied.
+// [step][kDbgStride] %globaltimer values (ns); returns the number of values copied.
 extern "C" int slq_debug_step_times(unsigned long long* host, int n) {
   if (!g_step_dbg || !host) return 0;
-  n = std::min(n, 32 * kMaxSteps);
+  n = std::min(n, kDbgStride * kMaxSteps);
   if (cudaMemcpy(host, g_step_dbg, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
 }

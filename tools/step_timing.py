@@ -19,10 +19,12 @@ for _ in range(3):
     dg.rules("normalized_laplacian", 0, 0, 100, 15).check()
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (ctypes.c_ulonglong * (32 * 128))()
+STRIDE = 32 + 4 * 160
+buf = (ctypes.c_ulonglong * (STRIDE * 128))()
 lib.slq_debug_step_times.restype = ctypes.c_int
-n = lib.slq_debug_step_times(buf, 32 * 128)
-t = np.array(buf[:n], dtype=np.float64).reshape(128, 32)
+n = lib.slq_debug_step_times(buf, STRIDE * 128)
+full = np.array(buf[:n], dtype=np.float64).reshape(128, STRIDE)
+t = full[:, :32]
 for i in range(14):
     row = t[i]
     k = [j for j in range(32) if row[j] > 0]
@@ -31,3 +33,15 @@ for i in range(14):
     wait = [stamps[2 * b + 2] - stamps[2 * b + 1] for b in range((len(stamps) - 1) // 2)]
     print(f"step {i:2d} total {stamps[-1] / 1e3:7.1f} us  work " + " ".join(f"{w / 1e3:6.1f}" for w in work)
           + "  | barrier " + " ".join(f"{w / 1e3:5.1f}" for w in wait))
+
+# per-CTA end of the two streaming phases (relative to CTA 0's kernel start), for the last steps
+for i in (0, 6, 13):
+    cta = full[i, 32:32 + 4 * 148].reshape(148, 4)
+    a_end = (cta[:, 1] - full[i, 0]) / 1e3
+    c_end = (cta[:, 2] - full[i, 0]) / 1e3
+    start = (cta[:, 0] - full[i, 0]) / 1e3
+    slow_a = np.argsort(a_end)[-8:]
+    print(f"step {i}: start spread {start.max() - start.min():.1f} us; phase A end min/med/max "
+          f"{a_end.min():.1f}/{np.median(a_end):.1f}/{a_end.max():.1f}; slowest CTAs {sorted(slow_a.tolist())}; "
+          f"phase C end min/med/max {c_end.min():.1f}/{np.median(c_end):.1f}/{c_end.max():.1f}; "
+          f"slowest {sorted(np.argsort(c_end)[-8:].tolist())}")
