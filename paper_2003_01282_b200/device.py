@@ -23,6 +23,16 @@ FOLD_MIN_FRACTION = 1.0 / 64
 FOLD_MIN_N = 256
 
 
+def worth_folding(row_offsets, n: int, nnz: int, min_fraction: float = FOLD_MIN_FRACTION) -> bool:
+    """Host-side pre-check of the isolated-vertex fold: at least FOLD_MIN_N vertices, some edges, and
+    empty rows (an upper bound of the foldable vertices) making up >= min_fraction of them."""
+    if n < FOLD_MIN_N or nnz <= 0:
+        return False
+    off = np.asarray(row_offsets)
+    empty = int(off.size - 1 - np.count_nonzero(off[1:] != off[:-1]))
+    return empty >= 1 and empty >= min_fraction * n
+
+
 class DeviceGraph:
     """Prepared CSR on one GPU: int32 columns, implicit unit weights, degrees, dinv, tiles."""
 
@@ -55,11 +65,8 @@ class DeviceGraph:
         _lib.check(rc)
         self._info = None
         # empty rows counted on the host first: graphs below the threshold never synchronise here
-        if fold is not None and self.n >= FOLD_MIN_N and g.nnz > 0:
-            off = np.asarray(g.row_offsets)
-            empty = int(off.size - 1 - np.count_nonzero(off[1:] != off[:-1]))
-            if empty >= 1 and empty >= fold * self.n:
-                self.fold_isolated(fold)
+        if fold is not None and worth_folding(g.row_offsets, self.n, g.nnz, fold):
+            self.fold_isolated(fold)
 
     def fold_isolated(self, min_fraction: float = FOLD_MIN_FRACTION) -> int:
         """Build (or with ``min_fraction < 0`` drop) the isolated-vertex fold; returns the number of

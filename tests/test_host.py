@@ -109,3 +109,19 @@ def test_rmat_device_reference_is_canonical():
     for r in range(0, g.n, 97):
         row = cols[off[r]:off[r + 1]]
         assert np.all(np.diff(row) > 0) and not np.any(row == r)
+
+
+def test_fold_precheck_counts_empty_rows():
+    from paper_2003_01282_b200.device import FOLD_MIN_N, worth_folding
+    from paper_2003_01282_b200.graphs import csr_from_edges
+
+    n = 4 * FOLD_MIN_N
+    dense = csr_from_edges(n, np.arange(n - 1), np.arange(1, n))            # a path: no empty row
+    assert not worth_folding(dense.row_offsets, n, dense.nnz)
+    sparse = csr_from_edges(n, np.arange(0, n // 2 - 1), np.arange(1, n // 2))   # half the vertices isolated
+    assert worth_folding(sparse.row_offsets, n, sparse.nnz)
+    assert not worth_folding(sparse.row_offsets, n, sparse.nnz, min_fraction=0.75)
+    small = csr_from_edges(10, [0], [1])                                     # below FOLD_MIN_N
+    assert not worth_folding(small.row_offsets, 10, small.nnz)
+    empty = csr_from_edges(n, [], [])                                        # no edges: nothing to fold
+    assert not worth_folding(empty.row_offsets, n, empty.nnz)
