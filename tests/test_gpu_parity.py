@@ -565,8 +565,18 @@ def test_spmm_half2_mapping_bitwise_equals_full_warp(cuda_device, tmp_path, coun
     assert np.array_equal(np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]), full)
 
 
+def _weighted_hub_graph():
+    g = _hub_graph()
+    rng = np.random.default_rng(8)
+    off, cols = np.asarray(g.row_offsets), np.asarray(g.col_indices)
+    rows = np.repeat(np.arange(g.n), np.diff(off))
+    keep = rows < cols                       # one weight per undirected edge
+    return csr_from_edges(g.n, rows[keep], cols[keep], rng.uniform(0.25, 4.0, int(keep.sum())))
+
+
+@pytest.mark.parametrize("weighted", [False, True])
 @pytest.mark.parametrize("dtype,tol", [("f64", FP64_TOL), ("f32", FP32_TOL)])
-def test_prescaled_gathers_match_oracle(cuda_device, tmp_path, dtype, tol):
+def test_prescaled_gathers_match_oracle(cuda_device, tmp_path, dtype, tol, weighted):
     # narrow-class normalized-Laplacian runs on large graphs gather dinv (.) u written by the step
     # kernel instead of u times a dinv[col] gather; forced on a small graph here (SLQ_PRESCALE_MIN_N=0):
     # heat within the north-star tolerance of the oracle, and within rounding of the unscaled gathers
@@ -576,15 +586,16 @@ def test_prescaled_gathers_match_oracle(cuda_device, tmp_path, dtype, tol):
 
     out = tmp_path / "heat.npy"
     code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests'); import numpy as np, golden; "
-            "from test_gpu_parity import _hub_graph, GRID; from paper_2003_01282_b200 import _lib; "
+            "from test_gpu_parity import _hub_graph, _weighted_hub_graph, GRID; from paper_2003_01282_b200 import _lib; "
             "from paper_2003_01282_b200.device import DeviceGraph; "
-            f"r = DeviceGraph(_hub_graph()).rules('normalized_laplacian', 0, 0, 24, 15, dtype='{dtype}'); "
+            f"g = {'_weighted_hub_graph' if weighted else '_hub_graph'}(); "
+            f"r = DeviceGraph(g).rules('normalized_laplacian', 0, 0, 24, 15, dtype='{dtype}'); "
             "v, _ = r.integrate(np.array(GRID.values), [_lib.FN_HEAT]); "
             f"np.save('{out}', v.cpu().numpy()[0])")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, SLQ_PRESCALE_MIN_N="0"), cwd=root)
     pre = np.load(out)
-    g = _hub_graph()
+    g = _weighted_hub_graph() if weighted else _hub_graph()
     r = DeviceGraph(g, cuda_device).rules("normalized_laplacian", 0, 0, 24, 15, dtype=dtype)
     plain, _ = r.integrate(np.array(GRID.values), [_lib.FN_HEAT])
     plain = plain.cpu().numpy()[0]
