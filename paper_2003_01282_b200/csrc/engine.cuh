@@ -1006,7 +1006,11 @@ constexpr int kStagedMaxLdc = 128;
 #ifndef SLQ_STEP_REVERSE
 #define SLQ_STEP_REVERSE 1
 #endif
-constexpr bool kReverseUpdate = SLQ_STEP_REVERSE != 0;   // update phases stream their chunks backwards
+// Streaming directions: phase A (dots) and the update phases run opposite ways, so each starts on
+// what the previous pass left in L2.  SLQ_STEP_REVERSE=1: A forward, update backward; =2: A backward
+// (the SpMM's tail of w), update forward.
+constexpr bool kReverseUpdate = SLQ_STEP_REVERSE == 1;
+constexpr bool kReverseDots = SLQ_STEP_REVERSE == 2;
 constexpr int kStages = 3;
 constexpr int kMaxStaged = kCgsBlock + 4;
 constexpr size_t kStagedSmem = 200 * 1024;   // + 20 KB static: within the 227 KB per CTA
@@ -1204,25 +1208,34 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
     }
   };
   int ch = ch0;
-  for (int64_t r0 = lo; r0 < hi; r0 += rt, ++ch) {
+  // kReverseDots: chunks backwards and rows backwards within them (the SpMM just wrote the tail of w,
+  // still in L2); every slot's row sequence is then the exact reverse of the ascending one
+  const int nch = chunk_count(lo, hi, rt);
+  for (int jc = 0; jc < nch; ++jc, ++ch) {
+    const int64_t r0 = lo + static_cast<int64_t>(kReverseDots ? nch - 1 - jc : jc) * rt;
     const int s = ch % kStages;
     mbar_wait(&ring.full[s], (ch / kStages) & 1);
     const int rows = static_cast<int>(hi - r0 < rt ? hi - r0 : rt);
     if (pv) {
       const VT* stage = ring.buf + s * stage_elems;
       const uint32_t* sbits = reinterpret_cast<const uint32_t*>(stage + static_cast<int64_t>(sa.nvec) * vstride);
-      // this thread's rows: (row - lo) % SL == slot, ascending; U rows per iteration (all
-      // shared-memory loads first, then the arithmetic in row order)
-      int r = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);
+      // this thread's rows: (row - lo) % SL == slot; U rows per iteration (all shared-memory loads
+      // first, then the arithmetic in row order)
       constexpr int U = NQ <= 2 ? 4 : (NQ <= 4 ? 2 : 1);
-      for (; r + SL * (U - 1) < rows; r += SL * U) {
+      constexpr int D = kReverseDots ? -SL : SL;
+      const int first = static_cast<int>(((L.slot - (r0 - lo)) % SL + SL) % SL);
+      const int last = first < rows ? first + SL * ((rows - 1 - first) / SL) : first - SL;
+      const int cnt = first < rows ? (last - first) / SL + 1 : 0;
+      int r = kReverseDots ? last : first;
+      int k = 0;
+      for (; k + U <= cnt; k += U, r += D * U) {
         T wv[U], uv[U][NQ];
 #pragma unroll
-        for (int j = 0; j < U; ++j) load_row(stage, sbits, r + SL * j, r0 + r + SL * j, wv[j], uv[j]);
+        for (int j = 0; j < U; ++j) load_row(stage, sbits, r + D * j, r0 + r + D * j, wv[j], uv[j]);
 #pragma unroll
         for (int j = 0; j < U; ++j) row_dots(wv[j], uv[j]);
       }
-      for (; r < rows; r += SL) {
+      for (; k < cnt; ++k, r += D) {
         T wv1, uv1[NQ];
         load_row(stage, sbits, r, r0 + r, wv1, uv1);
         row_dots(wv1, uv1);
@@ -1615,7 +1628,7 @@ cgs_step_kernel(StepArgs sa) {
   // A: u_k . w for k <= i (and u_0 . u_0 at i == 0)
   const int nqa = nk + (a.i == 0 ? 1 : 0);
   if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) staged_produce<VT>(st0, ring, ch, lo, hi);
+    if (threadIdx.x == 0) staged_produce<VT>(st0, ring, ch, lo, hi, kReverseDots);
   } else {
     phase_dots<VT, NK, M, SL>(st0, ring, ch, lo, hi, nqa);
   }
