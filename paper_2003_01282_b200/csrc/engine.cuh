@@ -991,7 +991,10 @@ cgs_update_kernel(CgsArgs a, int ldc_i, int G) {
 // u_{i+1} is bitwise independent of M as well: narrow chunks keep the whole CTA busy without
 // changing any result.
 constexpr int kPersist = 148;
-constexpr int64_t kStepMinRows = 512;   // small graphs use fewer step CTAs (cheaper grid barriers)
+#ifndef SLQ_STEP_MIN_ROWS
+#define SLQ_STEP_MIN_ROWS 64
+#endif
+constexpr int64_t kStepMinRows = SLQ_STEP_MIN_ROWS;   // small graphs use fewer step CTAs (cheaper grid barriers)
 
 // CTAs of the step kernel for n rows: one per SM, or fewer for small graphs.  A function of n only,
 // so every probe of a graph sees the same row partition.

@@ -14,9 +14,13 @@ from paper_2003_01282_b200 import _lib, synth
 from paper_2003_01282_b200.device import DeviceGraph
 
 dev = torch.device("cuda", 0)
-dg = DeviceGraph(synth.sbm(100_000, 10, 1e-3, 1e-5, seed=0), dev)
+which = sys.argv[1] if len(sys.argv) > 1 else "c2"
+if which == "c1":
+    dg, NV, S = DeviceGraph(synth.barabasi_albert(1000, 3, seed=0), dev), 10, 10
+else:
+    dg, NV, S = DeviceGraph(synth.sbm(100_000, 10, 1e-3, 1e-5, seed=0), dev), 100, 15
 for _ in range(3):
-    dg.rules("normalized_laplacian", 0, 0, 100, 15).check()
+    dg.rules("normalized_laplacian", 0, 0, NV, S).check()
 torch.cuda.synchronize()
 lib = _lib.load()
 STRIDE = 32 + 4 * 160
@@ -25,7 +29,7 @@ lib.slq_debug_step_times.restype = ctypes.c_int
 n = lib.slq_debug_step_times(buf, STRIDE * 128)
 full = np.array(buf[:n], dtype=np.float64).reshape(128, STRIDE)
 t = full[:, :32]
-for i in range(14):
+for i in range(S - 1):
     row = t[i]
     k = [j for j in range(32) if row[j] > 0]
     stamps = row[:max(k) + 1] - row[0]
@@ -35,8 +39,9 @@ for i in range(14):
           + "  | barrier " + " ".join(f"{w / 1e3:5.1f}" for w in wait))
 
 # per-CTA end of the two streaming phases (relative to CTA 0's kernel start), for the last steps
-for i in (0, 6, 13):
+for i in (0, (S - 1) // 2, S - 2):
     cta = full[i, 32:32 + 4 * 148].reshape(148, 4)
+    cta = cta[cta[:, 0] > 0] if (cta[:, 0] > 0).any() else cta
     a_end = (cta[:, 1] - full[i, 0]) / 1e3
     c_end = (cta[:, 2] - full[i, 0]) / 1e3
     start = (cta[:, 0] - full[i, 0]) / 1e3
