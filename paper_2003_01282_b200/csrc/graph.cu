@@ -230,7 +230,10 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   SLQ_CUDA(cudaFreeAsync(scratch, st));
   // tiles
   const int64_t total = nnz + kRowCost * n;
-  int64_t target = std::max<int64_t>(kMinTileCost, (total + kMaxTiles - 1) / kMaxTiles);
+  // small graphs get smaller tiles (down to 16 cost units) so their few rows still spread over
+  // ~4 warps per SM; large graphs keep >= kMinTileCost per tile (scheduling overhead)
+  const int64_t min_cost = std::min<int64_t>(kMinTileCost, std::max<int64_t>(16, total / (148 * 32)));
+  int64_t target = std::max<int64_t>(min_cost, (total + kMaxTiles - 1) / kMaxTiles);
   g->ntiles = std::max(1, ceil_div(total, target));
   SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (g->ntiles + 1), st));
   g->tile_rows = static_cast<int64_t*>(track(g, p));
