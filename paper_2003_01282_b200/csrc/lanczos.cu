@@ -123,16 +123,28 @@ static bool lean_schedule(const slq_graph* g, bool start_block, int S, int reort
 // still hand out (the pool keeps freed blocks), rounded down to a 32-byte sector multiple of
 // columns when more than one sector fits (a narrower chunk gathers whole sectors; the padded
 // tail of a wider chunk would not).  Results do not depend on the chunk width.
-static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bool lean) {
-  size_t freeb = 0, total = 0;
-  cudaMemGetInfo(&freeb, &total);
-  double avail = static_cast<double>(freeb);
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
-    uint64_t reserved = 0, used = 0;
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    if (reserved > used) avail += static_cast<double>(reserved - used);
+static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bool lean, cudaStream_t st) {
+  // memory queries are not allowed while the stream is being captured into a CUDA graph: reuse the
+  // last value seen on this device then
+  static double last_avail[64] = {0.0};
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  double avail = 0.0;
+  const int dev = g->device >= 0 && g->device < 64 ? g->device : 0;
+  if (cap != cudaStreamCaptureStatusNone && last_avail[dev] > 0.0) {
+    avail = last_avail[dev];
+  } else {
+    size_t freeb = 0, total = 0;
+    cudaMemGetInfo(&freeb, &total);
+    avail = static_cast<double>(freeb);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+      uint64_t reserved = 0, used = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      if (reserved > used) avail += static_cast<double>(reserved - used);
+    }
+    last_avail[dev] = avail;
   }
   const double budget = 0.9 * avail - static_cast<double>(1ull << 30);
   const int nvec = lean ? S : S + 2;
@@ -393,7 +405,7 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
     fold.orig = g;
     gr = g->folded;
   }
-  int cmax = choose_chunk(gr, count, S, vb, lean);
+  int cmax = choose_chunk(gr, count, S, vb, lean, st);
   if (fold.orig) cmax = std::min(cmax, kBlk);   // bitmask probes: <= 128 per chunk
   SLQ_TRACE("choose_chunk");
   for (int64_t done = 0; done < count;) {

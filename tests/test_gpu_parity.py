@@ -625,3 +625,28 @@ def test_spmm_vec2_mapping_bitwise_equals_scalar(cuda_device, tmp_path, count, d
     scalar = np.load(out)
     r = DeviceGraph(_hub_graph(), cuda_device).rules("normalized_laplacian", 1, 0, count, 12, dtype=dtype)
     assert np.array_equal(np.stack([r.nodes.cpu().numpy(), r.weights.cpu().numpy()]), scalar)
+
+
+@pytest.mark.parametrize("kind,fns", [("normalized_laplacian", [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM]),
+                                      ("density", [_lib.FN_XLOGX])])
+def test_captured_signature_replays_eager_results(cuda_device, kind, fns):
+    from paper_2003_01282_b200 import synth
+    from paper_2003_01282_b200.device import CapturedSignature
+
+    g = synth.barabasi_albert(1000, 3, seed=0)
+    dg = DeviceGraph(g, cuda_device)
+    t = None if kind == "density" else np.array(GRID.values)
+    eager = dg.rules(kind, 0, 0, 10, 10)
+    ev, es = eager.integrate(t, fns)
+    cap = CapturedSignature(dg, kind, 0, 10, 10, t, fns)
+    for _ in range(3):
+        v, s = cap.replay()
+        torch.cuda.synchronize()
+        cap.check()
+        assert torch.equal(v, ev) and torch.equal(s, es)
+    if kind == "density":
+        ref, _ = O.vnge(g, 10, 10, 0)
+        assert abs(-float(v[0, 0]) - ref) <= FP64_TOL * abs(ref)
+    else:
+        ref, _ = O.heat_trace(g, GRID.values, 10, 10, 0)
+        assert golden.rel_l2(v[0].cpu().numpy(), ref) <= FP64_TOL

@@ -77,6 +77,7 @@ def main():
     ap.add_argument("--check-probes", type=int, default=8)
     ap.add_argument("--dtype", default="f64")
     ap.add_argument("--graphs", type=int, default=10_000)
+    ap.add_argument("--graph", action="store_true", help="also time a CUDA-graph replay of the signature")
     args = ap.parse_args()
     if args.config == "c3":
         return run_c3(args)
@@ -104,6 +105,22 @@ def main():
         ms = float(np.median(times[1:]))
         units = g.nnz * cfg["n_v"] * cfg["s"]
         out[kind] = {"ms": ms, "units_per_s": units / (ms * 1e-3), "times": times}
+        if args.graph:
+            # the same signature captured once as a CUDA graph and replayed (device.CapturedSignature)
+            from paper_2003_01282_b200.device import CapturedSignature
+
+            cap = CapturedSignature(dg, KIND[kind], 0, cfg["n_v"], cfg["s"],
+                                    tgrid.cpu().numpy() if kind == "nl" else None, fns, dtype=args.dtype)
+            gt = []
+            for _ in range(args.reps + 1):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                cap.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                gt.append(e0.elapsed_time(e1))
+            cap.check()
+            out[kind]["graph_replay_ms"] = float(np.median(gt[1:]))
         if args.check_probes:
             from oracle import slq_oracle as O
 
