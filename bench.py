@@ -225,7 +225,7 @@ def run_ours(args):
         dg.device, dg.graph, dg.n, dg._info = dev, g, g.n, None
         dg.handle = ctypes.c_void_p()
         _lib.check(_lib.load().slq_graph_create(g.n, g.nnz, off_d.data_ptr(), cols_d.data_ptr(), None,
-                                                stream.cuda_stream, ctypes.byref(dg.handle)))
+                                                torch.cuda.current_stream().cuda_stream, ctypes.byref(dg.handle)))
         rules = dg.rules("normalized_laplacian", 0, rank * n_v, n_v, s, dtype=dtype)
         if world > 1:
             nodes, weights, steps = gather_rules_arrays(rules.nodes, rules.weights, rules.steps, total_probes)
@@ -260,6 +260,44 @@ def run_ours(args):
     torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in ev]
     launches = (_lib.launch_count() - launches0) // args.steps
+    times_eager = times
+    # One step captured as a CUDA graph (graph preparation, probes, Lanczos, rules, quadrature and
+    # aggregate: the same kernels, launched by one graph launch) and replayed K times; single rank only
+    # (the multi-rank step has a host all-gather).  BENCH_EAGER=1 reports the eager loop instead.
+    cuda_graph = world == 1 and not os.environ.get("BENCH_EAGER")
+    graph_note = None
+
+    def graph_times():
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step()
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg, capture_error_mode="thread_local"):
+            _, cap_status = step()
+        torch.cuda.synchronize()
+        cg.replay()
+        torch.cuda.synchronize()
+        _lib.check_status(int(cap_status.item()))
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(1)
+            gev[k][0].record(stream)
+            cg.replay()
+            gev[k][1].record(stream)
+        torch.cuda.synchronize()
+        _lib.check_status(int(cap_status.item()))
+        return [a.elapsed_time(b) for a, b in gev]
+
+    if cuda_graph:
+        try:
+            times = graph_times()
+        except Exception as ex:   # capture unavailable: report the eager loop (same kernels)
+            cuda_graph, graph_note = False, repr(ex)[:200]
+            times = times_eager
+            torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
     ms = float(np.mean(times))
     # same K steps again with per-launch CUDA events (kernel durations for the roofline)
@@ -350,6 +388,9 @@ def run_ours(args):
         "kernels": per_class,
         "ms_per_step_profiled": float(np.mean(ptimes)),
         "ms_steps": [round(t, 3) for t in times],
+        "launch": "one CUDA-graph replay per step (the eager step's kernels)" if cuda_graph else
+                  ("eager launches" + (f" (capture failed: {graph_note})" if graph_note else "")),
+        "ms_per_step_eager": float(np.mean(times_eager)),
         "host_submit_ms_total": round(host_ms, 3),
         "gpu_launches": launches,
         "clocks": clocks,
