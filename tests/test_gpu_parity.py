@@ -650,3 +650,49 @@ def test_captured_signature_replays_eager_results(cuda_device, kind, fns):
     else:
         ref, _ = O.heat_trace(g, GRID.values, 10, 10, 0)
         assert golden.rel_l2(v[0].cpu().numpy(), ref) <= FP64_TOL
+
+
+# analytic pins of the reference's own test strategy (tests/test_slq.py, tests/test_lanczos.py)
+def test_heat_at_t0_is_n(cuda_device):
+    # h(0) = n * mean_i sum_k tau_ik^2 = n (weights of every rule sum to 1; tests/test_slq.py:169-177)
+    from paper_2003_01282_b200 import synth
+
+    g = synth.barabasi_albert(500, 3, seed=2)
+    dg = DeviceGraph(g, cuda_device)
+    r = dg.rules("normalized_laplacian", 0, 0, 12, 10)
+    v, _ = r.integrate(np.array([0.0, 1e-2]), [_lib.FN_HEAT])
+    assert abs(float(v[0, 0]) - g.n) <= 1e-12 * g.n
+
+
+@pytest.mark.parametrize("kind", ["laplacian", "normalized_laplacian", "density"])
+def test_gauss_rule_exact_for_linear_f(cuda_device, kind):
+    # per-probe quadratic-form exactness (tests/test_slq.py:47-59, Gauss exactness tests/test_lanczos.py:154-172):
+    # sum_k tau_k^2 theta_k = q0^T M q0 with q0 = z / sqrt(n), z the probe re-derived from SeedSequence
+    from paper_2003_01282_b200 import synth
+
+    g = synth.barabasi_albert(800, 4, seed=5)
+    dg = DeviceGraph(g, cuda_device)
+    r = dg.rules(kind, 7, 0, 16, 10)
+    pv = r.quadrature(None, _lib.FN_IDENTITY).cpu().numpy()[0]      # per_vector [count]
+    op = O.make_block_operator(g, {"laplacian": O.LAPLACIAN, "normalized_laplacian": O.NORMALIZED_LAPLACIAN,
+                                   "density": O.DENSITY}[kind])
+    q0 = O.draw_probes(g.n, 7, range(16))
+    exact = np.einsum("nc,nc->c", q0, op.apply(q0))
+    assert np.max(np.abs(pv - exact) / np.abs(exact)) <= 1e-12
+
+
+def test_trace_estimate_unbiased_over_seeds(cuda_device):
+    # E[z^T L z] = tr L for Rademacher z (tests/test_slq.py:88-101): 200 seeds x 4 probes of the
+    # identity integrand on the normalized Laplacian average to n - #isolated within 4 standard errors
+    from paper_2003_01282_b200 import synth
+
+    g = synth.barabasi_albert(300, 2, seed=9)
+    dg = DeviceGraph(g, cuda_device)
+    ests = []
+    for seed in range(200):
+        r = dg.rules("normalized_laplacian", seed, 0, 4, 6)
+        v, _ = r.integrate(None, [_lib.FN_IDENTITY])
+        ests.append(float(v[0, 0]))
+    ests = np.array(ests)
+    tr = g.n - int(np.count_nonzero(np.diff(np.asarray(g.row_offsets)) == 0))
+    assert abs(ests.mean() - tr) <= 4 * ests.std(ddof=1) / np.sqrt(len(ests))
