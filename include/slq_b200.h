@@ -151,6 +151,13 @@ int slq_lanczos(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin
                 int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
                 void* stream);
 
+/* Debug export (lanczos_tridiagonalize(..., return_basis=True), lanczos.py:85,143-144): slq_lanczos
+ * plus the Lanczos vectors q_k = u_k / beta_{k-1} of every probe, basis[k][row][count] (k < s',
+ * float64; zero after a probe's breakdown).  Runs on the unfolded graph. */
+int slq_lanczos_basis(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
+                      int reorth, int dtype, double* basis, double* alpha, double* beta, int32_t* steps_out,
+                      void* stream);
+
 /* Same recurrence from caller-given unit start vectors q0[n][ldq] (column j = start vector j);
  * the lanczos_tridiagonalize(op, q0, s) entry (lanczos.py:79-104). */
 int slq_lanczos_start(const slq_graph* g, int kind, const double* q0, int64_t ldq, int64_t count,

@@ -54,6 +54,7 @@ _SIGS = {
     "slq_operator_apply": (_int, [_vp, _int, _vp, _vp, _i64, _i64, _vp]),
     "slq_lanczos": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "slq_lanczos_start": (_int, [_vp, _int, _vp, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "slq_lanczos_basis": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "slq_gauss_rules": (_int, [_vp, _vp, _vp, _i64, _int, _dbl, _dbl, _vp, _vp, _vp, _vp]),
     "slq_quadrature": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _i64, _int, _vp, _vp]),
     "slq_estimate": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp]),

@@ -40,6 +40,26 @@ __global__ void scatter_out_kernel(ChunkState s, int64_t col0, int S, double* al
   steps[col0 + p] = st;
 }
 
+// Debug export of the Lanczos basis (lanczos.py:85,143-144 return_basis): q_k = u_k r_k
+// into out[k][row][ldo] at column col0 + p; u_0 from the probe bitmask when the chunk kept it as bits.
+template <typename VT>
+__global__ void export_basis_kernel(const VT* __restrict__ basis, const uint32_t* __restrict__ bits,
+                                    const double* __restrict__ rsc, int cpad, int64_t n, int64_t ldc, int c, int S,
+                                    int64_t vs, double* __restrict__ out, int64_t ldo, int64_t col0) {
+  const int64_t total = static_cast<int64_t>(S) * n * c;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(idx / (n * c));
+    const int64_t rem = idx - static_cast<int64_t>(k) * n * c;
+    const int64_t row = rem / c;
+    const int p = static_cast<int>(rem - row * c);
+    double u;
+    if (k == 0 && bits) u = ((bits[row * kBitWords + (p >> 5)] >> (p & 31)) & 1u) ? 1.0 : -1.0;
+    else u = static_cast<double>(basis[static_cast<int64_t>(k) * vs + row * ldc + p]);
+    out[(static_cast<int64_t>(k) * n + row) * ldo + col0 + p] = u * rsc[static_cast<int64_t>(k) * cpad + p];
+  }
+}
+
 // alpha_i = q_i . w for the steps that do not run the staged step kernel (the last step, s > 17,
 // SLQ_STAGED=0): kAlphaCtas CTAs with fixed contiguous row ranges, 2 row slots per probe column,
 // per-CTA partials reduced by reduce_kernel (fixed stripes): deterministic and independent of c.
@@ -175,7 +195,7 @@ struct FoldRun {
 template <typename VT>
 static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0, const double* q0, int64_t ldq,
                      int c, int S, int reorth, double* alpha_out, double* beta_out, int32_t* steps_out, int64_t col0,
-                     cudaStream_t st, FoldRun fold = FoldRun{}) {
+                     cudaStream_t st, FoldRun fold = FoldRun{}, double* basis_out = nullptr, int64_t basis_ld = 0) {
   const double t_host0 = host_ms();
   const int64_t n = g->n;
   const int64_t n_probe = fold.orig ? fold.orig->n : n;   // probe length: ||v||^2 = n (slq.py:73)
@@ -366,6 +386,12 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     LaunchScope ls(K_REDUCE, st);
     scatter_out_kernel<<<ceil_div(c, 128), 128, 0, st>>>(s, col0, S, alpha_out, beta_out, steps_out);
   }
+  if (basis_out) {
+    LaunchScope ls(K_REDUCE, st);
+    const int64_t total = static_cast<int64_t>(S) * n * c;
+    export_basis_kernel<VT><<<std::max(1, std::min(ceil_div(total, 256), 148 * 16)), 256, 0, st>>>(
+        basis, all_staged ? bits : nullptr, s.rsc, cpad, n, ldc, c, S, vs, basis_out, basis_ld, col0);
+  }
   SLQ_CUDA(cudaGetLastError());
   SLQ_CUDA(cudaFreeAsync(ws, st));
   SLQ_TRACE("chunk done");
@@ -378,7 +404,7 @@ using namespace slq;
 
 static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, const double* q0,
                          int64_t ldq, int64_t count, int steps, int reorth, int dtype, double* alpha, double* beta,
-                         int32_t* steps_out, void* stream) {
+                         int32_t* steps_out, void* stream, double* basis_out = nullptr) {
   if (!g) return fail(SLQ_ERR_VALUE, "NULL graph");
   if (steps < 1) return fail(SLQ_ERR_VALUE, "step budget must be >= 1");
   if (count < 0 || probe_begin < 0) return fail(SLQ_ERR_VALUE, "negative probe range");
@@ -401,7 +427,7 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   const bool lean = lean_schedule(g, q0 != nullptr, S, reorth);
   FoldRun fold;
   const slq_graph* gr = g;
-  if (g->folded && lean) {
+  if (g->folded && lean && !basis_out) {   // the basis export runs on the unfolded graph
     fold.orig = g;
     gr = g->folded;
   }
@@ -412,8 +438,10 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
     const int c = static_cast<int>(std::min<int64_t>(cmax, count - done));
     const double* qc = q0 ? q0 + done : nullptr;
     rc = dtype == SLQ_F64
-             ? run_chunk<double>(gr, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st, fold)
-             : run_chunk<float>(gr, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st, fold);
+             ? run_chunk<double>(gr, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st,
+                                 fold, basis_out, count)
+             : run_chunk<float>(gr, kind, seed, probe_begin + done, qc, ldq, c, S, reorth, alpha, beta, steps_out, done, st,
+                                fold, basis_out, count);
     if (rc) return rc;
     done += c;
   }
@@ -499,4 +527,12 @@ extern "C" int slq_debug_step_times(unsigned long long* host, int n) {
   n = std::min(n, kDbgStride * kMaxSteps);
   if (cudaMemcpy(host, g_step_dbg, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
+}
+
+extern "C" int slq_lanczos_basis(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count,
+                                 int steps, int reorth, int dtype, double* basis, double* alpha, double* beta,
+                                 int32_t* steps_out, void* stream) {
+  if (!basis) return fail(SLQ_ERR_VALUE, "NULL basis output");
+  return lanczos_entry(g, kind, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta, steps_out,
+                       stream, basis);
 }

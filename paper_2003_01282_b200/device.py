@@ -230,6 +230,26 @@ class DeviceGraph:
         _lib.check(rc)
         return alpha, beta, st
 
+    def lanczos_basis(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1,
+                      dtype: str = "f64"):
+        """Debug export (``return_basis=True``, lanczos.py:85,143-144): Q [s', n, count] float64 with
+        Q[k, :, j] the k-th Lanczos vector of probe probe_begin+j, plus alpha, beta [count, s'] and
+        steps [count].  Runs on the unfolded graph."""
+        import torch
+
+        s = min(int(steps), self.n)
+        q = torch.zeros((s, self.n, count), dtype=torch.float64, device=self.device)
+        alpha = torch.zeros((count, s), dtype=torch.float64, device=self.device)
+        beta = torch.zeros((count, s), dtype=torch.float64, device=self.device)
+        st = torch.zeros(count, dtype=torch.int32, device=self.device)
+        code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_lanczos_basis(self.handle, KIND_CODES[kind], int(seed), int(probe_begin),
+                                                     int(count), int(steps), int(reorth), code, _lib.ptr(q),
+                                                     _lib.ptr(alpha), _lib.ptr(beta), _lib.ptr(st),
+                                                     _lib.stream_handle(self.device)))
+        return q, alpha, beta, st
+
     def rules(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1,
               dtype: str = "f64", status=None) -> "DeviceRules":
         """Gauss rules of probes [probe_begin, +count), asynchronously (errors land in ``status``)."""

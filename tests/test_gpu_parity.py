@@ -696,3 +696,29 @@ def test_trace_estimate_unbiased_over_seeds(cuda_device):
     ests = np.array(ests)
     tr = g.n - int(np.count_nonzero(np.diff(np.asarray(g.row_offsets)) == 0))
     assert abs(ests.mean() - tr) <= 4 * ests.std(ddof=1) / np.sqrt(len(ests))
+
+
+# the reference's Lanczos-basis tests (tests/test_lanczos.py:41-48, 76-99) on the device basis export
+@pytest.mark.parametrize("kind", ["laplacian", "normalized_laplacian", "density"])
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_lanczos_basis_orthonormal_and_tridiagonalizes(cuda_device, kind, dtype, tol):
+    from paper_2003_01282_b200 import synth
+
+    g = synth.barabasi_albert(600, 3, seed=4)
+    dg = DeviceGraph(g, cuda_device)
+    q, alpha, beta, st = dg.lanczos_basis(kind, 3, 0, 8, 12, dtype=dtype)
+    q, alpha, beta, st = (x.cpu().numpy() for x in (q, alpha, beta, st))
+    okind = {"laplacian": O.LAPLACIAN, "normalized_laplacian": O.NORMALIZED_LAPLACIAN, "density": O.DENSITY}[kind]
+    op = O.make_block_operator(g, okind)
+    hi = op.interval[1]
+    # q_0 is the probe / sqrt(n), bit for bit
+    assert np.array_equal(q[0], O.draw_probes(g.n, 3, range(8)))
+    for j in range(8):
+        m = int(st[j])
+        Q = q[:m, :, j].T                                   # n x m
+        assert np.max(np.abs(Q.T @ Q - np.eye(m))) <= tol                      # orthonormality
+        T = np.diag(alpha[j, :m]) + np.diag(beta[j, :m - 1], 1) + np.diag(beta[j, :m - 1], -1)
+        assert np.max(np.abs(Q.T @ op.apply(Q) - T)) <= tol * hi             # Q^T M Q = T
+    # the tridiagonals are the ones slq_lanczos returns
+    a2, b2, s2 = dg.tridiagonals(kind, 3, 0, 8, 12, dtype=dtype)
+    assert np.array_equal(a2.cpu().numpy(), alpha) and np.array_equal(s2.cpu().numpy(), st)
