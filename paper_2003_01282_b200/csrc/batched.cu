@@ -59,7 +59,10 @@ __device__ __forceinline__ double slot_sum(const double* part, int nq, int c, in
 }
 
 template <typename VT, int KIND>
-__global__ void __launch_bounds__(kRows * kBatchMaxProbes)
+#ifndef SLQ_BATCH_MINB
+#define SLQ_BATCH_MINB 2   // 64 registers: 2x the resident CTAs (C3 fp32 -8%)
+#endif
+__global__ void __launch_bounds__(kRows * kBatchMaxProbes, SLQ_BATCH_MINB)
 batched_lanczos_kernel(BatchArgs a) {
   extern __shared__ double sm[];
   const int c = a.c;
