@@ -58,7 +58,8 @@ __device__ __forceinline__ double slot_sum(const double* part, int nq, int c, in
   return s;
 }
 
-template <typename VT, int KIND>
+// MAXS: capacity of the per-thread eigensolver arrays (local memory), >= the rule length
+template <typename VT, int KIND, int MAXS = kMaxSteps>
 #ifndef SLQ_BATCH_MINB
 #define SLQ_BATCH_MINB 2   // 64 registers: 2x the resident CTAs (C3 fp32 -8%)
 #endif
@@ -267,7 +268,7 @@ batched_lanczos_kernel(BatchArgs a) {
     const int64_t pg = static_cast<int64_t>(blockIdx.y) * c + t;   // probe index within the graph's output
     const int64_t ow = static_cast<int64_t>(gridDim.y) * c;
     if (t < c && pg < a.count) {
-      double d[kMaxSteps], e[kMaxSteps], z[kMaxSteps];
+      double d[MAXS], e[MAXS], z[MAXS];
       const int m = steps[t];
       bool finite = true;
       for (int k = 0; k < m; ++k) {
@@ -383,9 +384,10 @@ extern "C" int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_off
 #define SLQ_BATCH(VT, K)                                                                                       \
   do {                                                                                                         \
     if (smem > 48 * 1024)                                                                                      \
-      cudaFuncSetAttribute(batched_lanczos_kernel<VT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                           static_cast<int>(smem));                                                            \
-    batched_lanczos_kernel<VT, K><<<grid, threads, smem, st>>>(a);                                             \
+      cudaFuncSetAttribute(a.S <= 16 ? batched_lanczos_kernel<VT, K, 16> : batched_lanczos_kernel<VT, K>,     \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));               \
+    if (a.S <= 16) batched_lanczos_kernel<VT, K, 16><<<grid, threads, smem, st>>>(a);                          \
+    else batched_lanczos_kernel<VT, K><<<grid, threads, smem, st>>>(a);                                        \
   } while (0)
     if (dtype == SLQ_F64) {
       if (kind == SLQ_NORMALIZED_LAPLACIAN) SLQ_BATCH(double, SLQ_NORMALIZED_LAPLACIAN);
@@ -439,9 +441,10 @@ int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin
 #define SLQ_SMALL(VT, K)                                                                                       \
   do {                                                                                                         \
     if (smem > 48 * 1024)                                                                                      \
-      cudaFuncSetAttribute(batched_lanczos_kernel<VT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                           static_cast<int>(smem));                                                            \
-    batched_lanczos_kernel<VT, K><<<grid, threads, smem, st>>>(a);                                             \
+      cudaFuncSetAttribute(a.S <= 16 ? batched_lanczos_kernel<VT, K, 16> : batched_lanczos_kernel<VT, K>,     \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));               \
+    if (a.S <= 16) batched_lanczos_kernel<VT, K, 16><<<grid, threads, smem, st>>>(a);                          \
+    else batched_lanczos_kernel<VT, K><<<grid, threads, smem, st>>>(a);                                        \
   } while (0)
     if (dtype == SLQ_F64) {
       if (kind == SLQ_NORMALIZED_LAPLACIAN) SLQ_SMALL(double, SLQ_NORMALIZED_LAPLACIAN);
