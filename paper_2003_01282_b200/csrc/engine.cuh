@@ -1164,6 +1164,24 @@ __device__ __forceinline__ T stage_u(const VT* e, const uint32_t* brow, int vstr
   return static_cast<T>(e[k * vstride]);
 }
 
+// Per-CTA partials: the consumers' per-slot sums go to a shared-memory scratch [slot][nq][cp] (the
+// idle stage ring), then are added over the slots in slot order and written as ONE partial row per
+// CTA, [cta][nq][cp]: the grid-wide reductions read gridDim.x rows instead of gridDim.x * SL.
+constexpr size_t kSlotScratchBytes = sizeof(double) * (kCgsBlock + 2) * (kStageSlots * kSlotThreads);
+template <int SL>
+__device__ __forceinline__ void cta_slot_reduce(const double* scratch, int nq, int cp, double* dst_cta) {
+  named_barrier_sync(2, blockDim.x - 32);   // consumer warps only
+  const int nt = blockDim.x - 32;
+  for (int idx = threadIdx.x - 32; idx < nq * cp; idx += nt) {
+    double v = scratch[idx];
+#pragma unroll
+    for (int sl = 1; sl < SL; ++sl) v += scratch[static_cast<int64_t>(sl) * nq * cp + idx];
+    dst_cta[idx] = v;
+  }
+  // the scratch is the stage ring: order these generic accesses before later bulk copies into it
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Phase A (consumer side): partials [cta*slots+slot][nq][cpad] of u_k . w (k < NK); at i == 0 also
 // u_0 . u_0 (q = 1) for G(0,0).
 template <typename VT, int NK, int M, int SL>
@@ -1248,8 +1266,10 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
   flush();
+  named_barrier_sync(2, blockDim.x - 32);   // every consumer warp is done reading the ring
+  double* scratch = reinterpret_cast<double*>(ring.buf);
   if (L.p < cp) {
-    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * SL + L.slot) * nq * cp + L.p;
+    double* dst = scratch + static_cast<int64_t>(L.slot) * nq * cp + L.p;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int kk = q * M + L.part;
@@ -1257,6 +1277,7 @@ __device__ __forceinline__ void phase_dots(const StagedArgs& sa, StageRing<VT>& 
     }
     if (NK == 1 && L.part == 0) dst[NK * cp] = g00;
   }
+  cta_slot_reduce<SL>(scratch, nq, cp, a.partial + static_cast<int64_t>(blockIdx.x) * nq * cp);
 }
 
 // sum_k coef_k u_k from this thread's chains ch[j] (chain j M + part), combined in the canonical
@@ -1442,8 +1463,10 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     if (lane == 0) mbar_arrive(&ring.empty[s]);
   }
   flush();
+  named_barrier_sync(2, blockDim.x - 32);   // every consumer warp is done reading the ring
+  double* scratch = reinterpret_cast<double*>(ring.buf);
   if (p < cp) {
-    double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * SL + L.slot) * nq * cp + p;
+    double* dst = scratch + static_cast<int64_t>(L.slot) * nq * cp + p;
     if (L.part == 0) {
       dst[0] = pv ? nb : 0.0;
       dst[cp] = pv ? nrm : 0.0;
@@ -1454,6 +1477,7 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
       if (kk < NK) dst[(2 + kk) * cp] = pv ? gr[q] : 0.0;
     }
   }
+  cta_slot_reduce<SL>(scratch, nq, cp, a.partial + static_cast<int64_t>(blockIdx.x) * nq * cp);
 }
 
 // Fixed-order stripe reduction of quantity q for 32 probes; returns the total in warp 0's lanes.
@@ -1593,7 +1617,7 @@ cgs_step_kernel(StepArgs sa) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nk = a.i + 1;
   const int nslot = S.S + 1;
-  const int nrows_partial = gridDim.x * SL;
+  const int nrows_partial = gridDim.x;   // one pre-reduced partial row per CTA
   int ch = 0;
   const StagedArgs& st0 = sa.pass[0];
   const int nch0 = chunk_count(lo, hi, st0.rt);
@@ -1750,11 +1774,12 @@ static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmA
   if (!staged_setup<VT>(a, false, bits, &sa.pass[0]) || !staged_setup<VT>(a, true, bits, &sa.pass[1])) return false;
   sa.red = red;
   sa.spmm = spmm;
-  const size_t smem = 128 + kStages * sizeof(VT) *
-                                std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, sa.pass[0].vstride,
-                                                            a.pre_dinv != nullptr),
-                                         stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, sa.pass[1].vstride,
-                                                            a.pre_dinv != nullptr));
+  const size_t smem = 128 + std::max(kSlotScratchBytes,
+                                     kStages * sizeof(VT) *
+                                         std::max(stage_elems_of<VT>(sa.pass[0].nvec, sa.pass[0].rt, sa.pass[0].vstride,
+                                                                     a.pre_dinv != nullptr),
+                                                  stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, sa.pass[1].vstride,
+                                                                     a.pre_dinv != nullptr)));
   LaunchScope ls(K_CGS_UPDATE, st);
   // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
   // so the software grid barrier is safe (coop_supported() checked the SM count).
