@@ -146,7 +146,7 @@ static bool lean_schedule(const slq_graph* g, bool start_block, int S, int reort
 static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bool lean, cudaStream_t st) {
   // memory queries are not allowed while the stream is being captured into a CUDA graph: reuse the
   // last value seen on this device then
-  static double last_avail[64] = {0.0};
+  thread_local double last_avail[64] = {0.0};   // per host thread: the library stays reentrant
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
   double avail = 0.0;
