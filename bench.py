@@ -1,20 +1,27 @@
-"""Benchmark: SLQ edge·probe·steps/s on BASELINE.json configs[1] (C2).
+"""Benchmark: SLQ edge·probe·steps/s on BASELINE.json's largest single-GPU configuration (C5).
 
-Workload (one "step" = one full signature computation over the graph):
-  SBM n=100,000, 10 equal blocks, p_in=1e-3, p_out=1e-5 (seeded synthetic), normalized Laplacian,
-  n_v=100 Rademacher probes x s=15 Lanczos steps (full CGS reorth, the reference default),
-  heat + wave traces on 250 log-spaced t in [1e-2, 1e2], fp64 (``--dtype f32`` for fp32 storage).
-  Units per step = nnz * n_v * s (one stored nonzero x one probe x one operator application).
+Default workload (``--config c5``, BASELINE configs[4]; one "step" = one whole signature):
+  R-MAT scale 27 (n = 134,217,728; edge factor 16; a=.57 b=.19 c=.19; symmetrised, deduplicated,
+  self-loops dropped; 4.22e9 stored nonzeros), generated on the device (seeded synthetic: the
+  paper's Friendster-scale datasets are not available); 128 Rademacher probes x 15
+  Lanczos steps with full CGS reorthogonalisation (the reference default for s <= 100), fp32
+  vector storage (int32 indices, implicit unit weights); heat + wave traces of the normalized
+  Laplacian on 250 log-spaced t in [1e-2, 1e2] (one Lanczos run) and VNGE on the density matrix
+  (a second run).  Units per step = 2 * nnz * n_v * s (stored nonzero x probe x operator
+  application, two operator runs).
+``--config c2`` (SBM n=100k, 100 x 15, heat+wave, fp64) and ``--config c4`` (R-MAT scale 20,
+100 x 15, heat + VNGE, fp64) are kept for comparison with round 1.
 
 Arms:
   default            hand-written sm_100a kernels through libslq_b200.so
-  --impl reference   the CPU oracle port of the reference algorithm (oracle/slq_oracle.py, numpy +
-                     scipy, all host threads) on the same config; rank 0 only.
+  --impl reference   the CPU oracle port of the reference algorithm (oracle/slq_oracle.py: numpy +
+                     scipy, all host threads) timed on a bounded sample of the same workload; rank 0.
 
-Timing: W warm-up steps, then K timed steps, each bracketed by CUDA events on the launching stream;
-L2 is flushed (256 MiB write) between timed steps, outside the events.  Multi-GPU: one process per
-GPU (torchrun), weak scaling: rank r runs probes [100r, 100r+100) and the rules are all-gathered
-over NCCL; device time = max over ranks.
+Timing: W warm-up steps, then K timed steps bracketed by CUDA events on the launching stream
+(inputs far larger than L2 at C5; L2 is also flushed between steps, outside the events).
+Multi-GPU (torchrun): STRONG scaling -- the CSR is replicated (each rank generates it on its GPU),
+rank r runs a balanced contiguous range of the 128 probes, one NCCL all-gather per operator
+assembles every rule on every rank; device time = max over ranks.
 """
 from __future__ import annotations
 
@@ -29,13 +36,31 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = {"workload": "C2 SBM n=100000 blocks=10 p_in=1e-3 p_out=1e-5, normalized Laplacian, "
-                        "heat+wave T=250 t in [1e-2,1e2]",
-            "graph": "sbm", "n": 100_000, "blocks": 10, "p_in": 1e-3, "p_out": 1e-5, "graph_seed": 0,
-            "n_v_per_gpu": 100, "lanczos_steps": 15, "T": 250, "reorth": "full CGS (reference default)",
-            "l2": "flushed between timed steps (256 MiB write), outside the timed events"}
 METRIC = "SLQ edge·probe·steps/sec"
 UNIT = "edge·probe·step/s"
+T_GRID = 250
+NL, P = "normalized_laplacian", "density"
+
+CONFIGS = {
+    "c5": {"workload": "C5 R-MAT scale 27 (ef 16, a=.57 b=.19 c=.19), 128 probes x 15 steps, fp32, "
+                       "heat+wave (normalized Laplacian) + VNGE (density), T=250 t in [1e-2,1e2]",
+           "graph": "rmat", "scale": 27, "edge_factor": 16, "abc": [0.57, 0.19, 0.19], "graph_seed": 0,
+           "n_v": 128, "lanczos_steps": 15, "T": T_GRID, "dtype": "f32", "ops": ["heat", "wave", "vnge"],
+           "reorth": "full CGS (reference default)", "graph_source": "device R-MAT generator",
+           "l2": "inputs >> L2 (17 GB CSR, 8 GB per Lanczos vector block); L2 also flushed between steps"},
+    "c4": {"workload": "C4 R-MAT scale 20 (ef 16, a=.57 b=.19 c=.19), 100 probes x 15 steps, fp64, "
+                       "heat (normalized Laplacian) + VNGE (density), T=250 t in [1e-2,1e2]",
+           "graph": "rmat", "scale": 20, "edge_factor": 16, "abc": [0.57, 0.19, 0.19], "graph_seed": 0,
+           "n_v": 100, "lanczos_steps": 15, "T": T_GRID, "dtype": "f64", "ops": ["heat", "vnge"],
+           "reorth": "full CGS (reference default)", "graph_source": "device R-MAT generator",
+           "l2": "flushed between timed steps (256 MiB write), outside the timed events"},
+    "c2": {"workload": "C2 SBM n=100000 blocks=10 p_in=1e-3 p_out=1e-5, 100 probes x 15 steps, fp64, "
+                       "heat+wave (normalized Laplacian), T=250 t in [1e-2,1e2]",
+           "graph": "sbm", "n": 100_000, "blocks": 10, "p_in": 1e-3, "p_out": 1e-5, "graph_seed": 0,
+           "n_v": 100, "lanczos_steps": 15, "T": T_GRID, "dtype": "f64", "ops": ["heat", "wave"],
+           "reorth": "full CGS (reference default)", "graph_source": "host SBM generator",
+           "l2": "flushed between timed steps (256 MiB write), outside the timed events"},
+}
 
 
 def log(*a):
@@ -49,9 +74,30 @@ def dist_env():
     return world, rank, local
 
 
+def operator_runs(cfg):
+    """[(kind, [integrand codes])]: heat/wave share one normalized-Laplacian run, VNGE is a density run."""
+    from paper_2003_01282_b200 import _lib
+
+    runs = []
+    nl = ([_lib.FN_HEAT] if "heat" in cfg["ops"] else []) + \
+         ([_lib.FN_WAVE_RE, _lib.FN_WAVE_IM] if "wave" in cfg["ops"] else [])
+    if nl:
+        runs.append((NL, nl))
+    if "vnge" in cfg["ops"]:
+        runs.append((P, [_lib.FN_XLOGX]))
+    return runs
+
+
+def config_dict(cfg, world):
+    c = {k: v for k, v in cfg.items() if k not in ("dtype",)}
+    c["parallelism"] = f"probe-sharded x{world} (CSR replicated)" if world > 1 else "single GPU"
+    c["scaling_mode"] = "strong: n_v probes split over the ranks"
+    return c
+
+
 class ClockSampler:
-    """SM clocks + throttle reasons sampled every 20 ms during the timed region (NVML; nvidia-smi
-    fallback).  Reasons reported: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap."""
+    """SM clocks + throttle reasons sampled every 20 ms during the timed region (NVML).  Reasons
+    reported: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap."""
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
                ("sw_power_cap", 0x4))
@@ -109,13 +155,6 @@ def spin_up(torch, dev, seconds=0.5):
         torch.cuda.synchronize(dev)
 
 
-def build_graph():
-    from paper_2003_01282_b200 import synth
-
-    return synth.sbm(WORKLOAD["n"], WORKLOAD["blocks"], WORKLOAD["p_in"], WORKLOAD["p_out"],
-                     seed=WORKLOAD["graph_seed"])
-
-
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -125,72 +164,158 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def cpu_baseline(g, n_v, s, grid, threads, max_probes=None):
-    """Oracle port of the reference algorithm timed on the host cores (bounded sample)."""
+# ----------------------------------------------------------------------------------- graphs
+def device_graph(cfg, dev):
+    """The workload graph on `dev` (R-MAT generated on the device; SBM built on the host)."""
+    from paper_2003_01282_b200.device import DeviceGraph
+
+    if cfg["graph"] == "rmat":
+        a, b, c = cfg["abc"]
+        return DeviceGraph.rmat(cfg["scale"], cfg["edge_factor"], a, b, c, seed=cfg["graph_seed"], device=dev), None
+    from paper_2003_01282_b200 import synth
+
+    g = synth.sbm(cfg["n"], cfg["blocks"], cfg["p_in"], cfg["p_out"], seed=cfg["graph_seed"])
+    return DeviceGraph(g, dev), g
+
+
+def host_csr(dg, g):
+    """(offsets int64 [n+1], cols int32 [nnz]) numpy arrays of the workload graph."""
+    import numpy as np
+
+    if g is not None:
+        return np.asarray(g.row_offsets, dtype=np.int64), np.asarray(g.col_indices, dtype=np.int32)
+    return dg.csr()
+
+
+# ----------------------------------------------------------------------------------- CPU arms
+def cpu_operator(off, cols, n, kind):
+    """The oracle port's operator (scipy CSR + degrees: the reference's make_operator arithmetic)."""
+    import numpy as np
+
+    from oracle import slq_oracle as O
+    from paper_2003_01282_b200.graphs import Graph
+
+    g = Graph.__new__(Graph)   # the oracle reads n, m, row_offsets, col_indices, weights
+    object.__setattr__(g, "n", int(n))
+    object.__setattr__(g, "m", int(cols.size // 2))
+    object.__setattr__(g, "row_offsets", off)
+    object.__setattr__(g, "col_indices", cols)
+    object.__setattr__(g, "weights", np.ones(cols.size))
+    return O.make_block_operator(g, kind)
+
+
+def cpu_sample(op, nnz, probes, steps, threads):
+    """The oracle port (numpy + scipy: the reference's per-probe arithmetic, probes spread over
+    `threads` host threads like the reference's thread map, slq.py:80-86) timed on the host:
+    `probes` probes x `steps` Lanczos steps (+ the heat grid when steps > 1).  Returns (units/s, s)."""
     from oracle import slq_oracle as O
 
-    probes = n_v if max_probes is None else min(n_v, max_probes)
     t0 = time.perf_counter()
-    op = O.make_block_operator(g, O.NORMALIZED_LAPLACIAN)
-    rules = O.slq_rules(op, probes, s, 0, threads=threads)
-    O.heat_from_rules(rules, g.n, grid)
-    O.wave_from_rules(rules, g.n, grid)
+    rules = O.slq_rules(op, probes, steps, 0, threads=threads)
+    if steps > 1:
+        O.heat_from_rules(rules, op.dim, O.time_grid(1e-2, 1e2, T_GRID))
     dt = time.perf_counter() - t0
-    units = g.nnz * probes * s
-    return units / dt, dt, probes
+    return nnz * probes * steps / dt, dt
 
 
-def run_reference(args):
-    world, rank, _ = dist_env()
+def big_graph(cfg):
+    return cfg["graph"] == "rmat" and cfg["scale"] >= 24
+
+
+def cpu_baseline_for(cfg, op, nnz, threads):
+    """Bounded CPU sample of the workload (about 10-30 s).  C5: one Lanczos step (SpMV + alpha) of one
+    probe per host thread on the real graph, operator built beforehand (the per-probe-step cost does
+    not depend on n_v; the full signature would take hours on the host); C2/C4: all probes,
+    all steps of the heat run."""
+    if big_graph(cfg):
+        probes, steps = threads, 1
+        sample = (f"{probes} probes (one per host thread) x 1 Lanczos step (SpMV + alpha) of the normalized "
+                  f"Laplacian on the same R-MAT-{cfg['scale']} graph, scipy operator built beforehand "
+                  f"(oracle/slq_oracle.py numpy+scipy port); per-unit rate, units = stored nonzero x probe x step")
+    else:
+        probes, steps = cfg["n_v"], cfg["lanczos_steps"]
+        sample = f"all {probes} probes x {steps} steps of the heat run (oracle port, numpy+scipy)"
+    v, dt = cpu_sample(op, nnz, probes, steps, threads)
+    return v, dt, sample
+
+
+def run_reference(args, cfg):
+    world, rank, local = dist_env()
     if rank != 0:
         return 0
     import numpy as np
 
-    from oracle import slq_oracle as O
-
-    g = build_graph()
-    s, n_v = WORKLOAD["lanczos_steps"], WORKLOAD["n_v_per_gpu"]
-    grid = O.time_grid(1e-2, 1e2, WORKLOAD["T"])
     threads = os.cpu_count() or 1
-    vals, times = [], []
+    t0 = time.perf_counter()
+    if cfg["graph"] == "rmat":
+        # input preparation only: the R-MAT graph is generated by the device generator and copied to
+        # the host (a host generator would take longer than the whole benchmark at scale 27)
+        import torch
+
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        dg, g = device_graph(cfg, torch.device("cuda", torch.cuda.current_device()))
+        off, cols = host_csr(dg, g)
+        n = dg.n
+        del dg
+        torch.cuda.empty_cache()
+        from paper_2003_01282_b200 import _lib
+
+        _lib.trim_pool()
+    else:
+        from paper_2003_01282_b200 import synth
+
+        g = synth.sbm(cfg["n"], cfg["blocks"], cfg["p_in"], cfg["p_out"], seed=cfg["graph_seed"])
+        off, cols, n = np.asarray(g.row_offsets), np.asarray(g.col_indices), g.n
+    op = cpu_operator(off, cols, n, NL)
+    log(f"reference arm: graph + operator ready in {time.perf_counter() - t0:.1f} s (n={n}, nnz={cols.size})")
+    vals, times, sample = [], [], ""
     for k in range(args.warmup + args.steps):
-        v, dt, probes = cpu_baseline(g, n_v, s, grid, threads, max_probes=args.ref_probes)
+        v, dt, sample = cpu_baseline_for(cfg, op, cols.size, threads)
         if k >= args.warmup:
             vals.append(v)
             times.append(dt)
     value = float(np.mean(vals))
-    sample = f"first {probes} of {n_v} probes of the C2 workload (per-probe cost is independent of n_v), oracle port"
+    units_step = len(operator_runs(cfg)) * cols.size * cfg["n_v"] * cfg["lanczos_steps"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SBM)",
-            "config": dict(WORKLOAD, parallelism="cpu threads"), "impl": "reference",
+            "warmup": args.warmup, "ms_per_step": 1e3 * units_step / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded)",
+            "config": config_dict(cfg, args.gpus), "impl": "reference",
+            "ms_per_sample": 1e3 * float(np.mean(times)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def algorithmic_bytes(g, c, s, vb):
-    """Per-class algorithmic DRAM bytes of one Lanczos run on one chunk of c probes."""
-    n, nnz = g.n, g.nnz
+# ----------------------------------------------------------------------------------- roofline
+def spmm_bytes_per_launch(n_rows, nnz, c, vb, s):
+    """Algorithmic DRAM bytes of one SpMM launch, averaged over the s launches of a chunk:
+    per nonzero one gathered c-wide row (no-reuse model) + its int32 column index; per row the offsets
+    (8 B), dinv/degree (16 B), its own row of the input vector and the output row.  Step 0 gathers the
+    16-byte probe bitmask rows instead of c*vb."""
     row = c * vb
-    spmm = s * (nnz * (row + 4) + n * (2 * row + 24))
-    # CGS step kernel, step i: phase A streams w, u_1..u_i and the probe bitmask (u_0, 16 B/row);
-    # phase C streams them again and writes u_{i+1}
-    step = sum(n * row * (2 * (i + 1) + 1) + 2 * n * 16 for i in range(s - 1))
-    return {"spmm": spmm, "cgs_step": step}
+    later = nnz * (row + 4) + n_rows * (2 * row + 24)
+    first = nnz * (16 + 4) + n_rows * (16 + row + 24)
+    return (first + (s - 1) * later) / s
 
 
-def run_ours(args):
+def step_bytes_per_launch(n_rows, c, vb, s):
+    """Algorithmic DRAM bytes of one CGS step-kernel launch, averaged over the s-1 launches: at step i,
+    phase A streams w, u_1..u_i and the probe bitmask; phase C streams them again and writes u_{i+1}."""
+    row = c * vb
+    tot = sum(n_rows * row * (2 * (i + 1) + 1) + 2 * n_rows * 16 for i in range(s - 1))
+    return tot / (s - 1)
+
+
+# ----------------------------------------------------------------------------------- our arm
+def run_ours(args, cfg):
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2003_01282_b200 import _lib
-    from paper_2003_01282_b200.descriptors import TimeGrid, netlsd_heat_wave_slq
     from paper_2003_01282_b200.device import DeviceGraph
-    from paper_2003_01282_b200.dist import gather_rules_arrays
-    from paper_2003_01282_b200.graphs import Graph
+    from paper_2003_01282_b200.dist import probe_ranges, sharded_rules
     from paper_2003_01282_b200.slq import SlqConfig
 
     world, rank, local = dist_env()
@@ -203,41 +328,44 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    g = build_graph()
-    s, n_v = WORKLOAD["lanczos_steps"], WORKLOAD["n_v_per_gpu"]
-    total_probes = n_v * world
-    grid = TimeGrid(1e-2, 1e2, WORKLOAD["T"])
-    dtype = args.dtype
+    dtype = args.dtype or cfg["dtype"]
     vb = 8 if dtype == "f64" else 4
-    tgrid = torch.tensor(np.array(grid.values), device=dev)
-    off_d = torch.tensor(np.array(g.row_offsets), device=dev)
-    cols_d = torch.tensor(np.array(g.col_indices), device=dev)
+    s, n_v = cfg["lanczos_steps"], cfg["n_v"]
+    runs = operator_runs(cfg)
+    scfg = SlqConfig(n_v=n_v, s=s, seed=0)
+    t0 = time.perf_counter()
+    dg, g = device_graph(cfg, dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    n, nnz = dg.n, dg.nnz
+    info = dg.info
+    n_rows = (n - info.isolated + 1) if dg.folded else n     # Lanczos vector rows (isolated-vertex fold)
+    log(f"rank {rank}: graph n={n} nnz={nnz} folded={dg.folded} ready in {gen_s:.1f} s")
+    tgrid = torch.tensor(np.geomspace(1e-2, 1e2, T_GRID), device=dev)
+    tgrid[0], tgrid[-1] = 1e-2, 1e2
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    fns = [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM]
+    def signature(graph):
+        outs, statuses = [], []
+        for kind, fns in runs:
+            if world > 1:
+                rules = sharded_rules(graph, kind, scfg, dtype=dtype)
+            else:
+                rules = graph.rules(kind, 0, 0, n_v, s, dtype=dtype)
+            vals, stds = rules.integrate(tgrid if kind == NL else None, fns)
+            outs.append((vals, stds))
+            statuses.append(rules.status)
+        return outs, statuses
 
-    def step():
-        # device-resident input: prepare + probes + Lanczos + rules + quadrature + aggregate (no host sync)
-        import ctypes
-
-        dg = DeviceGraph.__new__(DeviceGraph)
-        dg.device, dg.graph, dg.n, dg._info = dev, g, g.n, None
-        dg.handle = ctypes.c_void_p()
-        _lib.check(_lib.load().slq_graph_create(g.n, g.nnz, off_d.data_ptr(), cols_d.data_ptr(), None,
-                                                torch.cuda.current_stream().cuda_stream, ctypes.byref(dg.handle)))
-        rules = dg.rules("normalized_laplacian", 0, rank * n_v, n_v, s, dtype=dtype)
-        if world > 1:
-            nodes, weights, steps = gather_rules_arrays(rules.nodes, rules.weights, rules.steps, total_probes)
-            rules = type(rules)(nodes, weights, steps, g.n, status=rules.status)
-        out = rules.integrate(tgrid, fns)
-        del dg
-        return out, rules.status
+    def check(statuses):
+        for st in statuses:
+            _lib.check_status(int(st.item()))
 
     spin_up(torch, dev)
     for _ in range(args.warmup):
-        _, status = step()
-    _lib.check_status(int(status.item()))   # the device reported no error on the warm-up steps
+        _, statuses = signature(dg)
+    check(statuses)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -245,166 +373,176 @@ def run_ours(args):
     if sampler:
         sampler.start()
     launches0 = _lib.launch_count()
-    # Enqueue all K steps without a host sync in between (the host runs ahead of the GPU, so host
-    # jitter on a shared machine cannot starve it); each step is bracketed by its own events and
-    # the L2 flush sits between steps, outside the events.
-    torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     h0 = time.perf_counter()
     for k in range(args.steps):
         flush.fill_(1)
         ev[k][0].record(stream)
-        step()
+        _, statuses = signature(dg)
         ev[k][1].record(stream)
-    host_ms = 1e3 * (time.perf_counter() - h0)
     torch.cuda.synchronize()
-    times = [a.elapsed_time(b) for a, b in ev]
+    host_s = time.perf_counter() - h0
     launches = (_lib.launch_count() - launches0) // args.steps
+    check(statuses)
+    times = [a.elapsed_time(b) for a, b in ev]
     times_eager = times
-    # One step captured as a CUDA graph (graph preparation, probes, Lanczos, rules, quadrature and
-    # aggregate: the same kernels, launched by one graph launch) and replayed K times; single rank only
-    # (the multi-rank step has a host all-gather).  BENCH_EAGER=1 reports the eager loop instead.
-    cuda_graph = world == 1 and not os.environ.get("BENCH_EAGER")
+    # small graphs (C2): one step captured as a CUDA graph and replayed (the same kernels, one launch)
+    cuda_graph = world == 1 and cfg["graph"] == "sbm" and not os.environ.get("BENCH_EAGER")
     graph_note = None
-
-    def graph_times():
-        side = torch.cuda.Stream()
-        side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            step()
-        stream.wait_stream(side)
-        torch.cuda.synchronize()
-        cg = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(cg, capture_error_mode="thread_local"):
-            _, cap_status = step()
-        torch.cuda.synchronize()
-        cg.replay()
-        torch.cuda.synchronize()
-        _lib.check_status(int(cap_status.item()))
-        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for k in range(args.steps):
-            flush.fill_(1)
-            gev[k][0].record(stream)
-            cg.replay()
-            gev[k][1].record(stream)
-        torch.cuda.synchronize()
-        _lib.check_status(int(cap_status.item()))
-        return [a.elapsed_time(b) for a, b in gev]
-
     if cuda_graph:
         try:
-            times = graph_times()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                signature(dg)
+            stream.wait_stream(side)
+            torch.cuda.synchronize()
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, capture_error_mode="thread_local"):
+                _, cap_status = signature(dg)
+            torch.cuda.synchronize()
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for k in range(args.steps):
+                flush.fill_(1)
+                gev[k][0].record(stream)
+                cg.replay()
+                gev[k][1].record(stream)
+            torch.cuda.synchronize()
+            check(cap_status)
+            times = [a.elapsed_time(b) for a, b in gev]
         except Exception as ex:   # capture unavailable: report the eager loop (same kernels)
             cuda_graph, graph_note = False, repr(ex)[:200]
-            times = times_eager
             torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
     ms = float(np.mean(times))
-    # same K steps again with per-launch CUDA events (kernel durations for the roofline)
-    _lib.profile_begin()
-    pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.fill_(1)
-        pev[k][0].record(stream)
-        step()
-        pev[k][1].record(stream)
-    torch.cuda.synchronize()
-    ptimes = [a.elapsed_time(b) for a, b in pev]
-    prof = _lib.profile_end()
     if world > 1:
         t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        dist.barrier()
-    units_step = g.nnz * n_v * s * world
+    units_step = len(runs) * nnz * n_v * s
     value = units_step / (ms * 1e-3)
 
-    # ---- e2e through the public API with host (pinned) buffers ----
-    pin_off = torch.tensor(np.array(g.row_offsets)).pin_memory()
-    pin_cols = torch.tensor(np.array(g.col_indices)).pin_memory()
-    pin_w = torch.tensor(np.array(g.weights)).pin_memory()
+    # ---- one more step with per-launch CUDA events on the launching stream (kernel durations) ----
+    _lib.profile_begin()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.fill_(1)
+    e0.record(stream)
+    signature(dg)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_profiled = e0.elapsed_time(e1)
+    prof = _lib.profile_end()
+
+    # ---- e2e: host CSR (pinned, int32 columns) -> device graph -> signature -> host values ----
+    last_vals = [v.clone() for v, _ in signature(dg)[0]]
+    _lib.trim_pool()             # the Lanczos workspaces cached in the pool are not needed for the copy
+    off_h, cols_h = host_csr(dg, g)
+    torch.cuda.empty_cache()
+    pin_off = torch.from_numpy(np.ascontiguousarray(off_h)).pin_memory()
+    pin_cols = torch.from_numpy(np.ascontiguousarray(cols_h)).pin_memory()
+    del off_h, cols_h
+    folded = dg.folded
+    del dg                       # the e2e leg builds its own device graph from the host arrays
+    torch.cuda.synchronize()
+    h2d = pin_off.numel() * 8 + pin_cols.numel() * 4
+    d2h = 0
     e2e_times = []
-    cfg = SlqConfig(n_v=n_v, s=s, seed=0)
-    h2d = (g.n + 1) * 8 + g.nnz * 8
-    for k in range(args.warmup + args.steps):
-        gh = Graph(n=g.n, row_offsets=pin_off.numpy(), col_indices=pin_cols.numpy(), weights=pin_w.numpy(), m=g.m)
-        flush.fill_(1)
+    for k in range(args.e2e_reps + 1):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        heat, wave = netlsd_heat_wave_slq(gh, grid, cfg, dtype=dtype, with_hash=False)
-        torch.cuda.synchronize()
-        if k >= args.warmup:
-            e2e_times.append(time.perf_counter() - t0)
-    # the same call with the descriptor's graph_hash (SHA-256 of the host CSR bytes, descriptors.py
-    # graph_hash; SURVEY 8d asks for signature seconds with and without it)
-    hash_times = []
-    for k in range(2):
-        gh = Graph(n=g.n, row_offsets=pin_off.numpy(), col_indices=pin_cols.numpy(), weights=pin_w.numpy(), m=g.m)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        heat, wave = netlsd_heat_wave_slq(gh, grid, cfg, dtype=dtype, with_hash=True)
-        torch.cuda.synchronize()
-        hash_times.append(time.perf_counter() - t0)
-    d2h = 3 * 2 * WORKLOAD["T"] * 8
+        dg2 = DeviceGraph.from_csr32(n, pin_off, pin_cols, device=dev)   # H2D + prepare (+ fold)
+        outs, statuses = signature(dg2)
+        host_vals = [(v.cpu(), sd.cpu()) for v, sd in outs]              # D2H of the descriptors
+        check(statuses)
+        dt = time.perf_counter() - t0
+        del dg2, outs
+        if k >= 1:                                                       # rep 0: untimed warm-up
+            e2e_times.append(dt)
+        d2h = sum(v.numel() * 8 + sd.numel() * 8 for v, sd in host_vals)
     e2e_s = float(np.mean(e2e_times))
-    e2e_value = g.nnz * n_v * s / e2e_s
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = units_step / e2e_s
+    # the e2e descriptors equal the device-resident run's bit for bit (same graph, same probes)
+    same = all(torch.equal(hv.to(dev), dv) for (hv, _), dv in zip(host_vals, last_vals))
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return 0
     # ---- roofline of the dominant kernel class ----
     peak, peak_src = measured_peaks()
-    ab = algorithmic_bytes(g, n_v, s, vb)
+    b, e = probe_ranges(n_v, world)[0]
+    per_rank = e - b
+    nchunks = max(1, round(prof["spmm"]["launches"] / (len(runs) * s))) if prof["spmm"]["launches"] else 1
+    c = -(-per_rank // nchunks)
+    ab = {"spmm": spmm_bytes_per_launch(n_rows, nnz, c, vb, s), "cgs_step": step_bytes_per_launch(n_rows, c, vb, s)}
     per_class = {}
     for k, v in prof.items():
         if v["launches"] == 0:
             continue
-        t_ms = v["ms"]
-        per_class[k] = {"ms_per_step": t_ms / args.steps, "launches_per_step": v["launches"] / args.steps}
+        per_class[k] = {"ms_per_step": v["ms"], "launches_per_step": v["launches"],
+                        "ms_per_launch": v["ms"] / v["launches"]}
         if k in ab:
-            per_class[k]["GB_per_step"] = ab[k] / 1e9
-            per_class[k]["achieved_GBs"] = (ab[k] * args.steps / (t_ms * 1e-3) / 1e9) if t_ms > 0 else None
-    dom = max(ab, key=lambda k: per_class.get(k, {}).get("ms_per_step", 0.0))
+            per_class[k]["algorithmic_bytes_per_launch"] = ab[k]
+            per_class[k]["achieved_GBs"] = ab[k] / (per_class[k]["ms_per_launch"] * 1e-3) / 1e9
+    dom = max((k for k in ab if k in per_class), key=lambda k: per_class[k]["ms_per_step"])
     ach = per_class[dom]["achieved_GBs"]
-    traffic, traffic_src = args.traffic, "--traffic" if args.traffic else None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic_c2.json")
-    if traffic is None and os.path.exists(tpath):
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", f"r2_traffic_{args.config}.json")
+    if os.path.exists(tpath):
         with open(tpath) as f:
             tk = json.load(f)["kernels"].get(dom)
         if tk:
             traffic = tk["dram_bytes_per_launch"]
-            traffic_src = "profiles/r1_traffic_c2.json (ncu --set full, dram read+write per launch, avg over a signature)"
+            traffic_src = f"profiles/r2_traffic_{args.config}.json (ncu --set full: dram read+write per launch)"
+    roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": ab[dom], "ms_per_launch": per_class[dom]["ms_per_launch"],
+            "chunk_probes": c, "vector_rows": n_rows}
+    if traffic:
+        roof["dram_GBs"] = traffic / (per_class[dom]["ms_per_launch"] * 1e-3) / 1e9
+        roof["dram_frac"] = roof["dram_GBs"] / peak
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded SBM, BASELINE configs[1] shape)",
-        "config": dict(WORKLOAD, parallelism=f"probe-sharded x{world}" if world > 1 else "single GPU",
-                       total_probes=total_probes, nnz=g.nnz),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": ab[dom] / max(1.0, per_class[dom]["launches_per_step"]),
-                     "peak_source": peak_src},
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": dtype, "data": f"synthetic (seeded; {cfg['graph_source']})",
+        "config": dict(config_dict(cfg, world), total_probes=n_v, nnz=nnz, n=n,
+                       folded_isolated=folded, probes_per_rank=per_rank),
+        "roofline": roof,
         "kernels": per_class,
-        "ms_per_step_profiled": float(np.mean(ptimes)),
+        "ms_per_step_profiled": ms_profiled,
         "ms_steps": [round(t, 3) for t in times],
-        "launch": "one CUDA-graph replay per step (the eager step's kernels)" if cuda_graph else
+        "launch": "one CUDA-graph replay per step" if cuda_graph else
                   ("eager launches" + (f" (capture failed: {graph_note})" if graph_note else "")),
         "ms_per_step_eager": float(np.mean(times_eager)),
-        "host_submit_ms_total": round(host_ms, 3),
+        "host_submit_s_total": round(host_s, 3),
         "gpu_launches": launches,
+        "graph_build_s": round(gen_s, 3),
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": UNIT, "seconds_per_signature": e2e_s,
-                "ms_signatures": [round(1e3 * x, 3) for x in e2e_times],
+                "s_signatures": [round(x, 3) for x in e2e_times],
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "netlsd_heat_wave_slq(Graph on pinned host arrays) incl. H2D, device prepare, D2H",
-                "seconds_per_signature_with_graph_hash": float(np.min(hash_times))},
+                "api": "DeviceGraph.from_csr32 (slq_graph_create_i32: pinned host int64 offsets + int32 columns, "
+                       "H2D, device prepare, isolated-vertex fold) + slq_rules + slq_integrate per operator, "
+                       "D2H of values and std errors",
+                "values_equal_device_resident_run": bool(same)},
     }
     if not args.no_cpu_baseline and world == 1:
-        v, dt, probes = cpu_baseline(g, n_v, s, grid.values, os.cpu_count() or 1, max_probes=args.ref_probes)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                                "sample": f"first {probes} of {n_v} probes of the same C2 workload, {dt:.1f} s "
-                                          "(oracle/slq_oracle.py: numpy+scipy port of the reference)"}
+        threads = os.cpu_count() or 1
+        off_h, cols_h = pin_off.numpy().copy(), pin_cols.numpy().copy()
+        del pin_off, pin_cols
+        op = cpu_operator(off_h, cols_h, n, NL)
+        v, dt, sample = cpu_baseline_for(cfg, op, nnz, threads)
+        s1 = 1 if big_graph(cfg) else s
+        v1, dt1 = cpu_sample(op, nnz, 1, s1, 1)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{sample}; {dt:.1f} s",
+                                "value_1_thread": v1, "sample_1_thread": f"1 probe x {s1} step(s), 1 thread; {dt1:.1f} s"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -414,21 +552,21 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
-    ap.add_argument("--ref-probes", type=int, default=None,
-                    help="probes timed in the CPU arms (default: all n_v)")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
+    ap.add_argument("--dtype", choices=["f64", "f32"], default=None, help="vector storage (default: the config's)")
+    ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes/launch of the dominant kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
         args.warmup = 3
+    cfg = CONFIGS[args.config]
     if args.impl == "reference":
-        return run_reference(args)
-    return run_ours(args)
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
 
 
 if __name__ == "__main__":

@@ -26,8 +26,12 @@
  *     thread-local message.  The Python layer maps codes to the reference's
  *     exceptions (ValueError, TridiagonalEigenError, RuntimeError).
  *   - Reentrant: a graph handle is immutable after creation; concurrent calls
- *     on one handle from different streams are allowed (workspace is
- *     stream-ordered, allocated per call).
+ *     on one handle from different streams or host threads are allowed
+ *     (workspace is stream-ordered, allocated per call; lazily initialised
+ *     per-device state is atomic).  The persistent step kernel, which syncs
+ *     its CTAs through a software grid barrier, is launched as a COOPERATIVE
+ *     kernel: the driver makes all its CTAs co-resident or fails the launch,
+ *     so concurrent calls never deadlock (they may serialise on the SMs).
  */
 #ifndef SLQ_B200_H
 #define SLQ_B200_H
@@ -64,6 +68,15 @@ extern "C" {
 
 typedef struct slq_graph slq_graph;
 
+/* A probe seed of any size: the reference passes SlqConfig.seed (any non-negative Python int,
+ * slq.py:28-35,63-72) to numpy's SeedSequence, which splits it into little-endian uint32 words
+ * (0 -> one zero word).  The *_seeded entry points take that word list (seeds < 2^256); the plain
+ * uint64_t-seed entry points are the same streams for seeds < 2^64. */
+typedef struct slq_seed {
+  uint32_t words[8];
+  int32_t nwords;   /* 1..8 */
+} slq_seed;
+
 typedef struct slq_graph_info_t {
   int64_t n;
   int64_t nnz;          /* stored nonzeros = row_offsets[n] */
@@ -86,6 +99,11 @@ int slq_graph_create(int64_t n, int64_t nnz, const int64_t* offsets, const int64
 int slq_graph_create_host(int64_t n, int64_t nnz, const int64_t* offsets_host,
                           const int64_t* cols_host, const double* weights_host, void* stream,
                           slq_graph** out);
+/* Same from int32 column indices (host or device pointers): the compact CSR of the scale-27 workload
+ * ("int32 indices", BASELINE configs[4]); weights == NULL means implicit 1.0.  The column copy is
+ * adopted by the graph (no int64 staging); out-of-range columns are flagged as in slq_graph_create. */
+int slq_graph_create_i32(int64_t n, int64_t nnz, const int64_t* offsets, const int32_t* cols,
+                         const double* weights, void* stream, slq_graph** out);
 int slq_graph_info(const slq_graph* g, slq_graph_info_t* out);
 void slq_graph_destroy(slq_graph* g);
 
@@ -151,6 +169,10 @@ int slq_lanczos(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin
                 int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
                 void* stream);
 
+int slq_lanczos_seeded(const slq_graph* g, int kind, const slq_seed* seed, int64_t probe_begin, int64_t count,
+                       int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
+                       void* stream);
+
 /* Debug export (lanczos_tridiagonalize(..., return_basis=True), lanczos.py:85,143-144): slq_lanczos
  * plus the Lanczos vectors q_k = u_k / beta_{k-1} of every probe, basis[k][row][count] (k < s',
  * float64; zero after a probe's breakdown).  Runs on the unfolded graph. */
@@ -164,7 +186,13 @@ int slq_lanczos_start(const slq_graph* g, int kind, const double* q0, int64_t ld
                       int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
                       void* stream);
 
-/* Gauss rules of `count` tridiagonals (alpha/beta rows of length ld, steps[count]):
+/* slq_lanczos_start plus the basis export of slq_lanczos_basis: the
+ * lanczos_tridiagonalize(op, q0, s, return_basis=True) entry (lanczos.py:79-145). */
+int slq_lanczos_start_basis(const slq_graph* g, int kind, const double* q0, int64_t ldq, int64_t count, int steps,
+                            int reorth, int dtype, double* basis, double* alpha, double* beta, int32_t* steps_out,
+                            void* stream);
+
+/* Gauss rules of `count` tridiagonals (alpha/beta rows of length ld <= 4096, steps[count]):
  * nodes ascending, clamped to [lo, hi]; weights = squared first eigenvector entries.
  * info[p] = 0 ok, else the eigensolver failed for probe p (returns SLQ_ERR_EIGEN). */
 int slq_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count,
@@ -189,6 +217,10 @@ int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, 
               int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
               void* stream);
 
+int slq_rules_seeded(const slq_graph* g, int kind, const slq_seed* seed, int64_t probe_begin, int64_t count,
+                     int steps, int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out,
+                     int32_t* status, void* stream);
+
 /* For each integrand fns_host[f] (host array of SLQ_FN_*): quadrature over t[T] and the probe
  * aggregate: values[f][T], std_errors[f][T]; per_vector[f][T][count] if not NULL (slq.py:89-105). */
 int slq_integrate(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,
@@ -204,8 +236,11 @@ int slq_signature(const slq_graph* g, int kind, uint64_t seed, int64_t count, in
 /* Rademacher probes as +-1.0 into out[n][ld] (column j = probe probe_begin+j). */
 int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int64_t n, double* out,
                int64_t ld, void* stream);
+int slq_probes_seeded(const slq_seed* seed, int64_t probe_begin, int64_t count, int64_t n, double* out, int64_t ld,
+                      void* stream);
 /* Host: PCG64 (state_hi, state_lo, inc_hi, inc_lo) of SeedSequence(seed, spawn_key=(index,)). */
 int slq_probe_state(uint64_t seed, uint64_t index, uint64_t out_host[4]);
+int slq_probe_state_seeded(const slq_seed* seed, uint64_t index, uint64_t out_host[4]);
 
 /* Batched block-diagonal path (C3): many small graphs stacked in one block-diagonal CSR, one CTA
  * per graph.  vertex_offsets[G+1] (device int64) delimit the graphs; graph g uses probes
@@ -217,6 +252,10 @@ int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_offsets, int64
                         int kind, uint64_t seed, int n_v, int steps, int dtype, double* nodes,
                         double* weights, int32_t* steps_out, int32_t* status, void* stream);
 
+int slq_lanczos_batched_seeded(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs, int kind,
+                               const slq_seed* seed, int n_v, int steps, int dtype, double* nodes, double* weights,
+                               int32_t* steps_out, int32_t* status, void* stream);
+
 /* Per-graph quadrature + probe aggregate of batched rules: values/std_errors [G][T]
  * (value = n_g * mean over the graph's probes). */
 int slq_integrate_batched(const double* nodes, const double* weights, const int32_t* steps,
@@ -225,6 +264,12 @@ int slq_integrate_batched(const double* nodes, const double* weights, const int3
                           int32_t* status, void* stream);
 
 /* Diagnostics */
+/* Probe-steps of graph g that ran the conditional second CGS pass (lanczos.py:75-76), summed over
+ * every Lanczos call on g since it was created (synchronises the graph's creation stream). */
+int slq_graph_second_passes(const slq_graph* g, int64_t* out_host);
+/* Release the device memory the library's stream-ordered pool keeps cached on the current device
+ * (synchronises the device). */
+int slq_trim_pool(void);
 const char* slq_last_error(void);
 uint64_t slq_launch_count(void);                /* kernels launched by this library so far */
 void slq_profile_begin(void);                   /* start per-class CUDA-event timing */

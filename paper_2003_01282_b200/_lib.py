@@ -37,9 +37,38 @@ class GraphInfo(ctypes.Structure):
                 ("isolated", _i64), ("unit_weights", _i32), ("ntiles", _i32)]
 
 
+class Seed(ctypes.Structure):
+    """slq_seed: the seed's little-endian uint32 entropy words (numpy SeedSequence, slq.py:63-72)."""
+    _fields_ = [("words", ctypes.c_uint32 * 8), ("nwords", ctypes.c_int32)]
+
+
+def seed_arg(seed) -> "ctypes._Pointer":
+    """ctypes pointer to the slq_seed of a non-negative integer seed (< 2^256), split into uint32
+    words exactly as numpy's SeedSequence does; negative seeds raise ValueError like numpy."""
+    s = int(seed)
+    if s < 0:
+        raise ValueError("expected non-negative integer")
+    words = []
+    while True:
+        words.append(s & 0xFFFFFFFF)
+        s >>= 32
+        if not s:
+            break
+    if len(words) > 8:
+        raise ValueError("seeds of more than 256 bits are not supported by the device probe stream")
+    out = Seed()
+    for i, w in enumerate(words):
+        out.words[i] = w
+    out.nwords = len(words)
+    return ctypes.pointer(out)
+
+
+_SP = ctypes.POINTER(Seed)
+
 _SIGS = {
     "slq_graph_create": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "slq_graph_create_host": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
+    "slq_graph_create_i32": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "slq_graph_create_rmat": (_int, [_int, _int, _dbl, _dbl, _dbl, _u64, _vp, ctypes.POINTER(_vp)]),
     "slq_rmat_uniform_host": (_int, [_u64, _u64, _int, ctypes.POINTER(_dbl)]),
     "slq_graph_csr": (_int, [_vp, _vp, _vp, _vp]),
@@ -55,6 +84,7 @@ _SIGS = {
     "slq_lanczos": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "slq_lanczos_start": (_int, [_vp, _int, _vp, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "slq_lanczos_basis": (_int, [_vp, _int, _u64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "slq_lanczos_start_basis": (_int, [_vp, _int, _vp, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "slq_gauss_rules": (_int, [_vp, _vp, _vp, _i64, _int, _dbl, _dbl, _vp, _vp, _vp, _vp]),
     "slq_quadrature": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _i64, _int, _vp, _vp]),
     "slq_estimate": (_int, [_vp, _i64, _i64, _dbl, _vp, _vp, _vp]),
@@ -65,6 +95,13 @@ _SIGS = {
     "slq_signature": (_int, [_vp, _int, _u64, _i64, _int, _int, _int, _vp, _i64, _vp, _int, _vp, _vp, _vp, _vp]),
     "slq_lanczos_batched": (_int, [_vp, _vp, _i64, _int, _u64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "slq_integrate_batched": (_int, [_vp, _vp, _vp, _i64, _int, _int, _vp, _vp, _i64, _int, _vp, _vp, _vp, _vp]),
+    "slq_graph_second_passes": (_int, [_vp, ctypes.POINTER(_i64)]),
+    "slq_lanczos_seeded": (_int, [_vp, _int, _SP, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "slq_rules_seeded": (_int, [_vp, _int, _SP, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "slq_probes_seeded": (_int, [_SP, _i64, _i64, _i64, _vp, _i64, _vp]),
+    "slq_probe_state_seeded": (_int, [_SP, _u64, ctypes.POINTER(_u64)]),
+    "slq_lanczos_batched_seeded": (_int, [_vp, _vp, _i64, _int, _SP, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "slq_trim_pool": (_int, []),
     "slq_last_error": (ctypes.c_char_p, []),
     "slq_launch_count": (_u64, []),
     "slq_profile_begin": (None, []),
@@ -156,6 +193,11 @@ def require_cuda():
         raise SlqLibraryError("no CUDA device visible: the SLQ engine runs only on the GPU (no CPU fallback)")
     load()
     return torch
+
+
+def trim_pool() -> None:
+    """Give the library's cached stream-ordered pool memory on the current device back to the driver."""
+    check(load().slq_trim_pool())
 
 
 def launch_count() -> int:

@@ -59,8 +59,8 @@ class BatchedGraphs:
         status = torch.zeros(1, dtype=torch.int32, device=dev)
         code = {"normalized_laplacian": _lib.NORMALIZED_LAPLACIAN, "density": _lib.DENSITY}[kind]
         with torch.cuda.device(dev):
-            _lib.check(_lib.load().slq_lanczos_batched(
-                self.dg.handle, _lib.ptr(self.voff_d), G, code, int(cfg.seed), c, s,
+            _lib.check(_lib.load().slq_lanczos_batched_seeded(
+                self.dg.handle, _lib.ptr(self.voff_d), G, code, _lib.seed_arg(cfg.seed), c, s,
                 _lib.F64 if dtype == "f64" else _lib.F32, _lib.ptr(nodes), _lib.ptr(weights), _lib.ptr(steps),
                 _lib.ptr(status), _lib.stream_handle(dev)))
         return nodes, weights, steps, status

@@ -32,7 +32,7 @@ struct BatchArgs {
   const int64_t* voff;     // [G+1]
   int64_t G;
   int kind;
-  uint64_t seed;
+  SeedKey seed;
   int c;                   // probes per graph
   int S;                   // requested steps
   int64_t N;               // total vertices
@@ -244,6 +244,7 @@ batched_lanczos_kernel(BatchArgs a) {
             if (b < 0.5 * sqrt(nb[t])) {                 // lanczos.py:75
               again[t] = 1;
               *any_again = 1;
+              if (a.dflags) atomicAdd(const_cast<int*>(a.dflags) + 2, 1);   // second-pass counter
               commit = false;
             }
           } else {
@@ -355,9 +356,9 @@ __global__ void batched_integrate_kernel(const double* __restrict__ nodes, const
 
 using namespace slq;
 
-extern "C" int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs, int kind,
-                                   uint64_t seed, int n_v, int steps, int dtype, double* nodes, double* weights,
-                                   int32_t* steps_out, int32_t* status, void* stream) {
+static int lanczos_batched_entry(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs, int kind,
+                                 const SeedKey& seed, int n_v, int steps, int dtype, double* nodes, double* weights,
+                                 int32_t* steps_out, int32_t* status, void* stream) {
   if (!g || !vertex_offsets || !status) return fail(SLQ_ERR_VALUE, "NULL argument");
   if (n_v < 1 || n_v > kBatchMaxProbes) return fail(SLQ_ERR_VALUE, "batched path: 1 <= n_v <= 64");
   if (steps < 1 || steps > kMaxSteps) return fail(SLQ_ERR_VALUE, "steps must be in [1, 128]");
@@ -417,7 +418,14 @@ int64_t small_graph_max_n() {
   return v;
 }
 
-int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int S, int dtype,
+// Vertex offsets {0, n} of the single graph, written on the device: no host buffer is read inside
+// the call, so it can be captured into a CUDA graph (a pageable memcpy from a stack array cannot).
+static __global__ void single_graph_offsets_kernel(int64_t* voff, int64_t n) {
+  voff[0] = 0;
+  voff[1] = n;
+}
+
+int small_rules(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe_begin, int64_t count, int S, int dtype,
                 double* nodes, double* weights, int32_t* steps_out, int32_t* status, cudaStream_t st) {
   const int c = static_cast<int>(std::min<int64_t>(count, kBatchMaxProbes));
   const int64_t blocks = (count + c - 1) / c;
@@ -426,8 +434,7 @@ int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin
   int64_t* voff = nullptr;
   SLQ_CUDA(cudaMallocAsync(&vec, static_cast<size_t>(blocks) * (S + 1) * std::max<int64_t>(g->n, 1) * c * vb, st));
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&voff), 2 * sizeof(int64_t), st));
-  const int64_t hv[2] = {0, g->n};
-  SLQ_CUDA(cudaMemcpyAsync(voff, hv, sizeof(hv), cudaMemcpyHostToDevice, st));
+  single_graph_offsets_kernel<<<1, 1, 0, st>>>(voff, g->n);
   BatchArgs a{};
   a.offsets = g->offsets; a.cols = g->cols; a.weights = g->weights; a.degree = g->degree; a.dinv = g->dinv;
   a.dscal = g->dscal; a.voff = voff; a.G = 1; a.kind = kind; a.seed = seed; a.c = c;
@@ -462,6 +469,22 @@ int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin
 }
 
 }  // namespace slq
+
+extern "C" int slq_lanczos_batched(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs, int kind,
+                                   uint64_t seed, int n_v, int steps, int dtype, double* nodes, double* weights,
+                                   int32_t* steps_out, int32_t* status, void* stream) {
+  return lanczos_batched_entry(g, vertex_offsets, num_graphs, kind, seed_key_u64(seed), n_v, steps, dtype, nodes,
+                               weights, steps_out, status, stream);
+}
+
+extern "C" int slq_lanczos_batched_seeded(const slq_graph* g, const int64_t* vertex_offsets, int64_t num_graphs,
+                                          int kind, const slq_seed* seed, int n_v, int steps, int dtype, double* nodes,
+                                          double* weights, int32_t* steps_out, int32_t* status, void* stream) {
+  SeedKey k;
+  if (!seed_key_of(seed, &k)) return fail(SLQ_ERR_VALUE, "seed must have 1..8 entropy words");
+  return lanczos_batched_entry(g, vertex_offsets, num_graphs, kind, k, n_v, steps, dtype, nodes, weights, steps_out,
+                               status, stream);
+}
 
 extern "C" int slq_integrate_batched(const double* nodes, const double* weights, const int32_t* steps,
                                      int64_t num_graphs, int n_v, int ld, const int64_t* vertex_offsets,

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -29,7 +30,7 @@ constexpr int kMaxChunk = 256;       // probes per chunk (flat CGS CTAs of <= 51
 constexpr int kBitWords = 4;   // bitmask row stride in 32-bit words (16 B: bulk-copy aligned; c <= 128)
 
 template <typename VT>
-__global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* __restrict__ u,
+__global__ void probe_init_kernel(SeedKey seed, int64_t probe_begin, int c, int64_t n, VT* __restrict__ u,
                                   int64_t ldc, uint32_t* __restrict__ bits,
                                   const int32_t* __restrict__ remap) {
   const int lane = threadIdx.x & 31;
@@ -71,7 +72,7 @@ __global__ void probe_init_kernel(uint64_t seed, int64_t probe_begin, int c, int
 }
 
 template <typename VT>
-static void launch_probes(uint64_t seed, int64_t probe_begin, int c, int64_t n, VT* u, int64_t ldc,
+static void launch_probes(const SeedKey& seed, int64_t probe_begin, int c, int64_t n, VT* u, int64_t ldc,
                           cudaStream_t st, uint32_t* bits = nullptr, const int32_t* remap = nullptr) {
   const int64_t runs = (n + 2 * kProbeRun - 1) / (2 * kProbeRun);
   dim3 grid(ceil_div(runs, 4), ceil_div(c, 32));
@@ -103,11 +104,13 @@ struct ChunkState {
   double* cdot = nullptr;   // [S+1][cpad]  sum_rows u_k . w            (k <= i)
   double* gram = nullptr;   // [S+1][cpad]  sum_rows u_k . u_{i+1}      (k <= i), row of the new vector
   double* nrm2 = nullptr;   // [cpad]       ||u_{i+1}||^2
-  double* G = nullptr;      // [(S+1)*(S+1)][cpad]  G(k,j) = q_k . q_j
+  double* G = nullptr;      // [gstride*gstride][cpad]  G(k,j) = q_k . q_j (staged steps only: k, j <= 17)
+  int gstride = 0;          // min(S + 1, kCgsBlock + 2)
   int* steps = nullptr;     // [cpad]
   int* alive = nullptr;     // [cpad]
   int* again = nullptr;     // [cpad]
   int* any_again = nullptr; // [1]
+  int* second_passes = nullptr;   // graph counter: probe-steps that ran the second CGS pass (diagnostics)
   unsigned int* barrier = nullptr;   // [S] grid-barrier counters of the persistent step kernels
   unsigned long long* work = nullptr;   // [S][4] SpMM work counters
 };
@@ -167,6 +170,7 @@ static __device__ void apply_reduced(const ReduceArgs& a, int q, int p, double t
         if (a.reorth && b < 0.5 * sqrt(a.s.nb2[p])) {    // lanczos.py:75
           a.s.again[p] = 1;
           *a.s.any_again = 1;
+          if (a.s.second_passes) atomicAdd(a.s.second_passes, 1);
           break;
         }
       } else {
@@ -1111,7 +1115,7 @@ __device__ __forceinline__ void staged_produce(const StagedArgs& sa, StageRing<V
 
 // Gram-matrix entry G(k, j) of probe p (G is symmetric; stored as [(S+1)*(S+1)][cpad]).
 __device__ __forceinline__ double gram_at(const ChunkState& s, int k, int j, int p) {
-  return s.G[(static_cast<int64_t>(k) * (s.S + 1) + j) * s.cpad + p];
+  return s.G[(static_cast<int64_t>(k) * s.gstride + j) * s.cpad + p];
 }
 
 // Shared-memory stage layout: [slot][row][ldc] with slot 0 = source (w or u_{i+1}) and slot k = u_k
@@ -1519,7 +1523,7 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
   const ChunkState& S = a.s;
   const int ngroups = a.cpad / 32, cp = a.cpad;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nk = a.i + 1, nq = nk + 2, nslot = S.S + 1;
+  const int nk = a.i + 1, nq = nk + 2, nslot = S.gstride;
   // C / C': update
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) staged_produce<VT>(st, ring, ch, lo, hi, kReverseUpdate);
@@ -1549,6 +1553,7 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
     if (!SECOND && b < 0.5 * sqrt(S.nb2[p])) {
       S.again[p] = 1;
       *S.any_again = 1;
+      if (S.second_passes) atomicAdd(S.second_passes, 1);
       continue;
     }
     if (SECOND) S.again[p] = 0;
@@ -1616,7 +1621,6 @@ cgs_step_kernel(StepArgs sa) {
   const int ngroups = a.cpad / 32, cp = a.cpad;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nk = a.i + 1;
-  const int nslot = S.S + 1;
   const int nrows_partial = gridDim.x;   // one pre-reduced partial row per CTA
   int ch = 0;
   const StagedArgs& st0 = sa.pass[0];
@@ -1724,37 +1728,66 @@ static bool staged_setup(const CgsArgs& a, bool second, const uint32_t* bits, St
   return true;
 }
 
+// Whether the persistent step kernel can run on `dev`: the part must be able to hold its grid and
+// support cooperative launches (the launch itself then guarantees co-residency).
 static int coop_supported(int dev) {
-  static int v[64] = {0};
+  static std::atomic<int> v[64];
   if (dev < 0 || dev >= 64) return 0;
-  if (v[dev] == 0) {
-    int sms = 0;
+  int cur = v[dev].load(std::memory_order_acquire);
+  if (cur == 0) {
+    int sms = 0, coop = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    v[dev] = sms >= kPersist ? 1 : 2;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cur = (sms >= kPersist && coop) ? 1 : 2;
+    v[dev].store(cur, std::memory_order_release);
   }
-  return v[dev] == 1;
+  return cur == 1;
 }
 
 // Class launchers (instantiated per vector type and slot class in step_{f32,f64}_{wide,narrow}.cu).
-bool step_launch_f32_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
-bool step_launch_f32_narrow(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
-bool step_launch_f64_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
-bool step_launch_f64_narrow(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st);
+bool step_launch_f32_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st, cudaError_t* e);
+bool step_launch_f32_narrow(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st, cudaError_t* e);
+bool step_launch_f64_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st, cudaError_t* e);
+bool step_launch_f64_narrow(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st, cudaError_t* e);
+
+// The dynamic shared-memory opt-in is per device context: remember it per (instance, device).
+inline bool smem_optin(const void* fn, int bytes, std::atomic<bool>* done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  if (!done[dev].load(std::memory_order_acquire)) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+    done[dev].store(true, std::memory_order_release);
+  }
+  return true;
+}
+
+// The step kernel spins on a software grid barrier, so every CTA must be resident at once: it is
+// launched as a COOPERATIVE kernel (cudaLaunchAttributeCooperative), for which the driver guarantees
+// co-residency or fails the launch (cudaErrorCooperativeLaunchTooLarge) instead of hanging -- also
+// when other streams, processes (MPS) or green contexts hold part of the SMs.  Capturable in graphs.
+template <typename VT, int NK, int MM, int SL>
+inline cudaError_t launch_step_coop(const StepArgs& sa, int threads, size_t smem, cudaStream_t st) {
+  static std::atomic<bool> attr[64];
+  if (!smem_optin(reinterpret_cast<const void*>(cgs_step_kernel<VT, NK, MM, SL>), static_cast<int>(kStagedSmem), attr))
+    return cudaErrorInvalidDevice;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(step_ctas(sa.pass[0].a.n));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cgs_step_kernel<VT, NK, MM, SL>, sa);
+}
 
 template <typename VT, int SL, int MM>
-bool step_launch_one(const StepArgs& sa, int nk, int threads, size_t smem, cudaStream_t st) {
+bool step_launch_one(const StepArgs& sa, int nk, int threads, size_t smem, cudaStream_t st, cudaError_t* err) {
   switch (nk) {
-#define SLQ_STEP_K(K)                                                                                     \
-    case K: {                                                                                              \
-      static bool attr = false;                                                                            \
-      if (!attr) {                                                                                         \
-        cudaFuncSetAttribute(cgs_step_kernel<VT, K, MM, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                             static_cast<int>(kStagedSmem));                                               \
-        attr = true;                                                                                       \
-      }                                                                                                    \
-      cgs_step_kernel<VT, K, MM, SL><<<step_ctas(sa.pass[0].a.n), threads, smem, st>>>(sa);                \
-      return true;                                                                                         \
-    }
+#define SLQ_STEP_K(K) \
+    case K: *err = launch_step_coop<VT, K, MM, SL>(sa, threads, smem, st); return true;
     SLQ_STEP_K(1) SLQ_STEP_K(2) SLQ_STEP_K(3) SLQ_STEP_K(4) SLQ_STEP_K(5) SLQ_STEP_K(6) SLQ_STEP_K(7)
     SLQ_STEP_K(8) SLQ_STEP_K(9) SLQ_STEP_K(10) SLQ_STEP_K(11) SLQ_STEP_K(12) SLQ_STEP_K(13) SLQ_STEP_K(14)
     SLQ_STEP_K(15) SLQ_STEP_K(16)
@@ -1781,22 +1814,20 @@ static bool launch_cgs_step(const CgsArgs& a, const ReduceArgs& red, const SpmmA
                                                   stage_elems_of<VT>(sa.pass[1].nvec, sa.pass[1].rt, sa.pass[1].vstride,
                                                                      a.pre_dinv != nullptr)));
   LaunchScope ls(K_CGS_UPDATE, st);
-  // kPersist = 148 CTAs, at most one per SM by shared memory and all co-resident on a 148-SM part,
-  // so the software grid barrier is safe (coop_supported() checked the SM count).
+  // at most one CTA per SM by shared memory; the cooperative launch makes co-residency a driver
+  // guarantee (the software grid barrier never waits on a CTA that is not running)
   const StepGeom geo = step_geometry(a.ldc);
   const int threads = 32 + geo.slots * step_slot_threads(a.ldc, geo.parts);
   const bool narrow = geo.slots == kNarrowSlots;
+  cudaError_t e = cudaSuccess;
   bool ok;
-  if (sizeof(VT) == 4) ok = narrow ? step_launch_f32_narrow(sa, a.i + 1, geo.parts, threads, smem, st)
-                                   : step_launch_f32_wide(sa, a.i + 1, geo.parts, threads, smem, st);
-  else ok = narrow ? step_launch_f64_narrow(sa, a.i + 1, geo.parts, threads, smem, st)
-                   : step_launch_f64_wide(sa, a.i + 1, geo.parts, threads, smem, st);
+  if (sizeof(VT) == 4) ok = narrow ? step_launch_f32_narrow(sa, a.i + 1, geo.parts, threads, smem, st, &e)
+                                   : step_launch_f32_wide(sa, a.i + 1, geo.parts, threads, smem, st, &e);
+  else ok = narrow ? step_launch_f64_narrow(sa, a.i + 1, geo.parts, threads, smem, st, &e)
+                   : step_launch_f64_wide(sa, a.i + 1, geo.parts, threads, smem, st, &e);
   if (!ok) return false;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    *rc = cuda_fail(e, "cgs_step_kernel launch");
-    return true;
-  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) *rc = cuda_fail(e, "cgs_step_kernel cooperative launch");
   return true;
 }
 

@@ -32,6 +32,18 @@ __global__ void narrow_cols_kernel(const int64_t* __restrict__ cols, int32_t* __
   }
 }
 
+// int32 columns given by the caller: range check in place (out-of-range -> flag, clamped to 0)
+__global__ void check_cols_kernel(int32_t* __restrict__ cols, int64_t nnz, int64_t n, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = cols[i];
+    if (c < 0 || c >= n) {
+      *bad = 1;
+      cols[i] = 0;
+    }
+  }
+}
+
 __global__ void unit_weight_kernel(const double* __restrict__ w, int64_t nnz, int* __restrict__ nonunit) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -165,7 +177,7 @@ static void* track(slq_graph* g, void* p) {
 // cudaMallocAsync (adopt_off, adopt_cols: the graph frees them).
 static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols, const double* weights,
                        cudaStream_t st, int64_t* adopt_off = nullptr, int32_t* adopt_cols = nullptr,
-                       double* adopt_w = nullptr) {
+                       double* adopt_w = nullptr, bool check_adopted = false) {
   const int64_t n = g->n, nnz = g->nnz;
   void* p = nullptr;
   if (adopt_off) {
@@ -195,6 +207,9 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   if (nnz > 0 && !adopt_cols) {
     LaunchScope ls(K_PREPARE, st);
     narrow_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cols, const_cast<int32_t*>(g->cols), nnz, n, g->dflags);
+  } else if (nnz > 0 && check_adopted) {
+    LaunchScope ls(K_PREPARE, st);
+    check_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(const_cast<int32_t*>(g->cols), nnz, n, g->dflags);
   }
   if ((weights || adopt_w) && nnz > 0) {
     // explicit weights are kept even if all are 1.0 (w * t == t exactly, so results are identical)
@@ -439,6 +454,7 @@ static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
   f->nnz = nnz;
   f->stream = g->stream;
   f->device = g->device;
+  f->device_total_mem = g->device_total_mem;
   rc = graph_adopt(f, off_f, cols_f, st, w_f);
   if (rc) {
     slq_graph_destroy(f);
@@ -474,6 +490,7 @@ extern "C" int slq_graph_create(int64_t n, int64_t nnz, const int64_t* offsets, 
   g->stream = stream;
   cudaGetDevice(&g->device);
   ensure_pool(g->device);
+  { size_t fr = 0; cudaMemGetInfo(&fr, &g->device_total_mem); }
   int rc = graph_build(g, offsets, cols, weights, static_cast<cudaStream_t>(stream));
   if (rc != SLQ_OK) {
     slq_graph_destroy(g);
@@ -504,6 +521,54 @@ extern "C" int slq_graph_create_host(int64_t n, int64_t nnz, const int64_t* offs
   cudaFreeAsync(d_cols, st);
   if (d_w) cudaFreeAsync(d_w, st);
   return rc;
+}
+
+// int32 columns (the C5 data format: "int32 indices with fp32 values", implicit unit weights when
+// weights == NULL); host or device pointers.  The copies land in buffers the graph adopts, so the
+// device holds one int32 copy of the columns (no int64 staging).
+extern "C" int slq_graph_create_i32(int64_t n, int64_t nnz, const int64_t* offsets, const int32_t* cols,
+                                    const double* weights, void* stream, slq_graph** out) {
+  if (!out) return fail(SLQ_ERR_VALUE, "out must not be NULL");
+  *out = nullptr;
+  if (n < 0 || nnz < 0) return fail(SLQ_ERR_VALUE, "negative n or nnz");
+  if (n >= (int64_t(1) << 31)) return fail(SLQ_ERR_VALUE, "n >= 2^31 is not supported (int32 columns)");
+  if (!offsets || (nnz > 0 && !cols)) return fail(SLQ_ERR_VALUE, "NULL CSR array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  slq_graph* g = new slq_graph();
+  g->n = n;
+  g->nnz = nnz;
+  g->stream = stream;
+  cudaGetDevice(&g->device);
+  ensure_pool(g->device);
+  { size_t fr = 0; cudaMemGetInfo(&fr, &g->device_total_mem); }
+  int64_t* off = nullptr;
+  int32_t* c = nullptr;
+  double* w = nullptr;
+  auto cleanup = [&]() {
+    if (off) cudaFreeAsync(off, st);
+    if (c) cudaFreeAsync(c, st);
+    if (w) cudaFreeAsync(w, st);
+    delete g;
+  };
+  if (cudaMallocAsync(reinterpret_cast<void**>(&off), sizeof(int64_t) * (n + 1), st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(int32_t) * std::max<int64_t>(nnz, 1), st) != cudaSuccess ||
+      (weights && nnz > 0 && cudaMallocAsync(reinterpret_cast<void**>(&w), sizeof(double) * nnz, st) != cudaSuccess)) {
+    cleanup();
+    return fail(SLQ_ERR_ALLOC, "device allocation failed for the CSR");
+  }
+  if (cudaMemcpyAsync(off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, st) != cudaSuccess ||
+      (nnz > 0 && cudaMemcpyAsync(c, cols, sizeof(int32_t) * nnz, cudaMemcpyDefault, st) != cudaSuccess) ||
+      (w && cudaMemcpyAsync(w, weights, sizeof(double) * nnz, cudaMemcpyDefault, st) != cudaSuccess)) {
+    cleanup();
+    return cuda_fail(cudaGetLastError(), "CSR copy");
+  }
+  const int rc = graph_build(g, nullptr, nullptr, nullptr, st, off, c, w, /*check_adopted=*/true);
+  if (rc != SLQ_OK) {
+    slq_graph_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return SLQ_OK;
 }
 
 extern "C" int slq_graph_info(const slq_graph* g, slq_graph_info_t* out) {

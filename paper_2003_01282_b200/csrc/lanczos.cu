@@ -121,14 +121,14 @@ static bool staged_enabled() {
 }
 
 void ensure_pool(int dev) {
-  static bool done[64] = {false};
-  if (dev < 0 || dev >= 64 || done[dev]) return;
+  static std::atomic<bool> done[64];
+  if (dev < 0 || dev >= 64 || done[dev].load(std::memory_order_acquire)) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  done[dev] = true;
+  done[dev].store(true, std::memory_order_release);
 }
 
 static int64_t partial_rows(const slq_graph* g);
@@ -144,15 +144,17 @@ static bool lean_schedule(const slq_graph* g, bool start_block, int S, int reort
 // columns when more than one sector fits (a narrower chunk gathers whole sectors; the padded
 // tail of a wider chunk would not).  Results do not depend on the chunk width.
 static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bool lean, cudaStream_t st) {
-  // memory queries are not allowed while the stream is being captured into a CUDA graph: reuse the
-  // last value seen on this device then
-  thread_local double last_avail[64] = {0.0};   // per host thread: the library stays reentrant
+  // Memory queries are not allowed while the stream is being captured into a CUDA graph: a capture
+  // reuses the last value seen on this device by ANY host thread (process-wide, atomic), or, when no
+  // eager call ran yet, a conservative fixed budget (1/4 of the device's memory).
+  static std::atomic<double> last_avail[64];
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
   double avail = 0.0;
   const int dev = g->device >= 0 && g->device < 64 ? g->device : 0;
-  if (cap != cudaStreamCaptureStatusNone && last_avail[dev] > 0.0) {
-    avail = last_avail[dev];
+  if (cap != cudaStreamCaptureStatusNone) {
+    avail = last_avail[dev].load(std::memory_order_relaxed);
+    if (avail <= 0.0) avail = static_cast<double>(g->device_total_mem) / 4.0;
   } else {
     size_t freeb = 0, total = 0;
     cudaMemGetInfo(&freeb, &total);
@@ -164,7 +166,7 @@ static int choose_chunk(const slq_graph* g, int64_t count, int S, int vbytes, bo
       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
       if (reserved > used) avail += static_cast<double>(reserved - used);
     }
-    last_avail[dev] = avail;
+    last_avail[dev].store(avail, std::memory_order_relaxed);
   }
   const double budget = 0.9 * avail - static_cast<double>(1ull << 30);
   const int nvec = lean ? S : S + 2;
@@ -193,7 +195,7 @@ struct FoldRun {
 };
 
 template <typename VT>
-static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0, const double* q0, int64_t ldq,
+static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe0, const double* q0, int64_t ldq,
                      int c, int S, int reorth, double* alpha_out, double* beta_out, int32_t* steps_out, int64_t col0,
                      cudaStream_t st, FoldRun fold = FoldRun{}, double* basis_out = nullptr, int64_t basis_ld = 0) {
   const double t_host0 = host_ms();
@@ -216,7 +218,8 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   // all_staged: slots u_1..u_{S-1} and w only (lean_schedule); basis[0] is never addressed
   const int64_t nvec = all_staged ? S : S + 2;
   const size_t bytes_vec = static_cast<size_t>(vs) * vb * nvec;
-  const size_t bytes_state = sizeof(double) * cpad * (6 * (S + 1) + 3 + (S + 1) * (S + 1)) +
+  const int gstride = std::min(S + 1, kCgsBlock + 2);   // Gram matrix of the staged steps (i + 1 <= kCgsBlock)
+  const size_t bytes_state = sizeof(double) * cpad * (6 * (S + 1) + 3 + gstride * gstride) +
                              sizeof(int) * (3 * cpad + 4 + S + 4) + sizeof(unsigned long long) * (4 * S + 2);
   const size_t bytes_part = sizeof(double) * ptiles * nq_max * cpad;
   const size_t bytes_seg = sizeof(double) * g->max_seg * cpad;
@@ -228,6 +231,12 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   const size_t off_bits = off_seg + ((bytes_seg + 255) / 256) * 256;
   const size_t bytes_bits = sizeof(uint32_t) * kBitWords * static_cast<size_t>(std::max<int64_t>(n, 1));
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), off_bits + bytes_bits, st));
+  // every early return below frees the workspace (the pool never releases it to the device)
+  struct WsGuard {
+    void* p;
+    cudaStream_t s;
+    ~WsGuard() { if (p) cudaFreeAsync(p, s); }
+  } ws_guard{ws, st};
   SLQ_TRACE("after malloc");
   VT* basis = all_staged ? reinterpret_cast<VT*>(ws) - vs : reinterpret_cast<VT*>(ws);
   VT* wv = basis + (all_staged ? S : S + 1) * vs;
@@ -243,11 +252,13 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
   s.gram = s.cdot + (S + 1) * cpad;
   s.nrm2 = s.gram + (S + 1) * cpad;
   s.G = s.nrm2 + cpad;
-  int* istate = reinterpret_cast<int*>(s.G + (S + 1) * (S + 1) * cpad);
+  s.gstride = gstride;
+  int* istate = reinterpret_cast<int*>(s.G + static_cast<int64_t>(gstride) * gstride * cpad);
   s.steps = istate;
   s.alive = istate + cpad;
   s.again = istate + 2 * cpad;
   s.any_again = istate + 3 * cpad;
+  s.second_passes = (fold.orig ? fold.orig : g)->dflags + 2;
   s.barrier = reinterpret_cast<unsigned int*>(istate + 3 * cpad + 4);
   s.work = reinterpret_cast<unsigned long long*>(
       (reinterpret_cast<uintptr_t>(s.barrier + S) + 15) & ~static_cast<uintptr_t>(15));
@@ -334,7 +345,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
     sa.bits = (i == 0) ? bits : nullptr;
     sa.upre = (prescale && i >= 1 && i <= S - 2) ? static_cast<const void*>(basis + (i + 1) * vs) : nullptr;
     ca.pre_dinv = (prescale && i + 1 <= S - 2) ? g->dinv : nullptr;
-    ca.dbg = dbgbuf ? dbgbuf + kDbgStride * i : nullptr;
+    ca.dbg = (dbgbuf && i < kMaxSteps) ? dbgbuf + kDbgStride * i : nullptr;
     ca.i = i;
     ca.second = 0;
     // staged step kernel: alpha and the CGS coefficients come from its Gram form, so the SpMM only
@@ -393,6 +404,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
         basis, all_staged ? bits : nullptr, s.rsc, cpad, n, ldc, c, S, vs, basis_out, basis_ld, col0);
   }
   SLQ_CUDA(cudaGetLastError());
+  ws_guard.p = nullptr;
   SLQ_CUDA(cudaFreeAsync(ws, st));
   SLQ_TRACE("chunk done");
   return SLQ_OK;
@@ -402,7 +414,7 @@ static int run_chunk(const slq_graph* g, int kind, uint64_t seed, int64_t probe0
 
 using namespace slq;
 
-static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, const double* q0,
+static int lanczos_entry(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe_begin, const double* q0,
                          int64_t ldq, int64_t count, int steps, int reorth, int dtype, double* alpha, double* beta,
                          int32_t* steps_out, void* stream, double* basis_out = nullptr) {
   if (!g) return fail(SLQ_ERR_VALUE, "NULL graph");
@@ -414,7 +426,7 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   if (kind == SLQ_DENSITY && g->nnz == 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
   int rc = SLQ_OK;
   const int S = static_cast<int>(std::min<int64_t>(steps, g->n));   // lanczos.py:105
-  if (S > kMaxSteps) return fail(SLQ_ERR_VALUE, "steps > 128 not supported");
+  if (S > kMaxStepsLong) return fail(SLQ_ERR_VALUE, "steps > 4096 not supported");
   if (reorth < 0) reorth = S <= 100 ? 1 : 0;                          // lanczos.py:106-107
   if (count == 0) return SLQ_OK;
   if (q0 && ldq < count) return fail(SLQ_ERR_VALUE, "ldq < count");
@@ -451,7 +463,16 @@ static int lanczos_entry(const slq_graph* g, int kind, uint64_t seed, int64_t pr
 extern "C" int slq_lanczos(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count,
                            int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
                            void* stream) {
-  return lanczos_entry(g, kind, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta, steps_out,
+  return lanczos_entry(g, kind, seed_key_u64(seed), probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta,
+                       steps_out, stream);
+}
+
+extern "C" int slq_lanczos_seeded(const slq_graph* g, int kind, const slq_seed* seed, int64_t probe_begin,
+                                  int64_t count, int steps, int reorth, int dtype, double* alpha, double* beta,
+                                  int32_t* steps_out, void* stream) {
+  SeedKey k;
+  if (!seed_key_of(seed, &k)) return fail(SLQ_ERR_VALUE, "seed must have 1..8 entropy words");
+  return lanczos_entry(g, kind, k, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta, steps_out,
                        stream);
 }
 
@@ -459,7 +480,8 @@ extern "C" int slq_lanczos_start(const slq_graph* g, int kind, const double* q0,
                                  int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out,
                                  void* stream) {
   if (!q0) return fail(SLQ_ERR_VALUE, "NULL start block");
-  return lanczos_entry(g, kind, 0, 0, q0, ldq, count, steps, reorth, dtype, alpha, beta, steps_out, stream);
+  return lanczos_entry(g, kind, seed_key_u64(0), 0, q0, ldq, count, steps, reorth, dtype, alpha, beta, steps_out,
+                       stream);
 }
 
 extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x, double* y, int64_t ncols,
@@ -496,8 +518,8 @@ extern "C" int slq_operator_apply(const slq_graph* g, int kind, const double* x,
   return SLQ_OK;
 }
 
-extern "C" int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int64_t n, double* out, int64_t ld,
-                          void* stream) {
+static int probes_entry(const SeedKey& seed, int64_t probe_begin, int64_t count, int64_t n, double* out, int64_t ld,
+                        void* stream) {
   if (count < 0 || n < 0 || ld < count) return fail(SLQ_ERR_VALUE, "bad probe block shape");
   if (count == 0 || n == 0) return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -509,14 +531,38 @@ extern "C" int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int
   return SLQ_OK;
 }
 
-extern "C" int slq_probe_state(uint64_t seed, uint64_t index, uint64_t out_host[4]) {
-  if (!out_host) return fail(SLQ_ERR_VALUE, "NULL output");
+extern "C" int slq_probes(uint64_t seed, int64_t probe_begin, int64_t count, int64_t n, double* out, int64_t ld,
+                          void* stream) {
+  return probes_entry(seed_key_u64(seed), probe_begin, count, n, out, ld, stream);
+}
+
+extern "C" int slq_probes_seeded(const slq_seed* seed, int64_t probe_begin, int64_t count, int64_t n, double* out,
+                                 int64_t ld, void* stream) {
+  SeedKey k;
+  if (!seed_key_of(seed, &k)) return fail(SLQ_ERR_VALUE, "seed must have 1..8 entropy words");
+  return probes_entry(k, probe_begin, count, n, out, ld, stream);
+}
+
+static void probe_state_words(const SeedKey& k, uint64_t index, uint64_t out_host[4]) {
   u128 st, inc;
-  pcg64_seed_state(seed, index, &st, &inc);
+  pcg64_seed_state(k, index, &st, &inc);
   out_host[0] = static_cast<uint64_t>(st >> 64);
   out_host[1] = static_cast<uint64_t>(st);
   out_host[2] = static_cast<uint64_t>(inc >> 64);
   out_host[3] = static_cast<uint64_t>(inc);
+}
+
+extern "C" int slq_probe_state(uint64_t seed, uint64_t index, uint64_t out_host[4]) {
+  if (!out_host) return fail(SLQ_ERR_VALUE, "NULL output");
+  probe_state_words(seed_key_u64(seed), index, out_host);
+  return SLQ_OK;
+}
+
+extern "C" int slq_probe_state_seeded(const slq_seed* seed, uint64_t index, uint64_t out_host[4]) {
+  SeedKey k;
+  if (!out_host) return fail(SLQ_ERR_VALUE, "NULL output");
+  if (!seed_key_of(seed, &k)) return fail(SLQ_ERR_VALUE, "seed must have 1..8 entropy words");
+  probe_state_words(k, index, out_host);
   return SLQ_OK;
 }
 
@@ -533,6 +579,45 @@ extern "C" int slq_lanczos_basis(const slq_graph* g, int kind, uint64_t seed, in
                                  int steps, int reorth, int dtype, double* basis, double* alpha, double* beta,
                                  int32_t* steps_out, void* stream) {
   if (!basis) return fail(SLQ_ERR_VALUE, "NULL basis output");
-  return lanczos_entry(g, kind, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta, steps_out,
+  return lanczos_entry(g, kind, seed_key_u64(seed), probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta,
+                       steps_out, stream, basis);
+}
+
+// Diagnostics counter (slq_b200.h): probe-steps of this graph that ran the conditional second CGS
+// pass (lanczos.py:75-76), summed over every Lanczos call since the graph was created.  Synchronous.
+extern "C" int slq_graph_second_passes(const slq_graph* g, int64_t* out_host) {
+  if (!g || !out_host) return fail(SLQ_ERR_VALUE, "NULL argument");
+  int v = 0;
+  SLQ_CUDA(cudaMemcpyAsync(&v, g->dflags + 2, sizeof(int), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(g->stream)));
+  SLQ_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(g->stream)));
+  *out_host = v;
+  return SLQ_OK;
+}
+
+extern "C" int slq_lanczos_start_basis(const slq_graph* g, int kind, const double* q0, int64_t ldq, int64_t count,
+                                       int steps, int reorth, int dtype, double* basis, double* alpha, double* beta,
+                                       int32_t* steps_out, void* stream) {
+  if (!q0) return fail(SLQ_ERR_VALUE, "NULL start block");
+  if (!basis) return fail(SLQ_ERR_VALUE, "NULL basis output");
+  return lanczos_entry(g, kind, seed_key_u64(0), 0, q0, ldq, count, steps, reorth, dtype, alpha, beta, steps_out,
                        stream, basis);
+}
+
+// C++ entry for rules.cu (seed as a SeedKey)
+int lanczos_seeded_key(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe_begin, int64_t count,
+                       int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out, void* stream) {
+  return lanczos_entry(g, kind, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta, steps_out,
+                       stream);
+}
+
+// Return the memory the library's stream-ordered pool keeps cached on the current device to the
+// driver (the pool's release threshold is "never", so freed workspaces are reused across calls).
+extern "C" int slq_trim_pool(void) {
+  int dev = 0;
+  SLQ_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  SLQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  SLQ_CUDA(cudaDeviceSynchronize());
+  SLQ_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return SLQ_OK;
 }

@@ -6,6 +6,8 @@
 #pragma once
 #include <stdint.h>
 
+#include "../../include/slq_b200.h"
+
 namespace slq {
 
 typedef unsigned __int128 u128;
@@ -32,13 +34,38 @@ SLQ_HD uint32_t ss_mix(uint32_t x, uint32_t y) {
   return r ^ (r >> 16);
 }
 
-// Entropy words: seed as 1-2 little-endian uint32 words (zero-padded to the pool size of 4
-// because a spawn key is present), then the spawn key index as 1-2 words.
-SLQ_HD void pcg64_seed_state(uint64_t seed, uint64_t index, u128* state, u128* inc) {
-  uint32_t data[8];
+// The seed's run entropy: numpy's SeedSequence takes any non-negative int and splits it into
+// little-endian uint32 words (0 -> one zero word).  Up to 8 words (seeds < 2^256) are supported.
+constexpr int kSeedWords = 8;
+struct SeedKey {
+  uint32_t w[kSeedWords];
+  int nw;
+};
+
+SLQ_HD SeedKey seed_key_u64(uint64_t seed) {
+  SeedKey k{};
+  k.w[0] = static_cast<uint32_t>(seed);
+  k.nw = 1;
+  if (seed >> 32) k.w[k.nw++] = static_cast<uint32_t>(seed >> 32);
+  return k;
+}
+
+// C-ABI seed (slq_b200.h slq_seed) -> SeedKey; false for an invalid word count.
+inline bool seed_key_of(const slq_seed* s, SeedKey* out) {
+  if (!s || s->nwords < 1 || s->nwords > kSeedWords) return false;
+  SeedKey k{};
+  for (int i = 0; i < s->nwords; ++i) k.w[i] = s->words[i];
+  k.nw = s->nwords;
+  *out = k;
+  return true;
+}
+
+// Entropy words: the seed words (zero-padded to the pool size of 4 because a spawn key is present),
+// then the spawn key index as 1-2 words.
+SLQ_HD void pcg64_seed_state(const SeedKey& key, uint64_t index, u128* state, u128* inc) {
+  uint32_t data[kSeedWords + 2];
   int nd = 0;
-  data[nd++] = static_cast<uint32_t>(seed);
-  if (seed >> 32) data[nd++] = static_cast<uint32_t>(seed >> 32);
+  for (int i = 0; i < key.nw && i < kSeedWords; ++i) data[nd++] = key.w[i];
   while (nd < 4) data[nd++] = 0u;
   data[nd++] = static_cast<uint32_t>(index);
   if (index >> 32) data[nd++] = static_cast<uint32_t>(index >> 32);
@@ -71,6 +98,10 @@ SLQ_HD void pcg64_seed_state(uint64_t seed, uint64_t index, u128* state, u128* i
   st = st * mult + incv;   // step
   *state = st;
   *inc = incv;
+}
+
+SLQ_HD void pcg64_seed_state(uint64_t seed, uint64_t index, u128* state, u128* inc) {
+  pcg64_seed_state(seed_key_u64(seed), index, state, inc);
 }
 
 // Advance the LCG by `delta` steps in O(log delta) (Brown's jump-ahead).

@@ -138,6 +138,7 @@ extern "C" int slq_graph_create_rmat(int scale, int edge_factor, double a, doubl
   g->stream = stream;
   cudaGetDevice(&g->device);
   ensure_pool(g->device);
+  { size_t fr = 0; cudaMemGetInfo(&fr, &g->device_total_mem); }
   const int rc = graph_adopt(g, off, cols, st);
   if (rc != SLQ_OK) {
     slq_graph_destroy(g);
@@ -288,6 +289,7 @@ extern "C" int slq_graph_create_edges(int64_t n, int64_t m, const int64_t* u, co
   g->stream = stream;
   cudaGetDevice(&g->device);
   ensure_pool(g->device);
+  { size_t fr = 0; cudaMemGetInfo(&fr, &g->device_total_mem); }
   const int rc = graph_adopt(g, off, cols, st, w0);   // w0: max weights aligned with the unique keys
   if (rc != SLQ_OK) {
     slq_graph_destroy(g);

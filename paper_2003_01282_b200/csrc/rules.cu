@@ -10,6 +10,7 @@
 #include <cmath>
 
 #include "slq_common.cuh"
+#include "pcg64.cuh"
 #include "tridiag.cuh"
 
 namespace slq {
@@ -19,19 +20,13 @@ namespace slq {
 constexpr int kStEigen = 1, kStNanTri = 2, kStNanF = 4, kStBadCol = 8;
 
 // hi_kind >= 0: the clamp interval comes from the device graph scalars (no host round trip).
-// MAXS: capacity of the per-thread work arrays (local memory): sized to the rule length so the
-// arrays of a CTA stay L1-resident.
-template <int MAXS>
-__global__ void gauss_rules_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
-                                   const int32_t* __restrict__ steps, int64_t count, int ld, double lo,
-                                   double hi, double* __restrict__ nodes, double* __restrict__ weights,
-                                   int32_t* __restrict__ info, int* __restrict__ status, const double* dscal,
-                                   int hi_kind, const int* gflags) {
-  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (p == 0 && gflags && gflags[0]) atomicOr(status, kStBadCol);
-  if (p >= count) return;
-  if (hi_kind >= 0) hi = hi_kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (hi_kind == SLQ_DENSITY ? 1.0 : dscal[4]);
-  double d[MAXS], e[MAXS], z[MAXS];
+// One thread per probe; d, e, z are the thread's work arrays (local memory up to 128 steps, a global
+// scratch slice beyond).
+__device__ __forceinline__ void gauss_rule_one(const double* __restrict__ alpha, const double* __restrict__ beta,
+                                               const int32_t* __restrict__ steps, int64_t p, int ld, double lo,
+                                               double hi, double* __restrict__ nodes, double* __restrict__ weights,
+                                               int32_t* __restrict__ info, int* __restrict__ status, double* d,
+                                               double* e, double* z) {
   const int m = steps[p];
   const double* a = alpha + p * ld;
   const double* b = beta + p * ld;
@@ -64,6 +59,41 @@ __global__ void gauss_rules_kernel(const double* __restrict__ alpha, const doubl
     nodes[p * ld + k] = k < m ? fmin(fmax(d[k], lo), hi) : 0.0;
     weights[p * ld + k] = k < m ? z[k] : 0.0;
   }
+}
+
+__device__ __forceinline__ double clamp_hi(double hi, const double* dscal, int hi_kind) {
+  if (hi_kind < 0) return hi;
+  return hi_kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (hi_kind == SLQ_DENSITY ? 1.0 : dscal[4]);
+}
+
+// MAXS: capacity of the per-thread work arrays (local memory): sized to the rule length so the
+// arrays of a CTA stay L1-resident.
+template <int MAXS>
+__global__ void gauss_rules_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                                   const int32_t* __restrict__ steps, int64_t count, int ld, double lo,
+                                   double hi, double* __restrict__ nodes, double* __restrict__ weights,
+                                   int32_t* __restrict__ info, int* __restrict__ status, const double* dscal,
+                                   int hi_kind, const int* gflags) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p == 0 && gflags && gflags[0]) atomicOr(status, kStBadCol);
+  if (p >= count) return;
+  double d[MAXS], e[MAXS], z[MAXS];
+  gauss_rule_one(alpha, beta, steps, p, ld, lo, clamp_hi(hi, dscal, hi_kind), nodes, weights, info, status, d, e, z);
+}
+
+// Rules longer than kMaxSteps (s > 128: the reference accepts any step budget, lanczos.py:79-110):
+// the same solver on a global scratch slice [3][ld] per probe.
+__global__ void gauss_rules_long_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                                        const int32_t* __restrict__ steps, int64_t count, int ld, double lo,
+                                        double hi, double* __restrict__ nodes, double* __restrict__ weights,
+                                        int32_t* __restrict__ info, int* __restrict__ status, const double* dscal,
+                                        int hi_kind, const int* gflags, double* __restrict__ scratch) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p == 0 && gflags && gflags[0]) atomicOr(status, kStBadCol);
+  if (p >= count) return;
+  double* d = scratch + p * 3 * static_cast<int64_t>(ld);
+  gauss_rule_one(alpha, beta, steps, p, ld, lo, clamp_hi(hi, dscal, hi_kind), nodes, weights, info, status, d, d + ld,
+                 d + 2 * ld);
 }
 
 template <int FN>
@@ -196,9 +226,9 @@ integrate_kernel(const double* __restrict__ nodes, const double* __restrict__ we
   }
 }
 
-static void launch_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count, int ld,
-                               double lo, double hi, double* nodes, double* weights, int32_t* info, int* status,
-                               const double* dscal, int hi_kind, const int* gflags, cudaStream_t st) {
+static int launch_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count, int ld,
+                              double lo, double hi, double* nodes, double* weights, int32_t* info, int* status,
+                              const double* dscal, int hi_kind, const int* gflags, cudaStream_t st) {
   const int grid = ceil_div(count, 32);
   LaunchScope ls(K_EIG, st);
 #define SLQ_RULES(M) gauss_rules_kernel<M><<<grid, 32, 0, st>>>(alpha, beta, steps, count, ld, lo, hi, nodes, weights, \
@@ -206,8 +236,16 @@ static void launch_gauss_rules(const double* alpha, const double* beta, const in
   if (ld <= 16) SLQ_RULES(16);
   else if (ld <= 32) SLQ_RULES(32);
   else if (ld <= 64) SLQ_RULES(64);
-  else SLQ_RULES(kMaxSteps);
+  else if (ld <= kMaxSteps) SLQ_RULES(kMaxSteps);
+  else {
+    double* scratch = nullptr;
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * 3 * ld * count, st));
+    gauss_rules_long_kernel<<<grid, 32, 0, st>>>(alpha, beta, steps, count, ld, lo, hi, nodes, weights, info, status,
+                                                 dscal, hi_kind, gflags, scratch);
+    SLQ_CUDA(cudaFreeAsync(scratch, st));
+  }
 #undef SLQ_RULES
+  return SLQ_OK;
 }
 
 }  // namespace slq
@@ -217,13 +255,14 @@ using namespace slq;
 extern "C" int slq_gauss_rules(const double* alpha, const double* beta, const int32_t* steps, int64_t count,
                                int ld, double lo, double hi, double* nodes, double* weights, int32_t* info,
                                void* stream) {
-  if (count < 0 || ld < 1 || ld > kMaxSteps) return fail(SLQ_ERR_VALUE, "bad rule shape (ld must be in [1,128])");
+  if (count < 0 || ld < 1 || ld > kMaxStepsLong) return fail(SLQ_ERR_VALUE, "bad rule shape (ld must be in [1,4096])");
   if (count == 0) return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int* status = nullptr;
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&status), sizeof(int), st));
   SLQ_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
-  launch_gauss_rules(alpha, beta, steps, count, ld, lo, hi, nodes, weights, info, status, nullptr, -1, nullptr, st);
+  int rc = launch_gauss_rules(alpha, beta, steps, count, ld, lo, hi, nodes, weights, info, status, nullptr, -1, nullptr, st);
+  if (rc) return rc;
   int h = 0;
   SLQ_CUDA(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
   SLQ_CUDA(cudaStreamSynchronize(st));
@@ -278,9 +317,12 @@ extern "C" int slq_estimate(const double* per_vector, int64_t T, int64_t count, 
 }
 
 // ------------------------------------------------------------------ asynchronous composite entry points
-extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
-                         int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
-                         void* stream) {
+int lanczos_seeded_key(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe_begin, int64_t count,
+                       int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out, void* stream);
+
+static int rules_entry(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe_begin, int64_t count, int steps,
+                       int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
+                       void* stream) {
   if (!g || !status) return fail(SLQ_ERR_VALUE, "NULL argument");
   if (count == 0) return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -297,14 +339,30 @@ extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t pr
   }
   double* ab = nullptr;
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ab), sizeof(double) * 2 * count * S, st));
-  int rc = slq_lanczos(g, kind, seed, probe_begin, count, steps, reorth, dtype, ab, ab + count * S, steps_out, stream);
+  int rc = lanczos_seeded_key(g, kind, seed, probe_begin, count, steps, reorth, dtype, ab, ab + count * S, steps_out,
+                              stream);
   if (rc == SLQ_OK)
-    launch_gauss_rules(ab, ab + count * S, steps_out, count, S, 0.0, 0.0, nodes, weights, nullptr, status, g->dscal,
-                       kind, g->dflags, st);
+    rc = launch_gauss_rules(ab, ab + count * S, steps_out, count, S, 0.0, 0.0, nodes, weights, nullptr, status, g->dscal,
+                            kind, g->dflags, st);
   cudaFreeAsync(ab, st);
   if (rc) return rc;
   SLQ_CUDA(cudaGetLastError());
   return SLQ_OK;
+}
+
+extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
+                         int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
+                         void* stream) {
+  return rules_entry(g, kind, seed_key_u64(seed), probe_begin, count, steps, reorth, dtype, nodes, weights, steps_out,
+                     status, stream);
+}
+
+extern "C" int slq_rules_seeded(const slq_graph* g, int kind, const slq_seed* seed, int64_t probe_begin, int64_t count,
+                                int steps, int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out,
+                                int32_t* status, void* stream) {
+  SeedKey k;
+  if (!seed_key_of(seed, &k)) return fail(SLQ_ERR_VALUE, "seed must have 1..8 entropy words");
+  return rules_entry(g, kind, k, probe_begin, count, steps, reorth, dtype, nodes, weights, steps_out, status, stream);
 }
 
 extern "C" int slq_integrate(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,

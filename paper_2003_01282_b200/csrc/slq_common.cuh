@@ -11,7 +11,8 @@
 namespace slq {
 
 constexpr int kWarp = 32;
-constexpr int kMaxSteps = 128;     // largest Lanczos step count a rule can carry
+constexpr int kMaxSteps = 128;     // longest rule held in registers/local memory (longer: global scratch)
+constexpr int kMaxStepsLong = 4096;   // largest Lanczos step budget accepted (the reference has no cap)
 constexpr int kCgsBlock = 16;      // basis vectors handled per CGS sweep (register accumulators)
 constexpr int64_t kLongRow = 1024;  // rows with more nonzeros are split into segments ...
 constexpr int64_t kSeg = 1024;      // ... of this many nonzeros, one warp each
@@ -49,7 +50,8 @@ namespace slq {
 int fetch_host_scalars(slq_graph* g);
 // single small graph on the batched kernel (batched.cu); slq_rules routes n <= small_graph_max_n()
 int64_t small_graph_max_n();
-int small_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int S, int dtype,
+struct SeedKey;
+int small_rules(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe_begin, int64_t count, int S, int dtype,
                 double* nodes, double* weights, int32_t* steps_out, int32_t* status, cudaStream_t st);
 
 void launch_begin(KernelClass k, cudaStream_t s);
@@ -82,6 +84,7 @@ struct slq_graph {
   int64_t nnz = 0;
   int64_t m = 0;                 // undirected edges = nnz / 2 for simple graphs
   int device = 0;
+  size_t device_total_mem = 0;       // recorded at creation (chunk budget while a stream is captured)
   void* stream = nullptr;            // creation stream: owned buffers are freed on it
   const int64_t* offsets = nullptr;  // [n+1] device (owned copy)
   const int32_t* cols = nullptr;     // [nnz] device, narrowed to int32

@@ -3,10 +3,10 @@
 
 namespace slq {
 
-bool step_launch_f64_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st) {
+bool step_launch_f64_wide(const StepArgs& sa, int nk, int parts, int threads, size_t smem, cudaStream_t st, cudaError_t* e) {
   switch (parts) {
-    case 1: return step_launch_one<double, kStageSlots, 1>(sa, nk, threads, smem, st);
-    case 2: return step_launch_one<double, kStageSlots, 2>(sa, nk, threads, smem, st);
+    case 1: return step_launch_one<double, kStageSlots, 1>(sa, nk, threads, smem, st, e);
+    case 2: return step_launch_one<double, kStageSlots, 2>(sa, nk, threads, smem, st, e);
     default: return false;
   }
 }

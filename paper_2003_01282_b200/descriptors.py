@@ -16,7 +16,7 @@ from typing import IO
 import numpy as np
 
 from . import _lib
-from .graphs import Graph, graph_from_scipy
+from .graphs import Graph, as_graph, graph_from_scipy
 from .operators import OperatorKind, make_operator
 from .slq import SlqConfig, slq_rules
 
@@ -112,6 +112,7 @@ def netlsd_heat_wave_slq(g: Graph, grid: TimeGrid | None = None, cfg: SlqConfig 
     del threads
     import torch
 
+    g = as_graph(g)
     grid = grid or TimeGrid()
     cfg = cfg or SlqConfig()
     # the timescales go up first, while the stream is idle: a pageable upload queued behind the
@@ -146,6 +147,7 @@ def vnge_slq(g: Graph, cfg: SlqConfig | None = None, *, threads: int = 1, dtype:
              shard: bool = False, with_hash: bool = True) -> EntropyValue:
     """Von Neumann entropy -tr(P ln P) by SLQ on the GPU (descriptors.py:227-243)."""
     del threads
+    g = as_graph(g)
     cfg = cfg or SlqConfig()
     op = make_operator(g, OperatorKind.DENSITY)
     rules = slq_rules(op, cfg, dtype=dtype, shard=shard)

@@ -11,7 +11,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .graphs import Graph
+from .graphs import Graph, as_graph
 
 KIND_CODES = {"laplacian": _lib.LAPLACIAN, "normalized_laplacian": _lib.NORMALIZED_LAPLACIAN,
               "density": _lib.DENSITY}
@@ -41,6 +41,7 @@ class DeviceGraph:
     def __init__(self, g: Graph, device=None, *, from_device: bool = False,
                  fold: float | None = FOLD_MIN_FRACTION):
         torch = _lib.require_cuda()
+        g = as_graph(g)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.graph = g
         self.n = int(g.n)
@@ -94,6 +95,41 @@ class DeviceGraph:
         self._info = None
         self.n = int(self.info.n)
         self.nnz = int(self.info.nnz)
+        if fold is not None and self.n >= FOLD_MIN_N:
+            self.fold_isolated(fold)
+        return self
+
+    @classmethod
+    def from_csr32(cls, n: int, row_offsets, col_indices, weights=None, device=None,
+                   fold: float | None = FOLD_MIN_FRACTION) -> "DeviceGraph":
+        """Device graph from a compact CSR: int64 offsets [n+1] and int32 columns [nnz] (numpy arrays,
+        pinned host tensors or device tensors), optional float64 weights (None = implicit 1.0) --
+        the scale-27 workload's "int32 indices" format, uploaded without an int64 copy.  ``graph``
+        is None (no host ``Graph``; descriptors carry an empty hash)."""
+        torch = _lib.require_cuda()
+        self = cls.__new__(cls)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.graph = None
+        self.handle = ctypes.c_void_p()
+
+        def arr(x, dt):
+            if isinstance(x, torch.Tensor):
+                if x.dtype != dt:
+                    raise TypeError(f"expected {dt}, got {x.dtype}")
+                return x.contiguous()
+            return np.ascontiguousarray(x, dtype={torch.int64: np.int64, torch.int32: np.int32,
+                                                  torch.float64: np.float64}[dt])
+
+        off = arr(row_offsets, torch.int64)
+        cols = arr(col_indices, torch.int32)
+        w = None if weights is None else arr(weights, torch.float64)
+        nnz = int(cols.shape[0])
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_create_i32(int(n), nnz, _lib.ptr(off), _lib.ptr(cols), _lib.ptr(w),
+                                                        _lib.stream_handle(self.device), ctypes.byref(self.handle)))
+        self._info = None
+        self.n = int(n)
+        self.nnz = nnz
         if fold is not None and self.n >= FOLD_MIN_N:
             self.fold_isolated(fold)
         return self
@@ -171,6 +207,14 @@ class DeviceGraph:
                 pass
             self.handle = ctypes.c_void_p()
 
+    def second_passes(self) -> int:
+        """Probe-steps of this graph that ran the conditional second CGS pass (lanczos.py:75-76) since
+        it was created: a device counter (diagnostics; synchronises the graph's stream)."""
+        v = ctypes.c_int64()
+        with _lib.require_cuda().cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_second_passes(self.handle, ctypes.byref(v)))
+        return int(v.value)
+
     # -- operator set-up -----------------------------------------------------------
     def interval(self, kind: str) -> tuple[float, float]:
         lo, hi = ctypes.c_double(), ctypes.c_double()
@@ -220,8 +264,9 @@ class DeviceGraph:
         with torch.cuda.device(self.device):
             stream = _lib.stream_handle(self.device)
             if start is None:
-                rc = lib.slq_lanczos(self.handle, KIND_CODES[kind], int(seed), int(probe_begin), int(count), int(steps),
-                                     int(reorth), code, _lib.ptr(alpha), _lib.ptr(beta), _lib.ptr(st), stream)
+                rc = lib.slq_lanczos_seeded(self.handle, KIND_CODES[kind], _lib.seed_arg(seed), int(probe_begin),
+                                            int(count), int(steps), int(reorth), code, _lib.ptr(alpha), _lib.ptr(beta),
+                                            _lib.ptr(st), stream)
             else:
                 q0 = start.contiguous()
                 rc = lib.slq_lanczos_start(self.handle, KIND_CODES[kind], _lib.ptr(q0), q0.shape[1], int(count),
@@ -231,23 +276,33 @@ class DeviceGraph:
         return alpha, beta, st
 
     def lanczos_basis(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1,
-                      dtype: str = "f64"):
+                      dtype: str = "f64", start=None):
         """Debug export (``return_basis=True``, lanczos.py:85,143-144): Q [s', n, count] float64 with
-        Q[k, :, j] the k-th Lanczos vector of probe probe_begin+j, plus alpha, beta [count, s'] and
-        steps [count].  Runs on the unfolded graph."""
+        Q[k, :, j] the k-th Lanczos vector of probe probe_begin+j (or of start vector j of ``start``
+        [n, count]), plus alpha, beta [count, s'] and steps [count].  Runs on the unfolded graph."""
         import torch
 
         s = min(int(steps), self.n)
+        if start is not None:
+            count = int(start.shape[1])
         q = torch.zeros((s, self.n, count), dtype=torch.float64, device=self.device)
         alpha = torch.zeros((count, s), dtype=torch.float64, device=self.device)
         beta = torch.zeros((count, s), dtype=torch.float64, device=self.device)
         st = torch.zeros(count, dtype=torch.int32, device=self.device)
         code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
+        lib = _lib.load()
         with torch.cuda.device(self.device):
-            _lib.check(_lib.load().slq_lanczos_basis(self.handle, KIND_CODES[kind], int(seed), int(probe_begin),
-                                                     int(count), int(steps), int(reorth), code, _lib.ptr(q),
-                                                     _lib.ptr(alpha), _lib.ptr(beta), _lib.ptr(st),
-                                                     _lib.stream_handle(self.device)))
+            stream = _lib.stream_handle(self.device)
+            if start is None:
+                rc = lib.slq_lanczos_basis(self.handle, KIND_CODES[kind], int(seed), int(probe_begin), int(count),
+                                           int(steps), int(reorth), code, _lib.ptr(q), _lib.ptr(alpha),
+                                           _lib.ptr(beta), _lib.ptr(st), stream)
+            else:
+                q0 = start.contiguous()
+                rc = lib.slq_lanczos_start_basis(self.handle, KIND_CODES[kind], _lib.ptr(q0), q0.shape[1], count,
+                                                 int(steps), int(reorth), code, _lib.ptr(q), _lib.ptr(alpha),
+                                                 _lib.ptr(beta), _lib.ptr(st), stream)
+        _lib.check(rc)
         return q, alpha, beta, st
 
     def rules(self, kind: str, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1,
@@ -265,9 +320,10 @@ class DeviceGraph:
             raise ValueError("density matrix undefined for a graph without edges")
         code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
         with torch.cuda.device(self.device):
-            _lib.check(_lib.load().slq_rules(self.handle, KIND_CODES[kind], int(seed), int(probe_begin), int(count),
-                                             int(steps), int(reorth), code, _lib.ptr(nodes), _lib.ptr(weights),
-                                             _lib.ptr(st), _lib.ptr(status), _lib.stream_handle(self.device)))
+            _lib.check(_lib.load().slq_rules_seeded(self.handle, KIND_CODES[kind], _lib.seed_arg(seed), int(probe_begin),
+                                                    int(count), int(steps), int(reorth), code, _lib.ptr(nodes),
+                                                    _lib.ptr(weights), _lib.ptr(st), _lib.ptr(status),
+                                                    _lib.stream_handle(self.device)))
         return DeviceRules(nodes, weights, st, self.n, status=status)
 
 
@@ -369,6 +425,7 @@ def device_graph(g: Graph, device=None) -> DeviceGraph:
     """Cached DeviceGraph for a Graph (Graph arrays are read-only, so the cache stays valid)."""
     import torch
 
+    g = as_graph(g)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     key = str(dev)
     cache = g._device_cache
@@ -385,8 +442,8 @@ def device_probes(n: int, seed: int, probe_begin: int, count: int, device=None):
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     out = torch.empty((n, count), dtype=torch.float64, device=dev)
     with torch.cuda.device(dev):
-        _lib.check(_lib.load().slq_probes(int(seed), int(probe_begin), int(count), int(n), _lib.ptr(out), int(count),
-                                          _lib.stream_handle(dev)))
+        _lib.check(_lib.load().slq_probes_seeded(_lib.seed_arg(seed), int(probe_begin), int(count), int(n),
+                                                 _lib.ptr(out), int(count), _lib.stream_handle(dev)))
     return out
 
 

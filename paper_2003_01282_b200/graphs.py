@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["Graph", "csr_from_edges", "graph_from_scipy", "block_diagonal", "unique_sorted"]
+__all__ = ["Graph", "as_graph", "csr_from_edges", "graph_from_scipy", "block_diagonal", "unique_sorted"]
 
 
 def unique_sorted(keys: np.ndarray) -> np.ndarray:
@@ -78,6 +78,37 @@ class Graph:
             h.update(memoryview(np.ascontiguousarray(self.weights, dtype=np.float64)).cast("B"))
             self._hash.append(h.hexdigest())
         return self._hash[0]
+
+
+_FOREIGN: dict = {}   # id(foreign graph) -> (weakref, Graph view): one device copy per caller object
+
+
+def as_graph(g) -> "Graph":
+    """This package's ``Graph`` for any CSR graph object with the reference's fields.
+
+    The drop-in accepts the reference's own ``spectrace.Graph`` (``graphs.py:34-88``: n,
+    row_offsets, col_indices, weights, m) and any object carrying the same attributes.  The arrays
+    are viewed, not copied, and the view is cached per caller object (keyed by identity, dropped
+    when the caller's graph is garbage collected) so its device copy and content hash are built
+    once, as for a native ``Graph``."""
+    if isinstance(g, Graph):
+        return g
+    for attr in ("n", "row_offsets", "col_indices", "weights", "m"):
+        if not hasattr(g, attr):
+            raise TypeError(f"expected a CSR graph with n, row_offsets, col_indices, weights, m; got {type(g).__name__}")
+    import weakref
+
+    key = id(g)
+    hit = _FOREIGN.get(key)
+    if hit is not None and hit[0]() is g:
+        return hit[1]
+    view = Graph(int(g.n), np.asarray(g.row_offsets), np.asarray(g.col_indices), np.asarray(g.weights), int(g.m))
+    try:
+        ref = weakref.ref(g, lambda _r, key=key: _FOREIGN.pop(key, None))
+    except TypeError:     # not weak-referenceable: no cache
+        return view
+    _FOREIGN[key] = (ref, view)
+    return view
 
 
 def csr_from_edges(n: int, u, v, w=None) -> Graph:

@@ -50,14 +50,15 @@ def _require_graph_operator(op):
 
 
 def lanczos_tridiagonalize(op, q0, s: int, reorth: bool | None = None, *, return_basis: bool = False,
-                           dtype: str = "f64") -> Tridiagonal:
-    """Up to s Lanczos steps from the unit start vector q0 (lanczos.py:79-145)."""
+                           dtype: str = "f64"):
+    """Up to s Lanczos steps from the unit start vector q0 (lanczos.py:79-145).
+
+    Returns the Tridiagonal, plus the (steps x dim) basis of Lanczos vectors when ``return_basis``
+    is set (exported from the device recurrence)."""
     import torch
 
     if s < 1:
         raise ValueError(f"step budget must be >= 1, got {s}")
-    if return_basis:
-        raise NotImplementedError("return_basis is not exported by the device engine")
     dg = _require_graph_operator(op)
     n = op.dim
     q0 = np.asarray(q0, dtype=np.float64)
@@ -67,9 +68,15 @@ def lanczos_tridiagonalize(op, q0, s: int, reorth: bool | None = None, *, return
         raise ValueError("start vector must have unit norm")
     start = torch.as_tensor(q0.reshape(n, 1), device=dg.device)
     code = -1 if reorth is None else int(bool(reorth))
-    alpha, beta, st = dg.tridiagonals(op.kind.value, 0, 0, 1, s, reorth=code, dtype=dtype, start=start)
+    if return_basis:
+        q, alpha, beta, st = dg.lanczos_basis(op.kind.value, 0, 0, 1, s, reorth=code, dtype=dtype, start=start)
+    else:
+        alpha, beta, st = dg.tridiagonals(op.kind.value, 0, 0, 1, s, reorth=code, dtype=dtype, start=start)
     k = int(st[0])
-    return Tridiagonal(alpha=alpha[0, :k].cpu().numpy(), beta=beta[0, :k - 1].cpu().numpy(), steps=k)
+    tri = Tridiagonal(alpha=alpha[0, :k].cpu().numpy(), beta=beta[0, :k - 1].cpu().numpy(), steps=k)
+    if return_basis:
+        return tri, q[:k, :, 0].cpu().numpy()
+    return tri
 
 
 def quadrature_rule(tri: Tridiagonal) -> QuadratureRule:

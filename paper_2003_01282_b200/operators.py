@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _lib
 from .device import DeviceGraph, device_graph
-from .graphs import Graph
+from .graphs import Graph, as_graph
 
 __all__ = ["OperatorKind", "LinearOperator", "degrees", "make_operator", "trace", "trace_squared"]
 
@@ -44,6 +44,7 @@ class LinearOperator:
 
 def degrees(g: Graph, device=None) -> np.ndarray:
     """Weighted degree vector d = A.1, computed on the GPU (operators.py:58-62)."""
+    g = as_graph(g)
     if g.n == 0:
         return np.zeros(0)
     d, _ = device_graph(g, device).degrees()
@@ -55,7 +56,8 @@ def make_operator(g: Graph, kind: OperatorKind, device=None) -> LinearOperator:
 
     Raises ValueError for the density matrix of an edgeless graph, like the reference.
     """
-    kind = OperatorKind(kind)
+    kind = OperatorKind(getattr(kind, "value", kind))   # the reference's own OperatorKind members too
+    g = as_graph(g)
     dg = device_graph(g, device)
     interval = dg.interval(kind.value)    # raises ValueError for density without edges
 
@@ -67,7 +69,8 @@ def make_operator(g: Graph, kind: OperatorKind, device=None) -> LinearOperator:
 
 def trace(g: Graph, kind: OperatorKind) -> float:
     """Exact operator trace from the device-prepared degree statistics (operators.py:105-117)."""
-    kind = OperatorKind(kind)
+    kind = OperatorKind(getattr(kind, "value", kind))
+    g = as_graph(g)
     info = device_graph(g).info
     if kind is OperatorKind.LAPLACIAN:
         return float(info.trace_l)
@@ -84,7 +87,8 @@ def trace_squared(g: Graph, kind: OperatorKind) -> float:
     Fixed-order device sums (the reference uses numpy's pairwise sum): equal to rounding."""
     import ctypes
 
-    kind = OperatorKind(kind)
+    kind = OperatorKind(getattr(kind, "value", kind))
+    g = as_graph(g)
     if kind is OperatorKind.DENSITY and g.m == 0:
         raise ValueError("density matrix undefined for a graph without edges")
     out = ctypes.c_double()

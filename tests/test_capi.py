@@ -60,3 +60,28 @@ def test_host_rmat_uniform_matches_numpy_restatement(seed, sample, level):
         base = _splitmix64(np.array([np.uint64(seed) ^ np.uint64(0xD1B54A32D192ED03)], dtype=np.uint64))
         h = _splitmix64(base ^ (np.uint64(sample) * np.uint64(64) + np.uint64(level)))[0]
     assert out.value == float(h >> np.uint64(11)) / 2.0**53
+
+
+@pytest.mark.parametrize("seed,index", [(0, 3), (2**64 - 1, 0), (2**64, 5), (2**70 + 12345, 2**33 + 1),
+                                        (2**127 + 9, 1), (2**128 + 1, 2), (2**255 + 77, 4)])
+def test_seeded_probe_state_matches_numpy_for_any_seed(seed, index):
+    """slq_seed carries the seed's uint32 entropy words exactly as numpy's SeedSequence splits the
+    Python int (slq.py:70 accepts any non-negative int): the PCG64 state equals numpy's."""
+    import numpy as np
+
+    out = (ctypes.c_uint64 * 4)()
+    assert _lib.load().slq_probe_state_seeded(_lib.seed_arg(seed), index, out) == 0
+    st = np.random.PCG64(np.random.SeedSequence(entropy=seed, spawn_key=(index,))).state["state"]
+    assert (out[0] << 64) | out[1] == st["state"]
+    assert (out[2] << 64) | out[3] == st["inc"]
+    if seed < 2**64:
+        ref = (ctypes.c_uint64 * 4)()
+        assert _lib.load().slq_probe_state(seed, index, ref) == 0
+        assert list(ref) == list(out)
+
+
+def test_seed_arg_rejects_negative_and_oversized():
+    with pytest.raises(ValueError):
+        _lib.seed_arg(-1)
+    with pytest.raises(ValueError):
+        _lib.seed_arg(2**256)

@@ -47,9 +47,12 @@ def _worker(rank, world, port, n_v, width, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     b, e = probe_ranges(n_v, world)[rank]
     nodes, weights, steps = _rules_for(list(range(b, e)), width)
-    gn, gw, gs = gather_rules_arrays(torch.tensor(nodes), torch.tensor(weights), torch.tensor(steps), n_v)
-    if rank == 0:
-        out.put((gn.numpy(), gw.numpy(), gs.numpy()))
+    # rank 1 reports a device error word (bit 1: eigensolver failure); it must reach EVERY rank through
+    # the collective instead of one rank raising before it and leaving the other waiting
+    status = torch.tensor([1 if rank == 1 else 0], dtype=torch.int32)
+    gn, gw, gs, gst = gather_rules_arrays(torch.tensor(nodes), torch.tensor(weights), torch.tensor(steps), n_v,
+                                          status=status)
+    out.put((rank, gn.numpy(), gw.numpy(), gs.numpy(), int(gst.item())))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -62,10 +65,12 @@ def test_gather_rules_world2_matches_single(n_v, world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, n_v, 6, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=120)
+    res = sorted([q.get(timeout=120) for _ in range(world)])
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     ref = _rules_for(list(range(n_v)), 6)
-    for a, b in zip(got, ref):
-        assert np.array_equal(a, b)
+    for rank, *got, st in res:
+        for a, b in zip(got, ref):
+            assert np.array_equal(a, b)
+        assert st == 1, f"rank {rank} did not see rank 1's device error"

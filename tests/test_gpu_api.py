@@ -1,0 +1,342 @@
+"""Plugin-API parity on the GPU: the reference's public operator API
+(``slq_trace``, ``slq_trace_grid``, ``lanczos_tridiagonalize``) through the C ABI,
+against the oracle.  Also the rarely-taken branches of the recurrence: the
+conditional second CGS pass (``lanczos.py:70-76``, asserted to run through a
+device counter), ``reorth=False``, step budgets in (100, 128] and above 128,
+``return_basis``, seeds of any size, concurrent streams, and the reference's own
+``Graph`` / ``SlqConfig`` objects.
+
+Tolerances: fp64 descriptors within 1e-9 relative (rel-l2); per-probe nodes in
+absolute terms (<= 1e-11 * interval_hi), weights 1e-8 relative.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import golden
+from oracle import slq_oracle as O
+from paper_2003_01282_b200 import _lib
+from paper_2003_01282_b200.descriptors import TimeGrid, netlsd_slq, vnge_slq
+from paper_2003_01282_b200.device import DeviceGraph, device_probes
+from paper_2003_01282_b200.graphs import Graph, csr_from_edges
+from paper_2003_01282_b200.lanczos import lanczos_tridiagonalize, quadrature_rule
+from paper_2003_01282_b200.operators import OperatorKind, make_operator
+from paper_2003_01282_b200.slq import (SlqConfig, heat_family, slq_trace, slq_trace_grid, xlogx)
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FP64_TOL = 1e-9
+GRID = TimeGrid(1e-2, 1e2, 250)
+
+
+def complete_graph(n: int) -> Graph:
+    u, v = np.triu_indices(n, 1)
+    return csr_from_edges(n, u, v)
+
+
+def er_graph(n: int, p: float, seed: int) -> Graph:
+    rng = np.random.default_rng(seed)
+    u, v = np.triu_indices(n, 1)
+    keep = rng.random(u.size) < p
+    return csr_from_edges(n, u[keep], v[keep])
+
+
+def check_rules_vs_oracle(dr, ref, hi, node_tol=1e-11, w_tol=1e-8):
+    steps = dr.steps.cpu().numpy()
+    assert np.array_equal(steps, ref.steps)
+    nodes, weights = dr.nodes.cpu().numpy(), dr.weights.cpu().numpy()
+    w = ref.nodes.shape[1]
+    assert np.max(np.abs(nodes[:, :w] - ref.nodes)) <= node_tol * hi
+    assert np.allclose(weights[:, :w], ref.weights, rtol=w_tol, atol=1e-13)
+
+
+# ------------------------------------------------------------------ second CGS pass
+@pytest.mark.parametrize("kind", ["normalized_laplacian", "density"])
+def test_second_cgs_pass_runs_on_staged_step_kernel(cuda_device, kind):
+    # K_200: every Lanczos vector depends on a vertex only through its probe sign, so after one step
+    # the Krylov space is invariant and w' at step 1 is rounding noise INSIDE span{q0, q1}: the first
+    # CGS pass removes almost all of it and the conditional second pass (lanczos.py:75-76) must run,
+    # then the recurrence breaks down (lanczos.py:133-134).  n = 200 > 128 takes the persistent
+    # staged step kernel (not the one-CTA small-graph kernel).
+    g = complete_graph(200)
+    dg = DeviceGraph(g, cuda_device)
+    before = dg.second_passes()
+    dr = dg.rules(kind, 0, 0, 16, 6)
+    dr.check()
+    ran = dg.second_passes() - before
+    assert ran >= 8, f"second CGS pass ran for {ran} probe-steps"
+    ref = O.slq_rules(O.make_block_operator(g, kind), 16, 6, 0)
+    assert np.all(ref.steps == 2)
+    check_rules_vs_oracle(dr, ref, dg.interval(kind)[1])
+
+
+@pytest.mark.parametrize("kind", ["normalized_laplacian", "density"])
+def test_second_cgs_pass_on_start_vector_path(cuda_device, kind):
+    # caller-given start vectors (lanczos_tridiagonalize's entry) run the flat, non-staged kernels:
+    # their RED_NORM -> second pass -> RED_NORM2 branch, counted by the same device counter.  Whether
+    # a probe's first pass cancels below half is decided by rounding noise; over 32 start vectors on
+    # K_200 it happens for some (deterministically: the kernels' arithmetic is fixed)
+    g = complete_graph(200)
+    dg = DeviceGraph(g, cuda_device)
+    q0 = O.draw_probes(g.n, 7, range(32))
+    before = dg.second_passes()
+    alpha, beta, st = dg.tridiagonals(kind, 0, 0, 32, 6, start=torch.as_tensor(q0, device=cuda_device))
+    assert dg.second_passes() - before >= 1
+    ref = O.lanczos_block(O.make_block_operator(g, kind), q0, 6)
+    assert np.array_equal(st.cpu().numpy(), ref.steps)
+    assert np.allclose(alpha.cpu().numpy()[:, :2], ref.alpha[:, :2], rtol=1e-12, atol=1e-15)
+
+
+def test_second_pass_counter_stays_zero_on_well_conditioned_graph(cuda_device):
+    z = golden.load("sbm5k.npz")
+    dg = DeviceGraph(golden.graph(z), cuda_device)
+    dg.rules("normalized_laplacian", 0, 0, 8, 15).check()
+    assert dg.second_passes() == 0
+
+
+# ------------------------------------------------------------------ plugin API (slq.py)
+def test_slq_trace_grid_device_integrand_matches_oracle(cuda_device):
+    g = golden.graph(golden.load("sbm5k.npz"))
+    cfg = SlqConfig(n_v=24, s=15, seed=3)
+    op = make_operator(g, OperatorKind.NORMALIZED_LAPLACIAN)
+    est = slq_trace_grid(op, heat_family, GRID.values, cfg)
+    rules = O.slq_rules(O.make_block_operator(g, O.NORMALIZED_LAPLACIAN), 24, 15, 3)
+    pv = O.per_vector(rules, np.exp(-GRID.values[:, None, None] * rules.nodes[None]))
+    val, std = O.estimate(pv, g.n)
+    got = np.array([e.value for e in est])
+    assert golden.rel_l2(got, val) <= FP64_TOL
+    assert golden.rel_l2(np.array([e.std_error for e in est]), std) <= 1e-7
+    assert golden.rel_l2(np.stack([e.per_vector for e in est]), pv) <= FP64_TOL
+    # a host Python f takes the host integration of the same device rules (slq.py:89-95)
+    est_h = slq_trace_grid(op, lambda t: (lambda x: np.exp(-t * x)), GRID.values, cfg)
+    got_h = np.array([e.value for e in est_h])
+    assert golden.rel_l2(got_h, val) <= FP64_TOL
+    assert golden.rel_l2(got_h, got) <= 1e-13
+
+
+def test_slq_trace_density_xlogx_and_control_variate(cuda_device):
+    g = golden.graph(golden.load("rmat12.npz"))
+    cfg = SlqConfig(n_v=20, s=12, seed=1)
+    op = make_operator(g, OperatorKind.DENSITY)
+    rules = O.slq_rules(O.make_block_operator(g, O.DENSITY), 20, 12, 1)
+    pv = O.per_vector(rules, O.xlogx(rules.nodes))
+    val, std = O.estimate(pv, g.n)
+    est = slq_trace(op, xlogx, cfg)
+    assert abs(est.value - val) <= FP64_TOL * abs(val)
+    assert abs(est.std_error - std) <= 1e-7 * abs(std)
+    # control variate (slq.py:141-150): subtract c0 + c1 x + c2 x^2 at the nodes, add the exact trace
+    c = (0.1, -0.5, 2.0)
+    exact = 123.25
+    cv = slq_trace(op, xlogx, cfg, control_variate=(c, exact))
+    pv_cv = O.per_vector(rules, O.xlogx(rules.nodes) - (c[0] + c[1] * rules.nodes + c[2] * rules.nodes ** 2))
+    val_cv, std_cv = O.estimate(pv_cv, g.n)
+    assert abs(cv.value - (val_cv + exact)) <= FP64_TOL * abs(val_cv + exact)
+    assert abs(cv.std_error - std_cv) <= 1e-7 * abs(std_cv)
+
+
+def test_device_estimate_kernel_matches_host_aggregate(cuda_device):
+    # slq_quadrature + slq_estimate (rules.cu estimate_kernel), the path _finish takes for a list of
+    # Integrands of one code, against the reference's _estimate_from on the same per_vector
+    g = golden.graph(golden.load("c1_ba1000.npz"))
+    dg = DeviceGraph(g, cuda_device)
+    r = dg.rules("normalized_laplacian", 0, 0, 10, 10)
+    pv = r.quadrature(GRID.values, _lib.FN_HEAT)
+    val, std = r.estimate(pv)
+    pv_h = pv.cpu().numpy()
+    n_v = pv_h.shape[1]
+    ref_val = g.n * (pv_h.sum(axis=1) / n_v)
+    ref_std = np.std(g.n * pv_h, axis=1, ddof=1) / np.sqrt(n_v)
+    assert np.allclose(val.cpu().numpy(), ref_val, rtol=1e-14, atol=0)
+    assert np.allclose(std.cpu().numpy(), ref_std, rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------------ reorth off, long step budgets
+def test_reorth_off_matches_oracle(cuda_device):
+    g = golden.graph(golden.load("sbm5k.npz"))
+    op = O.make_block_operator(g, O.NORMALIZED_LAPLACIAN)
+    ref = O.slq_rules(op, 12, 15, 0, reorth=False)
+    dg = DeviceGraph(g, cuda_device)
+    dr = dg.rules("normalized_laplacian", 0, 0, 12, 15, reorth=0)
+    check_rules_vs_oracle(dr, ref, 2.0, node_tol=1e-10, w_tol=1e-6)
+    h, _ = O.heat_from_rules(ref, g.n, GRID.values)
+    v, _ = dr.integrate(GRID.values, [_lib.FN_HEAT])
+    assert golden.rel_l2(v[0].cpu().numpy(), h) <= FP64_TOL
+
+
+@pytest.mark.parametrize("s", [110, 128, 150])
+def test_step_budgets_above_100_default_to_reorth_off(cuda_device, s):
+    # lanczos.py:37,106-107: reorth is on only for s <= 100; s > 128 runs the long-rule eigensolver
+    g = er_graph(400, 0.03, seed=5)
+    cfg = SlqConfig(n_v=6, s=s, seed=2)
+    ref = O.slq_rules(O.make_block_operator(g, O.NORMALIZED_LAPLACIAN), 6, s, 2)   # reorth=None -> off
+    h_ref, _ = O.heat_from_rules(ref, g.n, GRID.values)
+    got = netlsd_slq(g, GRID, cfg)
+    # without reorthogonalisation the Lanczos vectors lose orthogonality after ~30 steps and the
+    # GPU's different (equally valid) rounding grows; the Gauss rules still integrate exp(-t x)
+    # to the same value (ghost Ritz values carry split weights)
+    assert golden.rel_l2(got.values, h_ref) <= 1e-6
+    dg = DeviceGraph(g, cuda_device)
+    dr = dg.rules("normalized_laplacian", 2, 0, 6, s)
+    assert np.array_equal(dr.steps.cpu().numpy(), ref.steps)
+    w = dr.weights.cpu().numpy()
+    st = dr.steps.cpu().numpy()
+    assert np.allclose([w[p, :st[p]].sum() for p in range(6)], 1.0, atol=1e-12)
+
+
+def test_reorth_on_above_100_when_forced(cuda_device):
+    g = er_graph(400, 0.03, seed=5)
+    ref = O.slq_rules(O.make_block_operator(g, O.DENSITY), 4, 120, 0, reorth=True)
+    dg = DeviceGraph(g, cuda_device)
+    dr = dg.rules("density", 0, 0, 4, 120, reorth=1)
+    check_rules_vs_oracle(dr, ref, 1.0, node_tol=1e-11, w_tol=1e-6)
+
+
+# ------------------------------------------------------------------ return_basis
+def test_return_basis_matches_reference_contract(cuda_device):
+    g = golden.graph(golden.load("rmat12.npz"))
+    op = make_operator(g, OperatorKind.NORMALIZED_LAPLACIAN)
+    q0 = O.draw_probes(g.n, 0, [5])[:, 0]
+    tri, basis = lanczos_tridiagonalize(op, q0, 12, return_basis=True)
+    assert basis.shape == (tri.steps, g.n)
+    assert np.array_equal(basis[0], q0)                         # basis[0] = q0 (lanczos.py:117-118)
+    assert np.allclose(basis @ basis.T, np.eye(tri.steps), atol=1e-12)
+    m = np.stack([op.apply(basis[k]) for k in range(tri.steps)])
+    assert np.allclose(basis @ m.T, tri.to_dense(), atol=1e-12)
+    ref = O.lanczos_block(O.make_block_operator(g, O.NORMALIZED_LAPLACIAN), q0[:, None], 12)
+    assert np.allclose(tri.alpha, ref.alpha[0], rtol=1e-11, atol=1e-14)
+    tri2 = lanczos_tridiagonalize(op, q0, 12)
+    assert np.array_equal(tri2.alpha, tri.alpha) and np.array_equal(tri2.beta, tri.beta)
+    rule = quadrature_rule(tri)
+    assert abs(rule.weights.sum() - 1.0) <= 1e-13
+
+
+# ------------------------------------------------------------------ seeds of any size
+@pytest.mark.parametrize("seed", [2 ** 64 - 1, 2 ** 64, 2 ** 70 + 12345, 2 ** 200 + 7])
+def test_big_seeds_match_numpy_stream(cuda_device, seed):
+    n = 1001
+    got = device_probes(n, seed, 3, 5, cuda_device).cpu().numpy()
+    ref = O.draw_probes(n, seed, range(3, 8)) * np.sqrt(n)
+    assert np.array_equal(got, np.round(ref))
+    g = golden.graph(golden.load("c1_ba1000.npz"))
+    h = netlsd_slq(g, GRID, SlqConfig(n_v=5, s=10, seed=seed))
+    h_ref, _ = O.heat_trace(g, GRID.values, 5, 10, seed)
+    assert golden.rel_l2(h.values, h_ref) <= FP64_TOL
+
+
+def test_negative_seed_raises_like_numpy(cuda_device):
+    g = golden.graph(golden.load("c1_ba1000.npz"))
+    with pytest.raises(ValueError):
+        np.random.SeedSequence(entropy=-1)
+    with pytest.raises(ValueError):
+        netlsd_slq(g, GRID, SlqConfig(n_v=2, s=4, seed=-1))
+
+
+# ------------------------------------------------------------------ concurrency
+def test_concurrent_signatures_on_two_streams(cuda_device):
+    # two host threads, two streams, one graph handle: the cooperative step kernel cannot deadlock
+    # and results are bitwise the serial ones.  Run in a subprocess with a hard timeout so a hang
+    # would fail the test instead of the box.
+    code = r"""
+import sys, threading
+sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+import numpy as np, torch, golden
+from paper_2003_01282_b200.device import DeviceGraph
+from paper_2003_01282_b200 import _lib
+g = golden.graph(golden.load('sbm5k.npz'))
+dg = DeviceGraph(g, 'cuda:0')
+t = np.geomspace(1e-2, 1e2, 250)
+ser = []
+for kind in ('normalized_laplacian', 'density'):
+    r = dg.rules(kind, 0, 0, 40, 15); v, _ = r.integrate(t if kind != 'density' else None,
+        [_lib.FN_HEAT] if kind != 'density' else [_lib.FN_XLOGX]); ser.append(v.cpu().numpy())
+out = [None, None]
+def work(i, kind):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            r = dg.rules(kind, 0, 0, 40, 15)
+            v, _ = r.integrate(t if kind != 'density' else None,
+                               [_lib.FN_HEAT] if kind != 'density' else [_lib.FN_XLOGX])
+        s.synchronize()
+        out[i] = v.cpu().numpy()
+th = [threading.Thread(target=work, args=(0, 'normalized_laplacian')), threading.Thread(target=work, args=(1, 'density'))]
+[x.start() for x in th]; [x.join() for x in th]
+assert np.array_equal(out[0], ser[0]) and np.array_equal(out[1], ser[1]), 'concurrent results differ'
+print('ok')
+"""
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ reference objects
+class _ForeignGraph:
+    """Duck-typed stand-in for the reference's frozen ``Graph`` dataclass (graphs.py:34-60)."""
+
+    def __init__(self, g):
+        self.n, self.m = g.n, g.m
+        self.row_offsets, self.col_indices, self.weights = g.row_offsets, g.col_indices, g.weights
+
+
+class _ForeignConfig:
+    def __init__(self, n_v, s, seed):
+        self.n_v, self.s, self.distribution, self.seed = n_v, s, "rademacher", seed
+
+
+def test_foreign_graph_and_config_objects(cuda_device):
+    g = golden.graph(golden.load("c1_ba1000.npz"))
+    fg = _ForeignGraph(g)
+    h = netlsd_slq(fg, GRID, _ForeignConfig(10, 10, 0))
+    v = vnge_slq(fg, _ForeignConfig(10, 10, 0))
+    assert np.array_equal(h.values, netlsd_slq(g, GRID, SlqConfig(10, 10, seed=0)).values)
+    assert v.value == vnge_slq(g, SlqConfig(10, 10, seed=0)).value
+    assert h.graph_hash == g.content_hash()
+
+
+def _spectrace():
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(path) and path not in sys.path:
+        sys.path.insert(0, path)
+    return pytest.importorskip("spectrace")
+
+
+def test_reference_package_routed_through_library(cuda_device):
+    """The reference's own public API with its ``_collect_rules`` seam (slq.py:80-86) routed through
+    libslq_b200.so by ``plugin.install``: same descriptors as the unpatched reference on the CPU."""
+    st = _spectrace()
+    from paper_2003_01282_b200 import plugin
+
+    z = golden.load("sbm5k.npz")
+    g = st.Graph(n=int(z["n"]), row_offsets=np.array(z["offsets"], dtype=np.int64),
+                 col_indices=np.array(z["cols"], dtype=np.int64),
+                 weights=np.array(z["weights"], dtype=np.float64), m=int(z["m"]))
+    grid = st.TimeGrid(1e-2, 1e2, 250)
+    cfg = st.SlqConfig(n_v=16, s=15, seed=0)
+    cpu_h = st.netlsd_slq(g, grid, cfg)
+    cpu_v = st.vnge_slq(g, cfg)
+    handle = plugin.install(st)
+    try:
+        gpu_h = st.netlsd_slq(g, grid, cfg)
+        gpu_v = st.vnge_slq(g, cfg)
+        op = st.make_operator(g, st.OperatorKind.NORMALIZED_LAPLACIAN)
+        wave_re = st.slq_trace_grid(op, lambda t: (lambda x: np.cos(t * x)), grid.values, cfg)
+        with pytest.raises(TypeError):
+            st.slq_trace(st.LinearOperator(dim=3, apply=lambda x: x, kind=None, interval=(0.0, 1.0)),
+                         lambda x: x, st.SlqConfig(n_v=2, s=2))
+    finally:
+        handle.uninstall()
+    assert handle.gpu_calls == 3
+    assert type(gpu_h) is type(cpu_h)
+    assert st.relative_error(gpu_h, cpu_h) <= FP64_TOL
+    assert abs(gpu_v.value - cpu_v.value) <= FP64_TOL * abs(cpu_v.value)
+    assert gpu_h.graph_hash == cpu_h.graph_hash
+    cpu_re = st.slq_trace_grid(st.make_operator(g, st.OperatorKind.NORMALIZED_LAPLACIAN),
+                               lambda t: (lambda x: np.cos(t * x)), grid.values, cfg)
+    assert golden.rel_l2([e.value for e in wave_re], [e.value for e in cpu_re]) <= FP64_TOL
+    # our entry points accept the reference's Graph/SlqConfig/TimeGrid objects directly
+    ours = netlsd_slq(g, grid, cfg)
+    assert golden.rel_l2(ours.values, cpu_h.values) <= FP64_TOL
