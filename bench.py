@@ -201,7 +201,13 @@ def cpu_operator(off, cols, n, kind):
     object.__setattr__(g, "row_offsets", off)
     object.__setattr__(g, "col_indices", cols)
     object.__setattr__(g, "weights", np.ones(cols.size))
-    return O.make_block_operator(g, kind)
+    op = O.make_block_operator(g, kind)
+    op.nnz = int(cols.size)
+    return op
+
+
+def op_nnz_of(op) -> int:
+    return int(op.nnz)
 
 
 def cpu_sample(op, nnz, probes, steps, threads):
@@ -222,12 +228,27 @@ def big_graph(cfg):
     return cfg["graph"] == "rmat" and cfg["scale"] >= 24
 
 
+def cpu_threads(nnz, n, want):
+    """Host threads for the C5 CPU sample: one probe per thread needs ~6 vectors of n doubles next to
+    the shared scipy matrix (int64 indices + float64 data); stay inside the free host memory."""
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        return want
+    matrix = nnz * 16 + n * 24
+    per_thread = 6 * n * 8
+    return int(max(1, min(want, (avail * 0.85 - matrix) // per_thread)))
+
+
 def cpu_baseline_for(cfg, op, nnz, threads):
     """Bounded CPU sample of the workload (about 10-30 s).  C5: one Lanczos step (SpMV + alpha) of one
     probe per host thread on the real graph, operator built beforehand (the per-probe-step cost does
     not depend on n_v; the full signature would take hours on the host); C2/C4: all probes,
     all steps of the heat run."""
     if big_graph(cfg):
+        threads = cpu_threads(nnz, op.dim, threads)
         probes, steps = threads, 1
         sample = (f"{probes} probes (one per host thread) x 1 Lanczos step (SpMV + alpha) of the normalized "
                   f"Laplacian on the same R-MAT-{cfg['scale']} graph, scipy operator built beforehand "
@@ -236,7 +257,7 @@ def cpu_baseline_for(cfg, op, nnz, threads):
         probes, steps = cfg["n_v"], cfg["lanczos_steps"]
         sample = f"all {probes} probes x {steps} steps of the heat run (oracle port, numpy+scipy)"
     v, dt = cpu_sample(op, nnz, probes, steps, threads)
-    return v, dt, sample
+    return v, dt, sample, threads
 
 
 def run_reference(args, cfg):
@@ -267,21 +288,23 @@ def run_reference(args, cfg):
         g = synth.sbm(cfg["n"], cfg["blocks"], cfg["p_in"], cfg["p_out"], seed=cfg["graph_seed"])
         off, cols, n = np.asarray(g.row_offsets), np.asarray(g.col_indices), g.n
     op = cpu_operator(off, cols, n, NL)
+    del off, cols
     log(f"reference arm: graph + operator ready in {time.perf_counter() - t0:.1f} s (n={n}, nnz={cols.size})")
+    nnz = op_nnz = int(op_nnz_of(op))
     vals, times, sample = [], [], ""
     for k in range(args.warmup + args.steps):
-        v, dt, sample = cpu_baseline_for(cfg, op, cols.size, threads)
+        v, dt, sample, used = cpu_baseline_for(cfg, op, nnz, threads)
         if k >= args.warmup:
             vals.append(v)
             times.append(dt)
     value = float(np.mean(vals))
-    units_step = len(operator_runs(cfg)) * cols.size * cfg["n_v"] * cfg["lanczos_steps"]
+    units_step = len(operator_runs(cfg)) * nnz * cfg["n_v"] * cfg["lanczos_steps"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * units_step / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded)",
             "config": config_dict(cfg, args.gpus), "impl": "reference",
             "ms_per_sample": 1e3 * float(np.mean(times)),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -386,6 +409,7 @@ def run_ours(args, cfg):
     check(statuses)
     times = [a.elapsed_time(b) for a, b in ev]
     times_eager = times
+    log(f"rank {rank}: timed steps {[round(t, 1) for t in times]} ms")
     # small graphs (C2): one step captured as a CUDA graph and replayed (the same kernels, one launch)
     cuda_graph = world == 1 and cfg["graph"] == "sbm" and not os.environ.get("BENCH_EAGER")
     graph_note = None
@@ -532,15 +556,20 @@ def run_ours(args, cfg):
                        "D2H of values and std errors",
                 "values_equal_device_resident_run": bool(same)},
     }
+    log(f"e2e: {e2e_s:.2f} s per signature; device {ms:.1f} ms per step; value {value:.4g}")
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
-        off_h, cols_h = pin_off.numpy().copy(), pin_cols.numpy().copy()
+        op = cpu_operator(pin_off.numpy(), pin_cols.numpy(), n, NL)   # scipy copies to int64 indices
         del pin_off, pin_cols
-        op = cpu_operator(off_h, cols_h, n, NL)
-        v, dt, sample = cpu_baseline_for(cfg, op, nnz, threads)
+        try:
+            torch._C._host_emptyCache()                                # give the pinned pages back
+        except Exception:
+            pass
+        v, dt, sample, used = cpu_baseline_for(cfg, op, nnz, threads)
+        log(f"cpu baseline: {v:.4g} units/s on {used} threads ({dt:.1f} s)")
         s1 = 1 if big_graph(cfg) else s
         v1, dt1 = cpu_sample(op, nnz, 1, s1, 1)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "port",
                                 "sample": f"{sample}; {dt:.1f} s",
                                 "value_1_thread": v1, "sample_1_thread": f"1 probe x {s1} step(s), 1 thread; {dt1:.1f} s"}
     print(json.dumps(line), flush=True)

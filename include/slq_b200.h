@@ -221,6 +221,14 @@ int slq_rules_seeded(const slq_graph* g, int kind, const slq_seed* seed, int64_t
                      int steps, int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out,
                      int32_t* status, void* stream);
 
+/* Synchronous host-buffer form of slq_rules_seeded for FFI bindings that have no device allocator
+ * (the reference's ctypes stub): the seam _collect_rules (slq.py:80-86) in one call.
+ * nodes_host/weights_host [count][s'], steps_host [count], s' = min(steps, n); the device status is
+ * mapped to the return code (SLQ_ERR_EIGEN / SLQ_ERR_VALUE).  Runs on (and synchronises) the graph's
+ * creation stream. */
+int slq_rules_host(const slq_graph* g, int kind, const slq_seed* seed, int64_t probe_begin, int64_t count,
+                   int steps, int reorth, int dtype, double* nodes_host, double* weights_host, int32_t* steps_host);
+
 /* For each integrand fns_host[f] (host array of SLQ_FN_*): quadrature over t[T] and the probe
  * aggregate: values[f][T], std_errors[f][T]; per_vector[f][T][count] if not NULL (slq.py:89-105). */
 int slq_integrate(const double* nodes, const double* weights, const int32_t* steps, int64_t count, int ld,

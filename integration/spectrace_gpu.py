@@ -1,0 +1,155 @@
+"""Reference-side binding (what a ``spectrace`` maintainer adds as ``spectrace/_gpu.py``).
+
+Plain ctypes + numpy over the C ABI of ``include/slq_b200.h`` -- no torch, no package of ours on
+the import path.  It replaces the reference's seam ``_collect_rules(op, cfg, threads)``
+(``/root/reference/pkg/src/spectrace/slq.py:80-86``) for operators built by ``make_operator``
+(``operators.py:65-102``): one ``slq_rules_host`` call returns every probe's Gauss rule, and the
+reference's own ``_apply_rule`` / ``_estimate_from`` / descriptor code runs on them unchanged.
+
+Source patch (two call sites in the reference):
+
+    # operators.py, end of make_operator:      return _gpu.register(op, g, kind)
+    # slq.py, first line of _collect_rules:    rules = _gpu.collect_rules(op, cfg)
+    #                                          if rules is not None: return rules
+
+``install(spectrace)`` applies the same two hooks at run time (used by the tests, which must not
+edit the reference).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import sys
+import weakref
+
+import numpy as np
+
+_LIB_PATH = os.environ.get("SLQ_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2003_01282_b200", "libslq_b200.so")
+_KIND = {"laplacian": 0, "normalized_laplacian": 1, "density": 2}
+_ERR_VALUE, _ERR_EIGEN = 1, 2
+
+
+class _Seed(ctypes.Structure):
+    _fields_ = [("words", ctypes.c_uint32 * 8), ("nwords", ctypes.c_int32)]
+
+
+def _load():
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    lib.slq_graph_create_host.argtypes = [i64, i64, vp, vp, vp, vp, ctypes.POINTER(vp)]
+    lib.slq_graph_fold_isolated.argtypes = [vp, ctypes.c_double, ctypes.POINTER(i64)]
+    lib.slq_graph_destroy.argtypes = [vp]
+    lib.slq_graph_destroy.restype = None
+    lib.slq_rules_host.argtypes = [vp, ctypes.c_int, ctypes.POINTER(_Seed), i64, i64, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, vp, vp, vp]
+    lib.slq_last_error.restype = ctypes.c_char_p
+    lib.slq_launch_count.restype = ctypes.c_uint64
+    return lib
+
+
+_lib = _load()
+_graphs: dict = {}   # id(op) -> (weakref(op), device graph handle, kind)
+
+
+def _check(rc: int, errors) -> None:
+    if rc == 0:
+        return
+    msg = _lib.slq_last_error().decode()
+    if rc == _ERR_VALUE:
+        raise ValueError(msg)
+    if rc == _ERR_EIGEN:
+        raise errors.TridiagonalEigenError(msg)
+    raise RuntimeError(msg)
+
+
+class _DeviceGraph:
+    """One device copy of a reference Graph (created lazily, freed with the operator)."""
+
+    def __init__(self, g, errors):
+        self.h = ctypes.c_void_p()
+        unit = bool(np.all(g.weights == 1.0))
+        off = np.ascontiguousarray(g.row_offsets, dtype=np.int64)
+        cols = np.ascontiguousarray(g.col_indices, dtype=np.int64)
+        w = None if unit else np.ascontiguousarray(g.weights, dtype=np.float64)
+        _check(_lib.slq_graph_create_host(g.n, int(off[-1]) if g.n else 0, off.ctypes.data, cols.ctypes.data,
+                                          None if w is None else w.ctypes.data, None, ctypes.byref(self.h)), errors)
+        if g.n >= 256 and np.count_nonzero(np.diff(off) == 0) * 64 >= g.n:   # isolated-vertex fold
+            m = ctypes.c_int64()
+            _check(_lib.slq_graph_fold_isolated(self.h, 1.0 / 64, ctypes.byref(m)), errors)
+
+    def __del__(self):
+        if self.h:
+            _lib.slq_graph_destroy(self.h)
+
+
+def register(op, g, kind):
+    """make_operator hook: remember the graph behind a graph operator."""
+    key = id(op)
+    _graphs[key] = (weakref.ref(op, lambda _r, key=key: _graphs.pop(key, None)), g, kind, [])
+    return op
+
+
+def collect_rules(op, cfg, errors, quadrature_rule_cls):
+    """_collect_rules replacement: the rules of probes 0..cfg.n_v-1 from the GPU, or None for an
+    operator make_operator did not build (the caller keeps its own code for those)."""
+    hit = _graphs.get(id(op))
+    if hit is None or hit[0]() is not op or cfg.distribution != "rademacher":
+        return None
+    _, g, kind, cache = hit
+    if not cache:
+        cache.append(_DeviceGraph(g, errors))
+    seed = _Seed()
+    v, k = int(cfg.seed), 0
+    if v < 0:
+        raise ValueError("expected non-negative integer")
+    while True:
+        seed.words[k] = v & 0xFFFFFFFF
+        v >>= 32
+        k += 1
+        if not v:
+            break
+    seed.nwords = k
+    s = min(cfg.s, g.n)
+    nodes = np.zeros((cfg.n_v, s))
+    weights = np.zeros((cfg.n_v, s))
+    steps = np.zeros(cfg.n_v, dtype=np.int32)
+    _check(_lib.slq_rules_host(cache[0].h, _KIND[kind.value], ctypes.byref(seed), 0, cfg.n_v, cfg.s, -1, 0,
+                               nodes.ctypes.data, weights.ctypes.data, steps.ctypes.data), errors)
+    return [quadrature_rule_cls(nodes=nodes[p, :steps[p]].copy(), weights=weights[p, :steps[p]].copy())
+            for p in range(cfg.n_v)]
+
+
+def install(spectrace):
+    """Apply the two hooks of the source patch to an imported spectrace package (run-time form)."""
+    ops = sys.modules[spectrace.__name__ + ".operators"]
+    slq = sys.modules[spectrace.__name__ + ".slq"]
+    lan = sys.modules[spectrace.__name__ + ".lanczos"]
+    errors = sys.modules[spectrace.__name__ + ".errors"]
+    orig_make, orig_collect = ops.make_operator, slq._collect_rules
+
+    def make_operator(g, kind):
+        return register(orig_make(g, kind), g, kind)
+
+    def _collect_rules(op, cfg, threads):
+        rules = collect_rules(op, cfg, errors, lan.QuadratureRule)
+        return rules if rules is not None else orig_collect(op, cfg, threads)
+
+    patched = []
+    for name, mod in list(sys.modules.items()):
+        if mod is not None and (name == spectrace.__name__ or name.startswith(spectrace.__name__ + ".")) \
+                and getattr(mod, "make_operator", None) is orig_make:
+            patched.append((mod, "make_operator", orig_make))
+            mod.make_operator = make_operator
+    patched.append((slq, "_collect_rules", orig_collect))
+    slq._collect_rules = _collect_rules
+
+    def uninstall():
+        for mod, name, orig in reversed(patched):
+            setattr(mod, name, orig)
+
+    return uninstall
+
+
+def launch_count() -> int:
+    return int(_lib.slq_launch_count())

@@ -17,7 +17,7 @@ _LAZY = {
     "degrees": "operators", "trace": "operators", "trace_squared": "operators",
     # lanczos.py mirror
     "Tridiagonal": "lanczos", "QuadratureRule": "lanczos", "quadrature_rule": "lanczos",
-    "lanczos_tridiagonalize": "lanczos",
+    "lanczos_tridiagonalize": "lanczos", "extremal_eigenvalues": "lanczos", "dense_spectrum": "lanczos",
     # slq.py mirror
     "SlqConfig": "slq", "SlqEstimate": "slq", "slq_trace": "slq", "slq_trace_grid": "slq",
     "slq_rules": "slq",
@@ -26,6 +26,8 @@ _LAZY = {
     "WaveTraceDescriptor": "descriptors", "netlsd_slq": "descriptors", "vnge_slq": "descriptors",
     "netlsd_wave_slq": "descriptors", "netlsd_heat_wave_slq": "descriptors",
     "netlsd_slq_sparse": "descriptors", "vnge_slq_sparse": "descriptors",
+    "netlsd_taylor": "descriptors", "netlsd_linear": "descriptors", "netlsd_exact": "descriptors",
+    "vnge_taylor": "descriptors", "vnge_finger": "descriptors", "vnge_exact": "descriptors",
     "relative_error": "descriptors", "descriptor_distance": "descriptors",
     "descriptor_to_json": "descriptors", "descriptor_from_json": "descriptors",
     # batched small graphs

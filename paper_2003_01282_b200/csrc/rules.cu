@@ -407,3 +407,43 @@ extern "C" int slq_signature(const slq_graph* g, int kind, uint64_t seed, int64_
   cudaFreeAsync(buf, st);
   return rc;
 }
+
+// Synchronous host-buffer variant of slq_rules_seeded for FFI bindings without a device allocator
+// (the reference's ctypes stub): probes [probe_begin, +count) of `seed`, rules
+// copied to host arrays nodes_host/weights_host [count][s'] and steps_host [count],
+// s' = min(steps, n).  The device status word is mapped to the return code (SLQ_ERR_EIGEN,
+// SLQ_ERR_VALUE for non-finite tridiagonals or out-of-range columns).  Runs on the graph's stream.
+extern "C" int slq_rules_host(const slq_graph* g, int kind, const slq_seed* seed, int64_t probe_begin, int64_t count,
+                              int steps, int reorth, int dtype, double* nodes_host, double* weights_host,
+                              int32_t* steps_host) {
+  if (!g || !nodes_host || !weights_host || !steps_host) return fail(SLQ_ERR_VALUE, "NULL argument");
+  if (steps < 1) return fail(SLQ_ERR_VALUE, "step budget must be >= 1");
+  if (count <= 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(g->stream);
+  const int64_t S = std::min<int64_t>(steps, std::max<int64_t>(g->n, 1));
+  char* buf = nullptr;
+  const size_t bn = sizeof(double) * count * S;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * bn + sizeof(int32_t) * (count + 1) + 16, st));
+  double* nodes = reinterpret_cast<double*>(buf);
+  double* weights = nodes + count * S;
+  int32_t* stp = reinterpret_cast<int32_t*>(buf + 2 * bn);
+  int32_t* status = stp + count;
+  int rc = cudaMemsetAsync(status, 0, sizeof(int32_t), st) == cudaSuccess ? SLQ_OK : SLQ_ERR_CUDA;
+  if (rc == SLQ_OK)
+    rc = slq_rules_seeded(g, kind, seed, probe_begin, count, steps, reorth, dtype, nodes, weights, stp, status, st);
+  int32_t hstatus = 0;
+  if (rc == SLQ_OK) {
+    if (cudaMemcpyAsync(nodes_host, nodes, bn, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(weights_host, weights, bn, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(steps_host, stp, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(&hstatus, status, sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = cuda_fail(cudaGetLastError(), "rules D2H");
+  }
+  cudaFreeAsync(buf, st);
+  if (rc) return rc;
+  SLQ_CUDA(cudaStreamSynchronize(st));
+  if (hstatus & kStBadCol) return fail(SLQ_ERR_VALUE, "column index out of range [0, n)");
+  if (hstatus & kStNanTri) return fail(SLQ_ERR_VALUE, "array must not contain infs or NaNs");
+  if (hstatus & kStEigen) return fail(SLQ_ERR_EIGEN, "tridiagonal eigensolver failed: no convergence");
+  return SLQ_OK;
+}

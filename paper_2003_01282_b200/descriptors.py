@@ -21,6 +21,7 @@ from .operators import OperatorKind, make_operator
 from .slq import SlqConfig, slq_rules
 
 __all__ = ["TimeGrid", "HeatTraceDescriptor", "WaveTraceDescriptor", "EntropyValue", "netlsd_slq",
+           "netlsd_taylor", "netlsd_linear", "netlsd_exact", "vnge_taylor", "vnge_finger", "vnge_exact",
            "netlsd_wave_slq", "netlsd_heat_wave_slq", "vnge_slq", "netlsd_slq_sparse", "vnge_slq_sparse",
            "descriptor_distance", "relative_error", "descriptor_to_json", "descriptor_from_json"]
 
@@ -154,6 +155,128 @@ def vnge_slq(g: Graph, cfg: SlqConfig | None = None, *, threads: int = 1, dtype:
     val, std, gh = _integrate_host(rules, None, [_lib.FN_XLOGX], lambda: _hash(g, with_hash))
     return EntropyValue(value=-float(val[0, 0]), method="slq", params=_params(cfg), graph_hash=gh,
                         std_error=float(std[0, 0]))
+
+
+# ------------------------------------------------------------------ trace-identity and spectral baselines
+def _heat_trace(eigenvalues: np.ndarray, grid: TimeGrid) -> np.ndarray:
+    lam = np.maximum(eigenvalues, 0.0)
+    return np.exp(-np.outer(grid.values, lam)).sum(axis=1)
+
+
+def netlsd_taylor(g, grid: TimeGrid | None = None) -> HeatTraceDescriptor:
+    """Second-order heat-trace expansion n - t tr + (t^2/2) tr^2 from the device trace identities
+    (descriptors.py:152-165; tr and tr^2 of the normalized Laplacian in one edge pass)."""
+    from .operators import trace, trace_squared
+
+    g = as_graph(g)
+    grid = grid or TimeGrid()
+    tr1 = trace(g, OperatorKind.NORMALIZED_LAPLACIAN)
+    tr2 = trace_squared(g, OperatorKind.NORMALIZED_LAPLACIAN)
+    t = grid.values
+    return HeatTraceDescriptor(grid=grid, values=g.n - t * tr1 + 0.5 * t * t * tr2, method="taylor", params={},
+                               graph_hash=g.content_hash())
+
+
+def netlsd_exact(g, grid: TimeGrid | None = None, *, cap: int | None = None) -> HeatTraceDescriptor:
+    """Heat trace from the full normalized-Laplacian spectrum (descriptors.py:108-121)."""
+    from .lanczos import DENSE_SPECTRUM_CAP, dense_spectrum
+
+    g = as_graph(g)
+    grid = grid or TimeGrid()
+    eigs = dense_spectrum(g, OperatorKind.NORMALIZED_LAPLACIAN, cap=cap or DENSE_SPECTRUM_CAP)
+    return HeatTraceDescriptor(grid=grid, values=_heat_trace(eigs, grid), method="exact", params={},
+                               graph_hash=g.content_hash())
+
+
+def netlsd_linear(g, grid: TimeGrid | None = None, k: int = 300, *, cap: int | None = None) -> HeatTraceDescriptor:
+    """Heat trace from k exact eigenvalues at each end (device Lanczos, ``extremal_eigenvalues``) with a
+    linearly interpolated interior; the dense route when 2k >= n (descriptors.py:168-199)."""
+    from .lanczos import extremal_eigenvalues
+
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    g = as_graph(g)
+    grid = grid or TimeGrid()
+    if 2 * k >= g.n:
+        exact = netlsd_exact(g, grid, cap=cap)
+        return HeatTraceDescriptor(grid=grid, values=exact.values, method="linear",
+                                   params={"k": k, "fallback": "exact"}, graph_hash=g.content_hash())
+    op = make_operator(g, OperatorKind.NORMALIZED_LAPLACIAN)
+    low = extremal_eigenvalues(op, k, "smallest")
+    high = extremal_eigenvalues(op, k, "largest")
+    interior_count = g.n - 2 * k
+    step = (high[0] - low[-1]) / (interior_count + 1)
+    interior = low[-1] + step * np.arange(1, interior_count + 1)
+    eigs = np.concatenate([low, interior, high])
+    return HeatTraceDescriptor(grid=grid, values=_heat_trace(eigs, grid), method="linear", params={"k": k},
+                               graph_hash=g.content_hash())
+
+
+def _entropy_from_spectrum(eigs: np.ndarray) -> float:
+    lam = np.clip(eigs, 0.0, 1.0)
+    pos = lam > 0
+    return float(-np.sum(lam[pos] * np.log(lam[pos])))
+
+
+def vnge_exact(g, *, cap: int | None = None) -> EntropyValue:
+    """Entropy from the full density-matrix spectrum (descriptors.py:208-216)."""
+    from .lanczos import DENSE_SPECTRUM_CAP, dense_spectrum
+
+    g = as_graph(g)
+    eigs = dense_spectrum(g, OperatorKind.DENSITY, cap=cap or DENSE_SPECTRUM_CAP)
+    return EntropyValue(value=_entropy_from_spectrum(eigs), method="exact", params={}, graph_hash=g.content_hash())
+
+
+def _taylor_quadratic(g) -> float:
+    from .operators import trace, trace_squared
+
+    tr_l = trace(g, OperatorKind.LAPLACIAN)
+    tr_l2 = trace_squared(g, OperatorKind.LAPLACIAN)
+    return 1.0 - tr_l2 / (tr_l * tr_l)
+
+
+def vnge_taylor(g, variant: str = "corrected") -> EntropyValue:
+    """Quadratic entropy expansion from the device trace identities (descriptors.py:252-275):
+    ``corrected`` Q = 1 - tr(L^2)/tr(L)^2; ``printed`` 1 - (tr(L) + 2 tr(L^2))/tr(L)^2 verbatim."""
+    from .operators import trace, trace_squared
+
+    if variant not in ("corrected", "printed"):
+        raise ValueError(f"variant must be 'corrected' or 'printed', got {variant!r}")
+    g = as_graph(g)
+    if g.m == 0:
+        raise ValueError("entropy undefined for a graph without edges")
+    if variant == "corrected":
+        value = _taylor_quadratic(g)
+    else:
+        tr_l = trace(g, OperatorKind.LAPLACIAN)
+        tr_l2 = trace_squared(g, OperatorKind.LAPLACIAN)
+        value = 1.0 - (tr_l + 2.0 * tr_l2) / (tr_l * tr_l)
+    return EntropyValue(value=value, method="taylor", params={"variant": variant}, graph_hash=g.content_hash())
+
+
+def vnge_finger(g, variant: str = "hat") -> EntropyValue:
+    """-Q ln(scale) (descriptors.py:278-305): ``hat`` takes the largest density eigenvalue from the
+    device Lanczos run of ``extremal_eigenvalues``; ``bar`` the bound 2 max_deg / tr(L)."""
+    from .lanczos import extremal_eigenvalues
+    from .operators import trace
+
+    if variant not in ("hat", "bar"):
+        raise ValueError(f"variant must be 'hat' or 'bar', got {variant!r}")
+    g = as_graph(g)
+    if g.m == 0:
+        raise ValueError("entropy undefined for a graph without edges")
+    q = _taylor_quadratic(g)
+    if variant == "hat":
+        op = make_operator(g, OperatorKind.DENSITY)
+        scale = float(extremal_eigenvalues(op, 1, "largest")[-1])
+    else:
+        from .device import device_graph
+
+        scale = 2.0 * float(device_graph(g).info.max_degree) / trace(g, OperatorKind.LAPLACIAN)
+    if scale <= 0:
+        raise ValueError(f"nonpositive spectral scale {scale} for log")
+    return EntropyValue(value=-q * np.log(scale), method="finger", params={"variant": variant},
+                        graph_hash=g.content_hash())
 
 
 def _grid_from_timescales(timescales) -> TimeGrid:

@@ -340,3 +340,30 @@ def test_reference_package_routed_through_library(cuda_device):
     # our entry points accept the reference's Graph/SlqConfig/TimeGrid objects directly
     ours = netlsd_slq(g, grid, cfg)
     assert golden.rel_l2(ours.values, cpu_h.values) <= FP64_TOL
+
+
+def test_ctypes_stub_routes_reference_seam(cuda_device):
+    """INTEGRATION.md §1's torch-free ctypes binding (integration/spectrace_gpu.py) installed into the
+    reference package: spectrace.netlsd_slq / vnge_slq run their _collect_rules seam on the GPU through
+    slq_rules_host and match the unpatched reference."""
+    st = _spectrace()
+    sys.path.insert(0, os.path.join(ROOT, "integration"))
+    import spectrace_gpu
+
+    z = golden.load("rmat12.npz")
+    g = st.Graph(n=int(z["n"]), row_offsets=np.array(z["offsets"], dtype=np.int64),
+                 col_indices=np.array(z["cols"], dtype=np.int64),
+                 weights=np.array(z["weights"], dtype=np.float64), m=int(z["m"]))
+    grid = st.TimeGrid(1e-2, 1e2, 250)
+    cfg = st.SlqConfig(n_v=12, s=15, seed=2 ** 70 + 1)
+    cpu_h, cpu_v = st.netlsd_slq(g, grid, cfg), st.vnge_slq(g, cfg)
+    uninstall = spectrace_gpu.install(st)
+    try:
+        before = spectrace_gpu.launch_count()
+        gpu_h, gpu_v = st.netlsd_slq(g, grid, cfg), st.vnge_slq(g, cfg)
+        launched = spectrace_gpu.launch_count() - before
+    finally:
+        uninstall()
+    assert launched > 0
+    assert st.relative_error(gpu_h, cpu_h) <= FP64_TOL
+    assert abs(gpu_v.value - cpu_v.value) <= FP64_TOL * abs(cpu_v.value)
