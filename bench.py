@@ -54,6 +54,12 @@ CONFIGS = {
            "n_v": 100, "lanczos_steps": 15, "T": T_GRID, "dtype": "f64", "ops": ["heat", "vnge"],
            "reorth": "full CGS (reference default)", "graph_source": "device R-MAT generator",
            "l2": "flushed between timed steps (256 MiB write), outside the timed events"},
+    "c3": {"workload": "C3 10,000 Erdos-Renyi graphs (n ~ U[20,200], p ~ U[0.05,0.3]) stacked block-diagonally, "
+                       "20 probes x 10 steps, fp32, per-graph heat trace, T=250 t in [1e-2,1e2]",
+           "graph": "er_batch", "graphs": 10_000, "graph_seed": 0, "n_v": 20, "lanczos_steps": 10, "T": T_GRID,
+           "dtype": "f32", "ops": ["heat"], "reorth": "full CGS (reference default)",
+           "graph_source": "host ER generator (synth.er_batch)",
+           "l2": "flushed between timed steps (256 MiB write), outside the timed events"},
     "c2": {"workload": "C2 SBM n=100000 blocks=10 p_in=1e-3 p_out=1e-5, 100 probes x 15 steps, fp64, "
                        "heat+wave (normalized Laplacian), T=250 t in [1e-2,1e2]",
            "graph": "sbm", "n": 100_000, "blocks": 10, "p_in": 1e-3, "p_out": 1e-5, "graph_seed": 0,
@@ -266,6 +272,27 @@ def run_reference(args, cfg):
         return 0
     import numpy as np
 
+    if cfg["graph"] == "er_batch":
+        graphs = er_graphs(cfg)
+        vals, times = [], []
+        count = 300
+        for k in range(args.warmup + args.steps):
+            v, dt = cpu_batch_sample(graphs, cfg, count)
+            if k >= args.warmup:
+                vals.append(v)
+                times.append(dt)
+        value = float(np.mean(vals))
+        units_step = sum(g.nnz * cfg["n_v"] * min(cfg["lanczos_steps"], g.n) for g in graphs)
+        sample = f"first {count} of {len(graphs)} graphs, per-graph oracle heat trace (numpy+scipy port, one thread)"
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * units_step / value, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded)",
+                "config": config_dict(cfg, args.gpus), "impl": "reference",
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
     if cfg["graph"] == "rmat":
@@ -302,7 +329,7 @@ def run_reference(args, cfg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * units_step / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (seeded)",
-            "config": config_dict(cfg, args.gpus), "impl": "reference",
+            "config": config_dict(cfg, args.gpus), "impl": "reference", "graph": {"n": int(n), "nnz": int(nnz)},
             "ms_per_sample": 1e3 * float(np.mean(times)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -328,6 +355,166 @@ def step_bytes_per_launch(n_rows, c, vb, s):
     row = c * vb
     tot = sum(n_rows * row * (2 * (i + 1) + 1) + 2 * n_rows * 16 for i in range(s - 1))
     return tot / (s - 1)
+
+
+# ----------------------------------------------------------------------------------- C3 (many small graphs)
+def er_graphs(cfg):
+    from paper_2003_01282_b200 import synth
+
+    return synth.er_batch(cfg["graphs"], seed=cfg["graph_seed"])
+
+
+def cpu_batch_sample(graphs, cfg, count):
+    """Oracle port on the first `count` graphs (per-graph netlsd heat, the reference's per-graph call)."""
+    from oracle import slq_oracle as O
+
+    t = O.time_grid(1e-2, 1e2, T_GRID)
+    units = 0
+    t0 = time.perf_counter()
+    for g in graphs[:count]:
+        O.heat_trace(g, t, cfg["n_v"], cfg["lanczos_steps"], 0, threads=1)
+        units += g.nnz * cfg["n_v"] * min(cfg["lanczos_steps"], g.n)
+    dt = time.perf_counter() - t0
+    return units / dt, dt
+
+
+def run_ours_batch(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_01282_b200 import _lib
+    from paper_2003_01282_b200.batched import netlsd_slq_batch
+    from paper_2003_01282_b200.dist import ShardedBatch, probe_ranges
+    from paper_2003_01282_b200.slq import SlqConfig
+
+    world, rank, local = dist_env()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    dtype = args.dtype or cfg["dtype"]
+    scfg = SlqConfig(n_v=cfg["n_v"], s=cfg["lanczos_steps"], seed=0)
+    t0 = time.perf_counter()
+    graphs = er_graphs(cfg)
+    sb = ShardedBatch(graphs, device=dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    tvals = np.geomspace(1e-2, 1e2, T_GRID)
+    tvals[0], tvals[-1] = 1e-2, 1e2
+    units_step = sum(g.nnz * cfg["n_v"] * min(cfg["lanczos_steps"], g.n) for g in graphs)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return sb.values("normalized_laplacian", scfg, tvals, _lib.FN_HEAT, dtype)
+
+    spin_up(torch, dev)
+    for _ in range(args.warmup):
+        _, _, status = step()
+    _lib.check_status(int(status.item()))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local) if (rank == 0 and not os.environ.get("BENCH_NO_CLOCKS")) else None
+    if sampler:
+        sampler.start()
+    launches0 = _lib.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(1)
+        ev[k][0].record(stream)
+        vals, stds, status = step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    launches = (_lib.launch_count() - launches0) // args.steps
+    _lib.check_status(int(status.item()))
+    clocks = sampler.stop() if sampler else None
+    times = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = units_step / (ms * 1e-3)
+    _lib.profile_begin()
+    step()
+    torch.cuda.synchronize()
+    prof = _lib.profile_end()
+    # e2e: the public API on host graphs (block-diagonal stacking, H2D, device run, D2H) for this rank's range
+    b, e = probe_ranges(len(graphs), world)[rank]
+    mine = graphs[b:e]
+    h2d = sum((g.n + 1) * 8 + g.nnz * 8 for g in mine)
+    e2e_times = []
+    for k in range(args.e2e_reps + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        hv, hs = netlsd_slq_batch(mine, TimeGridLike(tvals), scfg, dtype=dtype)
+        dt = time.perf_counter() - t1
+        if k >= 1:
+            e2e_times.append(dt)
+    e2e_s = float(np.mean(e2e_times))
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    peak, peak_src = measured_peaks()
+    nnz_total = sum(g.nnz for g in graphs)
+    n_total = sum(g.n for g in graphs)
+    bat = prof.get("batched", {"ms": 0.0, "launches": 0})
+    # algorithmic bytes of the batched Lanczos kernel: each step streams the graph's CSR (int32 columns +
+    # int64 offsets) and the c-wide vectors it reads/writes (rows of c * vb, 3 vectors); vectors of one
+    # graph are L2/SMEM-resident, so this is a streaming lower bound, not an HBM target (SURVEY §8d)
+    vb = 4 if dtype == "f32" else 8
+    s_ = cfg["lanczos_steps"]
+    local_nnz = sum(g.nnz for g in mine)
+    local_n = sum(g.n for g in mine)
+    alg = s_ * (local_nnz * 4 + local_n * 8 + 3 * local_n * cfg["n_v"] * vb)
+    bat_ms = bat["ms"] / max(1, bat["launches"])
+    roof = {"bound": "hbm", "kernel": "batched_lanczos", "achieved": alg / (bat_ms * 1e-3) / 1e9 if bat_ms else None,
+            "peak": peak, "unit": "GB/s", "frac": (alg / (bat_ms * 1e-3) / 1e9 / peak) if bat_ms else None,
+            "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+            "ms_per_launch": bat_ms, "note": "latency/SMEM-bound per-graph CTAs (SURVEY §8d: no HBM fraction target)"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dtype, "data": f"synthetic (seeded; {cfg['graph_source']})",
+            "config": config_dict(cfg, world),
+            "graph": {"graphs": len(graphs), "n": n_total, "nnz": nnz_total, "graphs_per_rank": e - b},
+            "roofline": roof,
+            "kernels": {k: v for k, v in prof.items() if v["launches"]},
+            "ms_steps": [round(t, 3) for t in times], "gpu_launches": launches, "graph_build_s": round(gen_s, 3),
+            "clocks": clocks,
+            "e2e": {"value": units_step / e2e_s, "unit": UNIT, "seconds_per_signature": e2e_s,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 2 * (e - b) * T_GRID * 8 + 4,
+                    "api": "netlsd_slq_batch(list of host Graphs): block-diagonal stacking, H2D, device run, D2H"}}
+    if not args.no_cpu_baseline and world == 1:
+        count = 300
+        v, dt = cpu_batch_sample(graphs, cfg, count)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"first {count} of {len(graphs)} graphs, per-graph oracle heat trace "
+                                          f"(numpy+scipy port, one thread; graphs are independent); {dt:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+class TimeGridLike:
+    """A TimeGrid carrying exactly the bench's t values (geomspace with pinned endpoints)."""
+
+    def __init__(self, values):
+        self.values = values
+        self.t_min, self.t_max, self.count = float(values[0]), float(values[-1]), len(values)
 
 
 # ----------------------------------------------------------------------------------- our arm
@@ -535,8 +722,8 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": dtype, "data": f"synthetic (seeded; {cfg['graph_source']})",
-        "config": dict(config_dict(cfg, world), total_probes=n_v, nnz=nnz, n=n,
-                       folded_isolated=folded, probes_per_rank=per_rank),
+        "config": config_dict(cfg, world),
+        "graph": {"n": n, "nnz": nnz, "folded_isolated": folded, "vector_rows": n_rows, "probes_per_rank": per_rank},
         "roofline": roof,
         "kernels": per_class,
         "ms_per_step_profiled": ms_profiled,
@@ -595,6 +782,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg["graph"] == "er_batch":
+        return run_ours_batch(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -348,7 +348,8 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
     int64_t myoff = 0;
     double mys = 1.0, myw = 1.0;
     if (lane < cnt) {
-      const int64_t col = __ldg(cols + base + lane);
+      const int32_t raw = __ldg(cols + base + lane);
+      const int64_t col = raw;
       myoff = BITS ? col * kBitWords : col * ldi;
       if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + col);
       if (WEIGHTED) myw = __ldg(wts + base + lane);
@@ -536,6 +537,71 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
   }
 }
 
+#ifndef SLQ_HALF2_PIPE
+#define SLQ_HALF2_PIPE 0    // pipelined HALF2 gather: pairs in flight per half-warp (0: off; measured slower)
+#endif
+// HALF2 (fp32 chunks of 17..32 probes, 128-byte rows), software-pipelined: the column indices of the
+// next 32 nonzeros are loaded before this batch's gathers are issued, and every pair of a batch is
+// issued in one predicated round of U loads (no serial tail loop), so a row costs about one gather
+// latency per 32 nonzeros instead of ~3.  Each half-warp still sums the positions of one parity of
+// the row in ascending order, and the halves are combined at the end: bitwise the two-chain order
+// of the narrow class (gather_range).
+template <typename VT, int KIND, bool WEIGHTED, int U>
+__device__ __forceinline__ void gather_half2_pipe(const int32_t* __restrict__ cols, const double* __restrict__ dinv,
+                                                  const double* __restrict__ wts, const VT* __restrict__ u,
+                                                  int64_t ldi, int pidx0, int64_t beg, int64_t end, double* acc) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr bool SK = KIND == SLQ_NORMALIZED_LAPLACIAN || WEIGHTED;
+  using V2 = typename std::conditional<std::is_same<VT, double>::value, double2, float2>::type;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 4;
+  double a0 = 0.0, a1 = 0.0;
+  // 32-bit column indices travel through the shuffles (one shuffle per gather); offsets are formed
+  // by the consumer lane
+  auto load = [&](int64_t b, int32_t& col, double& sc) {
+    col = 0;
+    sc = 1.0;
+    if (b + lane < end) {
+      col = __ldg(cols + b + lane);
+      if (KIND == SLQ_NORMALIZED_LAPLACIAN) sc = __ldg(dinv + col);
+      if (WEIGHTED) sc *= __ldg(wts + b + lane);
+    }
+  };
+  const VT* __restrict__ up = u + pidx0;
+  int32_t mycol;
+  double mys;
+  load(beg, mycol, mys);
+  for (int64_t base = beg; base < end; base += 32) {
+    const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
+    int32_t ncol = 0;
+    double ns = 1.0;
+    if (base + 32 < end) load(base + 32, ncol, ns);   // prefetch: independent of this batch's gathers
+    const int npairs = (cnt + 1) >> 1;
+    for (int m = 0; m < npairs; m += U) {
+      V2 xv[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int c = __shfl_sync(FULL, mycol, (2 * (m + q) + sub) & 31);
+        if (m + q < npairs) xv[q] = __ldg(reinterpret_cast<const V2*>(up + static_cast<int64_t>(c) * ldi));
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int kk = 2 * (m + q) + sub;
+        const double sk = SK ? __shfl_sync(FULL, mys, kk & 31) : 1.0;
+        if (m + q < npairs && kk < cnt) {
+          const double x0 = static_cast<double>(xv[q].x), x1 = static_cast<double>(xv[q].y);
+          a0 = SK ? fma(sk, x0, a0) : a0 + x0;
+          a1 = SK ? fma(sk, x1, a1) : a1 + x1;
+        }
+      }
+    }
+    mycol = ncol;
+    mys = ns;
+  }
+  acc[0] = a0 + __shfl_xor_sync(FULL, a0, 16);   // s_even + s_odd in both halves
+  acc[1] = a1 + __shfl_xor_sync(FULL, a1, 16);
+}
+
 // own-row value u[row][probe j of this lane] (from the bitmask on the first step).  u points at the
 // lane's first probe; probe j of the lane is PS j further, and `probe` is its index within the
 // 128-probe block (the bitmask word probe / 32, bit probe % 32).
@@ -557,11 +623,15 @@ __device__ __forceinline__ double own_value(const VT* u, int64_t ldi, const uint
 #ifndef SLQ_SPMM_MINB4
 #define SLQ_SPMM_MINB4 3   // resident CTAs per SM for PPL = 4 (80 registers: no spills in the 4-probe lanes)
 #endif
+#ifndef SLQ_SPMM_MINB_H2
+#define SLQ_SPMM_MINB_H2 4   // resident CTAs per SM for the pipelined HALF2 mapping
+#endif
 #ifndef SLQ_SPMM_MINB1
 #define SLQ_SPMM_MINB1 4   // resident CTAs per SM for PPL = 1 and 2
 #endif
 template <typename VT, int KIND, bool WEIGHTED, int PPL, bool BITS, bool EXACT, bool HALF, bool V2 = false>
-__global__ void __launch_bounds__(kSpmmWarps * 32, PPL == 4 ? SLQ_SPMM_MINB4 : SLQ_SPMM_MINB1)
+__global__ void __launch_bounds__(kSpmmWarps * 32,
+                                  PPL == 4 ? SLQ_SPMM_MINB4 : ((HALF && PPL == 2 && !BITS) ? SLQ_SPMM_MINB_H2 : SLQ_SPMM_MINB1))
 spmm_kernel(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   const int plane = HALF ? (lane & 15) : lane;   // HALF: two half-warps share probes 0..15 (0..31)
@@ -635,8 +705,13 @@ spmm_kernel(SpmmArgs a) {
       double acc[PPL];
 #pragma unroll
       for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-      gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg,
-                                                                  end, acc);
+      if constexpr (SLQ_HALF2_PIPE > 0 && HALF && PPL == 2 && !BITS && !EXACT) {
+        gather_half2_pipe<VT, KIND == kNLPre ? SLQ_LAPLACIAN : KIND, WEIGHTED, SLQ_HALF2_PIPE>(
+            a.cols, dinv, a.weights, ug, ldi, pidx[0], beg, end, acc);
+      } else {
+        gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg,
+                                                                    end, acc);
+      }
       const double d = __ldg(a.degree + row);
       const double dis = nl_kind<KIND>() ? __ldg(dinv + row) : 0.0;
 #pragma unroll

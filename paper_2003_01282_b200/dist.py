@@ -11,7 +11,7 @@ GPUs, gloo in the CPU tests.
 """
 from __future__ import annotations
 
-__all__ = ["probe_ranges", "gather_rules_arrays", "sharded_rules"]
+__all__ = ["probe_ranges", "gather_rules_arrays", "sharded_rules", "gather_rows", "ShardedBatch"]
 
 
 def probe_ranges(n_v: int, world: int) -> list[tuple[int, int]]:
@@ -87,3 +87,71 @@ def sharded_rules(dg, kind: str, cfg, *, dtype: str = "f64", reorth: int = -1, g
         steps = torch.zeros(0, dtype=torch.int32, device=dg.device)
     nodes, weights, steps, combined = gather_rules_arrays(nodes, weights, steps, cfg.n_v, group, status=status)
     return DeviceRules(nodes, weights, steps, dg.n, status=combined)
+
+
+def gather_rows(block, total: int, group=None):
+    """All-gather per-rank row blocks [count_r, ...] of a balanced contiguous partition of `total`
+    rows (``probe_ranges``) into the full [total, ...] block in row order, on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    ranges = probe_ranges(total, world)
+    cap = max(e - b for b, e in ranges)
+    pack = torch.zeros((cap,) + tuple(block.shape[1:]), dtype=block.dtype, device=block.device)
+    pack[:block.shape[0]] = block
+    on_host = dist.get_backend(group) == "gloo" and pack.is_cuda
+    if on_host:
+        pack = pack.cpu()
+    bufs = [torch.empty_like(pack) for _ in range(world)]
+    dist.all_gather(bufs, pack, group=group)
+    full = torch.cat([bufs[r][: e - b] for r, (b, e) in enumerate(ranges)], dim=0)
+    return full.to(block.device) if on_host else full
+
+
+class ShardedBatch:
+    """C3 over several GPUs: the collection of small graphs is split into balanced
+    contiguous GRAPH ranges, rank r stacks and solves its own range on its GPU (no data-path
+    collective: graphs are independent), and one all-gather assembles the per-graph signatures in
+    graph order.  Each graph's values are those of the single-GPU batched path bit for bit (the
+    batched kernel's arithmetic for a graph does not depend on the other graphs in the stack)."""
+
+    def __init__(self, graphs, device=None, group=None):
+        import torch.distributed as dist
+
+        from .batched import BatchedGraphs
+
+        self.group = group
+        self.total = len(graphs)
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        rank = dist.get_rank(group) if world > 1 else 0
+        self.world = world
+        self.begin, self.end = probe_ranges(self.total, world)[rank]
+        self.local = BatchedGraphs(graphs[self.begin:self.end], device=device) if self.end > self.begin else None
+
+    def values(self, kind: str, cfg, t, fn: int, dtype: str = "f64"):
+        """(values [G, T], std_errors [G, T], status [1] int32) on every rank, device tensors; the status
+        word is the OR over all graphs of all ranks (``_lib.check_status`` maps it to the exceptions)."""
+        import torch
+
+        T = 1 if t is None else len(t)
+        if self.local is not None:
+            rules = self.local.rules(kind, cfg, dtype)
+            vals, stds = self.local.integrate(rules, t, fn)
+            status = rules[3].to(torch.float64).reshape(1, 1).expand(vals.shape[0], 1)
+            block = torch.cat([vals, stds, status], dim=1)
+        else:
+            import torch.distributed as dist
+
+            dev = torch.device("cuda", torch.cuda.current_device())
+            block = torch.zeros((0, 2 * T + 1), dtype=torch.float64, device=dev)
+        if self.world > 1:
+            full = gather_rows(block, self.total, self.group)
+        else:
+            full = block
+        words = full[:, 2 * T].to(torch.int64)
+        status = torch.zeros(1, dtype=torch.int64, device=full.device)
+        for b in range(4):   # OR of the 4 status bits (rules.cu kSt*) over every graph
+            if words.numel():
+                status = status + (((words >> b) & 1).amax() << b)
+        return full[:, :T], full[:, T:2 * T], status.to(torch.int32)

@@ -74,3 +74,37 @@ def test_gather_rules_world2_matches_single(n_v, world):
         for a, b in zip(got, ref):
             assert np.array_equal(a, b)
         assert st == 1, f"rank {rank} did not see rank 1's device error"
+
+
+def _rows_worker(rank, world, port, total, out):
+    from paper_2003_01282_b200.dist import gather_rows
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = probe_ranges(total, world)[rank]
+    # a rank's per-graph signatures: a pure function of the graph index (C3 graph-range sharding)
+    block = torch.tensor([[np.sin(g + 0.1 * t) for t in range(5)] for g in range(b, e)], dtype=torch.float64)
+    block = block.reshape(e - b, 5)
+    full = gather_rows(block, total)
+    out.put((rank, full.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total,world", [(10, 2), (3, 2), (1, 2)])
+def test_graph_range_gather_world2(total, world):
+    """C3 sharding over GPUs (dist.ShardedBatch): balanced contiguous graph ranges, one all-gather of the
+    per-graph rows in graph order; every rank sees the single-rank array."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = np.array([[np.sin(g + 0.1 * t) for t in range(5)] for g in range(total)])
+    for _, full in res:
+        assert np.array_equal(full, ref)

@@ -125,3 +125,66 @@ def test_fold_precheck_counts_empty_rows():
     assert not worth_folding(small.row_offsets, 10, small.nnz)
     empty = csr_from_edges(n, [], [])                                        # no edges: nothing to fold
     assert not worth_folding(empty.row_offsets, n, empty.nnz)
+
+
+# ---------------------------------------------------------------- reference objects and the plugin seam
+class _ForeignGraph:
+    """Duck-typed stand-in for the reference's frozen Graph dataclass (graphs.py:34-60)."""
+
+    def __init__(self, g):
+        self.n, self.m = g.n, g.m
+        self.row_offsets, self.col_indices, self.weights = g.row_offsets, g.col_indices, g.weights
+
+
+def test_as_graph_views_and_caches_foreign_graphs():
+    from paper_2003_01282_b200.graphs import as_graph
+
+    g = golden.graph(golden.load("c1_ba1000.npz"))
+    assert as_graph(g) is g
+    fg = _ForeignGraph(g)
+    v = as_graph(fg)
+    assert v == g and v.content_hash() == g.content_hash()
+    assert as_graph(fg) is v                       # one view (and one device copy) per caller object
+    assert np.shares_memory(v.col_indices, g.col_indices)
+    with pytest.raises(TypeError):
+        as_graph(object())
+
+
+def _reference_package():
+    import os
+    import sys
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if os.path.isdir(path) and path not in sys.path:
+        sys.path.insert(0, path)
+    return pytest.importorskip("spectrace")
+
+
+def test_plugin_install_patches_and_restores_the_seam():
+    st = _reference_package()
+    from paper_2003_01282_b200 import plugin
+
+    orig_collect, orig_make = st.slq._collect_rules, st.operators.make_operator
+    orig_desc_make = st.descriptors.make_operator
+    h = plugin.install(st)
+    assert st.slq._collect_rules is not orig_collect
+    assert st.operators.make_operator is not orig_make and st.descriptors.make_operator is not orig_desc_make
+    h.uninstall()
+    assert st.slq._collect_rules is orig_collect
+    assert st.operators.make_operator is orig_make and st.descriptors.make_operator is orig_desc_make
+
+
+def test_ctypes_stub_loads_and_patches_without_torch():
+    import os
+    import sys
+
+    st = _reference_package()
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration"))
+    import spectrace_gpu
+
+    orig_collect = st.slq._collect_rules
+    uninstall = spectrace_gpu.install(st)
+    assert st.slq._collect_rules is not orig_collect
+    uninstall()
+    assert st.slq._collect_rules is orig_collect
+    assert spectrace_gpu.launch_count() >= 0
