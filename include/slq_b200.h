@@ -278,6 +278,11 @@ int slq_graph_second_passes(const slq_graph* g, int64_t* out_host);
 /* Release the device memory the library's stream-ordered pool keeps cached on the current device
  * (synchronises the device). */
 int slq_trim_pool(void);
+/* The device's persisting-L2 capacity and access-policy-window limit (bytes; SpMM hub window). */
+int slq_l2_limits(int64_t* persist_max, int64_t* window_max);
+/* The first `count` row lengths of the graph the Lanczos recurrence runs on (the isolated-vertex fold,
+ * degree-ordered, when there is one) and its row count. */
+int slq_graph_lanczos_rows(const slq_graph* g, int64_t* lengths_host, int64_t count, int64_t* rows_host);
 const char* slq_last_error(void);
 uint64_t slq_launch_count(void);                /* kernels launched by this library so far */
 void slq_profile_begin(void);                   /* start per-class CUDA-event timing */

@@ -103,6 +103,8 @@ _SIGS = {
     "slq_probe_state_seeded": (_int, [_SP, _u64, ctypes.POINTER(_u64)]),
     "slq_lanczos_batched_seeded": (_int, [_vp, _vp, _i64, _int, _SP, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "slq_trim_pool": (_int, []),
+    "slq_l2_limits": (_int, [ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "slq_graph_lanczos_rows": (_int, [_vp, _vp, _i64, ctypes.POINTER(_i64)]),
     "slq_last_error": (ctypes.c_char_p, []),
     "slq_launch_count": (_u64, []),
     "slq_profile_begin": (None, []),

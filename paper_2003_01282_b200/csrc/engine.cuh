@@ -274,6 +274,9 @@ struct SpmmArgs {
   unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
   const uint32_t* bits;      // first step: u_0 as a probe bitmask [n][kBitWords] (nullptr = use u)
   const void* upre;          // normalized Laplacian: dinv (.) u to gather (nullptr = gather u, times dinv[col])
+  // L2 persisting window over the gathered vector's first rows (degree-ordered fold: the hub rows);
+  // win_rows = 0: no window
+  int64_t win_rows = 0;
 };
 
 // SpMM-internal kind: the normalized Laplacian gathering the PRESCALED vector dinv (.) u (written by
@@ -774,6 +777,33 @@ static int ppl_for(int c) {
   return cb <= 32 ? 1 : (cb <= 64 ? 2 : 4);
 }
 
+// Launch one SpMM kernel; with a window, as cudaLaunchKernelEx carrying an access-policy window that
+// marks the hub rows of the gathered vector (u, the prescaled dinv (.) u, or the probe bitmask)
+// persisting in L2 and everything else streaming.
+template <typename VT, int KIND, bool W, int PPL, bool BITS, bool EXACT, bool HALF, bool V2 = false>
+static void spmm_go(const SpmmArgs& a, dim3 grid, cudaStream_t st) {
+  if (a.win_rows <= 0 || EXACT) {
+    spmm_kernel<VT, KIND, W, PPL, BITS, EXACT, HALF, V2><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    return;
+  }
+  const void* base = BITS ? static_cast<const void*>(a.bits) : (KIND == kNLPre ? a.upre : a.u);
+  const size_t row_bytes = BITS ? sizeof(uint32_t) * kBitWords : sizeof(VT) * static_cast<size_t>(a.ldc_in);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kSpmmWarps * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  at[0].val.accessPolicyWindow.num_bytes = row_bytes * static_cast<size_t>(a.win_rows);
+  at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, spmm_kernel<VT, KIND, W, PPL, BITS, EXACT, HALF, V2>, a);
+}
+
 template <typename VT, int KIND, bool W, int PPL>
 static void spmm_launch_one(SpmmArgs& a, int gy, cudaStream_t st) {
   // persistent: work is taken from the atomic counters; small graphs launch only the warps they can use
@@ -788,24 +818,24 @@ static void spmm_launch_one(SpmmArgs& a, int gy, cudaStream_t st) {
   const bool half2 = half2_on && std::is_same<VT, float>::value && PPL == 1 && !half && a.c <= 32 && a.ldc_in <= 32;
   if (!a.r) {
     if constexpr (std::is_same<VT, double>::value)
-      spmm_kernel<VT, KIND, W, PPL, false, true, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+      spmm_go<VT, KIND, W, PPL, false, true, false>(a, grid, st);
   } else if (half2) {
     // fp32 rows only: fp64 pairs (16-byte loads) do not fit the register budget without spills
     if constexpr (std::is_same<VT, float>::value) {
-      if (a.bits) spmm_kernel<VT, KIND, W, 2, true, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
-      else spmm_kernel<VT, KIND, W, 2, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+      if (a.bits) spmm_go<VT, KIND, W, 2, true, false, true>(a, grid, st);
+      else spmm_go<VT, KIND, W, 2, false, false, true>(a, grid, st);
     }
   } else if (half) {
-    if (a.bits) spmm_kernel<VT, KIND, W, 1, true, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
-    else spmm_kernel<VT, KIND, W, 1, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    if (a.bits) spmm_go<VT, KIND, W, 1, true, false, true>(a, grid, st);
+    else spmm_go<VT, KIND, W, 1, false, false, true>(a, grid, st);
   } else if (a.bits) {
-    spmm_kernel<VT, KIND, W, PPL, true, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    spmm_go<VT, KIND, W, PPL, true, false, false>(a, grid, st);
   } else if (PPL >= 2 && std::is_same<VT, double>::value && vec2_on()) {
     // fp64 rows only (measured: fp32 pairs are ~1.5% slower than the scalar mapping at C2 fp32)
     if constexpr (std::is_same<VT, double>::value)
-      spmm_kernel<VT, KIND, W, PPL, false, false, false, true><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+      spmm_go<VT, KIND, W, PPL, false, false, false, true>(a, grid, st);
   } else {
-    spmm_kernel<VT, KIND, W, PPL, false, false, false><<<grid, kSpmmWarps * 32, 0, st>>>(a);
+    spmm_go<VT, KIND, W, PPL, false, false, false>(a, grid, st);
   }
 }
 

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "slq_common.cuh"
@@ -368,6 +369,56 @@ __global__ void fold_cols_kernel(const int32_t* __restrict__ cols, const int32_t
     cols_f[e] = newid[cols[e]];
 }
 
+// Degree-ordered fold (default): the kept vertices are renumbered by DESCENDING degree (ties: original
+// order), so the rows most nonzeros reference (R-MAT hubs: the top 1M of 63M rows take 63% of the
+// column references) sit in the first few hundred MB of every Lanczos vector.  The SpMM's random
+// 128-byte row gathers then touch few 2 MB pages for most nonzeros: measured (gather_hot.cu) 36 ->
+// 52-56 G lines/s for 53-63% of gathers on a contiguous 64 MB hot set, no gain when the same hot set is
+// scattered (the gather rate over an 8 GB vector is bound by address translation, not by DRAM or L2).
+// Each row keeps its stored column order, so its in-row sum is bitwise the unfolded one; the
+// reductions over rows run in the new row order (equal to rounding).
+__global__ void fold_sort_keys_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ keep, int64_t n,
+                                      int32_t* __restrict__ keys, int32_t* __restrict__ ids) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    keys[v] = keep[v] ? static_cast<int32_t>(off[v + 1] - off[v]) : -1;   // dropped vertices sort last
+    ids[v] = static_cast<int32_t>(v);
+  }
+}
+
+// perm[r] = old vertex of new row r (r < n'): newid[old] = r, -1 for dropped vertices; row lengths in
+// the new order for the offsets scan (the trailing virtual row and the scan's end entry are empty)
+__global__ void fold_perm_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ perm, int64_t n,
+                                 int64_t nprime, int32_t* __restrict__ newid, int64_t* __restrict__ len_new) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n + 2; r += (int64_t)gridDim.x * blockDim.x) {
+    if (r < n) {
+      const int32_t v = perm[r];
+      newid[v] = r < nprime ? static_cast<int32_t>(r) : -1;
+    }
+    if (r <= nprime + 1) len_new[r] = r < nprime ? off[perm[r] + 1] - off[perm[r]] : 0;
+  }
+}
+
+// one warp per new row: copy the old row's columns (stored order) relabelled, and its weights
+__global__ void fold_rows_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                                 const double* __restrict__ w, const int32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ newid, const int64_t* __restrict__ off_f, int64_t nprime,
+                                 int32_t* __restrict__ cols_f, double* __restrict__ w_f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < nprime; r += warps) {
+    const int64_t src = off[perm[r]], dst = off_f[r], len = off_f[r + 1] - dst;
+    for (int64_t k = lane; k < len; k += 32) {
+      cols_f[dst + k] = newid[cols[src + k]];
+      if (w) w_f[dst + k] = w[src + k];
+    }
+  }
+}
+
+static bool fold_by_degree() {
+  static const bool v = [] { const char* e = getenv("SLQ_FOLD_ORDER"); return !(e && e[0] == 'm'); }();
+  return v;   // SLQ_FOLD_ORDER=monotone keeps the original vertex order (A/B)
+}
+
 static void drop_fold(slq_graph* g) {
   if (g->folded) slq_graph_destroy(g->folded);
   if (g->fold_remap) cudaFreeAsync(g->fold_remap, static_cast<cudaStream_t>(g->stream));
@@ -439,15 +490,60 @@ static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
   double* w_f = nullptr;
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&off_f), sizeof(int64_t) * (nprime + 2), st));
   SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cols_f), sizeof(int32_t) * nnz, st));
-  {
-    LaunchScope ls(K_PREPARE, st);
-    fold_offsets_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(g->offsets, keep, newid, n, nprime, nnz, off_f);
-    fold_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(g->cols, newid, nnz, cols_f);
-  }
-  SLQ_CUDA(cudaFreeAsync(newid, st));
-  if (g->weights) {
-    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w_f), sizeof(double) * nnz, st));
-    SLQ_CUDA(cudaMemcpyAsync(w_f, g->weights, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
+  if (g->weights) SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w_f), sizeof(double) * nnz, st));
+  if (fold_by_degree()) {
+    // keys/ids -> sorted by descending degree (stable: ties keep the original order)
+    int32_t *keys = nullptr, *ids = nullptr, *keys_s = nullptr, *perm = nullptr;
+    int64_t* len_new = nullptr;
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), sizeof(int32_t) * n, st));
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ids), sizeof(int32_t) * n, st));
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys_s), sizeof(int32_t) * n, st));
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&perm), sizeof(int32_t) * n, st));
+    {
+      LaunchScope ls(K_PREPARE, st);
+      fold_sort_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(g->offsets, keep, n, keys, ids);
+    }
+    size_t sb = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, keys, keys_s, ids, perm, static_cast<int>(n), 0, 32, st);
+    void* sorttmp = nullptr;
+    SLQ_CUDA(cudaMallocAsync(&sorttmp, sb + 16, st));
+    SLQ_CUDA(cub::DeviceRadixSort::SortPairsDescending(sorttmp, sb, keys, keys_s, ids, perm, static_cast<int>(n), 0,
+                                                       32, st));
+    SLQ_CUDA(cudaFreeAsync(sorttmp, st));
+    SLQ_CUDA(cudaFreeAsync(keys, st));
+    SLQ_CUDA(cudaFreeAsync(ids, st));
+    SLQ_CUDA(cudaFreeAsync(keys_s, st));
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&len_new), sizeof(int64_t) * (nprime + 2), st));
+    {
+      LaunchScope ls(K_PREPARE, st);
+      fold_perm_kernel<<<grid_for(n + 2, 256), 256, 0, st>>>(g->offsets, perm, n, nprime, newid, len_new);
+    }
+    size_t tb2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, len_new, off_f, static_cast<int>(nprime + 2), st);
+    void* scantmp = nullptr;
+    SLQ_CUDA(cudaMallocAsync(&scantmp, tb2 + 16, st));
+    SLQ_CUDA(cub::DeviceScan::ExclusiveSum(scantmp, tb2, len_new, off_f, static_cast<int>(nprime + 2), st));
+    SLQ_CUDA(cudaFreeAsync(scantmp, st));
+    SLQ_CUDA(cudaFreeAsync(len_new, st));
+    {
+      LaunchScope ls(K_PREPARE, st);
+      fold_rows_kernel<<<grid_for(nprime * 32, 256), 256, 0, st>>>(g->offsets, g->cols, g->weights, perm, newid, off_f,
+                                                                   nprime, cols_f, w_f);
+    }
+    SLQ_CUDA(cudaFreeAsync(perm, st));
+    // the remap (original vertex -> folded row, -1 dropped) is newid; keep[] is no longer needed
+    SLQ_CUDA(cudaFreeAsync(keep, st));
+    keep = newid;
+    newid = nullptr;
+  } else {
+    {
+      LaunchScope ls(K_PREPARE, st);
+      fold_offsets_kernel<<<grid_for(n + 1, 256), 256, 0, st>>>(g->offsets, keep, newid, n, nprime, nnz, off_f);
+      fold_cols_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(g->cols, newid, nnz, cols_f);
+    }
+    SLQ_CUDA(cudaFreeAsync(newid, st));
+    newid = nullptr;
+    if (g->weights) SLQ_CUDA(cudaMemcpyAsync(w_f, g->weights, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
   }
   slq_graph* f = new slq_graph();
   f->n = nprime + 1;
@@ -466,6 +562,7 @@ static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
   SLQ_CUDA(cudaMemcpyAsync(f->dscal, g->dscal, sizeof(double) * 8, cudaMemcpyDeviceToDevice, st));
   SLQ_CUDA(cudaStreamSynchronize(st));
   SLQ_CUDA(cudaGetLastError());
+  f->degree_ordered = fold_by_degree() ? 1 : 0;
   g->folded = f;
   g->fold_remap = keep;
   g->fold_m = m;
@@ -568,6 +665,23 @@ extern "C" int slq_graph_create_i32(int64_t n, int64_t nnz, const int64_t* offse
     return rc;
   }
   *out = g;
+  return SLQ_OK;
+}
+
+// Diagnostics: the first `count` row lengths of the Lanczos graph (the fold when there is one), host
+// array; returns the number of rows of that graph in *rows_host.  Synchronous.
+extern "C" int slq_graph_lanczos_rows(const slq_graph* g, int64_t* lengths_host, int64_t count, int64_t* rows_host) {
+  if (!g || !lengths_host || !rows_host || count < 0) return fail(SLQ_ERR_VALUE, "bad argument");
+  const slq_graph* f = g->folded ? g->folded : g;
+  cudaStream_t st = static_cast<cudaStream_t>(g->stream);
+  count = std::min<int64_t>(count, f->n);
+  std::vector<int64_t> off(static_cast<size_t>(count + 1));
+  if (count > 0) {
+    SLQ_CUDA(cudaMemcpyAsync(off.data(), f->offsets, sizeof(int64_t) * (count + 1), cudaMemcpyDeviceToHost, st));
+    SLQ_CUDA(cudaStreamSynchronize(st));
+  }
+  for (int64_t r = 0; r < count; ++r) lengths_host[r] = off[r + 1] - off[r];
+  *rows_host = f->n;
   return SLQ_OK;
 }
 

@@ -187,6 +187,39 @@ static int64_t partial_rows(const slq_graph* g) {
                             static_cast<int64_t>(kAlphaCtas)});
 }
 
+// Bytes of the SpMM's persisting L2 window on graph g (0: none): degree-ordered folds only, capped by
+// the device's persisting-L2 and window limits and SLQ_L2_WINDOW_MB; the persisting carve-out is set
+// once per device.
+static int64_t l2_window_bytes(const slq_graph* g) {
+  if (!g->degree_ordered) return 0;
+  // off by default: measured SpMM -5% but the persisting carve-out costs the CGS step kernel +39% of
+  // its L2 reuse; SLQ_L2_WINDOW_MB=-1 uses the device maximum, k caps it at k MB
+  static const long long env_mb = [] { const char* e = getenv("SLQ_L2_WINDOW_MB"); return e ? atoll(e) : 0ll; }();
+  if (env_mb == 0) return 0;
+  const int dev = g->device >= 0 && g->device < 64 ? g->device : 0;
+  static std::atomic<long long> cached[64];
+  long long v = cached[dev].load(std::memory_order_acquire);
+  if (v == 0) {
+    int persist = 0, maxwin = 0;
+    cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    long long bytes = std::min<long long>(persist, maxwin);
+    if (bytes > 0) {
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(static_cast<cudaStream_t>(g->stream), &cap);
+      if (cap == cudaStreamCaptureStatusNone &&
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(persist)) != cudaSuccess) {
+        cudaGetLastError();
+        bytes = 0;
+      }
+    }
+    v = bytes > 0 ? bytes : -1;
+    cached[dev].store(v, std::memory_order_release);
+  }
+  if (v < 0) return 0;
+  return env_mb > 0 ? std::min<long long>(v, env_mb << 20) : v;
+}
+
 // The recurrence runs on `g`; with an isolated-vertex fold, g is the folded graph and `orig` the
 // graph the probes and the start-vector norm belong to (probe stream positions are original vertex
 // ids, remapped to folded rows; the trailing row carries sqrt(m)).
@@ -286,6 +319,11 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   sa.dscal = g->dscal;
   sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad;
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));
+  // Degree-ordered fold: the first rows of every gathered vector are the hubs; an L2 access-policy
+  // window can keep them persisting across the SpMM (LRU alone evicts a hub row between its references
+  // when the cold rows stream through).  SLQ_L2_WINDOW_MB: off by default (see l2_window_bytes).
+  const int64_t win_bytes = l2_window_bytes(g);
+  const int64_t win_rows_vec = win_bytes > 0 ? std::min<int64_t>(n, win_bytes / (ldc * vb)) : 0;
 
   CgsArgs ca{};
   ca.n = n; ca.ldc = ldc; ca.vec_stride = vs; ca.rows_per_tile = g->rows_per_stream_tile;
@@ -343,6 +381,9 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
     sa.red = ra;
     sa.work = s.work + 4 * i;
     sa.bits = (i == 0) ? bits : nullptr;
+    sa.win_rows = sa.bits ? std::min<int64_t>(n, win_bytes / static_cast<int64_t>(sizeof(uint32_t) * kBitWords))
+                          : win_rows_vec;
+    if (win_bytes <= 0) sa.win_rows = 0;
     sa.upre = (prescale && i >= 1 && i <= S - 2) ? static_cast<const void*>(basis + (i + 1) * vs) : nullptr;
     ca.pre_dinv = (prescale && i + 1 <= S - 2) ? g->dinv : nullptr;
     ca.dbg = (dbgbuf && i < kMaxSteps) ? dbgbuf + kDbgStride * i : nullptr;
@@ -619,5 +660,16 @@ extern "C" int slq_trim_pool(void) {
   SLQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   SLQ_CUDA(cudaDeviceSynchronize());
   SLQ_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return SLQ_OK;
+}
+
+// Diagnostics: the device's persisting-L2 and access-policy-window limits (bytes).
+extern "C" int slq_l2_limits(int64_t* persist_max, int64_t* window_max) {
+  int dev = 0, p = 0, w = 0;
+  SLQ_CUDA(cudaGetDevice(&dev));
+  SLQ_CUDA(cudaDeviceGetAttribute(&p, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  SLQ_CUDA(cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  if (persist_max) *persist_max = p;
+  if (window_max) *window_max = w;
   return SLQ_OK;
 }

@@ -119,6 +119,7 @@ struct slq_graph {
   slq_graph* folded = nullptr;
   int32_t* fold_remap = nullptr;       // [n] original vertex -> folded row, -1 for folded-away rows
   int64_t fold_m = 0;                  // vertices folded into the trailing row
+  int degree_ordered = 0;              // (a fold) rows renumbered by descending degree: hubs first
   // owned device allocations
   void* owned[12] = {nullptr};
   int n_owned = 0;

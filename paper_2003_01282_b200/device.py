@@ -215,6 +215,15 @@ class DeviceGraph:
             _lib.check(_lib.load().slq_graph_second_passes(self.handle, ctypes.byref(v)))
         return int(v.value)
 
+    def lanczos_row_lengths(self, count: int):
+        """(first `count` row lengths, row count) of the graph the recurrence runs on (the fold, in
+        descending-degree order, when the graph is folded).  Diagnostics."""
+        out = np.zeros(int(count), dtype=np.int64)
+        rows = ctypes.c_int64()
+        with _lib.require_cuda().cuda.device(self.device):
+            _lib.check(_lib.load().slq_graph_lanczos_rows(self.handle, out.ctypes.data, int(count), ctypes.byref(rows)))
+        return out, int(rows.value)
+
     # -- operator set-up -----------------------------------------------------------
     def interval(self, kind: str) -> tuple[float, float]:
         lo, hi = ctypes.c_double(), ctypes.c_double()
