@@ -192,9 +192,11 @@ static int64_t partial_rows(const slq_graph* g) {
 // once per device.
 static int64_t l2_window_bytes(const slq_graph* g) {
   if (!g->degree_ordered) return 0;
-  // off by default: measured SpMM -5% but the persisting carve-out costs the CGS step kernel +39% of
-  // its L2 reuse; SLQ_L2_WINDOW_MB=-1 uses the device maximum, k caps it at k MB
-  static const long long env_mb = [] { const char* e = getenv("SLQ_L2_WINDOW_MB"); return e ? atoll(e) : 0ll; }();
+  // 32 MB by default (R-MAT-26, 32 probes: SpMM -2.7%, CGS step unchanged; the device maximum, 79 MB,
+  // gives SpMM -5% but costs the step kernel +39% of its L2 reuse).  SLQ_L2_WINDOW_MB=0 turns
+  // it off, -1 uses the device maximum, k sets k MB.  The carve-out (cudaLimitPersistingL2CacheSize,
+  // a device-wide setting) is sized to the window.
+  static const long long env_mb = [] { const char* e = getenv("SLQ_L2_WINDOW_MB"); return e ? atoll(e) : 32ll; }();
   if (env_mb == 0) return 0;
   const int dev = g->device >= 0 && g->device < 64 ? g->device : 0;
   static std::atomic<long long> cached[64];
@@ -204,11 +206,12 @@ static int64_t l2_window_bytes(const slq_graph* g) {
     cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
     long long bytes = std::min<long long>(persist, maxwin);
+    if (env_mb > 0) bytes = std::min<long long>(bytes, env_mb << 20);
     if (bytes > 0) {
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(static_cast<cudaStream_t>(g->stream), &cap);
       if (cap == cudaStreamCaptureStatusNone &&
-          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(persist)) != cudaSuccess) {
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(bytes)) != cudaSuccess) {
         cudaGetLastError();
         bytes = 0;
       }
@@ -216,8 +219,7 @@ static int64_t l2_window_bytes(const slq_graph* g) {
     v = bytes > 0 ? bytes : -1;
     cached[dev].store(v, std::memory_order_release);
   }
-  if (v < 0) return 0;
-  return env_mb > 0 ? std::min<long long>(v, env_mb << 20) : v;
+  return v < 0 ? 0 : v;
 }
 
 // The recurrence runs on `g`; with an isolated-vertex fold, g is the folded graph and `orig` the
@@ -321,7 +323,7 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));
   // Degree-ordered fold: the first rows of every gathered vector are the hubs; an L2 access-policy
   // window can keep them persisting across the SpMM (LRU alone evicts a hub row between its references
-  // when the cold rows stream through).  SLQ_L2_WINDOW_MB: off by default (see l2_window_bytes).
+  // when the cold rows stream through).  SLQ_L2_WINDOW_MB sizes it (see l2_window_bytes).
   const int64_t win_bytes = l2_window_bytes(g);
   const int64_t win_rows_vec = win_bytes > 0 ? std::min<int64_t>(n, win_bytes / (ldc * vb)) : 0;
 
