@@ -207,13 +207,7 @@ def cpu_operator(off, cols, n, kind):
     object.__setattr__(g, "row_offsets", off)
     object.__setattr__(g, "col_indices", cols)
     object.__setattr__(g, "weights", np.ones(cols.size))
-    op = O.make_block_operator(g, kind)
-    op.nnz = int(cols.size)
-    return op
-
-
-def op_nnz_of(op) -> int:
-    return int(op.nnz)
+    return O.make_block_operator(g, kind)
 
 
 def cpu_sample(op, nnz, probes, steps, threads):
@@ -234,36 +228,84 @@ def big_graph(cfg):
     return cfg["graph"] == "rmat" and cfg["scale"] >= 24
 
 
-def cpu_threads(nnz, n, want):
-    """Host threads for the C5 CPU sample: one probe per thread needs ~6 vectors of n doubles next to
-    the shared scipy matrix (int64 indices + float64 data); stay inside the free host memory."""
-    try:
-        import psutil
+def cpu_row_sample_operator(off, cols, n, every):
+    """The oracle port's normalized-Laplacian apply (operators.py:84-89 arithmetic: scipy csr_matvecs +
+    numpy elementwise) restricted to every `every`-th row of the graph, against full-length vectors:
+    the C5 sample.  Gathers still range over the whole vector, so the per-nonzero cost is the full
+    operator's.  Returns (apply(x [n, c]) -> y [rows, c], alpha(x, y) -> [c], sampled nnz)."""
+    import numpy as np
+    import scipy.sparse as sp
 
-        avail = psutil.virtual_memory().available
-    except Exception:
-        return want
-    matrix = nnz * 16 + n * 24
-    per_thread = 6 * n * 8
-    return int(max(1, min(want, (avail * 0.85 - matrix) // per_thread)))
+    deg = np.diff(off).astype(np.float64)          # unit weights: degree = row length (operators.py:58-62)
+    pos = deg > 0
+    dis = np.zeros(n)
+    dis[pos] = 1.0 / np.sqrt(deg[pos])
+    rows = np.arange(0, n, every, dtype=np.int64)
+    starts, ends = off[rows], off[rows + 1]
+    lens = ends - starts
+    sub_off = np.zeros(rows.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=sub_off[1:])
+    idx = np.repeat(starts - sub_off[:-1], lens) + np.arange(sub_off[-1], dtype=np.int64)
+    sub = sp.csr_matrix((np.ones(sub_off[-1]), cols[idx].astype(np.int64), sub_off), shape=(rows.size, n))
+    keep_r = pos[rows].astype(np.float64)[:, None]
+    dis_r = dis[rows][:, None]
+    disc = dis[:, None]
+
+    def apply(x):
+        return keep_r * x[rows] - dis_r * (sub @ (disc * x))
+
+    def alpha(x, y):
+        return np.einsum("nc,nc->c", x[rows], y)
+
+    return apply, alpha, int(sub_off[-1])
+
+
+def cpu_row_sample(sampler, n, probes, threads):
+    """`probes` unit Rademacher probes (one per host thread, like the reference's thread map over
+    probes, slq.py:80-86), each: one operator apply + alpha on the sampled rows.  Returns (units/s, s)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import slq_oracle as O
+
+    apply, alpha, nnz_s = sampler[:3]
+    qs = [O.draw_probes(n, 0, [p]) for p in range(probes)]   # outside the timed region
+    t0 = time.perf_counter()
+
+    def one(q):
+        return alpha(q, apply(q))
+
+    if threads > 1:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(one, qs))
+    else:
+        for q in qs:
+            one(q)
+    dt = time.perf_counter() - t0
+    return nnz_s * probes / dt, dt
 
 
 def cpu_baseline_for(cfg, op, nnz, threads):
-    """Bounded CPU sample of the workload (about 10-30 s).  C5: one Lanczos step (SpMV + alpha) of one
-    probe per host thread on the real graph, operator built beforehand (the per-probe-step cost does
-    not depend on n_v; the full signature would take hours on the host); C2/C4: all probes,
-    all steps of the heat run."""
+    """Bounded CPU sample of the workload (about 5-30 s).  C5 (`op` is a row sampler from
+    cpu_row_sample_operator): one Lanczos operator application + alpha of one probe per host thread on
+    every 8th row of the real graph (per-probe-step cost is independent of n_v; the full
+    signature would take hours on the host); C2/C4: all probes, all steps of the heat run."""
     if big_graph(cfg):
-        threads = cpu_threads(nnz, op.dim, threads)
-        probes, steps = threads, 1
-        sample = (f"{probes} probes (one per host thread) x 1 Lanczos step (SpMV + alpha) of the normalized "
-                  f"Laplacian on the same R-MAT-{cfg['scale']} graph, scipy operator built beforehand "
-                  f"(oracle/slq_oracle.py numpy+scipy port); per-unit rate, units = stored nonzero x probe x step")
-    else:
-        probes, steps = cfg["n_v"], cfg["lanczos_steps"]
-        sample = f"all {probes} probes x {steps} steps of the heat run (oracle port, numpy+scipy)"
+        v, dt = cpu_row_sample(op, op[3], threads, threads)
+        sample = (f"{threads} probes (one per host thread) x 1 Lanczos operator application + alpha of the "
+                  f"normalized Laplacian on every 8th row of the same R-MAT-{cfg['scale']} graph (full-length "
+                  f"vectors; numpy+scipy port of operators.py:84-89); units = sampled stored nonzeros x probes")
+        return v, dt, sample, threads
+    probes, steps = cfg["n_v"], cfg["lanczos_steps"]
+    sample = f"all {probes} probes x {steps} steps of the heat run (oracle port, numpy+scipy)"
     v, dt = cpu_sample(op, nnz, probes, steps, threads)
     return v, dt, sample, threads
+
+
+def cpu_op_for(cfg, off, cols, n):
+    """The CPU arm's operator: the C5 row sampler, or the full oracle operator for C2/C4."""
+    if big_graph(cfg):
+        return (*cpu_row_sample_operator(off, cols, n, 8), n)
+    return cpu_operator(off, cols, n, NL)
 
 
 def run_reference(args, cfg):
@@ -314,10 +356,10 @@ def run_reference(args, cfg):
 
         g = synth.sbm(cfg["n"], cfg["blocks"], cfg["p_in"], cfg["p_out"], seed=cfg["graph_seed"])
         off, cols, n = np.asarray(g.row_offsets), np.asarray(g.col_indices), g.n
-    op = cpu_operator(off, cols, n, NL)
+    op = cpu_op_for(cfg, off, cols, n)
+    nnz = int(cols.size)
     del off, cols
-    log(f"reference arm: graph + operator ready in {time.perf_counter() - t0:.1f} s (n={n}, nnz={cols.size})")
-    nnz = op_nnz = int(op_nnz_of(op))
+    log(f"reference arm: graph + operator ready in {time.perf_counter() - t0:.1f} s (n={n}, nnz={nnz})")
     vals, times, sample = [], [], ""
     for k in range(args.warmup + args.steps):
         v, dt, sample, used = cpu_baseline_for(cfg, op, nnz, threads)
@@ -746,7 +788,7 @@ def run_ours(args, cfg):
     log(f"e2e: {e2e_s:.2f} s per signature; device {ms:.1f} ms per step; value {value:.4g}")
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
-        op = cpu_operator(pin_off.numpy(), pin_cols.numpy(), n, NL)   # scipy copies to int64 indices
+        op = cpu_op_for(cfg, pin_off.numpy(), pin_cols.numpy(), n)      # copies what it keeps
         del pin_off, pin_cols
         try:
             torch._C._host_emptyCache()                                # give the pinned pages back
@@ -754,11 +796,18 @@ def run_ours(args, cfg):
             pass
         v, dt, sample, used = cpu_baseline_for(cfg, op, nnz, threads)
         log(f"cpu baseline: {v:.4g} units/s on {used} threads ({dt:.1f} s)")
-        s1 = 1 if big_graph(cfg) else s
-        v1, dt1 = cpu_sample(op, nnz, 1, s1, 1)
+        if big_graph(cfg):
+            v1, dt1 = cpu_row_sample(op, n, 1, 1)
+            s1 = 1
+        else:
+            s1 = s
+            v1, dt1 = cpu_sample(op, nnz, 1, s1, 1)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "port",
                                 "sample": f"{sample}; {dt:.1f} s",
-                                "value_1_thread": v1, "sample_1_thread": f"1 probe x {s1} step(s), 1 thread; {dt1:.1f} s"}
+                                "value_1_thread": v1,
+                                "sample_1_thread": (f"1 probe, 1 operator application + alpha on every 8th row, 1 thread; "
+                                                    f"{dt1:.1f} s") if big_graph(cfg) else
+                                                   f"1 probe x {s1} steps, 1 thread; {dt1:.1f} s"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

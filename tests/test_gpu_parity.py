@@ -338,7 +338,7 @@ def test_long_runs_use_fallback_kernels_and_match_oracle(cuda_device):
     assert abs(vnge_slq(g, SlqConfig(n_v=6, s=24, seed=0)).value - ref_v) <= FP64_TOL * abs(ref_v)
 
 
-def test_flat_kernels_match_staged(cuda_device):
+def test_flat_kernels_match_staged(cuda_device, tmp_path):
     # the non-staged streaming kernels (SLQ_STAGED=0) give the same rules within fp64 rounding
     import subprocess
     import sys
@@ -346,11 +346,11 @@ def test_flat_kernels_match_staged(cuda_device):
     code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests'); import numpy as np, golden; "
             "from paper_2003_01282_b200.device import DeviceGraph; "
             "g = golden.graph(golden.load('rmat12.npz')); r = DeviceGraph(g).rules('density', 0, 0, 16, 15); "
-            "np.save('/tmp/slq_flat_nodes.npy', r.nodes.cpu().numpy())")
+            f"np.save({str(tmp_path / 'flat_nodes.npy')!r}, r.nodes.cpu().numpy())")
     env = dict(__import__('os').environ, SLQ_STAGED="0")
     subprocess.run([sys.executable, "-c", code], check=True, env=env,
                    cwd=__import__('os').path.dirname(__import__('os').path.dirname(__file__)))
-    flat = np.load("/tmp/slq_flat_nodes.npy")
+    flat = np.load(tmp_path / "flat_nodes.npy")
     g = golden.graph(golden.load("rmat12.npz"))
     staged = DeviceGraph(g, cuda_device).rules("density", 0, 0, 16, 15).nodes.cpu().numpy()
     assert np.max(np.abs(flat - staged)) <= 1e-14
@@ -629,11 +629,12 @@ def test_spmm_vec2_mapping_bitwise_equals_scalar(cuda_device, tmp_path, count, d
 
 @pytest.mark.parametrize("kind,fns", [("normalized_laplacian", [_lib.FN_HEAT, _lib.FN_WAVE_RE, _lib.FN_WAVE_IM]),
                                       ("density", [_lib.FN_XLOGX])])
-def test_captured_signature_replays_eager_results(cuda_device, kind, fns):
+@pytest.mark.parametrize("n", [1000, 100])   # n <= 128 takes the one-CTA small-graph kernel inside the capture
+def test_captured_signature_replays_eager_results(cuda_device, kind, fns, n):
     from paper_2003_01282_b200 import synth
     from paper_2003_01282_b200.device import CapturedSignature
 
-    g = synth.barabasi_albert(1000, 3, seed=0)
+    g = synth.barabasi_albert(n, 3, seed=0)
     dg = DeviceGraph(g, cuda_device)
     t = None if kind == "density" else np.array(GRID.values)
     eager = dg.rules(kind, 0, 0, 10, 10)

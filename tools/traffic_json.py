@@ -16,13 +16,12 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(path):
+def main(path, n=100_000, c=100, vb=8, workload="C2 (bench.py), one signature after a warm-up signature"):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     col = {h: i for i, h in enumerate(hdr)}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
-    n, c, vb = 100_000, 100, 8      # C2 chunk geometry (bench.py WORKLOAD)
     kernels = {}
     for r in rows[2:]:
         name = r[col["Kernel Name"]]
@@ -42,7 +41,7 @@ def main(path):
         if cls == "cgs_step":
             nk = int(re.search(r"cgs_step_kernel<[^,]+, (\d+)", name).group(1))
             k["alg_bytes"] += n * c * vb * (2 * nk + 1) + 2 * n * 16
-    res = {"workload": "C2 (bench.py), one signature after a warm-up signature", "source": os.path.basename(path),
+    res = {"workload": workload, "source": os.path.basename(path),
            "kernels": {}}
     for cls, k in kernels.items():
         e = {"launches": k["launches"], "dram_bytes_per_launch": k["dram_bytes"] / k["launches"],
@@ -55,4 +54,13 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    ap.add_argument("--rows", type=int, default=100_000, help="Lanczos vector rows (folded rows at C5)")
+    ap.add_argument("--c", type=int, default=100, help="probes per chunk")
+    ap.add_argument("--vb", type=int, default=8, help="vector bytes per element")
+    ap.add_argument("--workload", default="C2 (bench.py), one signature after a warm-up signature")
+    a = ap.parse_args()
+    main(a.report, a.rows, a.c, a.vb, a.workload)
