@@ -260,6 +260,9 @@ def cpu_row_sample_operator(off, cols, n, every):
     return apply, alpha, int(sub_off[-1])
 
 
+_PROBE_CACHE: dict = {}
+
+
 def cpu_row_sample(sampler, n, probes, threads):
     """`probes` unit Rademacher probes (one per host thread, like the reference's thread map over
     probes, slq.py:80-86), each: one operator apply + alpha on the sampled rows.  Returns (units/s, s)."""
@@ -268,7 +271,11 @@ def cpu_row_sample(sampler, n, probes, threads):
     from oracle import slq_oracle as O
 
     apply, alpha, nnz_s = sampler[:3]
-    qs = [O.draw_probes(n, 0, [p]) for p in range(probes)]   # outside the timed region
+    key = (n, probes)
+    if key not in _PROBE_CACHE:                                # drawn once, outside the timed region
+        _PROBE_CACHE.clear()
+        _PROBE_CACHE[key] = [O.draw_probes(n, 0, [p]) for p in range(probes)]
+    qs = _PROBE_CACHE[key]
     t0 = time.perf_counter()
 
     def one(q):
@@ -551,6 +558,60 @@ def run_ours_batch(args, cfg):
     return 0
 
 
+class SharedHostCsr:
+    """The workload CSR (int64 offsets, int32 columns) in node-shared host memory for multi-rank e2e
+    legs: local rank 0 copies it from its device into files under /dev/shm (or $TMPDIR when /dev/shm
+    is too small), every rank maps them and page-locks its mapping (cudaHostRegister) so the H2D runs
+    at pinned speed.  Exposes torch views `offsets` / `cols` over the mapping."""
+
+    def __init__(self, dg, g, rank, local, world, torch, dist):
+        import shutil
+        import tempfile
+
+        import numpy as np
+
+        self.torch, self.dist, self.local = torch, dist, local
+        n, nnz = dg.n, dg.nnz
+        need = (n + 1) * 8 + nnz * 4
+        base = "/dev/shm" if shutil.disk_usage("/dev/shm").free > 1.2 * need else tempfile.gettempdir()
+        tag = os.environ.get("MASTER_PORT", "0")
+        self.paths = [os.path.join(base, f"slq_bench_{tag}_offsets.bin"), os.path.join(base, f"slq_bench_{tag}_cols.bin")]
+        if local == 0:
+            off_h, cols_h = host_csr(dg, g)
+            for path, arr in zip(self.paths, (off_h, cols_h)):
+                mm = np.memmap(path, dtype=arr.dtype, mode="w+", shape=arr.shape)
+                mm[:] = arr
+                mm.flush()
+                del mm
+            del off_h, cols_h
+        dist.barrier()
+        self.maps = [np.memmap(self.paths[0], dtype=np.int64, mode="r+", shape=(n + 1,)),
+                     np.memmap(self.paths[1], dtype=np.int32, mode="r+", shape=(nnz,))]
+        self.registered = []
+        cudart = torch.cuda.cudart()
+        for mm in self.maps:
+            ptr, nbytes = mm.ctypes.data, mm.nbytes
+            if int(cudart.cudaHostRegister(ptr, nbytes, 0)) == 0:
+                self.registered.append(ptr)
+        self.offsets = torch.from_numpy(self.maps[0])
+        self.cols = torch.from_numpy(self.maps[1])
+
+    def close(self):
+        cudart = self.torch.cuda.cudart()
+        for ptr in self.registered:
+            cudart.cudaHostUnregister(ptr)
+        self.registered = []
+        del self.offsets, self.cols
+        self.maps = []
+        self.dist.barrier()
+        if self.local == 0:
+            for path in self.paths:
+                try:
+                    os.unlink(path)
+                except OSError:
+                    pass
+
+
 class TimeGridLike:
     """A TimeGrid carrying exactly the bench's t values (geomspace with pinned endpoints)."""
 
@@ -690,11 +751,19 @@ def run_ours(args, cfg):
     # ---- e2e: host CSR (pinned, int32 columns) -> device graph -> signature -> host values ----
     last_vals = [v.clone() for v, _ in signature(dg)[0]]
     _lib.trim_pool()             # the Lanczos workspaces cached in the pool are not needed for the copy
-    off_h, cols_h = host_csr(dg, g)
-    torch.cuda.empty_cache()
-    pin_off = torch.from_numpy(np.ascontiguousarray(off_h)).pin_memory()
-    pin_cols = torch.from_numpy(np.ascontiguousarray(cols_h)).pin_memory()
-    del off_h, cols_h
+    if world == 1:
+        off_h, cols_h = host_csr(dg, g)
+        torch.cuda.empty_cache()
+        pin_off = torch.from_numpy(np.ascontiguousarray(off_h)).pin_memory()
+        pin_cols = torch.from_numpy(np.ascontiguousarray(cols_h)).pin_memory()
+        del off_h, cols_h
+        shared = None
+    else:
+        # N ranks on one node: ONE host copy of the CSR (18 GB at C5) in shared memory, page-locked by
+        # every rank, instead of N private pinned copies that would not fit the host
+        shared = SharedHostCsr(dg, g, rank, local, world, torch, dist)
+        pin_off, pin_cols = shared.offsets, shared.cols
+        torch.cuda.empty_cache()
     folded = dg.folded
     del dg                       # the e2e leg builds its own device graph from the host arrays
     torch.cuda.synchronize()
@@ -723,6 +792,8 @@ def run_ours(args, cfg):
     e2e_value = units_step / e2e_s
     # the e2e descriptors equal the device-resident run's bit for bit (same graph, same probes)
     same = all(torch.equal(hv.to(dev), dv) for (hv, _), dv in zip(host_vals, last_vals))
+    if shared is not None:
+        shared.close()
 
     if rank != 0:
         dist.destroy_process_group()
