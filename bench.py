@@ -559,10 +559,12 @@ def run_ours_batch(args, cfg):
 
 
 class SharedHostCsr:
-    """The workload CSR (int64 offsets, int32 columns) in node-shared host memory for multi-rank e2e
-    legs: local rank 0 copies it from its device into files under /dev/shm (or $TMPDIR when /dev/shm
-    is too small), every rank maps them and page-locks its mapping (cudaHostRegister) so the H2D runs
-    at pinned speed.  Exposes torch views `offsets` / `cols` over the mapping."""
+    """The workload CSR (int64 offsets, int32 columns) as ONE host copy shared by the ranks of a
+    multi-rank run (N private pinned copies of the 18 GB C5 CSR would not fit the host): local rank 0
+    writes it from its device to files in $TMPDIR (/tmp), every rank maps them read-only (one copy in
+    the page cache).  /dev/shm is not used: on the GPU boxes its writes fault (SIGBUS) well below the
+    size df reports.  The H2D copies run from this pageable mapping.  When the temp directory lacks the
+    space, each rank falls back to a private pinned copy.  Exposes torch views `offsets` / `cols`."""
 
     def __init__(self, dg, g, rank, local, world, torch, dist):
         import shutil
@@ -570,44 +572,37 @@ class SharedHostCsr:
 
         import numpy as np
 
-        self.torch, self.dist, self.local = torch, dist, local
+        self.dist, self.local = dist, local
         n, nnz = dg.n, dg.nnz
         need = (n + 1) * 8 + nnz * 4
-        base = "/dev/shm" if shutil.disk_usage("/dev/shm").free > 1.2 * need else tempfile.gettempdir()
+        base = tempfile.gettempdir()
+        ok = torch.tensor([1 if shutil.disk_usage(base).free > 1.5 * need else 0])
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every rank takes the same branch
+        self.paths = []
+        if not int(ok.item()):
+            off_h, cols_h = host_csr(dg, g)
+            self.offsets = torch.from_numpy(np.ascontiguousarray(off_h)).pin_memory()
+            self.cols = torch.from_numpy(np.ascontiguousarray(cols_h)).pin_memory()
+            return
         tag = os.environ.get("MASTER_PORT", "0")
         self.paths = [os.path.join(base, f"slq_bench_{tag}_offsets.bin"), os.path.join(base, f"slq_bench_{tag}_cols.bin")]
         if local == 0:
             off_h, cols_h = host_csr(dg, g)
-            for path, arr in zip(self.paths, (off_h, cols_h)):
-                mm = np.memmap(path, dtype=arr.dtype, mode="w+", shape=arr.shape)
-                mm[:] = arr
-                mm.flush()
-                del mm
+            np.ascontiguousarray(off_h, dtype=np.int64).tofile(self.paths[0])
+            np.ascontiguousarray(cols_h, dtype=np.int32).tofile(self.paths[1])
             del off_h, cols_h
         dist.barrier()
         self.maps = [np.memmap(self.paths[0], dtype=np.int64, mode="r+", shape=(n + 1,)),
                      np.memmap(self.paths[1], dtype=np.int32, mode="r+", shape=(nnz,))]
-        self.registered = []
-        cudart = torch.cuda.cudart()
-        for mm in self.maps:
-            ptr, nbytes = mm.ctypes.data, mm.nbytes
-            if int(cudart.cudaHostRegister(ptr, nbytes, 0)) == 0:
-                self.registered.append(ptr)
         self.offsets = torch.from_numpy(self.maps[0])
         self.cols = torch.from_numpy(self.maps[1])
 
     def close(self):
-        cudart = self.torch.cuda.cudart()
-        for ptr in self.registered:
-            cudart.cudaHostUnregister(ptr)
-        self.registered = []
-        del self.offsets, self.cols
-        self.maps = []
         self.dist.barrier()
         if self.local == 0:
             for path in self.paths:
                 try:
-                    os.unlink(path)
+                    os.unlink(path)   # mappings stay valid until released
                 except OSError:
                     pass
 
