@@ -940,6 +940,8 @@ struct CgsArgs {
   // normalized Laplacian, prescaled gathers: the update also writes dinv (.) u_{i+1} into the (still
   // unused) slot i+2 for the next SpMM (nullptr: not this step)
   const double* pre_dinv = nullptr;
+  void* pre_out = nullptr;         // where dinv (.) u_{i+1} goes (nullptr: the slot of u_{i+2}); the last
+                                   // step kernel writes it over w, which the last SpMM no longer needs
   unsigned long long* dbg = nullptr;   // SLQ_STEP_TIMING: %globaltimer of CTA 0 around each grid barrier
 };
 
@@ -1502,7 +1504,8 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
   const int rt = sa.rt, vstride = sa.vstride;
   const int64_t stage_elems = stage_elems_of<VT>(sa.nvec, rt, vstride, a.pre_dinv != nullptr);
   VT* out = const_cast<VT*>(static_cast<const VT*>(a.basis)) + static_cast<int64_t>(NK) * a.vec_stride + p;
-  VT* out_pre = a.pre_dinv ? out + a.vec_stride : nullptr;   // slot i+2: dinv (.) u_{i+1}
+  // dinv (.) u_{i+1}: slot i+2, or (last step kernel) the rows of w this CTA has already consumed
+  VT* out_pre = a.pre_dinv ? (a.pre_out ? static_cast<VT*>(a.pre_out) + p : out + a.vec_stride) : nullptr;
   double nb = 0.0, nrm = 0.0, gr[NQ];
   T bnb = T(0), bnrm = T(0), bgr[NQ];
 #pragma unroll

@@ -350,6 +350,10 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
     return e ? static_cast<int64_t>(atoll(e)) : (int64_t(1) << 22);
   }();
   const bool prescale = pre_env && kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && ldc <= 32 && n >= pre_min_n;
+  // The last SpMM (step S-1) is prescaled too: the last step kernel writes dinv (.) u_{S-1} over w (each
+  // CTA over rows it has already consumed), and that SpMM, which only feeds alpha_{S-1}, writes its
+  // output into the slot of u_1 (no longer needed).  Needs S >= 3 and no basis export.
+  const bool last_pre = prescale && S >= 3 && !basis_out;
   // SLQ_STEP_TIMING=1 (diagnostics): the step kernels stamp %globaltimer around their grid barriers
   static unsigned long long* dbgbuf = [] {
     unsigned long long* p = nullptr;
@@ -387,7 +391,17 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
                           : win_rows_vec;
     if (win_bytes <= 0) sa.win_rows = 0;
     sa.upre = (prescale && i >= 1 && i <= S - 2) ? static_cast<const void*>(basis + (i + 1) * vs) : nullptr;
+    sa.w = wv;
     ca.pre_dinv = (prescale && i + 1 <= S - 2) ? g->dinv : nullptr;
+    ca.pre_out = nullptr;
+    if (last_pre && i == S - 2) {   // the last step kernel: dinv (.) u_{S-1} over w
+      ca.pre_dinv = g->dinv;
+      ca.pre_out = wv;
+    }
+    if (last_pre && i == S - 1) {   // the last SpMM gathers it and writes into the slot of u_1
+      sa.upre = wv;
+      sa.w = basis + vs;
+    }
     ca.dbg = (dbgbuf && i < kMaxSteps) ? dbgbuf + kDbgStride * i : nullptr;
     ca.i = i;
     ca.second = 0;
@@ -404,7 +418,7 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
       {
         LaunchScope ls(K_REDUCE, st);
         alpha_dot_kernel<VT><<<dim3(kAlphaCtas, ceil_div(c, kBlk)), 2 * colsb, 0, st>>>(
-            basis + i * vs, s.rsc + i * cpad, wv, n, ldc, c, cpad, partial);
+            basis + i * vs, s.rsc + i * cpad, static_cast<const VT*>(sa.w), n, ldc, c, cpad, partial);
       }
       ReduceArgs rd = ra;
       rd.ntiles = kAlphaCtas;
