@@ -28,6 +28,9 @@ constexpr int kMaxChunk = 256;       // probes per chunk (flat CGS CTAs of <= 51
 // bits[row][kBitWords] with word g = probes 32g..32g+31 (bit set = +1).  A warp = 32 probes of one
 // group over a run of 2*kProbeRun rows.
 constexpr int kBitWords = 4;   // bitmask row stride in 32-bit words (16 B: bulk-copy aligned; c <= 128)
+// Step-0 records of the normalized Laplacian on large graphs: [bits (4 words) | dinv (2 words) | pad],
+// 32 bytes per row, so the first SpMM fetches one sector per nonzero instead of bits + dinv[col]
+constexpr int kRecWords = 8;
 
 template <typename VT>
 __global__ void probe_init_kernel(SeedKey seed, int64_t probe_begin, int c, int64_t n, VT* __restrict__ u,
@@ -78,6 +81,22 @@ static void launch_probes(const SeedKey& seed, int64_t probe_begin, int c, int64
   dim3 grid(ceil_div(runs, 4), ceil_div(c, 32));
   LaunchScope ls(K_PROBE, st);
   probe_init_kernel<VT><<<grid, 128, 0, st>>>(seed, probe_begin, c, n, u, ldc, bits, remap);
+}
+
+// [bits | dinv | pad] records of every row (kRecWords words) for the first normalized-Laplacian SpMM
+static __global__ void step0_records_kernel(const uint32_t* __restrict__ bits, const double* __restrict__ dinv,
+                                            int64_t n, uint32_t* __restrict__ rec) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 b = *reinterpret_cast<const uint4*>(bits + r * kBitWords);
+    const double d = dinv[r];
+    uint4 t;
+    t.x = static_cast<uint32_t>(__double_as_longlong(d));
+    t.y = static_cast<uint32_t>(static_cast<unsigned long long>(__double_as_longlong(d)) >> 32);
+    t.z = 0u;
+    t.w = 0u;
+    reinterpret_cast<uint4*>(rec + r * kRecWords)[0] = b;
+    reinterpret_cast<uint4*>(rec + r * kRecWords)[1] = t;
+  }
 }
 
 template <typename VT>
@@ -273,6 +292,8 @@ struct SpmmArgs {
   double* segpart;
   unsigned long long* work;  // [probe blocks] zeroed work counters of this launch
   const uint32_t* bits;      // first step: u_0 as a probe bitmask [n][kBitWords] (nullptr = use u)
+  const uint32_t* rec = nullptr;   // first step, normalized Laplacian: [n][kRecWords] bits + dinv records
+                                   // for the gathers (bits still serves the own-row values)
   const void* upre;          // normalized Laplacian: dinv (.) u to gather (nullptr = gather u, times dinv[col])
   // L2 persisting window over the gathered vector's first rows (degree-ordered fold: the hub rows);
   // win_rows = 0: no window
@@ -353,8 +374,12 @@ __device__ __forceinline__ void gather_range(const int32_t* __restrict__ cols, c
     if (lane < cnt) {
       const int32_t raw = __ldg(cols + base + lane);
       const int64_t col = raw;
-      myoff = BITS ? col * kBitWords : col * ldi;
-      if (KIND == SLQ_NORMALIZED_LAPLACIAN) mys = __ldg(dinv + col);
+      myoff = col * ldi;   // BITS: ldi is the bitmask row stride (kBitWords, or kRecWords for records)
+      if (KIND == SLQ_NORMALIZED_LAPLACIAN) {
+        // step-0 records [bits | dinv]: dinv comes from the same 32-byte sector as the gathered bits
+        mys = (BITS && ldi == kRecWords) ? __ldg(reinterpret_cast<const double*>(bits + col * kRecWords + kBitWords))
+                                         : __ldg(dinv + col);
+      }
       if (WEIGHTED) myw = __ldg(wts + base + lane);
       if (!EXACT && WEIGHTED) mys *= myw;   // s_c = dinv_c * w (or w)
     }
@@ -670,6 +695,9 @@ spmm_kernel(SpmmArgs a) {
   const int64_t* __restrict__ off = a.offsets;
   const double* __restrict__ dinv = a.dinv;
   const int64_t ldi = a.ldc_in;
+  // gathered bitmask rows: the step-0 records when present (stride kRecWords), else the bitmask
+  const uint32_t* gbits = (BITS && a.rec) ? a.rec : a.bits;
+  const int64_t gld = BITS ? (a.rec ? kRecWords : kBitWords) : ldi;
   const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
   const int64_t nseg = a.long_counts ? a.long_counts[1] : 0;
   unsigned long long* counter = a.work + blockIdx.y;   // [0..1] segments, [2..3] tiles (per probe block)
@@ -687,7 +715,7 @@ spmm_kernel(SpmmArgs a) {
     double acc[PPL];
 #pragma unroll
     for (int j = 0; j < PPL; ++j) acc[j] = 0.0;
-    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg,
+    gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, gld, gbits, pidx, beg,
                                                                 end, acc);
     double* dst = a.segpart + item * a.cpad + pbase;
 #pragma unroll
@@ -712,7 +740,7 @@ spmm_kernel(SpmmArgs a) {
         gather_half2_pipe<VT, KIND == kNLPre ? SLQ_LAPLACIAN : KIND, WEIGHTED, SLQ_HALF2_PIPE>(
             a.cols, dinv, a.weights, ug, ldi, pidx[0], beg, end, acc);
       } else {
-        gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, ldi, a.bits, pidx, beg,
+        gather_range<VT, KIND, WEIGHTED, PPL, BITS, EXACT, HALF, V2>(a.cols, dinv, a.weights, ug, gld, gbits, pidx, beg,
                                                                     end, acc);
       }
       const double d = __ldg(a.degree + row);
@@ -814,8 +842,9 @@ static void spmm_go(const SpmmArgs& a, dim3 grid, cudaStream_t st) {
     spmm_kernel<VT, KIND, W, PPL, BITS, EXACT, HALF, V2><<<grid, kSpmmWarps * 32, 0, st>>>(a);
     return;
   }
-  const void* base = BITS ? static_cast<const void*>(a.bits) : (KIND == kNLPre ? a.upre : a.u);
-  const size_t row_bytes = BITS ? sizeof(uint32_t) * kBitWords : sizeof(VT) * static_cast<size_t>(a.ldc_in);
+  const void* base = BITS ? static_cast<const void*>(a.rec ? a.rec : a.bits) : (KIND == kNLPre ? a.upre : a.u);
+  const size_t row_bytes = BITS ? sizeof(uint32_t) * (a.rec ? kRecWords : kBitWords)
+                                : sizeof(VT) * static_cast<size_t>(a.ldc_in);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kSpmmWarps * 32);

@@ -354,6 +354,11 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   // CTA over rows it has already consumed), and that SpMM, which only feeds alpha_{S-1}, writes its
   // output into the slot of u_1 (no longer needed).  Needs S >= 3 and no basis export.
   const bool last_pre = prescale && S >= 3 && !basis_out;
+  // Step 0 of the normalized Laplacian on large graphs gathers the probe bitmask AND dinv[col]: two
+  // random line requests per nonzero.  32-byte [bits | dinv] records (built into the slot of u_1, free
+  // until the first step kernel writes u_1) make it one; values and arithmetic are unchanged.
+  const bool rec_on = kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && bits != nullptr && S >= 2 &&
+                      ldc * vb >= static_cast<int64_t>(sizeof(uint32_t)) * kRecWords && n >= pre_min_n && pre_env;
   // SLQ_STEP_TIMING=1 (diagnostics): the step kernels stamp %globaltimer around their grid barriers
   static unsigned long long* dbgbuf = [] {
     unsigned long long* p = nullptr;
@@ -387,6 +392,13 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
     sa.red = ra;
     sa.work = s.work + 4 * i;
     sa.bits = (i == 0) ? bits : nullptr;
+    sa.rec = nullptr;
+    if (i == 0 && rec_on) {   // [bits | dinv] records in the (still unused) slot of u_1
+      uint32_t* rec = reinterpret_cast<uint32_t*>(basis + vs);
+      LaunchScope ls(K_PROBE, st);
+      step0_records_kernel<<<std::max(1, std::min(ceil_div(n, 256), 148 * 16)), 256, 0, st>>>(bits, g->dinv, n, rec);
+      sa.rec = rec;
+    }
     sa.win_rows = sa.bits ? std::min<int64_t>(n, win_bytes / static_cast<int64_t>(sizeof(uint32_t) * kBitWords))
                           : win_rows_vec;
     if (win_bytes <= 0) sa.win_rows = 0;
