@@ -576,7 +576,8 @@ class SharedHostCsr:
         n, nnz = dg.n, dg.nnz
         need = (n + 1) * 8 + nnz * 4
         base = tempfile.gettempdir()
-        ok = torch.tensor([1 if shutil.disk_usage(base).free > 1.5 * need else 0])
+        ok = torch.tensor([1 if shutil.disk_usage(base).free > 1.5 * need else 0],
+                          device=dg.device if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)   # every rank takes the same branch
         self.paths = []
         if not int(ok.item()):
