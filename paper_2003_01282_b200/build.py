@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libslq_b200.so")
-SOURCES = ["capi.cu", "graph.cu", "lanczos.cu", "spmm_f32.cu", "spmm_f64.cu", "step_f32_wide.cu", "step_f32_narrow.cu",
+SOURCES = ["capi.cu", "graph.cu", "lanczos.cu", "spmm_f32.cu", "spmm_f64.cu", "spmm_flat.cu", "step_f32_wide.cu", "step_f32_narrow.cu",
            "step_f64_wide.cu", "step_f64_narrow.cu", "rules.cu", "batched.cu", "rmat.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -274,6 +274,10 @@ struct SpmmArgs {
   const double* dinv;
   const int64_t* tile_rows;
   int ntiles;
+  // fine row tiles + sizes for the flat kernel (spmm_flat.cu); ftile_rows = nullptr: not used
+  const int64_t* ftile_rows = nullptr;
+  int nftiles = 0;
+  int64_t n_rows = 0, nnz_total = 0;
   const double* dscal;     // device graph scalars; density scale 1/tr L = dscal[3]
   const void* u;           // [n][ldc] input (unnormalised)
   const double* r;         // [cpad] per-probe scale (nullptr = 1.0)
@@ -299,6 +303,8 @@ struct SpmmArgs {
   // win_rows = 0: no window
   int64_t win_rows = 0;
 };
+
+bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st);   // spmm_flat.cu
 
 // SpMM-internal kind: the normalized Laplacian gathering the PRESCALED vector dinv (.) u (written by
 // the previous step kernel), so no dinv[col] gather per nonzero; the epilogue is the normalized one.
@@ -939,7 +945,9 @@ static void launch_spmm_main(int kind, SpmmArgs& a, int gy, cudaStream_t st) {
 template <typename VT>
 static void launch_spmm(int kind, SpmmArgs a, cudaStream_t st, bool finish = true) {
   const int gy = ceil_div(a.c, kSpmmBlk);
-  launch_spmm_main<VT>(kind, a, gy, st);
+  bool flat = false;
+  if constexpr (std::is_same<VT, float>::value) flat = launch_spmm_flat_f32(kind, a, st);
+  if (!flat) launch_spmm_main<VT>(kind, a, gy, st);
   if (finish && a.long_counts && a.max_long > 0) {
     LaunchScope ls(K_SPMM, st);
     if (kind == SLQ_NORMALIZED_LAPLACIAN) long_finish_dispatch<VT, SLQ_NORMALIZED_LAPLACIAN>(a, gy, st);

@@ -19,6 +19,8 @@ namespace slq {
 constexpr int kMaxTiles = 148 * 256;  // SpMM warp tiles (dynamically scheduled): ~8 per resident warp
 constexpr int kMaxStreamTiles = 148 * 16;
 constexpr int64_t kMinTileCost = 64;
+constexpr int64_t kFlatTileCost = 4096;   // flat SpMM work item (nonzeros + kRowCost per row)
+constexpr int64_t kFlatMinNnz = int64_t(1) << 24;
 constexpr int64_t kRowCost = 2;       // per-row overhead in nonzero-equivalents
 constexpr int64_t kMinStreamRows = 128;
 
@@ -251,11 +253,20 @@ static int graph_build(slq_graph* g, const int64_t* offsets, const int64_t* cols
   const int64_t min_cost = std::min<int64_t>(kMinTileCost, std::max<int64_t>(16, total / (148 * 32)));
   int64_t target = std::max<int64_t>(min_cost, (total + kMaxTiles - 1) / kMaxTiles);
   g->ntiles = std::max(1, ceil_div(total, target));
-  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (g->ntiles + 1), st));
+  // fine tiles for the flat SpMM (spmm_flat.cu): large graphs only (SLQ_SPMM_FLAT=0 off, =1 any graph)
+  static const int flat_env = [] { const char* e = getenv("SLQ_SPMM_FLAT"); return e ? atoi(e) : -1; }();
+  const bool flat = flat_env != 0 && n > 0 && nnz > 0 && (flat_env > 0 || nnz >= kFlatMinNnz);
+  g->nftiles = flat ? std::max(1, ceil_div(total, kFlatTileCost)) : 0;
+  SLQ_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (g->ntiles + 1 + (flat ? g->nftiles + 1 : 0)), st));
   g->tile_rows = static_cast<int64_t*>(track(g, p));
+  g->ftile_rows = flat ? g->tile_rows + g->ntiles + 1 : nullptr;
   {
     LaunchScope ls(K_PREPARE, st);
     tile_kernel<<<ceil_div(g->ntiles + 1, 256), 256, 0, st>>>(g->offsets, n, target, g->ntiles, g->tile_rows);
+  }
+  if (flat) {
+    LaunchScope ls(K_PREPARE, st);
+    tile_kernel<<<ceil_div(g->nftiles + 1, 256), 256, 0, st>>>(g->offsets, n, kFlatTileCost, g->nftiles, g->ftile_rows);
   }
   g->rows_per_stream_tile = std::max<int64_t>(kMinStreamRows, (n + kMaxStreamTiles - 1) / kMaxStreamTiles);
   g->ntiles_stream = std::max(1, ceil_div(n, g->rows_per_stream_tile));

@@ -318,6 +318,7 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   SpmmArgs sa{};
   sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
+  sa.ftile_rows = g->ftile_rows; sa.nftiles = g->nftiles; sa.n_rows = n; sa.nnz_total = g->nnz;
   sa.dscal = g->dscal;
   sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad;
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));

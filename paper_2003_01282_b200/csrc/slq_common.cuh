@@ -94,6 +94,8 @@ struct slq_graph {
   // SpMM tiles: contiguous row ranges with bounded (nnz + row) cost, fixed per graph
   int ntiles = 0;
   int64_t* tile_rows = nullptr;      // [ntiles+1] device
+  int nftiles = 0;                   // fine tiles of the flat SpMM (large graphs; same allocation)
+  int64_t* ftile_rows = nullptr;     // [nftiles+1] device
   // streaming tiles (pass B): contiguous equal row ranges
   int ntiles_stream = 0;
   int64_t rows_per_stream_tile = 0;

@@ -1,0 +1,356 @@
+// Flat SpMM for large degree-ordered graphs, fp32 chunks of 17..32 probes (128-byte rows): the C5
+// gather.
+//
+// The warp-per-row kernel (engine.cuh: spmm_kernel) walks offsets -> columns -> gathers -> epilogue
+// as one dependent chain per row and holds the gathered rows in registers, so a warp keeps ~10 line
+// requests in flight and the DRAM misses run at ~0.6 of the random-line rate the B200 sustains.
+// Here the gathered rows are STAGED IN SHARED MEMORY by cp.async (LDGSTS, 16 bytes per lane): a
+// QUARTER-warp (8 lanes x 16 bytes = one 128-byte row of the vector) owns one CSR row, a warp walks a
+// QUAD of four consecutive rows in lockstep (the degree-ordered fold makes neighbouring rows equally
+// long), and the nonzeros of successive quads are FLATTENED into batches of kFlatU slots per quarter
+// (32 line requests per warp and batch).  A ring of kFlatNB batches per warp keeps kFlatNB - 1 batches
+// in flight whatever the row lengths are, at no register cost.
+//
+//   * work items (atomic counter): quads of long-row segments first, then graph-fixed fine row tiles;
+//   * a batch is kFlatU slots of one quad: slot q of quarter i gathers the vector row of nonzero
+//     j + q of the quarter's row; slots past the row's end are zero-filled by the copy (src-size 0),
+//     so consumption is one unconditional unrolled loop; a batch starts at an even j, so a slot's
+//     chain (even / odd position) is a compile-time choice;
+//   * the quad's last batch also copies the rows' own values, degree and dinv, and its consumption
+//     ends with the operator epilogue and the store (or the store of a segment's partial sums);
+//   * lane `sub` of a quarter loads the column index of the quarter's slot `sub` two batches ahead of
+//     the copies; row ends come from a register block of 32 prefetched offsets;
+//   * loop: wait for the oldest batch (cp.async.wait_group), consume it from shared memory, issue
+//     the newest batch into the buffer freed one iteration ago, generate the batch after that.
+//
+// Arithmetic = the narrow class of gather_range (engine.cuh): a row is summed as two chains (even /
+// odd positions from the row start, ascending), acc = s_even + s_odd, then the same epilogue, so the
+// results are bitwise those of spmm_kernel's HALF2 / full-warp mappings (adding the +0.0 of a
+// zero-filled slot never changes an accumulator, which starts at +0.0 and so is never -0.0).
+#include "engine.cuh"
+
+namespace slq {
+
+#ifndef SLQ_FLAT_NB
+#define SLQ_FLAT_NB 3
+#endif
+#ifndef SLQ_FLAT_WARPS
+#define SLQ_FLAT_WARPS 8
+#endif
+#ifndef SLQ_FLAT_CTAS
+#define SLQ_FLAT_CTAS 2
+#endif
+constexpr int kFlatU = 8;
+constexpr int kFlatNB = SLQ_FLAT_NB;           // batches in the ring (kFlatNB - 1 in flight)
+constexpr int kFlatThreads = 32 * SLQ_FLAT_WARPS;
+constexpr int kFlatCtasPerSm = SLQ_FLAT_CTAS;
+constexpr int kFlatBatchBytes = kFlatU * 4 * 128;   // gathered rows of one batch
+constexpr int kFlatOwnBytes = 4 * 128 + 4 * 16;     // own rows + (degree, dinv) of one batch
+constexpr int kFlatWarpBytes = kFlatNB * (kFlatBatchBytes + kFlatOwnBytes);
+constexpr int kFlatSmem = SLQ_FLAT_WARPS * kFlatWarpBytes;
+
+constexpr int PH_NZ = 0, PH_ITEM = 2, PH_DONE = 3;
+constexpr int kOffBlock = 28;   // rows per offsets block (32 prefetched offsets: a quad needs 5)
+constexpr int GF_OK = 1, GF_LIVE = 2, GF_END = 4, GF_SEG = 8;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel(SpmmArgs a) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr bool NL = nl_kind<KIND>();
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & 7;
+  const int qid = lane >> 3;
+  const int qbase = lane & 24;
+
+  // probes 4 sub .. 4 sub + 3 of the chunk
+  bool pv[4];
+  double rj[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    pv[j] = 4 * sub + j < a.c;
+    rj[j] = pv[j] ? __ldg(a.r + 4 * sub + j) : 1.0;
+  }
+  const bool all4 = pv[3];
+  // 16 bytes of a row per lane; lanes past the row's end (ldc < 32) copy nothing (zero fill)
+  const int lane_bytes = 4 * sub + 3 < a.ldc_in ? 16 : 0;
+  const uint32_t strideb = static_cast<uint32_t>(a.ldc_in) * 4u;   // row stride in bytes
+  const char* __restrict__ ugb =
+      static_cast<const char*>(KIND == kNLPre ? a.upre : a.u) + (lane_bytes ? 16 * sub : 0);   // gathered vector
+  const char* __restrict__ uob = static_cast<const char*>(a.u) + (lane_bytes ? 16 * sub : 0);   // own values
+  extern __shared__ __align__(128) unsigned char flat_smem[];
+  const uint32_t sm_ring = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
+                           (threadIdx.x >> 5) * kFlatWarpBytes + lane * 16;        // + buf * batch + q * 512
+  const uint32_t sm_own = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
+                          (threadIdx.x >> 5) * kFlatWarpBytes + kFlatNB * kFlatBatchBytes;   // + buf * own
+  float* __restrict__ w = static_cast<float*>(a.w) + 4 * sub;
+  const int64_t* __restrict__ off = a.offsets;
+  const int32_t* __restrict__ cols = a.cols;
+  const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
+  const bool has_long = a.long_counts != nullptr;
+  const long long nseg = has_long ? a.long_counts[1] : 0;
+  const long long nsq = (nseg + 3) >> 2;   // segment quads
+  const long long nitems = nsq + a.nftiles;
+  const int64_t nrows = a.n_rows;   // offsets has nrows + 1 entries
+
+  // ---- cursor: warp-uniform control; qpos / dq / rowok are per quarter
+  int phase = PH_ITEM;
+  bool isseg = false;
+  int R = 0, Rend = 0;        // first row (segment) of the current quad, end of the item
+  int obase = 0;
+  int64_t offA = 0, offB = 0;   // off[obase + lane], off[obase + kOffBlock + lane]
+  int64_t qpos = 0;           // first nonzero of this quarter's row (segment)
+  int dq = 0, dmax = 0, dmin = 0, j = 0;
+  bool rowok = false;
+
+  auto load_off = [&](int64_t r) -> int64_t { return __ldg(off + (r < nrows ? r : nrows)); };
+  auto enter_quad = [&]() {
+    if (R >= Rend) { phase = PH_ITEM; return; }
+    if (isseg) {
+      const int sg = R + qid;
+      rowok = sg < Rend;
+      int64_t p0 = 0, p1 = 0;
+      if (rowok) {
+        p0 = a.seg_begin[sg];
+        const int64_t re = __ldg(off + a.seg_row[sg] + 1);
+        p1 = p0 + kSeg < re ? p0 + kSeg : re;
+      }
+      qpos = p0;
+      dq = static_cast<int>(p1 - p0);
+    } else {
+      int idx = R - obase;
+      if (idx >= kOffBlock) {
+        obase += kOffBlock;
+        idx -= kOffBlock;
+        offA = offB;
+        offB = load_off(static_cast<int64_t>(obase) + kOffBlock + lane);
+      }
+      const int64_t p0 = __shfl_sync(FULL, offA, idx + qid);
+      const int64_t p1 = __shfl_sync(FULL, offA, idx + qid + 1);
+      rowok = R + qid < Rend;
+      int64_t d = rowok ? p1 - p0 : 0;
+      if (has_long && d > kLongRow) { rowok = false; d = 0; }   // summed from its segments
+      qpos = p0;
+      dq = static_cast<int>(d);
+    }
+    dmax = __reduce_max_sync(FULL, dq);
+    dmin = __reduce_min_sync(FULL, dq);
+    j = 0;
+    phase = PH_NZ;
+  };
+  auto fetch_item = [&]() {
+    for (;;) {
+      long long item = 0;
+      if (lane == 0) item = static_cast<long long>(atomicAdd(a.work, 1ull));
+      item = __shfl_sync(FULL, item, 0);
+      if (item >= nitems) { phase = PH_DONE; return; }
+      if (item < nsq) {
+        isseg = true;
+        R = static_cast<int>(4 * item);
+        Rend = static_cast<int>(R + 4 < nseg ? R + 4 : nseg);
+      } else {
+        const long long t = item - nsq;
+        const int64_t rb = a.ftile_rows[t], re = a.ftile_rows[t + 1];
+        if (rb >= re) continue;
+        isseg = false;
+        R = static_cast<int>(rb);
+        Rend = static_cast<int>(re);
+        obase = R;
+        offA = load_off(static_cast<int64_t>(obase) + lane);
+        offB = load_off(static_cast<int64_t>(obase) + kOffBlock + lane);
+      }
+      enter_quad();
+      return;
+    }
+  };
+
+  // ---- one batch: nv = this quarter's valid slots, r0 = the quad's first row / segment (uniform),
+  // flags: GF_OK (this quarter has a row), uniform GF_LIVE / GF_END (the quad's last batch) / GF_SEG
+  struct Group { int nv, r0, fl; };
+  auto gen = [&](Group& g, int64_t& mypos) {
+    if (phase == PH_ITEM) fetch_item();
+    mypos = -1;
+    g.nv = 0;
+    g.r0 = R;
+    g.fl = 0;
+    if (phase == PH_DONE) return;
+    const int rem = dq - j;
+    g.nv = rem < 0 ? 0 : (rem > kFlatU ? kFlatU : rem);
+    if (sub < g.nv) mypos = qpos + j + sub;
+    j += kFlatU;
+    g.fl = GF_LIVE | (rowok ? GF_OK : 0) | (isseg ? GF_SEG : 0);
+    if (j >= dmax) {
+      g.fl |= GF_END;
+      R += 4;
+      enter_quad();
+    }
+  };
+
+  // ---- consumer state
+  double ae[4], ao[4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) ae[jj] = ao[jj] = 0.0;
+
+  auto finish_row = [&](int64_t r, const float4& ownv, double d, double dis) {
+    const float own[4] = {ownv.x, ownv.y, ownv.z, ownv.w};
+    float y[4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const double tot = ae[jj] + ao[jj];
+      const double x = __dmul_rn(static_cast<double>(own[jj]), rj[jj]);
+      y[jj] = static_cast<float>(op_epilogue<KIND>(x, __dmul_rn(tot, rj[jj]), d, dis, scale));
+    }
+    float* dst = w + r * a.ldc_out;
+    if (all4) {
+      *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+        if (pv[jj]) dst[jj] = y[jj];
+    }
+  };
+  auto finish_seg = [&](int64_t sg) {
+    double* dst = a.segpart + sg * a.cpad + 4 * sub;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (pv[jj]) dst[jj] = ae[jj] + ao[jj];
+  };
+  auto consume = [&](const Group& g, int buf) {
+    if (!(g.fl & GF_LIVE)) return;
+    const uint32_t base = sm_ring + buf * kFlatBatchBytes;
+#pragma unroll
+    for (int q = 0; q < kFlatU; ++q) {
+      const float4 x = lds128(base + q * 512);
+      if (q & 1) {
+        ao[0] += static_cast<double>(x.x); ao[1] += static_cast<double>(x.y);
+        ao[2] += static_cast<double>(x.z); ao[3] += static_cast<double>(x.w);
+      } else {
+        ae[0] += static_cast<double>(x.x); ae[1] += static_cast<double>(x.y);
+        ae[2] += static_cast<double>(x.z); ae[3] += static_cast<double>(x.w);
+      }
+    }
+    if (g.fl & GF_END) {
+      if (g.fl & GF_OK) {
+        if (g.fl & GF_SEG) {
+          finish_seg(static_cast<int64_t>(g.r0) + qid);
+        } else {
+          const uint32_t ob = sm_own + buf * kFlatOwnBytes;
+          const float4 ownv = lds128(ob + lane * 16);
+          const double d = lds64(ob + 512 + qid * 16);
+          const double dis = NL ? lds64(ob + 512 + qid * 16 + 8) : 0.0;
+          finish_row(static_cast<int64_t>(g.r0) + qid, ownv, d, dis);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) ae[jj] = ao[jj] = 0.0;
+    }
+  };
+  auto issue = [&](const Group& g, int32_t col, int buf) {
+    if (g.fl & GF_LIVE) {
+      const uint32_t base = sm_ring + buf * kFlatBatchBytes;
+#pragma unroll
+      for (int q = 0; q < kFlatU; ++q) {
+        const uint32_t c = static_cast<uint32_t>(__shfl_sync(FULL, col, qbase | q));
+        cp_async16(base + q * 512, ugb + static_cast<uint64_t>(c) * strideb, q < g.nv ? lane_bytes : 0);
+      }
+      if ((g.fl & (GF_END | GF_SEG | GF_OK)) == (GF_END | GF_OK)) {
+        const int64_t r = static_cast<int64_t>(g.r0) + qid;
+        const uint32_t ob = sm_own + buf * kFlatOwnBytes;
+        cp_async16(ob + lane * 16, uob + static_cast<uint64_t>(r) * strideb, lane_bytes);
+        if (sub == 0) cp_async8(ob + 512 + qid * 16, a.degree + r);
+        if (NL && sub == 1) cp_async8(ob + 512 + qid * 16 + 8, a.dinv + r);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // g0: consumed this iteration; g1 .. g[NB-2]: in flight; gi: issued this iteration; gp: generated,
+  // its column indices loading
+  static_assert(kFlatNB == 3 || kFlatNB == 4, "ring depth");
+  Group dead{0, 0, 0};
+  Group g0 = dead, g1 = dead, g2 = dead, gi, gp;
+  int64_t mypos;
+  gen(gi, mypos);
+  int32_t col_i = mypos >= 0 ? __ldg(cols + mypos) : 0;
+  gen(gp, mypos);
+  int32_t col_p = mypos >= 0 ? __ldg(cols + mypos) : 0;
+  int ibuf = 0;   // buffer of the batch issued this iteration; the consumed one is ibuf + 1 (mod NB)
+
+  while ((g0.fl | g1.fl | g2.fl | gi.fl | gp.fl) & GF_LIVE) {
+    cp_async_wait<kFlatNB - 2>();
+    __syncwarp();
+    const int cbuf = ibuf + 1 == kFlatNB ? 0 : ibuf + 1;
+    consume(g0, cbuf);
+    issue(gi, col_i, ibuf);
+    ibuf = cbuf;
+    g0 = g1;
+    if (kFlatNB == 4) { g1 = g2; g2 = gi; } else { g1 = gi; }
+    gi = gp;
+    col_i = col_p;
+    gen(gp, mypos);
+    col_p = mypos >= 0 ? __ldg(cols + mypos) : 0;
+  }
+}
+
+template <int KIND>
+static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
+  const dim3 grid(148 * kFlatCtasPerSm);
+  static std::atomic<bool> attr[64];
+  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<KIND>), kFlatSmem, attr)) return false;
+  if (a.win_rows <= 0) {
+    spmm_flat_kernel<KIND><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
+    return true;
+  }
+  const void* base = KIND == kNLPre ? a.upre : a.u;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kFlatThreads);
+  cfg.dynamicSmemBytes = kFlatSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  at[0].val.accessPolicyWindow.num_bytes = sizeof(float) * static_cast<size_t>(a.ldc_in) * static_cast<size_t>(a.win_rows);
+  at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<KIND>, a);
+  l2_demote(base, at[0].val.accessPolicyWindow.num_bytes, st);
+  return true;
+}
+
+// True when the flat kernel took the launch (fp32 rows of 17..32 probes, unit weights, a gathered
+// vector, the Lanczos path, a graph with fine tiles); the caller falls back to spmm_kernel otherwise.
+bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st) {
+  if (!a.ftile_rows || a.nftiles <= 0 || a.weights || a.bits || !a.r) return false;
+  if (a.ldc_in <= 16 || a.ldc_in > 32 || a.ldc_out > 32 || a.c > 32 || (a.ldc_in & 3) || (a.ldc_out & 3)) return false;
+  if (a.n_rows >= (int64_t(1) << 29) || a.max_seg >= (int64_t(1) << 29)) return false;
+  if (kind == SLQ_NORMALIZED_LAPLACIAN && !a.upre) return false;   // dinv[col] per nonzero: spmm_kernel
+  LaunchScope ls(K_SPMM, st);
+  if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<kNLPre>(a, st);
+  if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY>(a, st);
+  return flat_go<SLQ_LAPLACIAN>(a, st);
+}
+
+}  // namespace slq
