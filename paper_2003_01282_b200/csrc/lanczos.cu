@@ -318,7 +318,11 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   SpmmArgs sa{};
   sa.offsets = g->offsets; sa.cols = g->cols; sa.weights = g->weights; sa.degree = g->degree; sa.dinv = g->dinv;
   sa.tile_rows = g->tile_rows; sa.ntiles = g->ntiles;
-  sa.ftile_rows = g->ftile_rows; sa.nftiles = g->nftiles; sa.n_rows = n; sa.nnz_total = g->nnz;
+  // flat SpMM (spmm_flat.cu): walks quads of neighbouring rows in lockstep, so it needs the
+  // degree-ordered fold (SLQ_SPMM_FLAT=1 forces it on any graph: same results, wasted slots)
+  static const bool flat_forced = [] { const char* e = getenv("SLQ_SPMM_FLAT"); return e && atoi(e) > 0; }();
+  if (g->ftile_rows && (g->degree_ordered || flat_forced)) { sa.ftile_rows = g->ftile_rows; sa.nftiles = g->nftiles; }
+  sa.n_rows = n; sa.nnz_total = g->nnz;
   sa.dscal = g->dscal;
   sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad;
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));

@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   const char* __restrict__ ugb =
       static_cast<const char*>(KIND == kNLPre ? a.upre : a.u) + (lane_bytes ? 16 * sub : 0);   // gathered vector
   const char* __restrict__ uob = static_cast<const char*>(a.u) + (lane_bytes ? 16 * sub : 0);   // own values
+  // keep the per-lane base pointers whole, so a gather address is one IMAD.WIDE (col * stride + base)
+  asm volatile("" : "+l"(ugb));
+  asm volatile("" : "+l"(uob));
   extern __shared__ __align__(128) unsigned char flat_smem[];
   const uint32_t sm_ring = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
                            (threadIdx.x >> 5) * kFlatWarpBytes + lane * 16;        // + buf * batch + q * 512
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     }
   };
 
-  // ---- one batch: nv = this quarter's valid slots, r0 = the quad's first row / segment (uniform),
+  // ---- one batch: nv = bit mask of the slots this lane copies, r0 = the quad's first row / segment (uniform),
   // flags: GF_OK (this quarter has a row), uniform GF_LIVE / GF_END (the quad's last batch) / GF_SEG
   struct Group { int nv, r0, fl; };
   auto gen = [&](Group& g, int64_t& mypos) {
@@ -194,8 +197,9 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     g.fl = 0;
     if (phase == PH_DONE) return;
     const int rem = dq - j;
-    g.nv = rem < 0 ? 0 : (rem > kFlatU ? kFlatU : rem);
-    if (sub < g.nv) mypos = qpos + j + sub;
+    const int nv = rem < 0 ? 0 : (rem > kFlatU ? kFlatU : rem);
+    if (sub < nv) mypos = qpos + j + sub;
+    g.nv = lane_bytes ? (1 << nv) - 1 : 0;   // slots this lane copies (the others are zero-filled)
     j += kFlatU;
     g.fl = GF_LIVE | (rowok ? GF_OK : 0) | (isseg ? GF_SEG : 0);
     if (j >= dmax) {
@@ -235,7 +239,6 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
       if (pv[jj]) dst[jj] = ae[jj] + ao[jj];
   };
   auto consume = [&](const Group& g, int buf) {
-    if (!(g.fl & GF_LIVE)) return;
     const uint32_t base = sm_ring + buf * kFlatBatchBytes;
 #pragma unroll
     for (int q = 0; q < kFlatU; ++q) {
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
 #pragma unroll
       for (int q = 0; q < kFlatU; ++q) {
         const uint32_t c = static_cast<uint32_t>(__shfl_sync(FULL, col, qbase | q));
-        cp_async16(base + q * 512, ugb + static_cast<uint64_t>(c) * strideb, q < g.nv ? lane_bytes : 0);
+        cp_async16(base + q * 512, ugb + static_cast<uint64_t>(c) * strideb, ((g.nv >> q) & 1) ? 16 : 0);
       }
       if ((g.fl & (GF_END | GF_SEG | GF_OK)) == (GF_END | GF_OK)) {
         const int64_t r = static_cast<int64_t>(g.r0) + qid;
@@ -283,32 +286,44 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     cp_async_commit();
   };
 
-  // g0: consumed this iteration; g1 .. g[NB-2]: in flight; gi: issued this iteration; gp: generated,
-  // its column indices loading
+  // g0: consumed this iteration; g1 (g2): in flight; gi: issued this iteration; gp: generated, its
+  // column indices loading.  Live batches are contiguous: once a dead batch is generated (no items
+  // left) every later one is dead, so the loop runs while the batch to consume is live.
   static_assert(kFlatNB == 3 || kFlatNB == 4, "ring depth");
-  Group dead{0, 0, 0};
-  Group g0 = dead, g1 = dead, g2 = dead, gi, gp;
+  Group g0, g1, g2, gi, gp;
   int64_t mypos;
-  gen(gi, mypos);
-  int32_t col_i = mypos >= 0 ? __ldg(cols + mypos) : 0;
-  gen(gp, mypos);
-  int32_t col_p = mypos >= 0 ? __ldg(cols + mypos) : 0;
-  int ibuf = 0;   // buffer of the batch issued this iteration; the consumed one is ibuf + 1 (mod NB)
-
-  while ((g0.fl | g1.fl | g2.fl | gi.fl | gp.fl) & GF_LIVE) {
+  int32_t col_i, col_p;
+  auto next = [&](Group& g, int32_t& col) {
+    gen(g, mypos);
+    col = mypos >= 0 ? __ldg(cols + mypos) : 0;
+  };
+  // prologue: issue the first NB - 1 batches
+  next(g0, col_i);
+  issue(g0, col_i, 0);
+  next(g1, col_i);
+  issue(g1, col_i, 1);
+  if (kFlatNB == 4) {
+    next(g2, col_i);
+    issue(g2, col_i, 2);
+  }
+  next(gi, col_i);
+  next(gp, col_p);
+  int cbuf = 0;            // buffer of the batch consumed this iteration
+  int ibuf = kFlatNB - 1;  // buffer of the batch issued this iteration (consumed one iteration ago)
+  while (g0.fl & GF_LIVE) {
     cp_async_wait<kFlatNB - 2>();
     __syncwarp();
-    const int cbuf = ibuf + 1 == kFlatNB ? 0 : ibuf + 1;
     consume(g0, cbuf);
     issue(gi, col_i, ibuf);
     ibuf = cbuf;
+    cbuf = cbuf + 1 == kFlatNB ? 0 : cbuf + 1;
     g0 = g1;
     if (kFlatNB == 4) { g1 = g2; g2 = gi; } else { g1 = gi; }
     gi = gp;
     col_i = col_p;
-    gen(gp, mypos);
-    col_p = mypos >= 0 ? __ldg(cols + mypos) : 0;
+    next(gp, col_p);
   }
+  cp_async_wait<0>();
 }
 
 template <int KIND>
