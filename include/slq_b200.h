@@ -221,6 +221,19 @@ int slq_rules_seeded(const slq_graph* g, int kind, const slq_seed* seed, int64_t
                      int steps, int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out,
                      int32_t* status, void* stream);
 
+/* Heat/wave + VNGE of one signature share their probes (slq.py:63-72: same seed, same stream): the
+ * normalized-Laplacian rules (netlsd_slq, descriptors.py:124-149) AND the density-matrix rules
+ * (vnge_slq, descriptors.py:227-243) of probes [probe_begin, +count) in one call.  With 9..16 fp32
+ * probes on a large folded graph (a rank's share of 128 probes on 8 GPUs) both Lanczos runs travel
+ * in ONE block of 32 interleaved columns, so each step gathers one 128-byte row per nonzero for both
+ * operators (half the passes over the graph); per-probe results are bitwise those of two
+ * slq_rules_seeded calls.  Otherwise it is those two calls.  *paired (host, may be NULL) = 1 when
+ * the fused block ran. */
+int slq_rules_pair_seeded(const slq_graph* g, const slq_seed* seed, int64_t probe_begin, int64_t count, int steps,
+                          int reorth, int dtype, double* nodes_nl, double* weights_nl, int32_t* steps_nl,
+                          double* nodes_p, double* weights_p, int32_t* steps_p, int32_t* status, int32_t* paired,
+                          void* stream);
+
 /* Synchronous host-buffer form of slq_rules_seeded for FFI bindings that have no device allocator
  * (the reference's ctypes stub): the seam _collect_rules (slq.py:80-86) in one call.
  * nodes_host/weights_host [count][s'], steps_host [count], s' = min(steps, n); the device status is

@@ -98,6 +98,7 @@ _SIGS = {
     "slq_graph_second_passes": (_int, [_vp, ctypes.POINTER(_i64)]),
     "slq_lanczos_seeded": (_int, [_vp, _int, _SP, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "slq_rules_seeded": (_int, [_vp, _int, _SP, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "slq_rules_pair_seeded": (_int, [_vp, _SP, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "slq_rules_host": (_int, [_vp, _int, _SP, _i64, _i64, _int, _int, _int, _vp, _vp, _vp]),
     "slq_probes_seeded": (_int, [_SP, _i64, _i64, _i64, _vp, _i64, _vp]),
     "slq_probe_state_seeded": (_int, [_SP, _u64, ctypes.POINTER(_u64)]),

@@ -162,7 +162,12 @@ struct ReduceArgs {
   int kind;                // operator kind: breakdown tolerance 1e-12 * interval_hi (lanczos.py:36,110)
   const double* dscal;     // device graph scalars (Laplacian interval_hi = dscal[4])
   ChunkState s;
+  // operator-pair chunk (slq_rules_pair): columns >= split belong to kind2 (same probes, second
+  // operator); split >= c: a plain chunk
+  int kind2 = -1;
+  int split = 1 << 30;
 };
+__host__ __device__ __forceinline__ int kind_of_column(const ReduceArgs& a, int p) { return p < a.split ? a.kind : a.kind2; }
 
 constexpr int kReduceWarps = 16;
 constexpr int kStripes = 16;   // fixed partition of the partial rows: the sum order never depends on
@@ -196,7 +201,8 @@ static __device__ void apply_reduced(const ReduceArgs& a, int q, int p, double t
         if (!a.s.again[p]) break;
         a.s.again[p] = 0;
       }
-      const double hi = a.kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (a.kind == SLQ_DENSITY ? 1.0 : a.dscal[4]);
+      const int kd = kind_of_column(a, p);
+      const double hi = kd == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (kd == SLQ_DENSITY ? 1.0 : a.dscal[4]);
       if (b <= 1e-12 * hi) {                             // lanczos.py:133-134
         a.s.steps[p] = a.i + 1;
         a.s.alive[p] = 0;
@@ -302,6 +308,8 @@ struct SpmmArgs {
   // L2 persisting window over the gathered vector's first rows (degree-ordered fold: the hub rows);
   // win_rows = 0: no window
   int64_t win_rows = 0;
+  // operator-pair chunk: columns >= split use the density epilogue (and plain gathers); flat kernel only
+  int split = 1 << 30;
 };
 
 bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st);   // spmm_flat.cu
@@ -793,7 +801,8 @@ spmm_long_finish_kernel(SpmmArgs a) {
         const double own = a.bits ? (((a.bits[row * kBitWords + (p >> 5)] >> (p & 31)) & 1u) ? 1.0 : -1.0)
                                   : ldg_f64(u + row * a.ldc_in + 32 * j);
         const double x = __dmul_rn(own, rj);
-        const double y = op_epilogue<KIND>(x, acc, d, dis, scale);
+        const double y = p < a.split ? op_epilogue<KIND>(x, acc, d, dis, a.dscal[3])
+                                     : op_epilogue<SLQ_DENSITY>(x, acc, d, dis, a.dscal[3]);
         w[row * a.ldc_out + 32 * j] = from_f64<VT>(y);
       }
     }
@@ -979,6 +988,7 @@ struct CgsArgs {
   const double* pre_dinv = nullptr;
   void* pre_out = nullptr;         // where dinv (.) u_{i+1} goes (nullptr: the slot of u_{i+2}); the last
                                    // step kernel writes it over w, which the last SpMM no longer needs
+  int pre_split = 1 << 30;         // operator-pair chunk: columns >= pre_split are copied unscaled
   unsigned long long* dbg = nullptr;   // SLQ_STEP_TIMING: %globaltimer of CTA 0 around each grid barrier
 };
 
@@ -1599,7 +1609,7 @@ __device__ __forceinline__ void phase_update(const StagedArgs& sa, StageRing<VT>
     const double* sdinv = stage_dinv<VT>(stage, sa.nvec, rt, vstride);
     auto load_row = [&](int rr, T& src, T& ui, T& uim1, T* uk, double& dv) {
       const VT* e = stage + pr + rr * ldc;
-      dv = out_pre ? sdinv[(r0 & 1) + rr] : 0.0;   // staged dinv window
+      dv = out_pre ? (p < a.pre_split ? sdinv[(r0 & 1) + rr] : 1.0) : 0.0;   // staged dinv window
       const uint32_t* brow = sbits + rr * kBitWords;
       const bool virt = r0 + rr == a.virt_row;
       src = static_cast<T>(e[0]);
@@ -1731,8 +1741,8 @@ __device__ __forceinline__ void update_pass(const StepArgs& sa, const StagedArgs
       continue;
     }
     if (SECOND) S.again[p] = 0;
-    const double hi_int = sa.red.kind == SLQ_NORMALIZED_LAPLACIAN ? 2.0
-                          : (sa.red.kind == SLQ_DENSITY ? 1.0 : sa.red.dscal[4]);   // interval_hi
+    const int kd = kind_of_column(sa.red, p);
+    const double hi_int = kd == SLQ_NORMALIZED_LAPLACIAN ? 2.0 : (kd == SLQ_DENSITY ? 1.0 : sa.red.dscal[4]);   // interval_hi
     if (b <= 1e-12 * hi_int) {
       S.steps[p] = a.i + 1;
       S.alive[p] = 0;
@@ -1821,8 +1831,9 @@ cgs_step_kernel(StepArgs sa) {
                                    : to_f64(uu[row * sp.ldc_in + p]);
         const double x = __dmul_rn(own, sp.r[p]);
         double y;
-        if (sa.red.kind == SLQ_NORMALIZED_LAPLACIAN) y = op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, acc, d, dis, scale);
-        else if (sa.red.kind == SLQ_DENSITY) y = op_epilogue<SLQ_DENSITY>(x, acc, d, dis, scale);
+        const int kd = kind_of_column(sa.red, p);
+        if (kd == SLQ_NORMALIZED_LAPLACIAN) y = op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, acc, d, dis, scale);
+        else if (kd == SLQ_DENSITY) y = op_epilogue<SLQ_DENSITY>(x, acc, d, dis, scale);
         else y = op_epilogue<SLQ_LAPLACIAN>(x, acc, d, dis, scale);
         ww[row * sp.ldc_out + p] = from_f64<VT>(y);
       }

@@ -225,6 +225,23 @@ static int64_t l2_window_bytes(const slq_graph* g) {
 // The recurrence runs on `g`; with an isolated-vertex fold, g is the folded graph and `orig` the
 // graph the probes and the start-vector norm belong to (probe stream positions are original vertex
 // ids, remapped to folded rows; the trailing row carries sqrt(m)).
+// Operator-pair chunk: duplicate the probe bits of columns [0, split) into columns [split, 2 split)
+// (word 0 of every bitmask row; 2 split <= 32).
+static __global__ void pair_bits_kernel(uint32_t* __restrict__ bits, int64_t n, int split) {
+  const uint32_t mask = (1u << split) - 1u;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = bits[r * kBitWords] & mask;
+    bits[r * kBitWords] = w | (w << split);
+  }
+}
+
+// set when run_chunk refuses an operator-pair chunk (the caller then runs the two operators apart)
+static thread_local bool tl_pair_refused = false;
+static int pair_fail(const char* msg) {
+  tl_pair_refused = true;
+  return fail(SLQ_ERR_VALUE, msg);
+}
+
 struct FoldRun {
   const slq_graph* orig = nullptr;   // nullptr: no fold
 };
@@ -232,7 +249,12 @@ struct FoldRun {
 template <typename VT>
 static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t probe0, const double* q0, int64_t ldq,
                      int c, int S, int reorth, double* alpha_out, double* beta_out, int32_t* steps_out, int64_t col0,
-                     cudaStream_t st, FoldRun fold = FoldRun{}, double* basis_out = nullptr, int64_t basis_ld = 0) {
+                     cudaStream_t st, FoldRun fold = FoldRun{}, double* basis_out = nullptr, int64_t basis_ld = 0,
+                     int kind2 = -1, int split = 0) {
+  // kind2 >= 0: an operator-PAIR chunk -- columns [0, split) run `kind` on probes probe0 .. probe0 +
+  // split - 1, columns [split, c) run `kind2` on the SAME probes (column split + j = probe probe0 + j);
+  // the flat SpMM serves both runs with one gather per nonzero (slq_rules_pair)
+  const bool pair = kind2 >= 0;
   const double t_host0 = host_ms();
   const int64_t n = g->n;
   const int64_t n_probe = fold.orig ? fold.orig->n : n;   // probe length: ||v||^2 = n (slq.py:73)
@@ -309,10 +331,15 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
     copy_start_kernel<VT><<<std::max(1, std::min(ceil_div(n * c, 256), 148 * 16)), 256, 0, st>>>(q0, ldq, c, n, basis, ldc);
   } else if (fold.orig) {
     if (!all_staged) return fail(SLQ_ERR_VALUE, "isolated-vertex fold needs the all-staged schedule");
-    launch_probes<VT>(seed, probe0, c, n_probe, nullptr, ldc, st, bits, fold.orig->fold_remap);
+    launch_probes<VT>(seed, probe0, pair ? split : c, n_probe, nullptr, ldc, st, bits, fold.orig->fold_remap);
     SLQ_CUDA(cudaMemsetAsync(bits + (n - 1) * kBitWords, 0xff, sizeof(uint32_t) * kBitWords, st));
   } else {
-    launch_probes<VT>(seed, probe0, c, n, all_staged ? nullptr : basis, ldc, st, bits);
+    if (pair && !all_staged) return pair_fail("operator-pair chunk needs the all-staged schedule");
+    launch_probes<VT>(seed, probe0, pair ? split : c, n, all_staged ? nullptr : basis, ldc, st, bits);
+  }
+  if (pair) {   // the second operator's columns carry the same probes
+    LaunchScope ls(K_PROBE, st);
+    pair_bits_kernel<<<std::max(1, std::min(ceil_div(n, 256), 148 * 16)), 256, 0, st>>>(bits, n, split);
   }
 
   SpmmArgs sa{};
@@ -323,6 +350,12 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   static const bool flat_forced = [] { const char* e = getenv("SLQ_SPMM_FLAT"); return e && atoi(e) > 0; }();
   if (g->ftile_rows && (g->degree_ordered || flat_forced)) { sa.ftile_rows = g->ftile_rows; sa.nftiles = g->nftiles; }
   sa.n_rows = n; sa.nnz_total = g->nnz;
+  if (pair) {
+    sa.split = split;
+    if (!sa.ftile_rows || !std::is_same<VT, float>::value || ldc <= 16 || ldc > 32 || (split & 3) || g->weights ||
+        !all_staged || c != 2 * split || n >= (int64_t(1) << 29) || g->max_seg >= (int64_t(1) << 29))
+      return pair_fail("operator-pair chunk needs the flat SpMM (fp32, 17..32 columns, unit weights, staged steps)");
+  }
   sa.dscal = g->dscal;
   sa.w = wv; sa.ldc_in = ldc; sa.ldc_out = ldc; sa.c = c; sa.cpad = cpad;
   set_long_rows(sa, g, reinterpret_cast<double*>(ws + off_seg));
@@ -343,6 +376,7 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
 
   ReduceArgs ra{};
   ra.partial = partial; ra.cpad = cpad; ra.c = c; ra.s = s; ra.kind = kind; ra.dscal = g->dscal; ra.reorth = reorth;
+  if (pair) { ra.kind2 = kind2; ra.split = split; ca.pre_split = split; }
 
   // Prescaled gathers (normalized Laplacian, narrow class, graphs whose dinv does not stay in L2):
   // step kernel i also writes dinv (.) u_{i+1} into the slot of u_{i+2} (unused until step kernel i+1),
@@ -362,8 +396,11 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   // Step 0 of the normalized Laplacian on large graphs gathers the probe bitmask AND dinv[col]: two
   // random line requests per nonzero.  32-byte [bits | dinv] records (built into the slot of u_1, free
   // until the first step kernel writes u_1) make it one; values and arithmetic are unchanged.
+  if (pair && !(prescale && last_pre && kind == SLQ_NORMALIZED_LAPLACIAN && kind2 == SLQ_DENSITY))
+    return pair_fail("operator-pair chunk needs prescaled normalized-Laplacian gathers + density");
   const bool rec_on = kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && bits != nullptr && S >= 2 &&
                       ldc * vb >= static_cast<int64_t>(sizeof(uint32_t)) * kRecWords && n >= pre_min_n && pre_env;
+  if (pair && !rec_on) return pair_fail("operator-pair chunk needs the first-step records");
   // SLQ_STEP_TIMING=1 (diagnostics): the step kernels stamp %globaltimer around their grid barriers
   static unsigned long long* dbgbuf = [] {
     unsigned long long* p = nullptr;
@@ -682,6 +719,65 @@ int lanczos_seeded_key(const slq_graph* g, int kind, const SeedKey& seed, int64_
                        int steps, int reorth, int dtype, double* alpha, double* beta, int32_t* steps_out, void* stream) {
   return lanczos_entry(g, kind, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha, beta, steps_out,
                        stream);
+}
+
+// Normalized Laplacian + density matrix on the SAME probes (heat/wave + VNGE of one signature).  With
+// <= 16 probes (a rank's share of 128 probes on 8 GPUs) a single operator fills only half of a
+// 128-byte gathered row, and the SpMM is bound by line requests, not bytes: the pair chunk interleaves
+// both operators' columns in one row, so ONE pass over the graph per Lanczos step serves both runs.
+// Per-probe arithmetic is that of the separate narrow-class runs (bitwise).  *paired = 1 when the pair
+// chunk ran; otherwise (count > 16, fp64, small or unfolded graphs ...) the operators run apart.
+int lanczos_pair_key(const slq_graph* g, const SeedKey& seed, int64_t probe_begin, int64_t count, int steps, int reorth,
+                     int dtype, double* alpha_a, double* beta_a, int32_t* steps_a, double* alpha_b, double* beta_b,
+                     int32_t* steps_b, void* stream, int* paired) {
+  if (paired) *paired = 0;
+  if (!g) return fail(SLQ_ERR_VALUE, "NULL graph");
+  static const bool pair_env = [] { const char* e = getenv("SLQ_PAIR"); return !(e && e[0] == '0'); }();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int S = static_cast<int>(std::min<int64_t>(steps, std::max<int64_t>(g->n, 1)));
+  const int ro = reorth < 0 ? (S <= 100 ? 1 : 0) : reorth;
+  const int split = static_cast<int>((count + 3) / 4 * 4);
+  if (pair_env && dtype == SLQ_F32 && count >= 9 && count <= 16 && steps >= 3 && probe_begin >= 0 && g->n > 0 &&
+      g->nnz > 0 && S >= 3 && S <= kMaxStepsLong && lean_schedule(g, false, S, ro)) {
+    ensure_pool(g->device);
+    FoldRun fold;
+    const slq_graph* gr = g;
+    if (g->folded) {
+      fold.orig = g;
+      gr = g->folded;
+    }
+    char* tmp = nullptr;
+    const size_t bn = sizeof(double) * 2 * split * S;
+    SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), 2 * bn + sizeof(int32_t) * 2 * split + 16, st));
+    double* ta = reinterpret_cast<double*>(tmp);
+    double* tb = ta + 2 * split * S;
+    int32_t* ts = reinterpret_cast<int32_t*>(tmp + 2 * bn);
+    tl_pair_refused = false;
+    int rc = run_chunk<float>(gr, SLQ_NORMALIZED_LAPLACIAN, seed, probe_begin, nullptr, 0, 2 * split, S, ro, ta, tb, ts, 0,
+                              st, fold, nullptr, 0, SLQ_DENSITY, split);
+    if (rc == SLQ_OK) {
+      const size_t row = sizeof(double) * S;
+      cudaMemcpyAsync(alpha_a, ta, row * count, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(beta_a, tb, row * count, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(steps_a, ts, sizeof(int32_t) * count, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(alpha_b, ta + static_cast<int64_t>(split) * S, row * count, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(beta_b, tb + static_cast<int64_t>(split) * S, row * count, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(steps_b, ts + split, sizeof(int32_t) * count, cudaMemcpyDeviceToDevice, st);
+    }
+    cudaFreeAsync(tmp, st);
+    if (rc == SLQ_OK) {
+      SLQ_CUDA(cudaGetLastError());
+      if (paired) *paired = 1;
+      return SLQ_OK;
+    }
+    if (!tl_pair_refused) return rc;
+    set_error("");   // refused: run the operators apart
+  }
+  int rc = lanczos_entry(g, SLQ_NORMALIZED_LAPLACIAN, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha_a,
+                         beta_a, steps_a, stream);
+  if (rc) return rc;
+  return lanczos_entry(g, SLQ_DENSITY, seed, probe_begin, nullptr, 0, count, steps, reorth, dtype, alpha_b, beta_b,
+                       steps_b, stream);
 }
 
 // Return the memory the library's stream-ordered pool keeps cached on the current device to the

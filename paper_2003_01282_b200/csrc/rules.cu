@@ -350,6 +350,50 @@ static int rules_entry(const slq_graph* g, int kind, const SeedKey& seed, int64_
   return SLQ_OK;
 }
 
+int lanczos_pair_key(const slq_graph* g, const SeedKey& seed, int64_t probe_begin, int64_t count, int steps, int reorth,
+                     int dtype, double* alpha_a, double* beta_a, int32_t* steps_a, double* alpha_b, double* beta_b,
+                     int32_t* steps_b, void* stream, int* paired);
+
+extern "C" int slq_rules_pair_seeded(const slq_graph* g, const slq_seed* seed, int64_t probe_begin, int64_t count,
+                                     int steps, int reorth, int dtype, double* nodes_nl, double* weights_nl,
+                                     int32_t* steps_nl, double* nodes_p, double* weights_p, int32_t* steps_p,
+                                     int32_t* status, int32_t* paired, void* stream) {
+  if (!g || !status) return fail(SLQ_ERR_VALUE, "NULL argument");
+  SeedKey k;
+  if (!seed_key_of(seed, &k)) return fail(SLQ_ERR_VALUE, "seed must have 1..8 entropy words");
+  if (steps < 1) return fail(SLQ_ERR_VALUE, "step budget must be >= 1");
+  if (count < 0 || probe_begin < 0) return fail(SLQ_ERR_VALUE, "negative probe range");
+  if (g->nnz == 0) return fail(SLQ_ERR_VALUE, "density matrix undefined for a graph without edges");
+  if (paired) *paired = 0;
+  if (count == 0) return SLQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int S = static_cast<int>(std::min<int64_t>(steps, std::max<int64_t>(g->n, 1)));
+  if (g->n <= small_graph_max_n()) {   // small graphs: the batched kernel, one operator at a time
+    int rc = rules_entry(g, SLQ_NORMALIZED_LAPLACIAN, k, probe_begin, count, steps, reorth, dtype, nodes_nl, weights_nl,
+                         steps_nl, status, stream);
+    if (rc) return rc;
+    return rules_entry(g, SLQ_DENSITY, k, probe_begin, count, steps, reorth, dtype, nodes_p, weights_p, steps_p, status,
+                       stream);
+  }
+  double* ab = nullptr;
+  const int64_t cs = count * S;
+  SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ab), sizeof(double) * 4 * cs, st));
+  int used = 0;
+  int rc = lanczos_pair_key(g, k, probe_begin, count, steps, reorth, dtype, ab, ab + cs, steps_nl, ab + 2 * cs, ab + 3 * cs,
+                            steps_p, stream, &used);
+  if (rc == SLQ_OK)
+    rc = launch_gauss_rules(ab, ab + cs, steps_nl, count, S, 0.0, 0.0, nodes_nl, weights_nl, nullptr, status, g->dscal,
+                            SLQ_NORMALIZED_LAPLACIAN, g->dflags, st);
+  if (rc == SLQ_OK)
+    rc = launch_gauss_rules(ab + 2 * cs, ab + 3 * cs, steps_p, count, S, 0.0, 0.0, nodes_p, weights_p, nullptr, status,
+                            g->dscal, SLQ_DENSITY, g->dflags, st);
+  cudaFreeAsync(ab, st);
+  if (rc) return rc;
+  if (paired) *paired = used;
+  SLQ_CUDA(cudaGetLastError());
+  return SLQ_OK;
+}
+
 extern "C" int slq_rules(const slq_graph* g, int kind, uint64_t seed, int64_t probe_begin, int64_t count, int steps,
                          int reorth, int dtype, double* nodes, double* weights, int32_t* steps_out, int32_t* status,
                          void* stream) {

@@ -40,6 +40,9 @@ namespace slq {
 #ifndef SLQ_FLAT_CTAS
 #define SLQ_FLAT_CTAS 2
 #endif
+#ifndef SLQ_FLAT_MIX
+#define SLQ_FLAT_MIX 0
+#endif
 constexpr int kFlatU = 8;
 constexpr int kFlatNB = SLQ_FLAT_NB;           // batches in the ring (kFlatNB - 1 in flight)
 constexpr int kFlatThreads = 32 * SLQ_FLAT_WARPS;
@@ -50,6 +53,10 @@ constexpr int kFlatWarpBytes = kFlatNB * (kFlatBatchBytes + kFlatOwnBytes);
 constexpr int kFlatSmem = SLQ_FLAT_WARPS * kFlatWarpBytes;
 
 constexpr int PH_NZ = 0, PH_ITEM = 2, PH_DONE = 3;
+// Operator-pair chunk (slq_rules_pair): columns < a.split run the normalized Laplacian (prescaled
+// gathers / first-step records), the others the density matrix on the SAME probes -- one 128-byte
+// gather per nonzero serves both Lanczos runs.  a.split is a multiple of 4 (a lane = 4 columns).
+constexpr int kPair = 5;
 constexpr int kOffBlock = 28;   // rows per offsets block (32 prefetched offsets: a quad needs 5)
 constexpr int GF_OK = 1, GF_LIVE = 2, GF_END = 4, GF_SEG = 8;
 
@@ -67,16 +74,26 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
 }
 
-template <int KIND>
+// BITS: the first step.  u_0 is the +-1 probe bitmask (bits[row][kBitWords], word 0 = probes 0..31);
+// a slot gathers one 16-byte bitmask row -- for the normalized Laplacian the 32-byte [bits | dinv]
+// record (a.rec), so dinv[col] comes from the same sector -- copied by ONE lane (lane `sub` copies its
+// quarter's slot `sub`: the column index it loaded itself), 32 bytes of shared memory per slot.
+template <int KIND, bool BITS>
 __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel(SpmmArgs a) {
   constexpr unsigned FULL = 0xffffffffu;
-  constexpr bool NL = nl_kind<KIND>();
+  constexpr bool NL = nl_kind<KIND>() || KIND == kPair;   // dinv[row] in the epilogue
+  constexpr bool REC = KIND == SLQ_NORMALIZED_LAPLACIAN || KIND == kPair;   // BITS: gathers [bits | dinv] records
   const int lane = threadIdx.x & 31;
   const int sub = lane & 7;
   const int qid = lane >> 3;
@@ -91,16 +108,22 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     rj[j] = pv[j] ? __ldg(a.r + 4 * sub + j) : 1.0;
   }
   const bool all4 = pv[3];
+  const bool lane_nl = KIND != kPair || 4 * sub < a.split;   // pair chunk: this lane's operator
   // 16 bytes of a row per lane; lanes past the row's end (ldc < 32) copy nothing (zero fill)
   const int lane_bytes = 4 * sub + 3 < a.ldc_in ? 16 : 0;
   const uint32_t strideb = static_cast<uint32_t>(a.ldc_in) * 4u;   // row stride in bytes
   const char* __restrict__ ugb =
-      static_cast<const char*>(KIND == kNLPre ? a.upre : a.u) + (lane_bytes ? 16 * sub : 0);   // gathered vector
+      static_cast<const char*>((KIND == kNLPre || KIND == kPair) ? a.upre : a.u) + (lane_bytes ? 16 * sub : 0);   // gathered vector
   const char* __restrict__ uob = static_cast<const char*>(a.u) + (lane_bytes ? 16 * sub : 0);   // own values
   // keep the per-lane base pointers whole, so a gather address is one IMAD.WIDE (col * stride + base)
   asm volatile("" : "+l"(ugb));
   asm volatile("" : "+l"(uob));
   extern __shared__ __align__(128) unsigned char flat_smem[];
+  const uint32_t sm_warp = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
+                           (threadIdx.x >> 5) * kFlatWarpBytes;   // BITS: + buf * batch + (q * 4 + qid) * 32
+  const unsigned char* __restrict__ recb = reinterpret_cast<const unsigned char*>(
+      (BITS && REC) ? a.rec : a.bits);
+  constexpr uint32_t rec_stride = 4u * ((BITS && REC) ? kRecWords : kBitWords);
   const uint32_t sm_ring = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
                            (threadIdx.x >> 5) * kFlatWarpBytes + lane * 16;        // + buf * batch + q * 512
   const uint32_t sm_own = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
@@ -108,7 +131,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   float* __restrict__ w = static_cast<float*>(a.w) + 4 * sub;
   const int64_t* __restrict__ off = a.offsets;
   const int32_t* __restrict__ cols = a.cols;
-  const double scale = KIND == SLQ_DENSITY ? a.dscal[3] : 0.0;
+  const double scale = (KIND == SLQ_DENSITY || KIND == kPair) ? a.dscal[3] : 0.0;
   const bool has_long = a.long_counts != nullptr;
   const long long nseg = has_long ? a.long_counts[1] : 0;
   const long long nsq = (nseg + 3) >> 2;   // segment quads
@@ -166,6 +189,11 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
       if (lane == 0) item = static_cast<long long>(atomicAdd(a.work, 1ull));
       item = __shfl_sync(FULL, item, 0);
       if (item >= nitems) { phase = PH_DONE; return; }
+#if SLQ_FLAT_MIX
+      // the item list runs from the long rows to the shortest ones (degree order): take items from
+      // both ends alternately, so the low-parallelism batches of short rows overlap the full ones
+      item = (item & 1) ? nitems - 1 - (item >> 1) : (item >> 1);
+#endif
       if (item < nsq) {
         isseg = true;
         R = static_cast<int>(4 * item);
@@ -199,7 +227,8 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     const int rem = dq - j;
     const int nv = rem < 0 ? 0 : (rem > kFlatU ? kFlatU : rem);
     if (sub < nv) mypos = qpos + j + sub;
-    g.nv = lane_bytes ? (1 << nv) - 1 : 0;   // slots this lane copies (the others are zero-filled)
+    // slots this lane copies (the others are zero-filled); BITS: the quarter's valid slots
+    g.nv = (BITS || lane_bytes) ? (1 << nv) - 1 : 0;
     j += kFlatU;
     g.fl = GF_LIVE | (rowok ? GF_OK : 0) | (isseg ? GF_SEG : 0);
     if (j >= dmax) {
@@ -221,7 +250,12 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     for (int jj = 0; jj < 4; ++jj) {
       const double tot = ae[jj] + ao[jj];
       const double x = __dmul_rn(static_cast<double>(own[jj]), rj[jj]);
-      y[jj] = static_cast<float>(op_epilogue<KIND>(x, __dmul_rn(tot, rj[jj]), d, dis, scale));
+      const double sc = __dmul_rn(tot, rj[jj]);
+      if constexpr (KIND == kPair)
+        y[jj] = static_cast<float>(lane_nl ? op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, sc, d, dis, scale)
+                                           : op_epilogue<SLQ_DENSITY>(x, sc, d, dis, scale));
+      else
+        y[jj] = static_cast<float>(op_epilogue<KIND>(x, sc, d, dis, scale));
     }
     float* dst = w + r * a.ldc_out;
     if (all4) {
@@ -239,16 +273,34 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
       if (pv[jj]) dst[jj] = ae[jj] + ao[jj];
   };
   auto consume = [&](const Group& g, int buf) {
-    const uint32_t base = sm_ring + buf * kFlatBatchBytes;
+    if constexpr (BITS) {
+      const uint32_t base = sm_warp + buf * kFlatBatchBytes + qid * 32;
 #pragma unroll
-    for (int q = 0; q < kFlatU; ++q) {
-      const float4 x = lds128(base + q * 512);
-      if (q & 1) {
-        ao[0] += static_cast<double>(x.x); ao[1] += static_cast<double>(x.y);
-        ao[2] += static_cast<double>(x.z); ao[3] += static_cast<double>(x.w);
-      } else {
-        ae[0] += static_cast<double>(x.x); ae[1] += static_cast<double>(x.y);
-        ae[2] += static_cast<double>(x.z); ae[3] += static_cast<double>(x.w);
+      for (int q = 0; q < kFlatU; ++q) {
+        const uint32_t wd = lds32(base + q * 128) >> (4 * sub);
+        // s_c: dinv[col] (normalized Laplacian; a zero-filled slot has dinv = 0), else 1 for a valid
+        // slot and 0 for a zero-filled one: fma(s_c, +-1, acc) is the reference term or acc itself
+        const double one = ((g.nv >> q) & 1) ? 1.0 : 0.0;
+        const double sk = KIND == SLQ_NORMALIZED_LAPLACIAN ? lds64(base + q * 128 + 16)
+                          : (KIND == kPair ? (lane_nl ? lds64(base + q * 128 + 16) : one) : one);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const double x = ((wd >> jj) & 1u) ? 1.0 : -1.0;
+          if (q & 1) ao[jj] = fma(sk, x, ao[jj]); else ae[jj] = fma(sk, x, ae[jj]);
+        }
+      }
+    } else {
+      const uint32_t base = sm_ring + buf * kFlatBatchBytes;
+#pragma unroll
+      for (int q = 0; q < kFlatU; ++q) {
+        const float4 x = lds128(base + q * 512);
+        if (q & 1) {
+          ao[0] += static_cast<double>(x.x); ao[1] += static_cast<double>(x.y);
+          ao[2] += static_cast<double>(x.z); ao[3] += static_cast<double>(x.w);
+        } else {
+          ae[0] += static_cast<double>(x.x); ae[1] += static_cast<double>(x.y);
+          ae[2] += static_cast<double>(x.z); ae[3] += static_cast<double>(x.w);
+        }
       }
     }
     if (g.fl & GF_END) {
@@ -257,7 +309,16 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
           finish_seg(static_cast<int64_t>(g.r0) + qid);
         } else {
           const uint32_t ob = sm_own + buf * kFlatOwnBytes;
-          const float4 ownv = lds128(ob + lane * 16);
+          float4 ownv;
+          if constexpr (BITS) {
+            const uint32_t wd = lds32(ob + qid * 128) >> (4 * sub);
+            ownv.x = (wd & 1u) ? 1.f : -1.f;
+            ownv.y = (wd & 2u) ? 1.f : -1.f;
+            ownv.z = (wd & 4u) ? 1.f : -1.f;
+            ownv.w = (wd & 8u) ? 1.f : -1.f;
+          } else {
+            ownv = lds128(ob + lane * 16);
+          }
           const double d = lds64(ob + 512 + qid * 16);
           const double dis = NL ? lds64(ob + 512 + qid * 16 + 8) : 0.0;
           finish_row(static_cast<int64_t>(g.r0) + qid, ownv, d, dis);
@@ -269,16 +330,29 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   };
   auto issue = [&](const Group& g, int32_t col, int buf) {
     if (g.fl & GF_LIVE) {
-      const uint32_t base = sm_ring + buf * kFlatBatchBytes;
+      if constexpr (BITS) {
+        // this lane's own slot: the column index it loaded; invalid slots are zero-filled
+        const uint32_t dst = sm_warp + buf * kFlatBatchBytes + (sub * 4 + qid) * 32;
+        const unsigned char* src = recb + static_cast<uint64_t>(static_cast<uint32_t>(col)) * rec_stride;
+        const int nb = ((g.nv >> sub) & 1) ? 16 : 0;
+        cp_async16(dst, src, nb);
+        if (REC) cp_async16(dst + 16, src + 16, nb);
+      } else {
+        const uint32_t base = sm_ring + buf * kFlatBatchBytes;
 #pragma unroll
-      for (int q = 0; q < kFlatU; ++q) {
-        const uint32_t c = static_cast<uint32_t>(__shfl_sync(FULL, col, qbase | q));
-        cp_async16(base + q * 512, ugb + static_cast<uint64_t>(c) * strideb, ((g.nv >> q) & 1) ? 16 : 0);
+        for (int q = 0; q < kFlatU; ++q) {
+          const uint32_t c = static_cast<uint32_t>(__shfl_sync(FULL, col, qbase | q));
+          cp_async16(base + q * 512, ugb + static_cast<uint64_t>(c) * strideb, ((g.nv >> q) & 1) ? 16 : 0);
+        }
       }
       if ((g.fl & (GF_END | GF_SEG | GF_OK)) == (GF_END | GF_OK)) {
         const int64_t r = static_cast<int64_t>(g.r0) + qid;
         const uint32_t ob = sm_own + buf * kFlatOwnBytes;
-        cp_async16(ob + lane * 16, uob + static_cast<uint64_t>(r) * strideb, lane_bytes);
+        if constexpr (BITS) {
+          if (sub == 2) cp_async16(ob + qid * 128, a.bits + r * kBitWords, 16);
+        } else {
+          cp_async16(ob + lane * 16, uob + static_cast<uint64_t>(r) * strideb, lane_bytes);
+        }
         if (sub == 0) cp_async8(ob + 512 + qid * 16, a.degree + r);
         if (NL && sub == 1) cp_async8(ob + 512 + qid * 16 + 8, a.dinv + r);
       }
@@ -326,16 +400,20 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   cp_async_wait<0>();
 }
 
-template <int KIND>
+template <int KIND, bool BITS>
 static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
   const dim3 grid(148 * kFlatCtasPerSm);
   static std::atomic<bool> attr[64];
-  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<KIND>), kFlatSmem, attr)) return false;
+  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<KIND, BITS>), kFlatSmem, attr)) return false;
   if (a.win_rows <= 0) {
-    spmm_flat_kernel<KIND><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
+    spmm_flat_kernel<KIND, BITS><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
     return true;
   }
-  const void* base = KIND == kNLPre ? a.upre : a.u;
+  constexpr bool REC = KIND == SLQ_NORMALIZED_LAPLACIAN || KIND == kPair;
+  const void* base = BITS ? static_cast<const void*>(REC ? a.rec : a.bits)
+                          : ((KIND == kNLPre || KIND == kPair) ? a.upre : a.u);
+  const size_t row_bytes = BITS ? sizeof(uint32_t) * (REC ? kRecWords : kBitWords)
+                                : sizeof(float) * static_cast<size_t>(a.ldc_in);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kFlatThreads);
@@ -344,13 +422,13 @@ static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeAccessPolicyWindow;
   at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  at[0].val.accessPolicyWindow.num_bytes = sizeof(float) * static_cast<size_t>(a.ldc_in) * static_cast<size_t>(a.win_rows);
+  at[0].val.accessPolicyWindow.num_bytes = row_bytes * static_cast<size_t>(a.win_rows);
   at[0].val.accessPolicyWindow.hitRatio = 1.0f;
   at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
   at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<KIND>, a);
+  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<KIND, BITS>, a);
   l2_demote(base, at[0].val.accessPolicyWindow.num_bytes, st);
   return true;
 }
@@ -358,14 +436,23 @@ static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
 // True when the flat kernel took the launch (fp32 rows of 17..32 probes, unit weights, a gathered
 // vector, the Lanczos path, a graph with fine tiles); the caller falls back to spmm_kernel otherwise.
 bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st) {
-  if (!a.ftile_rows || a.nftiles <= 0 || a.weights || a.bits || !a.r) return false;
+  if (!a.ftile_rows || a.nftiles <= 0 || a.weights || !a.r) return false;
   if (a.ldc_in <= 16 || a.ldc_in > 32 || a.ldc_out > 32 || a.c > 32 || (a.ldc_in & 3) || (a.ldc_out & 3)) return false;
   if (a.n_rows >= (int64_t(1) << 29) || a.max_seg >= (int64_t(1) << 29)) return false;
-  if (kind == SLQ_NORMALIZED_LAPLACIAN && !a.upre) return false;   // dinv[col] per nonzero: spmm_kernel
+  // the normalized Laplacian needs dinv[col] per nonzero: prescaled gathers, or the first step's records
+  if (kind == SLQ_NORMALIZED_LAPLACIAN && !(a.bits ? a.rec != nullptr : a.upre != nullptr)) return false;
+  const bool pair = a.split < a.c;
+  if (pair && (kind != SLQ_NORMALIZED_LAPLACIAN || (a.split & 3))) return false;
   LaunchScope ls(K_SPMM, st);
-  if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<kNLPre>(a, st);
-  if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY>(a, st);
-  return flat_go<SLQ_LAPLACIAN>(a, st);
+  if (pair) return a.bits ? flat_go<kPair, true>(a, st) : flat_go<kPair, false>(a, st);
+  if (a.bits) {
+    if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<SLQ_NORMALIZED_LAPLACIAN, true>(a, st);
+    if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, true>(a, st);
+    return flat_go<SLQ_LAPLACIAN, true>(a, st);
+  }
+  if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<kNLPre, false>(a, st);
+  if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, false>(a, st);
+  return flat_go<SLQ_LAPLACIAN, false>(a, st);
 }
 
 }  // namespace slq

@@ -336,6 +336,34 @@ class DeviceGraph:
         return DeviceRules(nodes, weights, st, self.n, status=status)
 
 
+    def rules_pair(self, seed: int, probe_begin: int, count: int, steps: int, *, reorth: int = -1, dtype: str = "f32",
+                   status=None):
+        """Normalized-Laplacian and density-matrix rules of the same probes in one call
+        (``slq_rules_pair_seeded``): with 9..16 fp32 probes on a large folded graph both Lanczos runs
+        share every gathered row.  Returns ``(rules_nl, rules_density, paired)``; per-probe results
+        are bitwise those of two ``rules`` calls."""
+        import ctypes
+
+        import torch
+
+        if self.nnz == 0:
+            raise ValueError("density matrix undefined for a graph without edges")
+        s = min(int(steps), self.n)
+        out = [torch.zeros((count, s), dtype=torch.float64, device=self.device) for _ in range(4)]
+        st = [torch.zeros(count, dtype=torch.int32, device=self.device) for _ in range(2)]
+        if status is None:
+            status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        code = _lib.F64 if dtype in ("f64", "float64", np.float64) else _lib.F32
+        paired = ctypes.c_int32(0)
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.load().slq_rules_pair_seeded(
+                self.handle, _lib.seed_arg(seed), int(probe_begin), int(count), int(steps), int(reorth), code,
+                _lib.ptr(out[0]), _lib.ptr(out[1]), _lib.ptr(st[0]), _lib.ptr(out[2]), _lib.ptr(out[3]), _lib.ptr(st[1]),
+                _lib.ptr(status), ctypes.addressof(paired), _lib.stream_handle(self.device)))
+        return (DeviceRules(out[0], out[1], st[0], self.n, status=status),
+                DeviceRules(out[2], out[3], st[1], self.n, status=status), bool(paired.value))
+
+
 @dataclass
 class DeviceRules:
     nodes: object      # torch [count, s] float64 (clamped, ascending, zero padded)

@@ -25,7 +25,7 @@ def main(path, n=100_000, c=100, vb=8, workload="C2 (bench.py), one signature af
     kernels = {}
     for r in rows[2:]:
         name = r[col["Kernel Name"]]
-        cls = "cgs_step" if "cgs_step" in name else ("spmm" if "spmm_kernel" in name else None)
+        cls = "cgs_step" if "cgs_step" in name else ("spmm" if ("spmm_kernel" in name or "spmm_flat_kernel" in name) else None)
         if cls is None:
             continue
 
