@@ -11,7 +11,8 @@ GPUs, gloo in the CPU tests.
 """
 from __future__ import annotations
 
-__all__ = ["probe_ranges", "gather_rules_arrays", "sharded_rules", "gather_rows", "ShardedBatch"]
+__all__ = ["probe_ranges", "gather_rules_arrays", "sharded_rules", "sharded_rules_pair", "pair_applies", "gather_rows",
+           "ShardedBatch"]
 
 
 def probe_ranges(n_v: int, world: int) -> list[tuple[int, int]]:
@@ -87,6 +88,46 @@ def sharded_rules(dg, kind: str, cfg, *, dtype: str = "f64", reorth: int = -1, g
         steps = torch.zeros(0, dtype=torch.int32, device=dg.device)
     nodes, weights, steps, combined = gather_rules_arrays(nodes, weights, steps, cfg.n_v, group, status=status)
     return DeviceRules(nodes, weights, steps, dg.n, status=combined)
+
+
+def pair_applies(n_v: int, world: int, dtype: str) -> bool:
+    """Whether every rank's probe share fits the operator-pair block (9..16 fp32 probes): the same
+    decision on every rank, from the probe count and the world size only."""
+    sizes = [e - b for b, e in probe_ranges(n_v, world)]
+    return dtype in ("f32", "float32") and min(sizes) >= 9 and max(sizes) <= 16
+
+
+def sharded_rules_pair(dg, cfg, *, dtype: str = "f32", reorth: int = -1, group=None):
+    """Normalized-Laplacian AND density rules of probes 0..cfg.n_v-1 (heat/wave + VNGE of one
+    signature), probes sharded over the ranks.  Each rank calls ``dg.rules_pair`` on its range: with
+    9..16 probes per rank (128 probes on 8 GPUs) both Lanczos runs share every gathered row, so a
+    rank makes ONE pass over the graph per step instead of two -- pure probe sharding then scales
+    to 8 GPUs (a single operator's 16 probes would fill only half of each gathered 128-byte row).
+    One all-gather per operator; returns ``(rules_nl, rules_density)`` on every rank, bitwise the
+    rules of ``sharded_rules`` per operator."""
+    import torch
+    import torch.distributed as dist
+
+    from .device import DeviceRules
+
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    b, e = probe_ranges(cfg.n_v, world)[rank]
+    status = torch.zeros(1, dtype=torch.int32, device=dg.device)
+    width = min(cfg.s, dg.n)
+    if e > b:
+        nl, dens, _ = dg.rules_pair(cfg.seed, b, e - b, cfg.s, reorth=reorth, dtype=dtype, status=status)
+        blocks = [(nl.nodes, nl.weights, nl.steps), (dens.nodes, dens.weights, dens.steps)]
+    else:
+        z = torch.zeros((0, width), dtype=torch.float64, device=dg.device)
+        blocks = [(z, z.clone(), torch.zeros(0, dtype=torch.int32, device=dg.device))] * 2
+    if world == 1:
+        return tuple(DeviceRules(n_, w_, s_, dg.n, status=status) for n_, w_, s_ in blocks)
+    out = []
+    for n_, w_, s_ in blocks:
+        nodes, weights, steps, combined = gather_rules_arrays(n_, w_, s_, cfg.n_v, group, status=status)
+        out.append(DeviceRules(nodes, weights, steps, dg.n, status=combined))
+    return tuple(out)
 
 
 def gather_rows(block, total: int, group=None):

@@ -108,3 +108,66 @@ def test_graph_range_gather_world2(total, world):
     ref = np.array([[np.sin(g + 0.1 * t) for t in range(5)] for g in range(total)])
     for _, full in res:
         assert np.array_equal(full, ref)
+
+
+class _FakeRules:
+    def __init__(self, nodes, weights, steps):
+        self.nodes, self.weights, self.steps = torch.tensor(nodes), torch.tensor(weights), torch.tensor(steps)
+
+
+class _FakePairGraph:
+    """Stands in for DeviceGraph.rules_pair on the CPU: rules are a pure function of (operator, probe)."""
+    device = torch.device("cpu")
+    n = 50
+
+    def rules_pair(self, seed, probe_begin, count, steps, *, reorth=-1, dtype="f32", status=None):
+        probes = list(range(probe_begin, probe_begin + count))
+        nl = _FakeRules(*_rules_for(probes, steps))
+        dens = _FakeRules(*_rules_for([1000 + p for p in probes], steps))
+        return nl, dens, True
+
+
+class _Cfg:
+    n_v, s, seed = 24, 6, 0
+
+
+def _pair_worker(rank, world, port, out):
+    from paper_2003_01282_b200.dist import sharded_rules_pair
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nl, dens = sharded_rules_pair(_FakePairGraph(), _Cfg())
+    out.put((rank, nl.nodes.numpy(), nl.weights.numpy(), nl.steps.numpy(), dens.nodes.numpy(),
+             dens.weights.numpy(), dens.steps.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_pair_applies_only_for_9_to_16_fp32_probes_per_rank():
+    from paper_2003_01282_b200.dist import pair_applies
+
+    assert pair_applies(128, 8, "f32") and pair_applies(24, 2, "f32")
+    assert not pair_applies(128, 4, "f32")      # 32 probes per rank: a full row per operator already
+    assert not pair_applies(128, 16, "f32")     # 8 probes per rank
+    assert not pair_applies(128, 8, "f64")
+    assert pair_applies(100, 8, "f32")
+
+
+def test_sharded_rules_pair_world2_matches_single():
+    """Operator-pair sharding (dist.sharded_rules_pair): each rank's pair block covers its own probe
+    range, one all-gather per operator puts both rule sets in probe order on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pair_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref_nl = _rules_for(list(range(24)), 6)
+    ref_p = _rules_for([1000 + p for p in range(24)], 6)
+    for _, *got in res:
+        for a, b in zip(got, list(ref_nl) + list(ref_p)):
+            assert np.array_equal(a, b)

@@ -75,3 +75,50 @@ def test_flat_spmm_heat_matches_oracle(cuda_device, tmp_path):
     g = synth.barabasi_albert(3000, 3, seed=1)
     ref, _ = O.heat_trace(g, np.logspace(-2, 2, 250), 32, 12, 0)
     assert golden.rel_l2(np.load(tmp_path / "new.npy"), ref) <= 1e-4
+
+
+PAIR_CHILD = r"""
+import sys, json, torch
+sys.path.insert(0, %r)
+from paper_2003_01282_b200.device import DeviceGraph
+dg = DeviceGraph.rmat(15, 16, seed=0, device=torch.device('cuda', 0))
+res = []
+for count, p0 in ((16, 0), (16, 40), (12, 3), (10, 0), (20, 0), (4, 0)):
+    a, b, paired = dg.rules_pair(0, p0, count, 12)
+    a.check()
+    ra = dg.rules('normalized_laplacian', 0, p0, count, 12, dtype='f32')
+    rb = dg.rules('density', 0, p0, count, 12, dtype='f32')
+    eq = all(torch.equal(x, y) for x, y in ((a.nodes, ra.nodes), (a.weights, ra.weights), (a.steps, ra.steps),
+                                            (b.nodes, rb.nodes), (b.weights, rb.weights), (b.steps, rb.steps)))
+    res.append([count, p0, bool(paired), bool(eq)])
+print(json.dumps(res))
+""" % ROOT
+
+
+def test_operator_pair_block_bitwise_equals_separate_runs(cuda_device):
+    """slq_rules_pair_seeded: the normalized-Laplacian and density Lanczos runs of the same probes in
+    one 32-column block (one gather per nonzero for both) give, per probe, the bits of two separate
+    slq_rules_seeded calls; probe counts outside 9..16 take the separate runs."""
+    env = dict(os.environ, SLQ_SPMM_FLAT="1", SLQ_PRESCALE_MIN_N="0")
+    r = subprocess.run([sys.executable, "-c", PAIR_CHILD], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(eq for *_, eq in res), res
+    assert [paired for _, _, paired, _ in res] == [True, True, True, True, False, False], res
+
+
+def test_operator_pair_falls_back_on_small_graphs(cuda_device):
+    """Without the flat SpMM (a small host graph, default environment) the pair entry runs the two
+    operators apart: same results as ``rules``, ``paired`` False."""
+    import torch
+
+    from paper_2003_01282_b200 import synth
+    from paper_2003_01282_b200.device import DeviceGraph
+
+    dg = DeviceGraph(synth.barabasi_albert(1000, 3, seed=0), cuda_device)
+    a, b, paired = dg.rules_pair(0, 0, 16, 10)
+    assert not paired
+    ra = dg.rules("normalized_laplacian", 0, 0, 16, 10, dtype="f32")
+    rb = dg.rules("density", 0, 0, 16, 10, dtype="f32")
+    assert torch.equal(a.nodes, ra.nodes) and torch.equal(a.weights, ra.weights)
+    assert torch.equal(b.nodes, rb.nodes) and torch.equal(b.weights, rb.weights)
