@@ -194,7 +194,7 @@ static int64_t l2_window_bytes(const slq_graph* g) {
   if (!g->degree_ordered) return 0;
   // 32 MB by default (R-MAT-26, 32 probes: SpMM -2.7%, CGS step unchanged; the device maximum, 79 MB,
   // gives SpMM -5% but costs the step kernel +39% of its L2 reuse).  SLQ_L2_WINDOW_MB=0 turns
-  // it off, -1 uses the device maximum, k sets k MB.  The carve-out (cudaLimitPersistingL2CacheSize,
+  // it off, -1 uses the device maximum (at most 64 MB), k sets k MB.  The carve-out (cudaLimitPersistingL2CacheSize,
   // a device-wide setting) is sized to the window.
   static const long long env_mb = [] { const char* e = getenv("SLQ_L2_WINDOW_MB"); return e ? atoll(e) : 32ll; }();
   if (env_mb == 0) return 0;
@@ -207,6 +207,7 @@ static int64_t l2_window_bytes(const slq_graph* g) {
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
     long long bytes = std::min<long long>(persist, maxwin);
     if (env_mb > 0) bytes = std::min<long long>(bytes, env_mb << 20);
+    else bytes = std::min<long long>(bytes, 64ll << 20);   // -1: the largest window the launches accept
     if (bytes > 0) {
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
       cudaStreamIsCapturing(static_cast<cudaStream_t>(g->stream), &cap);
@@ -222,9 +223,6 @@ static int64_t l2_window_bytes(const slq_graph* g) {
   return v < 0 ? 0 : v;
 }
 
-// The recurrence runs on `g`; with an isolated-vertex fold, g is the folded graph and `orig` the
-// graph the probes and the start-vector norm belong to (probe stream positions are original vertex
-// ids, remapped to folded rows; the trailing row carries sqrt(m)).
 // Operator-pair chunk: duplicate the probe bits of columns [0, split) into columns [split, 2 split)
 // (word 0 of every bitmask row; 2 split <= 32).
 static __global__ void pair_bits_kernel(uint32_t* __restrict__ bits, int64_t n, int split) {
@@ -242,6 +240,9 @@ static int pair_fail(const char* msg) {
   return fail(SLQ_ERR_VALUE, msg);
 }
 
+// The recurrence runs on `g`; with an isolated-vertex fold, g is the folded graph and `orig` the
+// graph the probes and the start-vector norm belong to (probe stream positions are original vertex
+// ids, remapped to folded rows; the trailing row carries sqrt(m)).
 struct FoldRun {
   const slq_graph* orig = nullptr;   // nullptr: no fold
 };

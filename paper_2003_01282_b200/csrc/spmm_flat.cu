@@ -40,6 +40,9 @@ namespace slq {
 #ifndef SLQ_FLAT_CTAS
 #define SLQ_FLAT_CTAS 2
 #endif
+#ifndef SLQ_FLAT_CVT
+#define SLQ_FLAT_CVT 1   // 1: integer widening + DFMA instead of F2F.F64.F32 + DADD (same bits for finite inputs)
+#endif
 #ifndef SLQ_FLAT_MIX
 #define SLQ_FLAT_MIX 0
 #endif
@@ -294,6 +297,25 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
 #pragma unroll
       for (int q = 0; q < kFlatU; ++q) {
         const float4 x = lds128(base + q * 512);
+#if SLQ_FLAT_CVT
+        // acc + double(x) without the conversion instruction (the XU pipe converts 4 lanes per clock):
+        // the double with exponent field = x's 8-bit exponent and mantissa = x's (three integer
+        // instructions) is x * 2^-896 exactly -- also for zeros and subnormals, whose exponent field
+        // is 0 in both formats -- and fma(that, 2^896, acc) rounds acc + x once, like the add.
+        // (Inf/NaN inputs come out as 2^128 * 1.m: still non-finite after the fp32 store.)
+        const double k896 = __hiloint2double(0x77f00000, 0);   // 2^896
+        auto wide = [](float v) {
+          const int f = __float_as_int(v);
+          return __hiloint2double((f >> 3) & static_cast<int>(0x8fffffffu), f << 29);
+        };
+        if (q & 1) {
+          ao[0] = fma(wide(x.x), k896, ao[0]); ao[1] = fma(wide(x.y), k896, ao[1]);
+          ao[2] = fma(wide(x.z), k896, ao[2]); ao[3] = fma(wide(x.w), k896, ao[3]);
+        } else {
+          ae[0] = fma(wide(x.x), k896, ae[0]); ae[1] = fma(wide(x.y), k896, ae[1]);
+          ae[2] = fma(wide(x.z), k896, ae[2]); ae[3] = fma(wide(x.w), k896, ae[3]);
+        }
+#else
         if (q & 1) {
           ao[0] += static_cast<double>(x.x); ao[1] += static_cast<double>(x.y);
           ao[2] += static_cast<double>(x.z); ao[3] += static_cast<double>(x.w);
@@ -301,6 +323,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
           ae[0] += static_cast<double>(x.x); ae[1] += static_cast<double>(x.y);
           ae[2] += static_cast<double>(x.z); ae[3] += static_cast<double>(x.w);
         }
+#endif
       }
     }
     if (g.fl & GF_END) {
