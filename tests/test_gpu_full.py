@@ -138,6 +138,7 @@ def test_c5_rmat27_full_size_properties(cuda_device):
     # a probe prefix is bitwise the prefix run (chunk independence: 4 chunks of 32 vs one of 8)
     pre = dg.rules("normalized_laplacian", 0, 0, 8, 15, dtype="f32")
     assert torch.equal(pre.nodes, rules.nodes[:8]) and torch.equal(pre.weights, rules.weights[:8])
+    nl_16_32 = (rules.nodes[16:32].clone(), rules.weights[16:32].clone())
     del rules, pre
     # alpha_0 = z^T L z / n through the exact (bit-exact fp64) operator apply
     a, _, _ = dg.tridiagonals("normalized_laplacian", 0, 0, 4, 2, dtype="f32")
@@ -163,3 +164,10 @@ def test_c5_rmat27_full_size_properties(cuda_device):
     vp, _ = rp.integrate(None, [_lib.FN_XLOGX])
     rp.check()
     assert 0.0 < -float(vp[0, 0]) < np.log(dg.n - dg.info.isolated)
+    # the operator-pair block (a rank's share on 8 GPUs: probes 16..31 of both operators in one
+    # 32-column block) is bitwise the full runs' rules of those probes
+    pair_nl, pair_p, paired = dg.rules_pair(0, 16, 16, 15)
+    pair_nl.check()
+    assert paired
+    assert torch.equal(pair_nl.nodes, nl_16_32[0]) and torch.equal(pair_nl.weights, nl_16_32[1])
+    assert torch.equal(pair_p.nodes, rp.nodes[16:32]) and torch.equal(pair_p.weights, rp.weights[16:32])
