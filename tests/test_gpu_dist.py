@@ -185,3 +185,55 @@ def test_graph_range_sharding_bitwise_equals_single_gpu(cuda_device):
     for _, v, s, st in res:
         assert st == 0
         assert np.array_equal(v, vals.cpu().numpy()) and np.array_equal(s, stds.cpu().numpy())
+
+
+def _worker_pair(rank, world, port, out, env):
+    import torch.distributed as dist
+
+    os.environ.update(env)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2003_01282_b200.device import DeviceGraph
+    from paper_2003_01282_b200.dist import pair_applies, sharded_rules_pair
+    from paper_2003_01282_b200.slq import SlqConfig
+
+    dg = DeviceGraph.rmat(14, 16, seed=5, device=torch.device("cuda", 0))
+    cfg = SlqConfig(n_v=24, s=12, seed=0)
+    if world > 1:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        assert pair_applies(cfg.n_v, world, "f32")
+        nl, dens = sharded_rules_pair(dg, cfg, dtype="f32")
+    else:
+        nl = dg.rules("normalized_laplacian", 0, 0, cfg.n_v, cfg.s, dtype="f32")
+        dens = dg.rules("density", 0, 0, cfg.n_v, cfg.s, dtype="f32")
+    nl.check()
+    dens.check()
+    if rank == 0:
+        out.put((dg.folded, nl.nodes.cpu().numpy(), nl.weights.cpu().numpy(), nl.steps.cpu().numpy(),
+                 dens.nodes.cpu().numpy(), dens.weights.cpu().numpy(), dens.steps.cpu().numpy()))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_two_ranks_operator_pair_bitwise_equal_single_rank(cuda_device):
+    """C5 on 8 GPUs in miniature: 24 probes over two ranks = 12 per rank, so each rank runs ONE
+    operator-pair block (normalized Laplacian + density interleaved, dist.sharded_rules_pair); the
+    assembled rules of both operators are bitwise the single-rank separate runs' (24-probe chunks)."""
+    env = {"SLQ_PRESCALE_MIN_N": "0", "SLQ_SPMM_FLAT": "1"}
+    ctx = mp.get_context("spawn")
+    res = []
+    for world in (1, 2):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_worker_pair, args=(r, world, port, q, env)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res.append(q.get(timeout=300))
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+    one, two = res
+    assert one[0] > 0 and one[0] == two[0]
+    for a, b in zip(one[1:], two[1:]):
+        assert np.array_equal(a, b)

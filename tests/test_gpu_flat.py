@@ -35,6 +35,14 @@ mode, out_path = sys.argv[1], sys.argv[2]
 dev = torch.device('cuda', 0)
 if mode == 'rmat':
     dg = DeviceGraph.rmat(15, 16, seed=0, device=dev)          # folded, degree ordered, long rows
+elif mode == 'iso':
+    # unfolded, not degree ordered, a third of the rows EMPTY (ragged quads, rows of length 0)
+    from paper_2003_01282_b200.graphs import csr_from_edges
+    rng = np.random.default_rng(7)
+    n, m = 4001, 20000
+    live = np.flatnonzero(rng.random(n) > 0.33)
+    dg = DeviceGraph(csr_from_edges(n, live[rng.integers(0, live.size, m)], live[rng.integers(0, live.size, m)]),
+                     dev, fold=None)
 else:
     dg = DeviceGraph(synth.barabasi_albert(3000, 3, seed=1), dev, fold=None)   # not degree ordered
 res = {}
@@ -58,7 +66,7 @@ def _run(mode, flat, out_path):
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
-@pytest.mark.parametrize("mode", ["rmat", "ba"])
+@pytest.mark.parametrize("mode", ["rmat", "ba", "iso"])
 def test_flat_spmm_bitwise_equals_warp_per_row(cuda_device, tmp_path, mode):
     old = _run(mode, "0", tmp_path / "old.npy")
     new = _run(mode, "1", tmp_path / "new.npy")
