@@ -389,7 +389,11 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
     const char* e = getenv("SLQ_PRESCALE_MIN_N");
     return e ? static_cast<int64_t>(atoll(e)) : (int64_t(1) << 22);
   }();
-  const bool prescale = pre_env && kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && ldc <= 32 && n >= pre_min_n;
+  // ... or any graph the flat SpMM runs on (fine tiles + degree-ordered rows: a property of the graph
+  // too): its normalized-Laplacian gathers are the prescaled ones (R-MAT-22, 32 probes: SpMM + step
+  // kernels 67.1 -> 42.7 ms per run; R-MAT-20: 16.9 -> 14.7 ms)
+  const bool pre_size = n >= pre_min_n || (g->ftile_rows && g->degree_ordered);
+  const bool prescale = pre_env && kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && ldc <= 32 && pre_size;
   // The last SpMM (step S-1) is prescaled too: the last step kernel writes dinv (.) u_{S-1} over w (each
   // CTA over rows it has already consumed), and that SpMM, which only feeds alpha_{S-1}, writes its
   // output into the slot of u_1 (no longer needed).  Needs S >= 3 and no basis export.
@@ -400,7 +404,7 @@ static int run_chunk(const slq_graph* g, int kind, const SeedKey& seed, int64_t 
   if (pair && !(prescale && last_pre && kind == SLQ_NORMALIZED_LAPLACIAN && kind2 == SLQ_DENSITY))
     return pair_fail("operator-pair chunk needs prescaled normalized-Laplacian gathers + density");
   const bool rec_on = kind == SLQ_NORMALIZED_LAPLACIAN && all_staged && bits != nullptr && S >= 2 &&
-                      ldc * vb >= static_cast<int64_t>(sizeof(uint32_t)) * kRecWords && n >= pre_min_n && pre_env;
+                      ldc * vb >= static_cast<int64_t>(sizeof(uint32_t)) * kRecWords && pre_size && pre_env;
   if (pair && !rec_on) return pair_fail("operator-pair chunk needs the first-step records");
   // SLQ_STEP_TIMING=1 (diagnostics): the step kernels stamp %globaltimer around their grid barriers
   static unsigned long long* dbgbuf = [] {

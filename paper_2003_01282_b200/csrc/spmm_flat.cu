@@ -51,7 +51,7 @@ constexpr int kFlatNB = SLQ_FLAT_NB;           // batches in the ring (kFlatNB -
 constexpr int kFlatThreads = 32 * SLQ_FLAT_WARPS;
 constexpr int kFlatCtasPerSm = SLQ_FLAT_CTAS;
 constexpr int kFlatBatchBytes = kFlatU * 4 * 128;   // gathered rows of one batch
-constexpr int kFlatOwnBytes = 4 * 128 + 4 * 16;     // own rows + (degree, dinv) of one batch
+constexpr int kFlatOwnBytes = 512 + 8 * 16;         // own rows + (degree, dinv) of up to 8 rows
 constexpr int kFlatWarpBytes = kFlatNB * (kFlatBatchBytes + kFlatOwnBytes);
 constexpr int kFlatSmem = SLQ_FLAT_WARPS * kFlatWarpBytes;
 
@@ -60,7 +60,6 @@ constexpr int PH_NZ = 0, PH_ITEM = 2, PH_DONE = 3;
 // gathers / first-step records), the others the density matrix on the SAME probes -- one 128-byte
 // gather per nonzero serves both Lanczos runs.  a.split is a multiple of 4 (a lane = 4 columns).
 constexpr int kPair = 5;
-constexpr int kOffBlock = 28;   // rows per offsets block (32 prefetched offsets: a quad needs 5)
 constexpr int GF_OK = 1, GF_LIVE = 2, GF_END = 4, GF_SEG = 8;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
@@ -92,15 +91,23 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
 // a slot gathers one 16-byte bitmask row -- for the normalized Laplacian the 32-byte [bits | dinv]
 // record (a.rec), so dinv[col] comes from the same sector -- copied by ONE lane (lane `sub` copies its
 // quarter's slot `sub`: the column index it loaded itself), 32 bytes of shared memory per slot.
-template <int KIND, bool BITS>
+//
+// L = lanes per row of the vector: 8 (rows of 17..32 probes, 128 bytes: a quad of CSR rows per warp) or
+// 4 (rows of <= 16 probes, 64 bytes: eight CSR rows per warp; a lane then loads the column indices of
+// two slots).  Shared-memory addressing is the same: a slot's rows of all the warp's CSR rows are 512
+// contiguous bytes, lane l's 16 bytes at offset 16 l.
+template <int KIND, bool BITS, int L>
 __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel(SpmmArgs a) {
+  static_assert(L == 8 || L == 4, "lanes per gathered row");
+  constexpr int RPW = 32 / L;            // CSR rows a warp walks in lockstep
+  constexpr int kOffBlock = 32 - RPW;    // rows per offsets block (32 prefetched offsets: RPW + 1 per group)
   constexpr unsigned FULL = 0xffffffffu;
   constexpr bool NL = nl_kind<KIND>() || KIND == kPair;   // dinv[row] in the epilogue
   constexpr bool REC = KIND == SLQ_NORMALIZED_LAPLACIAN || KIND == kPair;   // BITS: gathers [bits | dinv] records
   const int lane = threadIdx.x & 31;
-  const int sub = lane & 7;
-  const int qid = lane >> 3;
-  const int qbase = lane & 24;
+  const int sub = lane & (L - 1);
+  const int qid = lane / L;
+  const int qbase = lane & ~(L - 1);
 
   // probes 4 sub .. 4 sub + 3 of the chunk
   bool pv[4];
@@ -123,7 +130,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   asm volatile("" : "+l"(uob));
   extern __shared__ __align__(128) unsigned char flat_smem[];
   const uint32_t sm_warp = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
-                           (threadIdx.x >> 5) * kFlatWarpBytes;   // BITS: + buf * batch + (q * 4 + qid) * 32
+                           (threadIdx.x >> 5) * kFlatWarpBytes;   // BITS: + buf * batch + (q * RPW + qid) * 32
   const unsigned char* __restrict__ recb = reinterpret_cast<const unsigned char*>(
       (BITS && REC) ? a.rec : a.bits);
   constexpr uint32_t rec_stride = 4u * ((BITS && REC) ? kRecWords : kBitWords);
@@ -137,7 +144,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   const double scale = (KIND == SLQ_DENSITY || KIND == kPair) ? a.dscal[3] : 0.0;
   const bool has_long = a.long_counts != nullptr;
   const long long nseg = has_long ? a.long_counts[1] : 0;
-  const long long nsq = (nseg + 3) >> 2;   // segment quads
+  const long long nsq = (nseg + RPW - 1) / RPW;   // groups of RPW segments
   const long long nitems = nsq + a.nftiles;
   const int64_t nrows = a.n_rows;   // offsets has nrows + 1 entries
 
@@ -199,8 +206,8 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
 #endif
       if (item < nsq) {
         isseg = true;
-        R = static_cast<int>(4 * item);
-        Rend = static_cast<int>(R + 4 < nseg ? R + 4 : nseg);
+        R = static_cast<int>(RPW * item);
+        Rend = static_cast<int>(R + RPW < nseg ? R + RPW : nseg);
       } else {
         const long long t = item - nsq;
         const int64_t rb = a.ftile_rows[t], re = a.ftile_rows[t + 1];
@@ -220,9 +227,10 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   // ---- one batch: nv = bit mask of the slots this lane copies, r0 = the quad's first row / segment (uniform),
   // flags: GF_OK (this quarter has a row), uniform GF_LIVE / GF_END (the quad's last batch) / GF_SEG
   struct Group { int nv, r0, fl; };
-  auto gen = [&](Group& g, int64_t& mypos) {
+  auto gen = [&](Group& g, int64_t& mypos, int64_t& mypos2) {
     if (phase == PH_ITEM) fetch_item();
     mypos = -1;
+    mypos2 = -1;
     g.nv = 0;
     g.r0 = R;
     g.fl = 0;
@@ -230,13 +238,14 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
     const int rem = dq - j;
     const int nv = rem < 0 ? 0 : (rem > kFlatU ? kFlatU : rem);
     if (sub < nv) mypos = qpos + j + sub;
+    if (L == 4 && sub + 4 < nv) mypos2 = qpos + j + sub + 4;   // 4 lanes per row: two slots per lane
     // slots this lane copies (the others are zero-filled); BITS: the quarter's valid slots
     g.nv = (BITS || lane_bytes) ? (1 << nv) - 1 : 0;
     j += kFlatU;
     g.fl = GF_LIVE | (rowok ? GF_OK : 0) | (isseg ? GF_SEG : 0);
     if (j >= dmax) {
       g.fl |= GF_END;
-      R += 4;
+      R += RPW;
       enter_quad();
     }
   };
@@ -278,14 +287,15 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   auto consume = [&](const Group& g, int buf) {
     if constexpr (BITS) {
       const uint32_t base = sm_warp + buf * kFlatBatchBytes + qid * 32;
+      constexpr int kSlotRec = RPW * 32;   // bytes of one slot's records
 #pragma unroll
       for (int q = 0; q < kFlatU; ++q) {
-        const uint32_t wd = lds32(base + q * 128) >> (4 * sub);
+        const uint32_t wd = lds32(base + q * kSlotRec) >> (4 * sub);
         // s_c: dinv[col] (normalized Laplacian; a zero-filled slot has dinv = 0), else 1 for a valid
         // slot and 0 for a zero-filled one: fma(s_c, +-1, acc) is the reference term or acc itself
         const double one = ((g.nv >> q) & 1) ? 1.0 : 0.0;
-        const double sk = KIND == SLQ_NORMALIZED_LAPLACIAN ? lds64(base + q * 128 + 16)
-                          : (KIND == kPair ? (lane_nl ? lds64(base + q * 128 + 16) : one) : one);
+        const double sk = KIND == SLQ_NORMALIZED_LAPLACIAN ? lds64(base + q * kSlotRec + 16)
+                          : (KIND == kPair ? (lane_nl ? lds64(base + q * kSlotRec + 16) : one) : one);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const double x = ((wd >> jj) & 1u) ? 1.0 : -1.0;
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
           const uint32_t ob = sm_own + buf * kFlatOwnBytes;
           float4 ownv;
           if constexpr (BITS) {
-            const uint32_t wd = lds32(ob + qid * 128) >> (4 * sub);
+            const uint32_t wd = lds32(ob + qid * (L * 16)) >> (4 * sub);
             ownv.x = (wd & 1u) ? 1.f : -1.f;
             ownv.y = (wd & 2u) ? 1.f : -1.f;
             ownv.z = (wd & 4u) ? 1.f : -1.f;
@@ -351,20 +361,27 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
       for (int jj = 0; jj < 4; ++jj) ae[jj] = ao[jj] = 0.0;
     }
   };
-  auto issue = [&](const Group& g, int32_t col, int buf) {
+  auto issue = [&](const Group& g, int32_t col, int32_t col2, int buf) {
     if (g.fl & GF_LIVE) {
       if constexpr (BITS) {
         // this lane's own slot: the column index it loaded; invalid slots are zero-filled
-        const uint32_t dst = sm_warp + buf * kFlatBatchBytes + (sub * 4 + qid) * 32;
+        const uint32_t dst = sm_warp + buf * kFlatBatchBytes + (sub * RPW + qid) * 32;
         const unsigned char* src = recb + static_cast<uint64_t>(static_cast<uint32_t>(col)) * rec_stride;
         const int nb = ((g.nv >> sub) & 1) ? 16 : 0;
         cp_async16(dst, src, nb);
         if (REC) cp_async16(dst + 16, src + 16, nb);
+        if (L == 4) {   // this lane's second slot
+          const uint32_t dst2 = dst + 4 * RPW * 32;
+          const unsigned char* src2 = recb + static_cast<uint64_t>(static_cast<uint32_t>(col2)) * rec_stride;
+          const int nb2 = ((g.nv >> (sub + 4)) & 1) ? 16 : 0;
+          cp_async16(dst2, src2, nb2);
+          if (REC) cp_async16(dst2 + 16, src2 + 16, nb2);
+        }
       } else {
         const uint32_t base = sm_ring + buf * kFlatBatchBytes;
 #pragma unroll
         for (int q = 0; q < kFlatU; ++q) {
-          const uint32_t c = static_cast<uint32_t>(__shfl_sync(FULL, col, qbase | q));
+          const uint32_t c = static_cast<uint32_t>(__shfl_sync(FULL, q < L ? col : col2, qbase | (q & (L - 1))));
           cp_async16(base + q * 512, ugb + static_cast<uint64_t>(c) * strideb, ((g.nv >> q) & 1) ? 16 : 0);
         }
       }
@@ -372,7 +389,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
         const int64_t r = static_cast<int64_t>(g.r0) + qid;
         const uint32_t ob = sm_own + buf * kFlatOwnBytes;
         if constexpr (BITS) {
-          if (sub == 2) cp_async16(ob + qid * 128, a.bits + r * kBitWords, 16);
+          if (sub == 2) cp_async16(ob + qid * (L * 16), a.bits + r * kBitWords, 16);
         } else {
           cp_async16(ob + lane * 16, uob + static_cast<uint64_t>(r) * strideb, lane_bytes);
         }
@@ -388,48 +405,50 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   // left) every later one is dead, so the loop runs while the batch to consume is live.
   static_assert(kFlatNB == 3 || kFlatNB == 4, "ring depth");
   Group g0, g1, g2, gi, gp;
-  int64_t mypos;
-  int32_t col_i, col_p;
-  auto next = [&](Group& g, int32_t& col) {
-    gen(g, mypos);
+  int64_t mypos, mypos2;
+  int32_t col_i, col_p, col2_i = 0, col2_p = 0;
+  auto next = [&](Group& g, int32_t& col, int32_t& col2) {
+    gen(g, mypos, mypos2);
     col = mypos >= 0 ? __ldg(cols + mypos) : 0;
+    if (L == 4) col2 = mypos2 >= 0 ? __ldg(cols + mypos2) : 0;
   };
   // prologue: issue the first NB - 1 batches
-  next(g0, col_i);
-  issue(g0, col_i, 0);
-  next(g1, col_i);
-  issue(g1, col_i, 1);
+  next(g0, col_i, col2_i);
+  issue(g0, col_i, col2_i, 0);
+  next(g1, col_i, col2_i);
+  issue(g1, col_i, col2_i, 1);
   if (kFlatNB == 4) {
-    next(g2, col_i);
-    issue(g2, col_i, 2);
+    next(g2, col_i, col2_i);
+    issue(g2, col_i, col2_i, 2);
   }
-  next(gi, col_i);
-  next(gp, col_p);
+  next(gi, col_i, col2_i);
+  next(gp, col_p, col2_p);
   int cbuf = 0;            // buffer of the batch consumed this iteration
   int ibuf = kFlatNB - 1;  // buffer of the batch issued this iteration (consumed one iteration ago)
   while (g0.fl & GF_LIVE) {
     cp_async_wait<kFlatNB - 2>();
     __syncwarp();
     consume(g0, cbuf);
-    issue(gi, col_i, ibuf);
+    issue(gi, col_i, col2_i, ibuf);
     ibuf = cbuf;
     cbuf = cbuf + 1 == kFlatNB ? 0 : cbuf + 1;
     g0 = g1;
     if (kFlatNB == 4) { g1 = g2; g2 = gi; } else { g1 = gi; }
     gi = gp;
     col_i = col_p;
-    next(gp, col_p);
+    col2_i = col2_p;
+    next(gp, col_p, col2_p);
   }
   cp_async_wait<0>();
 }
 
-template <int KIND, bool BITS>
+template <int KIND, bool BITS, int L = 8>
 static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
   const dim3 grid(148 * kFlatCtasPerSm);
   static std::atomic<bool> attr[64];
-  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<KIND, BITS>), kFlatSmem, attr)) return false;
+  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<KIND, BITS, L>), kFlatSmem, attr)) return false;
   if (a.win_rows <= 0) {
-    spmm_flat_kernel<KIND, BITS><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
+    spmm_flat_kernel<KIND, BITS, L><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
     return true;
   }
   constexpr bool REC = KIND == SLQ_NORMALIZED_LAPLACIAN || KIND == kPair;
@@ -451,7 +470,7 @@ static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
   at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<KIND, BITS>, a);
+  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<KIND, BITS, L>, a);
   l2_demote(base, at[0].val.accessPolicyWindow.num_bytes, st);
   return true;
 }
@@ -460,14 +479,25 @@ static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
 // vector, the Lanczos path, a graph with fine tiles); the caller falls back to spmm_kernel otherwise.
 bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st) {
   if (!a.ftile_rows || a.nftiles <= 0 || a.weights || !a.r) return false;
-  if (a.ldc_in <= 16 || a.ldc_in > 32 || a.ldc_out > 32 || a.c > 32 || (a.ldc_in & 3) || (a.ldc_out & 3)) return false;
+  if (a.ldc_in > 32 || a.ldc_out > 32 || a.c > 32 || (a.ldc_in & 3) || (a.ldc_out & 3) || a.ldc_in < 4) return false;
+  const bool narrow = a.ldc_in <= 16;   // 64-byte rows: 4 lanes per row
   if (a.n_rows >= (int64_t(1) << 29) || a.max_seg >= (int64_t(1) << 29)) return false;
   // the normalized Laplacian needs dinv[col] per nonzero: prescaled gathers, or the first step's records
   if (kind == SLQ_NORMALIZED_LAPLACIAN && !(a.bits ? a.rec != nullptr : a.upre != nullptr)) return false;
   const bool pair = a.split < a.c;
-  if (pair && (kind != SLQ_NORMALIZED_LAPLACIAN || (a.split & 3))) return false;
+  if (pair && (kind != SLQ_NORMALIZED_LAPLACIAN || (a.split & 3) || narrow)) return false;
   LaunchScope ls(K_SPMM, st);
   if (pair) return a.bits ? flat_go<kPair, true>(a, st) : flat_go<kPair, false>(a, st);
+  if (narrow) {
+    if (a.bits) {
+      if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<SLQ_NORMALIZED_LAPLACIAN, true, 4>(a, st);
+      if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, true, 4>(a, st);
+      return flat_go<SLQ_LAPLACIAN, true, 4>(a, st);
+    }
+    if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<kNLPre, false, 4>(a, st);
+    if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, false, 4>(a, st);
+    return flat_go<SLQ_LAPLACIAN, false, 4>(a, st);
+  }
   if (a.bits) {
     if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<SLQ_NORMALIZED_LAPLACIAN, true>(a, st);
     if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, true>(a, st);

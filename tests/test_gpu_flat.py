@@ -47,7 +47,7 @@ else:
     dg = DeviceGraph(synth.barabasi_albert(3000, 3, seed=1), dev, fold=None)   # not degree ordered
 res = {}
 for kind in ('normalized_laplacian', 'density', 'laplacian'):
-    for nv in (32, 24, 19):
+    for nv in (32, 24, 19, 16, 12, 8, 5):
         a, b, s = dg.tridiagonals(kind, 0, 0, nv, 12, dtype='f32')
         blob = a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()
         res[kind + '/' + str(nv)] = hashlib.sha256(blob).hexdigest()
@@ -70,7 +70,7 @@ def _run(mode, flat, out_path):
 def test_flat_spmm_bitwise_equals_warp_per_row(cuda_device, tmp_path, mode):
     old = _run(mode, "0", tmp_path / "old.npy")
     new = _run(mode, "1", tmp_path / "new.npy")
-    assert old.keys() == new.keys() and len(old) == 9
+    assert old.keys() == new.keys() and len(old) == 21
     assert [k for k in old if old[k] != new[k]] == []
     assert np.array_equal(np.load(tmp_path / "old.npy"), np.load(tmp_path / "new.npy"))
 

@@ -21,7 +21,7 @@ scale = int(sys.argv[1])
 dg = DeviceGraph.rmat(scale, 16, seed=0, device=torch.device('cuda', 0))
 out = {}
 for kind in ('normalized_laplacian', 'density', 'laplacian'):
-    for nv in (32, 24, 19):
+    for nv in (32, 24, 19, 16, 12, 8, 5):
         a, b, s = dg.tridiagonals(kind, 0, 0, nv, 15, dtype='f32')
         h = hashlib.sha256(a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()).hexdigest()
         out[f'{kind}/{nv}'] = [h[:16], float(a[0, 0]), float(a[-1, -1])]
