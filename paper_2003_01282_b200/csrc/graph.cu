@@ -451,9 +451,14 @@ static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
   int rc = fetch_host_scalars(g);
   if (rc) return rc;
   const int64_t n = g->n, nnz = g->nnz;
+  // Large unit-weight graphs are "folded" even without (enough) isolated vertices: the fold's degree
+  // order is what the flat SpMM (spmm_flat.cu) needs, the trailing row then stands for m >= 0 vertices
+  // (m = 0: a row that stays 0).  SLQ_FOLD_RELABEL=0 turns this off.
+  static const bool relabel_env = [] { const char* e = getenv("SLQ_FOLD_RELABEL"); return !(e && e[0] == '0'); }();
+  const bool relabel = relabel_env && fold_by_degree() && nnz >= kFlatMinNnz && !g->weights && n < (int64_t(1) << 29);
   // degree-0 vertices bound the foldable ones from above; nothing to do below the threshold
-  if (g->bad_columns || nnz == 0 || g->isolated < 1 ||
-      static_cast<double>(g->isolated) < min_fraction * static_cast<double>(n))
+  if (g->bad_columns || nnz == 0) return SLQ_OK;
+  if (!relabel && (g->isolated < 1 || static_cast<double>(g->isolated) < min_fraction * static_cast<double>(n)))
     return SLQ_OK;
   cudaStream_t st = static_cast<cudaStream_t>(g->stream);
   {
@@ -491,7 +496,7 @@ static int graph_fold(slq_graph* g, double min_fraction, int64_t* folded_out) {
   SLQ_CUDA(cudaMemcpyAsync(&nprime32, newid + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   SLQ_CUDA(cudaStreamSynchronize(st));
   const int64_t nprime = nprime32, m = n - nprime;
-  if (m < 1 || static_cast<double>(m) < min_fraction * static_cast<double>(n)) {
+  if (!relabel && (m < 1 || static_cast<double>(m) < min_fraction * static_cast<double>(n))) {
     cudaFreeAsync(keep, st);
     cudaFreeAsync(newid, st);
     return SLQ_OK;

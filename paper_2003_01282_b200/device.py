@@ -21,6 +21,7 @@ KIND_CODES = {"laplacian": _lib.LAPLACIAN, "normalized_laplacian": _lib.NORMALIZ
 # empty rows (and at least FOLD_MIN_N vertices) run the Lanczos recurrence on the folded graph.
 FOLD_MIN_FRACTION = 1.0 / 64
 FOLD_MIN_N = 256
+FLAT_MIN_NNZ = 1 << 24   # csrc/graph.cu kFlatMinNnz: graphs the flat SpMM (and so the degree order) applies to
 
 
 def worth_folding(row_offsets, n: int, nnz: int, min_fraction: float = FOLD_MIN_FRACTION) -> bool:
@@ -28,6 +29,8 @@ def worth_folding(row_offsets, n: int, nnz: int, min_fraction: float = FOLD_MIN_
     empty rows (an upper bound of the foldable vertices) making up >= min_fraction of them."""
     if n < FOLD_MIN_N or nnz <= 0:
         return False
+    if nnz >= FLAT_MIN_NNZ:
+        return True    # large graphs: the fold's degree order feeds the flat SpMM (the library decides)
     off = np.asarray(row_offsets)
     empty = int(off.size - 1 - np.count_nonzero(off[1:] != off[:-1]))
     return empty >= 1 and empty >= min_fraction * n

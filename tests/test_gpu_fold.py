@@ -163,3 +163,34 @@ def test_fold_nearly_all_isolated(cuda_device, kind):
     r2 = plain.rules(kind, 0, 0, 20, 15)
     assert np.allclose(r1.nodes.cpu().numpy(), r2.nodes.cpu().numpy(), rtol=0, atol=1e-12)
     assert np.allclose(r1.weights.cpu().numpy(), r2.weights.cpu().numpy(), rtol=0, atol=1e-12)
+
+
+def test_large_graph_without_isolated_vertices_is_degree_ordered(cuda_device):
+    """Large unit-weight graphs get the fold's degree order even with NO isolated vertex (m = 0: the
+    trailing row stays zero), because the flat SpMM (csrc/spmm_flat.cu) needs it.  The relabelled run
+    (flat SpMM, prescaled gathers) matches the unfolded run (warp-per-row SpMM) and the CPU oracle."""
+    rng = np.random.default_rng(11)
+    n = 1 << 19
+    ring = np.arange(n, dtype=np.int64)
+    u = np.concatenate([ring, rng.integers(0, n, 17 * n)])
+    v = np.concatenate([(ring + 1) % n, rng.integers(0, n, 17 * n)])
+    g = csr_from_edges(n, u, v)
+    assert g.nnz >= 1 << 24 and int(np.min(np.diff(np.asarray(g.row_offsets)))) >= 2
+    dg = DeviceGraph(g, cuda_device)
+    assert dg.folded == 0                       # nothing folded away ...
+    lens, rows = dg.lanczos_row_lengths(64)
+    assert rows == n + 1                        # ... but the recurrence runs on the relabelled graph
+    assert np.all(np.diff(lens) <= 0) and lens[0] == int(np.max(np.diff(np.asarray(g.row_offsets))))
+    plain = DeviceGraph(g, cuda_device, fold=None)
+    t = np.array(GRID.values)
+    for kind, fn in (("normalized_laplacian", _lib.FN_HEAT), ("density", _lib.FN_XLOGX)):
+        a = dg.rules(kind, 0, 0, 8, 12, dtype="f32")
+        b = plain.rules(kind, 0, 0, 8, 12, dtype="f32")
+        a.check()
+        b.check()
+        va, _ = a.integrate(t if fn == _lib.FN_HEAT else None, [fn])
+        vb, _ = b.integrate(t if fn == _lib.FN_HEAT else None, [fn])
+        assert golden.rel_l2(va.cpu().numpy(), vb.cpu().numpy()) <= 1e-5
+        if fn == _lib.FN_HEAT:
+            ref, _ = O.heat_trace(g, GRID.values, 8, 12, 0, threads=8)
+            assert golden.rel_l2(va[0].cpu().numpy(), ref) <= FP32_TOL

@@ -125,6 +125,8 @@ def test_fold_precheck_counts_empty_rows():
     assert not worth_folding(small.row_offsets, 10, small.nnz)
     empty = csr_from_edges(n, [], [])                                        # no edges: nothing to fold
     assert not worth_folding(empty.row_offsets, n, empty.nnz)
+    # large graphs always go to the library (it relabels them by degree for the flat SpMM)
+    assert worth_folding(dense.row_offsets, n, 1 << 24)
 
 
 # ---------------------------------------------------------------- reference objects and the plugin seam
