@@ -313,6 +313,7 @@ struct SpmmArgs {
 };
 
 bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st);   // spmm_flat.cu
+bool launch_spmm_flat_f64(int kind, const SpmmArgs& a, cudaStream_t st);
 
 // SpMM-internal kind: the normalized Laplacian gathering the PRESCALED vector dinv (.) u (written by
 // the previous step kernel), so no dinv[col] gather per nonzero; the epilogue is the normalized one.
@@ -956,6 +957,7 @@ static void launch_spmm(int kind, SpmmArgs a, cudaStream_t st, bool finish = tru
   const int gy = ceil_div(a.c, kSpmmBlk);
   bool flat = false;
   if constexpr (std::is_same<VT, float>::value) flat = launch_spmm_flat_f32(kind, a, st);
+  else flat = launch_spmm_flat_f64(kind, a, st);
   if (!flat) launch_spmm_main<VT>(kind, a, gy, st);
   if (finish && a.long_counts && a.max_long > 0) {
     LaunchScope ls(K_SPMM, st);

@@ -76,6 +76,11 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ double2 lds128d(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -96,8 +101,10 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
 // 4 (rows of <= 16 probes, 64 bytes: eight CSR rows per warp; a lane then loads the column indices of
 // two slots).  Shared-memory addressing is the same: a slot's rows of all the warp's CSR rows are 512
 // contiguous bytes, lane l's 16 bytes at offset 16 l.
-template <int KIND, bool BITS, int L>
+// VT = float (4 probes per lane) or double (2 probes per lane: rows of <= 16 fp64 probes).
+template <typename VT, int KIND, bool BITS, int L>
 __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel(SpmmArgs a) {
+  constexpr int EPL = 16 / static_cast<int>(sizeof(VT));   // probes per lane (one 16-byte piece of a row)
   static_assert(L == 8 || L == 4, "lanes per gathered row");
   constexpr int RPW = 32 / L;            // CSR rows a warp walks in lockstep
   constexpr int kOffBlock = 32 - RPW;    // rows per offsets block (32 prefetched offsets: RPW + 1 per group)
@@ -109,19 +116,19 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   const int qid = lane / L;
   const int qbase = lane & ~(L - 1);
 
-  // probes 4 sub .. 4 sub + 3 of the chunk
-  bool pv[4];
-  double rj[4];
+  // probes EPL sub .. EPL sub + EPL - 1 of the chunk
+  bool pv[EPL];
+  double rj[EPL];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    pv[j] = 4 * sub + j < a.c;
-    rj[j] = pv[j] ? __ldg(a.r + 4 * sub + j) : 1.0;
+  for (int j = 0; j < EPL; ++j) {
+    pv[j] = EPL * sub + j < a.c;
+    rj[j] = pv[j] ? __ldg(a.r + EPL * sub + j) : 1.0;
   }
-  const bool all4 = pv[3];
-  const bool lane_nl = KIND != kPair || 4 * sub < a.split;   // pair chunk: this lane's operator
-  // 16 bytes of a row per lane; lanes past the row's end (ldc < 32) copy nothing (zero fill)
-  const int lane_bytes = 4 * sub + 3 < a.ldc_in ? 16 : 0;
-  const uint32_t strideb = static_cast<uint32_t>(a.ldc_in) * 4u;   // row stride in bytes
+  const bool all4 = pv[EPL - 1];
+  const bool lane_nl = KIND != kPair || EPL * sub < a.split;   // pair chunk: this lane's operator
+  // 16 bytes of a row per lane; lanes past the row's end copy nothing (zero fill)
+  const int lane_bytes = EPL * sub + EPL - 1 < a.ldc_in ? 16 : 0;
+  const uint32_t strideb = static_cast<uint32_t>(a.ldc_in) * static_cast<uint32_t>(sizeof(VT));   // row stride in bytes
   const char* __restrict__ ugb =
       static_cast<const char*>((KIND == kNLPre || KIND == kPair) ? a.upre : a.u) + (lane_bytes ? 16 * sub : 0);   // gathered vector
   const char* __restrict__ uob = static_cast<const char*>(a.u) + (lane_bytes ? 16 * sub : 0);   // own values
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
                            (threadIdx.x >> 5) * kFlatWarpBytes + lane * 16;        // + buf * batch + q * 512
   const uint32_t sm_own = static_cast<uint32_t>(__cvta_generic_to_shared(flat_smem)) +
                           (threadIdx.x >> 5) * kFlatWarpBytes + kFlatNB * kFlatBatchBytes;   // + buf * own
-  float* __restrict__ w = static_cast<float*>(a.w) + 4 * sub;
+  VT* __restrict__ w = static_cast<VT*>(a.w) + EPL * sub;
   const int64_t* __restrict__ off = a.offsets;
   const int32_t* __restrict__ cols = a.cols;
   const double scale = (KIND == SLQ_DENSITY || KIND == kPair) ? a.dscal[3] : 0.0;
@@ -251,37 +258,37 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   };
 
   // ---- consumer state
-  double ae[4], ao[4];
+  double ae[EPL], ao[EPL];
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) ae[jj] = ao[jj] = 0.0;
+  for (int jj = 0; jj < EPL; ++jj) ae[jj] = ao[jj] = 0.0;
 
-  auto finish_row = [&](int64_t r, const float4& ownv, double d, double dis) {
-    const float own[4] = {ownv.x, ownv.y, ownv.z, ownv.w};
-    float y[4];
+  auto finish_row = [&](int64_t r, const double (&own)[EPL], double d, double dis) {
+    VT y[EPL];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
+    for (int jj = 0; jj < EPL; ++jj) {
       const double tot = ae[jj] + ao[jj];
-      const double x = __dmul_rn(static_cast<double>(own[jj]), rj[jj]);
+      const double x = __dmul_rn(own[jj], rj[jj]);
       const double sc = __dmul_rn(tot, rj[jj]);
       if constexpr (KIND == kPair)
-        y[jj] = static_cast<float>(lane_nl ? op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, sc, d, dis, scale)
-                                           : op_epilogue<SLQ_DENSITY>(x, sc, d, dis, scale));
+        y[jj] = from_f64<VT>(lane_nl ? op_epilogue<SLQ_NORMALIZED_LAPLACIAN>(x, sc, d, dis, scale)
+                                     : op_epilogue<SLQ_DENSITY>(x, sc, d, dis, scale));
       else
-        y[jj] = static_cast<float>(op_epilogue<KIND>(x, sc, d, dis, scale));
+        y[jj] = from_f64<VT>(op_epilogue<KIND>(x, sc, d, dis, scale));
     }
-    float* dst = w + r * a.ldc_out;
+    VT* dst = w + r * a.ldc_out;
     if (all4) {
-      *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+      if constexpr (EPL == 4) *reinterpret_cast<float4*>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+      else *reinterpret_cast<double2*>(dst) = make_double2(y[0], y[1]);
     } else {
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
+      for (int jj = 0; jj < EPL; ++jj)
         if (pv[jj]) dst[jj] = y[jj];
     }
   };
   auto finish_seg = [&](int64_t sg) {
-    double* dst = a.segpart + sg * a.cpad + 4 * sub;
+    double* dst = a.segpart + sg * a.cpad + EPL * sub;
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
+    for (int jj = 0; jj < EPL; ++jj)
       if (pv[jj]) dst[jj] = ae[jj] + ao[jj];
   };
   auto consume = [&](const Group& g, int buf) {
@@ -290,14 +297,14 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
       constexpr int kSlotRec = RPW * 32;   // bytes of one slot's records
 #pragma unroll
       for (int q = 0; q < kFlatU; ++q) {
-        const uint32_t wd = lds32(base + q * kSlotRec) >> (4 * sub);
+        const uint32_t wd = lds32(base + q * kSlotRec) >> (EPL * sub);
         // s_c: dinv[col] (normalized Laplacian; a zero-filled slot has dinv = 0), else 1 for a valid
         // slot and 0 for a zero-filled one: fma(s_c, +-1, acc) is the reference term or acc itself
         const double one = ((g.nv >> q) & 1) ? 1.0 : 0.0;
         const double sk = KIND == SLQ_NORMALIZED_LAPLACIAN ? lds64(base + q * kSlotRec + 16)
                           : (KIND == kPair ? (lane_nl ? lds64(base + q * kSlotRec + 16) : one) : one);
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
+        for (int jj = 0; jj < EPL; ++jj) {
           const double x = ((wd >> jj) & 1u) ? 1.0 : -1.0;
           if (q & 1) ao[jj] = fma(sk, x, ao[jj]); else ae[jj] = fma(sk, x, ae[jj]);
         }
@@ -306,6 +313,10 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
       const uint32_t base = sm_ring + buf * kFlatBatchBytes;
 #pragma unroll
       for (int q = 0; q < kFlatU; ++q) {
+        if constexpr (EPL == 2) {
+          const double2 x = lds128d(base + q * 512);
+          if (q & 1) { ao[0] += x.x; ao[1] += x.y; } else { ae[0] += x.x; ae[1] += x.y; }
+        } else {
         const float4 x = lds128(base + q * 512);
 #if SLQ_FLAT_CVT
         // acc + double(x) without the conversion instruction (the XU pipe converts 4 lanes per clock):
@@ -334,6 +345,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
           ae[2] += static_cast<double>(x.z); ae[3] += static_cast<double>(x.w);
         }
 #endif
+        }
       }
     }
     if (g.fl & GF_END) {
@@ -342,15 +354,18 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
           finish_seg(static_cast<int64_t>(g.r0) + qid);
         } else {
           const uint32_t ob = sm_own + buf * kFlatOwnBytes;
-          float4 ownv;
+          double ownv[EPL];
           if constexpr (BITS) {
-            const uint32_t wd = lds32(ob + qid * (L * 16)) >> (4 * sub);
-            ownv.x = (wd & 1u) ? 1.f : -1.f;
-            ownv.y = (wd & 2u) ? 1.f : -1.f;
-            ownv.z = (wd & 4u) ? 1.f : -1.f;
-            ownv.w = (wd & 8u) ? 1.f : -1.f;
+            const uint32_t wd = lds32(ob + qid * (L * 16)) >> (EPL * sub);
+#pragma unroll
+            for (int jj = 0; jj < EPL; ++jj) ownv[jj] = ((wd >> jj) & 1u) ? 1.0 : -1.0;
+          } else if constexpr (EPL == 2) {
+            const double2 v = lds128d(ob + lane * 16);
+            ownv[0] = v.x; ownv[1] = v.y;
           } else {
-            ownv = lds128(ob + lane * 16);
+            const float4 v = lds128(ob + lane * 16);
+            ownv[0] = static_cast<double>(v.x); ownv[1] = static_cast<double>(v.y);
+            ownv[2] = static_cast<double>(v.z); ownv[3] = static_cast<double>(v.w);
           }
           const double d = lds64(ob + 512 + qid * 16);
           const double dis = NL ? lds64(ob + 512 + qid * 16 + 8) : 0.0;
@@ -358,7 +373,7 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
         }
       }
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) ae[jj] = ao[jj] = 0.0;
+      for (int jj = 0; jj < EPL; ++jj) ae[jj] = ao[jj] = 0.0;
     }
   };
   auto issue = [&](const Group& g, int32_t col, int32_t col2, int buf) {
@@ -442,20 +457,20 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
   cp_async_wait<0>();
 }
 
-template <int KIND, bool BITS, int L = 8>
+template <typename VT, int KIND, bool BITS, int L = 8>
 static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
   const dim3 grid(148 * kFlatCtasPerSm);
   static std::atomic<bool> attr[64];
-  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<KIND, BITS, L>), kFlatSmem, attr)) return false;
+  if (!smem_optin(reinterpret_cast<const void*>(spmm_flat_kernel<VT, KIND, BITS, L>), kFlatSmem, attr)) return false;
   if (a.win_rows <= 0) {
-    spmm_flat_kernel<KIND, BITS, L><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
+    spmm_flat_kernel<VT, KIND, BITS, L><<<grid, kFlatThreads, kFlatSmem, st>>>(a);
     return true;
   }
   constexpr bool REC = KIND == SLQ_NORMALIZED_LAPLACIAN || KIND == kPair;
   const void* base = BITS ? static_cast<const void*>(REC ? a.rec : a.bits)
                           : ((KIND == kNLPre || KIND == kPair) ? a.upre : a.u);
   const size_t row_bytes = BITS ? sizeof(uint32_t) * (REC ? kRecWords : kBitWords)
-                                : sizeof(float) * static_cast<size_t>(a.ldc_in);
+                                : sizeof(VT) * static_cast<size_t>(a.ldc_in);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kFlatThreads);
@@ -470,42 +485,52 @@ static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
   at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<KIND, BITS, L>, a);
+  cudaLaunchKernelEx(&cfg, spmm_flat_kernel<VT, KIND, BITS, L>, a);
   l2_demote(base, at[0].val.accessPolicyWindow.num_bytes, st);
   return true;
 }
 
-// True when the flat kernel took the launch (fp32 rows of 17..32 probes, unit weights, a gathered
-// vector, the Lanczos path, a graph with fine tiles); the caller falls back to spmm_kernel otherwise.
-bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st) {
+// True when the flat kernel took the launch (gathered rows of <= 128 bytes: <= 32 fp32 or <= 16 fp64
+// probes, unit weights, the Lanczos path, a graph with fine tiles); the caller falls back to spmm_kernel.
+template <typename VT>
+static bool launch_flat(int kind, const SpmmArgs& a, cudaStream_t st) {
+  constexpr int EPL = 16 / static_cast<int>(sizeof(VT));
+  constexpr int kMaxCols = 8 * EPL;   // 128-byte rows
   if (!a.ftile_rows || a.nftiles <= 0 || a.weights || !a.r) return false;
-  if (a.ldc_in > 32 || a.ldc_out > 32 || a.c > 32 || (a.ldc_in & 3) || (a.ldc_out & 3) || a.ldc_in < 4) return false;
-  const bool narrow = a.ldc_in <= 16;   // 64-byte rows: 4 lanes per row
+  if (a.ldc_in > kMaxCols || a.ldc_out > kMaxCols || a.c > kMaxCols || (a.ldc_in & (EPL - 1)) || (a.ldc_out & (EPL - 1)) ||
+      a.ldc_in < EPL)
+    return false;
+  const bool narrow = a.ldc_in <= 4 * EPL;   // 64-byte rows: 4 lanes per row
   if (a.n_rows >= (int64_t(1) << 29) || a.max_seg >= (int64_t(1) << 29)) return false;
   // the normalized Laplacian needs dinv[col] per nonzero: prescaled gathers, or the first step's records
   if (kind == SLQ_NORMALIZED_LAPLACIAN && !(a.bits ? a.rec != nullptr : a.upre != nullptr)) return false;
   const bool pair = a.split < a.c;
-  if (pair && (kind != SLQ_NORMALIZED_LAPLACIAN || (a.split & 3) || narrow)) return false;
+  if (pair && (kind != SLQ_NORMALIZED_LAPLACIAN || (a.split & (EPL - 1)) || narrow || EPL != 4)) return false;
   LaunchScope ls(K_SPMM, st);
-  if (pair) return a.bits ? flat_go<kPair, true>(a, st) : flat_go<kPair, false>(a, st);
+  if constexpr (EPL == 4) {
+    if (pair) return a.bits ? flat_go<VT, kPair, true>(a, st) : flat_go<VT, kPair, false>(a, st);
+  }
   if (narrow) {
     if (a.bits) {
-      if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<SLQ_NORMALIZED_LAPLACIAN, true, 4>(a, st);
-      if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, true, 4>(a, st);
-      return flat_go<SLQ_LAPLACIAN, true, 4>(a, st);
+      if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<VT, SLQ_NORMALIZED_LAPLACIAN, true, 4>(a, st);
+      if (kind == SLQ_DENSITY) return flat_go<VT, SLQ_DENSITY, true, 4>(a, st);
+      return flat_go<VT, SLQ_LAPLACIAN, true, 4>(a, st);
     }
-    if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<kNLPre, false, 4>(a, st);
-    if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, false, 4>(a, st);
-    return flat_go<SLQ_LAPLACIAN, false, 4>(a, st);
+    if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<VT, kNLPre, false, 4>(a, st);
+    if (kind == SLQ_DENSITY) return flat_go<VT, SLQ_DENSITY, false, 4>(a, st);
+    return flat_go<VT, SLQ_LAPLACIAN, false, 4>(a, st);
   }
   if (a.bits) {
-    if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<SLQ_NORMALIZED_LAPLACIAN, true>(a, st);
-    if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, true>(a, st);
-    return flat_go<SLQ_LAPLACIAN, true>(a, st);
+    if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<VT, SLQ_NORMALIZED_LAPLACIAN, true>(a, st);
+    if (kind == SLQ_DENSITY) return flat_go<VT, SLQ_DENSITY, true>(a, st);
+    return flat_go<VT, SLQ_LAPLACIAN, true>(a, st);
   }
-  if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<kNLPre, false>(a, st);
-  if (kind == SLQ_DENSITY) return flat_go<SLQ_DENSITY, false>(a, st);
-  return flat_go<SLQ_LAPLACIAN, false>(a, st);
+  if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<VT, kNLPre, false>(a, st);
+  if (kind == SLQ_DENSITY) return flat_go<VT, SLQ_DENSITY, false>(a, st);
+  return flat_go<VT, SLQ_LAPLACIAN, false>(a, st);
 }
+
+bool launch_spmm_flat_f32(int kind, const SpmmArgs& a, cudaStream_t st) { return launch_flat<float>(kind, a, st); }
+bool launch_spmm_flat_f64(int kind, const SpmmArgs& a, cudaStream_t st) { return launch_flat<double>(kind, a, st); }
 
 }  // namespace slq

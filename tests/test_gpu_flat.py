@@ -47,10 +47,11 @@ else:
     dg = DeviceGraph(synth.barabasi_albert(3000, 3, seed=1), dev, fold=None)   # not degree ordered
 res = {}
 for kind in ('normalized_laplacian', 'density', 'laplacian'):
-    for nv in (32, 24, 19, 16, 12, 8, 5):
-        a, b, s = dg.tridiagonals(kind, 0, 0, nv, 12, dtype='f32')
+    for nv, dt in ((32, 'f32'), (24, 'f32'), (19, 'f32'), (16, 'f32'), (12, 'f32'), (8, 'f32'), (5, 'f32'),
+                   (16, 'f64'), (11, 'f64'), (8, 'f64'), (3, 'f64')):
+        a, b, s = dg.tridiagonals(kind, 0, 0, nv, 12, dtype=dt)
         blob = a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()
-        res[kind + '/' + str(nv)] = hashlib.sha256(blob).hexdigest()
+        res[kind + '/' + str(nv) + '/' + dt] = hashlib.sha256(blob).hexdigest()
 vals, _ = dg.rules('normalized_laplacian', 0, 0, 32, 12, dtype='f32').integrate(
     np.logspace(-2, 2, 250), [_lib.FN_HEAT])
 np.save(out_path, vals.cpu().numpy()[0])
@@ -70,7 +71,7 @@ def _run(mode, flat, out_path):
 def test_flat_spmm_bitwise_equals_warp_per_row(cuda_device, tmp_path, mode):
     old = _run(mode, "0", tmp_path / "old.npy")
     new = _run(mode, "1", tmp_path / "new.npy")
-    assert old.keys() == new.keys() and len(old) == 21
+    assert old.keys() == new.keys() and len(old) == 33
     assert [k for k in old if old[k] != new[k]] == []
     assert np.array_equal(np.load(tmp_path / "old.npy"), np.load(tmp_path / "new.npy"))
 

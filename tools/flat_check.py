@@ -21,10 +21,11 @@ scale = int(sys.argv[1])
 dg = DeviceGraph.rmat(scale, 16, seed=0, device=torch.device('cuda', 0))
 out = {}
 for kind in ('normalized_laplacian', 'density', 'laplacian'):
-    for nv in (32, 24, 19, 16, 12, 8, 5):
-        a, b, s = dg.tridiagonals(kind, 0, 0, nv, 15, dtype='f32')
+    for nv, dt in ((32, 'f32'), (24, 'f32'), (19, 'f32'), (16, 'f32'), (12, 'f32'), (8, 'f32'), (5, 'f32'),
+                   (16, 'f64'), (11, 'f64'), (8, 'f64'), (3, 'f64')):
+        a, b, s = dg.tridiagonals(kind, 0, 0, nv, 15, dtype=dt)
         h = hashlib.sha256(a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()).hexdigest()
-        out[f'{kind}/{nv}'] = [h[:16], float(a[0, 0]), float(a[-1, -1])]
+        out[f'{kind}/{nv}/{dt}'] = [h[:16], float(a[0, 0]), float(a[-1, -1])]
 print(json.dumps(out))
 """ % ROOT
 

@@ -20,11 +20,12 @@ ap.add_argument("--scale", type=int, default=25)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--skip-c2", action="store_true")
 ap.add_argument("--nv", type=int, default=16, help="probes of the R-MAT case (32: the folded C5 chunk width)")
+ap.add_argument("--rmat-dtype", default="f32")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 out = {"lib": _lib.LIB_PATH, "env": {k: v for k, v in os.environ.items() if k.startswith("SLQ_")}}
 cases = [("c2", lambda: DeviceGraph(synth.sbm(100_000, 10, 1e-3, 1e-5, seed=0), dev), 100, "f64"),
-         (f"drmat{args.scale}", lambda: DeviceGraph.rmat(args.scale, 16, seed=0, device=dev), args.nv, "f32")]
+         (f"drmat{args.scale}", lambda: DeviceGraph.rmat(args.scale, 16, seed=0, device=dev), args.nv, args.rmat_dtype)]
 for name, make, nv, dt in cases[1:] if args.skip_c2 else cases:
     dg = make()
     for _ in range(2):
