@@ -97,15 +97,15 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
 // record (a.rec), so dinv[col] comes from the same sector -- copied by ONE lane (lane `sub` copies its
 // quarter's slot `sub`: the column index it loaded itself), 32 bytes of shared memory per slot.
 //
-// L = lanes per row of the vector: 8 (rows of 17..32 probes, 128 bytes: a quad of CSR rows per warp) or
-// 4 (rows of <= 16 probes, 64 bytes: eight CSR rows per warp; a lane then loads the column indices of
-// two slots).  Shared-memory addressing is the same: a slot's rows of all the warp's CSR rows are 512
+// L = lanes per row of the vector: 8 (128-byte rows: a quad of CSR rows per warp), 4 (64-byte rows:
+// eight CSR rows per warp; a lane then loads the column indices of two slots) or 16 (256-byte rows of
+// 17..32 fp64 probes: two CSR rows per warp).  Shared-memory addressing is the same: a slot's rows of all the warp's CSR rows are 512
 // contiguous bytes, lane l's 16 bytes at offset 16 l.
 // VT = float (4 probes per lane) or double (2 probes per lane: rows of <= 16 fp64 probes).
 template <typename VT, int KIND, bool BITS, int L>
 __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel(SpmmArgs a) {
   constexpr int EPL = 16 / static_cast<int>(sizeof(VT));   // probes per lane (one 16-byte piece of a row)
-  static_assert(L == 8 || L == 4, "lanes per gathered row");
+  static_assert(L == 16 || L == 8 || L == 4, "lanes per gathered row");
   constexpr int RPW = 32 / L;            // CSR rows a warp walks in lockstep
   constexpr int kOffBlock = 32 - RPW;    // rows per offsets block (32 prefetched offsets: RPW + 1 per group)
   constexpr unsigned FULL = 0xffffffffu;
@@ -383,8 +383,10 @@ __global__ void __launch_bounds__(kFlatThreads, kFlatCtasPerSm) spmm_flat_kernel
         const uint32_t dst = sm_warp + buf * kFlatBatchBytes + (sub * RPW + qid) * 32;
         const unsigned char* src = recb + static_cast<uint64_t>(static_cast<uint32_t>(col)) * rec_stride;
         const int nb = ((g.nv >> sub) & 1) ? 16 : 0;
-        cp_async16(dst, src, nb);
-        if (REC) cp_async16(dst + 16, src + 16, nb);
+        if (L <= kFlatU || sub < kFlatU) {
+          cp_async16(dst, src, nb);
+          if (REC) cp_async16(dst + 16, src + 16, nb);
+        }
         if (L == 4) {   // this lane's second slot
           const uint32_t dst2 = dst + 4 * RPW * 32;
           const unsigned char* src2 = recb + static_cast<uint64_t>(static_cast<uint32_t>(col2)) * rec_stride;
@@ -495,12 +497,13 @@ static bool flat_go(const SpmmArgs& a, cudaStream_t st) {
 template <typename VT>
 static bool launch_flat(int kind, const SpmmArgs& a, cudaStream_t st) {
   constexpr int EPL = 16 / static_cast<int>(sizeof(VT));
-  constexpr int kMaxCols = 8 * EPL;   // 128-byte rows
+  constexpr int kMaxCols = EPL == 2 ? 32 : 32;   // 128-byte rows (fp32), 256-byte rows (fp64): the narrow class
   if (!a.ftile_rows || a.nftiles <= 0 || a.weights || !a.r) return false;
   if (a.ldc_in > kMaxCols || a.ldc_out > kMaxCols || a.c > kMaxCols || (a.ldc_in & (EPL - 1)) || (a.ldc_out & (EPL - 1)) ||
       a.ldc_in < EPL)
     return false;
   const bool narrow = a.ldc_in <= 4 * EPL;   // 64-byte rows: 4 lanes per row
+  const bool wide16 = a.ldc_in > 8 * EPL;    // 256-byte rows (17..32 fp64 probes): 16 lanes per row
   if (a.n_rows >= (int64_t(1) << 29) || a.max_seg >= (int64_t(1) << 29)) return false;
   // the normalized Laplacian needs dinv[col] per nonzero: prescaled gathers, or the first step's records
   if (kind == SLQ_NORMALIZED_LAPLACIAN && !(a.bits ? a.rec != nullptr : a.upre != nullptr)) return false;
@@ -509,6 +512,18 @@ static bool launch_flat(int kind, const SpmmArgs& a, cudaStream_t st) {
   LaunchScope ls(K_SPMM, st);
   if constexpr (EPL == 4) {
     if (pair) return a.bits ? flat_go<VT, kPair, true>(a, st) : flat_go<VT, kPair, false>(a, st);
+  }
+  if constexpr (EPL == 2) {
+    if (wide16) {
+      if (a.bits) {
+        if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<VT, SLQ_NORMALIZED_LAPLACIAN, true, 16>(a, st);
+        if (kind == SLQ_DENSITY) return flat_go<VT, SLQ_DENSITY, true, 16>(a, st);
+        return flat_go<VT, SLQ_LAPLACIAN, true, 16>(a, st);
+      }
+      if (kind == SLQ_NORMALIZED_LAPLACIAN) return flat_go<VT, kNLPre, false, 16>(a, st);
+      if (kind == SLQ_DENSITY) return flat_go<VT, SLQ_DENSITY, false, 16>(a, st);
+      return flat_go<VT, SLQ_LAPLACIAN, false, 16>(a, st);
+    }
   }
   if (narrow) {
     if (a.bits) {

@@ -48,7 +48,7 @@ else:
 res = {}
 for kind in ('normalized_laplacian', 'density', 'laplacian'):
     for nv, dt in ((32, 'f32'), (24, 'f32'), (19, 'f32'), (16, 'f32'), (12, 'f32'), (8, 'f32'), (5, 'f32'),
-                   (16, 'f64'), (11, 'f64'), (8, 'f64'), (3, 'f64')):
+                   (32, 'f64'), (19, 'f64'), (16, 'f64'), (11, 'f64'), (8, 'f64'), (3, 'f64')):
         a, b, s = dg.tridiagonals(kind, 0, 0, nv, 12, dtype=dt)
         blob = a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()
         res[kind + '/' + str(nv) + '/' + dt] = hashlib.sha256(blob).hexdigest()
@@ -71,7 +71,7 @@ def _run(mode, flat, out_path):
 def test_flat_spmm_bitwise_equals_warp_per_row(cuda_device, tmp_path, mode):
     old = _run(mode, "0", tmp_path / "old.npy")
     new = _run(mode, "1", tmp_path / "new.npy")
-    assert old.keys() == new.keys() and len(old) == 33
+    assert old.keys() == new.keys() and len(old) == 39
     assert [k for k in old if old[k] != new[k]] == []
     assert np.array_equal(np.load(tmp_path / "old.npy"), np.load(tmp_path / "new.npy"))
 

@@ -22,7 +22,7 @@ dg = DeviceGraph.rmat(scale, 16, seed=0, device=torch.device('cuda', 0))
 out = {}
 for kind in ('normalized_laplacian', 'density', 'laplacian'):
     for nv, dt in ((32, 'f32'), (24, 'f32'), (19, 'f32'), (16, 'f32'), (12, 'f32'), (8, 'f32'), (5, 'f32'),
-                   (16, 'f64'), (11, 'f64'), (8, 'f64'), (3, 'f64')):
+                   (32, 'f64'), (19, 'f64'), (16, 'f64'), (11, 'f64'), (8, 'f64'), (3, 'f64')):
         a, b, s = dg.tridiagonals(kind, 0, 0, nv, 15, dtype=dt)
         h = hashlib.sha256(a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()).hexdigest()
         out[f'{kind}/{nv}/{dt}'] = [h[:16], float(a[0, 0]), float(a[-1, -1])]
