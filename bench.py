@@ -177,6 +177,10 @@ def device_graph(cfg, dev):
 
     if cfg["graph"] == "rmat":
         a, b, c = cfg["abc"]
+        test_scale = os.environ.get("BENCH_TEST_RMAT_SCALE")   # tests only: a small stand-in graph (the
+        if test_scale:                                         # line then says so in config.workload)
+            cfg["scale"] = int(test_scale)
+            cfg["workload"] = f"TEST RUN at R-MAT scale {test_scale}, NOT the benchmark: " + cfg["workload"]
         return DeviceGraph.rmat(cfg["scale"], cfg["edge_factor"], a, b, c, seed=cfg["graph_seed"], device=dev), None
     from paper_2003_01282_b200 import synth
 

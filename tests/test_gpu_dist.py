@@ -237,3 +237,27 @@ def test_two_ranks_operator_pair_bitwise_equal_single_rank(cuda_device):
     assert one[0] > 0 and one[0] == two[0]
     for a, b in zip(one[1:], two[1:]):
         assert np.array_equal(a, b)
+
+
+def test_bench_eight_ranks_use_the_operator_pair_block(cuda_device, tmp_path):
+    """`bench.py --gpus 8` as the driver launches it (torchrun, one process per rank; here gloo ranks
+    on one GPU and a scale-14 stand-in graph): 128 probes over 8 ranks = 16 per rank, so every rank
+    runs the operator-pair block; the line is the contract's and the end-to-end values equal the
+    device-resident run's."""
+    import json
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo", BENCH_TEST_RMAT_SCALE="14", BENCH_NO_CLOCKS="1",
+               SLQ_SPMM_FLAT="1", SLQ_PRESCALE_MIN_N="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "8", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "8", "--steps", "1", "--warmup", "3",
+           "--no-cpu-baseline", "--e2e-reps", "1"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 8 and line["scaling"] == "strong"
+    assert line["graph"]["probes_per_rank"] == 16 and line["graph"]["operator_pair_block"] is True
+    assert line["config"]["workload"].startswith("TEST RUN")
+    assert line["e2e"]["values_equal_device_resident_run"] is True
+    assert line["gpu_launches"] > 0 and line["value"] > 0
