@@ -131,3 +131,26 @@ def test_operator_pair_falls_back_on_small_graphs(cuda_device):
     rb = dg.rules("density", 0, 0, 16, 10, dtype="f32")
     assert torch.equal(a.nodes, ra.nodes) and torch.equal(a.weights, ra.weights)
     assert torch.equal(b.nodes, rb.nodes) and torch.equal(b.weights, rb.weights)
+
+
+def test_captured_signature_on_the_flat_path(cuda_device):
+    """A whole signature captured as a CUDA graph (device.CapturedSignature) on a graph that takes the
+    flat SpMM by default (R-MAT-20: >= 2^24 nonzeros, degree-ordered fold): the cp.async kernels, their
+    shared-memory opt-in and the L2 window attribute are capturable; replays equal the eager run."""
+    import torch
+
+    from paper_2003_01282_b200 import _lib
+    from paper_2003_01282_b200.device import CapturedSignature, DeviceGraph
+
+    dg = DeviceGraph.rmat(20, 16, seed=0, device=cuda_device)
+    assert dg.nnz >= 1 << 24
+    t = np.geomspace(1e-2, 1e2, 64)
+    for kind, fns, tt, nv, dt in (("normalized_laplacian", [_lib.FN_HEAT], t, 32, "f32"),
+                                  ("density", [_lib.FN_XLOGX], None, 16, "f32"),
+                                  ("normalized_laplacian", [_lib.FN_HEAT], t, 16, "f64")):
+        cap = CapturedSignature(dg, kind, 0, nv, 12, tt, fns, dtype=dt)
+        first = cap.replay()[0].clone()
+        cap.check()
+        second = cap.replay()[0].clone()
+        eager, _ = dg.rules(kind, 0, 0, nv, 12, dtype=dt).integrate(tt, fns)
+        assert torch.equal(first, eager) and torch.equal(first, second)
