@@ -1,5 +1,7 @@
-// Flat SpMM for large degree-ordered graphs, fp32 chunks of 17..32 probes (128-byte rows): the C5
-// gather.
+// Flat SpMM for large degree-ordered graphs, chunks of <= 32 probes (the narrow class: gathered rows
+// of <= 128 bytes in fp32, <= 256 bytes in fp64): the C5 gather.  Described for its main shape, fp32
+// rows of 17..32 probes (128 bytes, 8 lanes per row, four CSR rows per warp); see L and VT below for
+// 64-byte and 256-byte rows.
 //
 // The warp-per-row kernel (engine.cuh: spmm_kernel) walks offsets -> columns -> gathers -> epilogue
 // as one dependent chain per row and holds the gathered rows in registers, so a warp keeps ~10 line
