@@ -75,7 +75,7 @@ class _DeviceGraph:
         _check(_lib.slq_graph_create_host(g.n, int(off[-1]) if g.n else 0, off.ctypes.data, cols.ctypes.data,
                                           None if w is None else w.ctypes.data, None, ctypes.byref(self.h)), errors)
         # isolated-vertex fold; large graphs always ask (the library also relabels them by degree)
-        if g.n >= 256 and (g.nnz >= 1 << 24 or np.count_nonzero(np.diff(off) == 0) * 64 >= g.n):
+        if g.n >= 256 and (int(off[-1]) >= 1 << 24 or np.count_nonzero(np.diff(off) == 0) * 64 >= g.n):
             m = ctypes.c_int64()
             _check(_lib.slq_graph_fold_isolated(self.h, 1.0 / 64, ctypes.byref(m)), errors)
 
