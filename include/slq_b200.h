@@ -134,8 +134,11 @@ int slq_rmat_uniform_host(uint64_t seed, uint64_t sample, int level, double* out
  * operator gives 0 there, operators.py:76-99) evolve in the Lanczos recurrence as the probe sign times
  * one per-probe scalar, so the recurrence can run on the graph without them plus ONE trailing empty
  * row standing for all m of them (value sqrt(m) times that scalar): dot products agree with the
- * unfolded ones to rounding, the Lanczos vectors lose m rows.  Builds the fold when m >= 1 and
- * m >= min_fraction * n (min_fraction < 0 drops an existing fold); *folded_host = m (0: not folded).
+ * unfolded ones to rounding, the Lanczos vectors lose m rows.  The kept rows are renumbered by
+ * descending degree (every row keeps its columns in stored order, so row sums are bitwise the
+ * unfolded ones).  Builds the fold when m >= 1 and m >= min_fraction * n (min_fraction < 0 drops an
+ * existing fold); unit-weight graphs with >= 2^24 nonzeros are folded for ANY m >= 0, because the
+ * degree order is what the flat SpMM needs (m = 0: the trailing row stays zero).  *folded_host = m.
  * Afterwards slq_lanczos / slq_rules / slq_signature on g use the fold whenever the all-staged
  * schedule runs (generated probes, reorth on, 2 <= s' <= 17, <= 128 probes per chunk); the operator
  * apply, degrees, CSR export and the batched path keep using g itself.  Synchronises the creation
