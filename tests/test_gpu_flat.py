@@ -154,3 +154,49 @@ def test_captured_signature_on_the_flat_path(cuda_device):
         second = cap.replay()[0].clone()
         eager, _ = dg.rules(kind, 0, 0, nv, 12, dtype=dt).integrate(tt, fns)
         assert torch.equal(first, eager) and torch.equal(first, second)
+
+
+FUZZ_CHILD = r"""
+import sys, json, hashlib
+import numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2003_01282_b200.device import DeviceGraph
+from paper_2003_01282_b200.graphs import csr_from_edges
+dev = torch.device('cuda', 0)
+rng = np.random.default_rng(20260321)
+res = []
+for case in range(24):
+    n = int(rng.integers(200, 6000))
+    m = int(rng.integers(n // 2, 12 * n))
+    live = np.flatnonzero(rng.random(n) > rng.choice([0.0, 0.2, 0.6]))
+    if live.size < 2:
+        live = np.arange(n)
+    hub = live[: max(1, live.size // 50)]
+    u = np.where(rng.random(m) < 0.3, hub[rng.integers(0, hub.size, m)], live[rng.integers(0, live.size, m)])
+    v = live[rng.integers(0, live.size, m)]
+    g = csr_from_edges(n, u, v)
+    fold = None if case %% 3 == 0 else 0.0
+    dg = DeviceGraph(g, dev, fold=fold)
+    kind = ('normalized_laplacian', 'density', 'laplacian')[case %% 3]
+    dt = 'f64' if case %% 4 == 3 else 'f32'
+    nv = int(rng.integers(1, 33))
+    steps = int(rng.integers(3, 16))
+    a, b, s = dg.tridiagonals(kind, int(rng.integers(0, 1000)), int(rng.integers(0, 50)), nv, steps, dtype=dt)
+    blob = a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes() + s.cpu().numpy().tobytes()
+    res.append([n, int(g.nnz), kind, dt, nv, steps, hashlib.sha256(blob).hexdigest()[:16]])
+print(json.dumps(res))
+""" % ROOT
+
+
+def test_flat_spmm_fuzz_bitwise(cuda_device):
+    """24 random graphs (hubs, up to 60%% empty rows, folded or not), operator kinds, fp32 and fp64,
+    1..32 probes, 3..15 steps, random seeds and probe offsets: the flat SpMM forced on gives the bits
+    of the warp-per-row kernel."""
+    out = {}
+    for flat in ("0", "1"):
+        env = dict(os.environ, SLQ_SPMM_FLAT=flat, SLQ_PRESCALE_MIN_N="0")
+        r = subprocess.run([sys.executable, "-c", FUZZ_CHILD], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out[flat] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(out["0"]) == 24
+    assert [c for c, d in zip(out["0"], out["1"]) if c != d] == []
