@@ -751,6 +751,8 @@ int lanczos_pair_key(const slq_graph* g, const SeedKey& seed, int64_t probe_begi
       fold.orig = g;
       gr = g->folded;
     }
+    // the pair block is ONE chunk of 2 * split columns: run the operators apart if it does not fit
+    const bool fits = choose_chunk(gr, 2 * split, S, 4, true, st) >= 2 * split;
     char* tmp = nullptr;
     const size_t bn = sizeof(double) * 2 * split * S;
     SLQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), 2 * bn + sizeof(int32_t) * 2 * split + 16, st));
@@ -758,8 +760,9 @@ int lanczos_pair_key(const slq_graph* g, const SeedKey& seed, int64_t probe_begi
     double* tb = ta + 2 * split * S;
     int32_t* ts = reinterpret_cast<int32_t*>(tmp + 2 * bn);
     tl_pair_refused = false;
-    int rc = run_chunk<float>(gr, SLQ_NORMALIZED_LAPLACIAN, seed, probe_begin, nullptr, 0, 2 * split, S, ro, ta, tb, ts, 0,
-                              st, fold, nullptr, 0, SLQ_DENSITY, split);
+    int rc = fits ? run_chunk<float>(gr, SLQ_NORMALIZED_LAPLACIAN, seed, probe_begin, nullptr, 0, 2 * split, S, ro, ta, tb,
+                                     ts, 0, st, fold, nullptr, 0, SLQ_DENSITY, split)
+                  : pair_fail("operator-pair chunk does not fit the device memory");
     if (rc == SLQ_OK) {
       const size_t row = sizeof(double) * S;
       cudaMemcpyAsync(alpha_a, ta, row * count, cudaMemcpyDeviceToDevice, st);
